@@ -1,0 +1,348 @@
+/*
+ * biscale_gpu.h — C ABI of the B200 (sm_100a) decision-evaluation path of
+ * BiScale (arXiv 2602.18755).  Plain C: POD structs, plain pointers and
+ * sizes, no torch or CUDA types.  Every entry point returns an int status
+ * (BS_OK or one code per exception class of the reference's
+ * proj/include/pdsim/errors.hpp:10-56); the message is read back with
+ * bs_last_error().
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj/include/pdsim/):
+ *
+ *   bs_models_upload        ModelSet (perfmodel.hpp:494-503) held by every
+ *                           controller as `const ModelSet*` (dvfs.hpp:336)
+ *   bs_predict              predict_latency / predict_power
+ *                           (perfmodel.hpp:262-272), NdGrid::interpolate
+ *                           (perfmodel.hpp:150-193)
+ *   bs_project_batches      project_batches (dvfs.hpp:63-100)
+ *   bs_mpc_greedy           greedy_freq_select (dvfs.hpp:185-259), i.e.
+ *                           PrefillMpcController::run (dvfs.hpp:325-333)
+ *   bs_mpc_exhaustive       the exhaustive MPC oracle loop
+ *                           (tests/test_dvfs.cpp:74-94,
+ *                           tests/acceptance_main.cpp:245-261) over
+ *                           meets_slo (dvfs.hpp:105-122) and
+ *                           MpcEvaluator::time_weighted_power (dvfs.hpp:163-171)
+ *   bs_mpc_eval_codes       meets_slo + time_weighted_power for given
+ *                           assignments (per-trajectory parity probe)
+ *   bs_mpc_tables           the (k, f) -> (lat, pow) memo of MpcEvaluator::eval
+ *                           (dvfs.hpp:150-160)
+ *   bs_decode_pick          select_decode_freq_ex (dvfs.hpp:274-293), i.e.
+ *                           DecodePolicyController::decide (dvfs.hpp:347-350)
+ *   bs_goodput_table        build_config_table (placement.hpp:240-260) over
+ *                           evaluate_candidate / max_goodput
+ *                           (placement.hpp:154-238)
+ *   bs_placement_solve      solve_placement (placement.hpp:357-416)
+ *   bs_placement_max_throughput  solve_max_throughput (placement.hpp:421-499)
+ *
+ * Threading: a context is not thread-safe (one per host thread, each with its
+ * own CUDA stream).  Uploaded models are immutable; kernels are re-entrant.
+ * Ownership: the context owns device memory and streams; the caller owns
+ * every host array passed in or out; nothing is retained after return.
+ */
+#ifndef BISCALE_GPU_H_
+#define BISCALE_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_ABI_VERSION 1
+
+/* Hard limits of the device path (validated; ParameterError beyond them). */
+#define BS_MAX_RANK 4      /* grid axes: sum_len, n_requests, tp, freq_mhz */
+#define BS_MAX_K 16        /* MPC horizon (projected batches) */
+#define BS_MAX_CAND 32     /* MPC candidate rungs after ladder.select(N) */
+#define BS_MAX_LEVELS 32   /* greedy expansion levels (<= N-2) */
+#define BS_MAX_LADDER 64   /* decode ladder rungs */
+
+/* Status codes: one per exception class of errors.hpp. */
+enum bs_status {
+  BS_OK = 0,
+  BS_PARAMETER_ERROR = 1,  /* pdsim::ParameterError  (errors.hpp:10) */
+  BS_MODEL_ERROR = 2,      /* pdsim::ModelError      (errors.hpp:15) */
+  BS_SIMULATION_ERROR = 3, /* pdsim::SimulationError (errors.hpp:20) */
+  BS_CONFIG_ERROR = 4,     /* pdsim::ConfigError     (errors.hpp:25) */
+  BS_ACCOUNTING_ERROR = 5, /* pdsim::AccountingError (errors.hpp:30) */
+  BS_IO_ERROR = 6,         /* pdsim::IoError         (errors.hpp:40) */
+  BS_INFEASIBLE_ERROR = 7, /* pdsim::InfeasibleError (errors.hpp:47) */
+  BS_CUDA_ERROR = 100      /* device/runtime failure (no reference analogue) */
+};
+
+/* Axis roles: the axis names query_coords understands (perfmodel.hpp:204-207,
+ * 241-258).  BS_AXIS_UNKNOWN reproduces "grid: unknown axis" ModelError. */
+enum bs_axis_role {
+  BS_AXIS_UNKNOWN = -1,
+  BS_AXIS_SUM_LEN = 0,
+  BS_AXIS_N_REQUESTS = 1,
+  BS_AXIS_TP = 2,
+  BS_AXIS_FREQ = 3
+};
+
+enum bs_phase { BS_PHASE_PREFILL = 0, BS_PHASE_DECODE = 1 };
+
+/* One NdGrid (perfmodel.hpp:116-201): row-major values, last axis fastest. */
+typedef struct bs_grid {
+  int32_t rank;                    /* 1..BS_MAX_RANK */
+  int32_t role[BS_MAX_RANK];       /* enum bs_axis_role per axis */
+  int32_t n_knots[BS_MAX_RANK];    /* knots per axis (>= 1, strictly increasing) */
+  const double* knots[BS_MAX_RANK];
+  const double* values;            /* prod(n_knots) doubles */
+} bs_grid;
+
+/* IdlePowerModel::TpEntry (perfmodel.hpp:230-237). */
+typedef struct bs_idle_entry {
+  int32_t tp;
+  int32_t n;
+  const double* freqs_mhz;
+  const double* idle_w;
+} bs_idle_entry;
+
+/* ModelSet (perfmodel.hpp:494-503). */
+typedef struct bs_model_set {
+  bs_grid latency_prefill;
+  bs_grid latency_decode;
+  bs_grid power_prefill;
+  bs_grid power_decode;
+  int32_t n_idle;
+  const bs_idle_entry* idle;
+} bs_model_set;
+
+/* BatchFeatures (perfmodel.hpp:30-51); only n_requests and sum_len reach the
+ * grids (perfmodel.hpp:245-249). */
+typedef struct bs_features {
+  int64_t n_requests;
+  int64_t sum_len;
+} bs_features;
+
+/* SchedulerPolicy (scheduler.hpp:11-22). */
+typedef struct bs_scheduler_policy {
+  int64_t max_batch_tokens;   /* default 8192 */
+  int64_t max_batch_requests; /* default 256 */
+  int64_t kv_capacity_tokens; /* default 1000000 */
+  int32_t chunking;           /* default 1 */
+  int32_t _pad;
+} bs_scheduler_policy;
+
+/* MpcConfig (dvfs.hpp:17-34) with its SLOSpec (slo.hpp:7-16). */
+typedef struct bs_mpc_config {
+  int32_t horizon_K;          /* default 8 */
+  int32_t ladder_N;           /* default 7 */
+  int32_t n_ladder;
+  int32_t _pad;
+  const double* ladder_mhz;   /* FrequencyLadder::freqs_mhz, strictly increasing */
+  double ttft_ms;             /* SLOSpec::ttft_ms, default 600 */
+  double tpot_ms;             /* SLOSpec::tpot_ms, default 100 */
+  double percentile;          /* SLOSpec::percentile, default 0.99 */
+  double switch_latency_ms;   /* default 30 */
+  double margin;              /* default 0.05 */
+} bs_mpc_config;
+
+/* SnapshotWaiting (controller.hpp:26-31). */
+typedef struct bs_waiting {
+  int64_t id;
+  double arrival_ms;
+  int64_t total_len;
+  int64_t remaining_len;
+} bs_waiting;
+
+/* QueueSnapshot (controller.hpp:45-55) restricted to what the prefill MPC
+ * reads (dvfs.hpp:63-122, 325-333): the running batch enters the projection
+ * through ids/completes/arrivals/work_remaining/features only. */
+typedef struct bs_snapshot {
+  double now_ms;
+  double current_freq_mhz;
+  double target_freq_mhz;
+  double running_work_remaining;
+  bs_features running_features;
+  int32_t tp;
+  int32_t running_active;
+  int32_t n_waiting;
+  int32_t n_running;
+  const bs_waiting* waiting;
+  const uint8_t* running_completes;  /* n_running flags */
+  const double* running_arrivals_ms; /* n_running */
+} bs_snapshot;
+
+/* One MPC decision problem: a snapshot plus the index of its controller
+ * configuration in the cfgs/policies arrays passed alongside. */
+typedef struct bs_mpc_problem {
+  bs_snapshot snap;
+  int32_t cfg_index;
+  int32_t _pad;
+} bs_mpc_problem;
+
+/* GreedyLevelStats (dvfs.hpp:124-131). */
+typedef struct bs_level_stats {
+  int32_t level;
+  int32_t k_prime;
+  double replaced_mhz;
+  int64_t mutations;
+  int64_t feasible_mutations;
+  int32_t accepted;
+  int32_t _pad;
+} bs_level_stats;
+
+/* GreedyResult (dvfs.hpp:133-139) / exhaustive result, plus the controller's
+ * FreqDecision (controller.hpp:67-71) as PrefillMpcController::run derives it
+ * (dvfs.hpp:328-331). */
+typedef struct bs_mpc_result {
+  int32_t status;             /* per-problem status (bs_status) */
+  int32_t K;                  /* projection length; assignment length */
+  int32_t feasible;           /* GreedyResult::feasible */
+  int32_t n_levels;
+  int64_t eval_count;
+  double objective_w;
+  double freqs_mhz[BS_MAX_K]; /* assignment */
+  int32_t freq_index[BS_MAX_K]; /* index into the ascending candidate rungs */
+  double decision_freq_mhz;   /* FreqDecision::freq_mhz */
+  uint64_t feasible_count;    /* exhaustive: # feasible trajectories */
+  uint64_t trajectories;      /* exhaustive: N^K */
+  uint64_t best_code;         /* exhaustive: argmin code, batch 0 most significant */
+  bs_level_stats levels[BS_MAX_LEVELS];
+} bs_mpc_result;
+
+/* ProjectedBatch (dvfs.hpp:54-59), device-side summary. */
+typedef struct bs_projected_batch {
+  bs_features features;
+  double work_fraction;
+  double min_completing_arrival_ms; /* +inf when nothing completes */
+  int32_t n_completing;
+  int32_t _pad;
+} bs_projected_batch;
+
+/* DecodePolicyConfig (dvfs.hpp:36-48). */
+typedef struct bs_decode_config {
+  double tbt_slo_ms;          /* default 100 */
+  double kv_threshold;        /* default 0.9 */
+  double margin;              /* default 0 */
+  int32_t n_ladder;
+  int32_t _pad;
+  const double* ladder_mhz;
+} bs_decode_config;
+
+/* Inputs of select_decode_freq_ex (dvfs.hpp:274-275): batch features,
+ * KVCacheState (controller.hpp:16-24) and tp. */
+typedef struct bs_decode_query {
+  bs_features batch;
+  int64_t kv_capacity_tokens;
+  int64_t kv_used_tokens;
+  int32_t tp;
+  int32_t cfg_index;
+} bs_decode_query;
+
+/* DecodeDecision (dvfs.hpp:268-272). */
+typedef struct bs_decode_result {
+  double freq_mhz;
+  int64_t eval_count;
+  int32_t kv_override;
+  int32_t status;
+} bs_decode_result;
+
+typedef struct bs_ctx_s* bs_ctx_t;
+typedef struct bs_models_s* bs_models_t;
+
+/* --- context and models ---------------------------------------------------- */
+
+int bs_abi_version(void);
+int bs_ctx_create(int device, bs_ctx_t* out);
+void bs_ctx_destroy(bs_ctx_t ctx);
+const char* bs_last_error(bs_ctx_t ctx);
+/* Device the context runs on and its SM count (for host-side grid sizing). */
+int bs_ctx_info(bs_ctx_t ctx, int* device, int* sm_count);
+/* Synchronise the context's stream. */
+int bs_ctx_sync(bs_ctx_t ctx);
+/* Number of kernels the context launched since creation (instrumentation). */
+int64_t bs_ctx_kernel_launches(bs_ctx_t ctx);
+/* The context's cudaStream_t (as void*), for event timing by the caller. */
+void* bs_ctx_stream(bs_ctx_t ctx);
+/* Host<->device bytes moved by the last one-shot entry point. */
+int bs_ctx_last_transfer(bs_ctx_t ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+/* FP64 issue microbenchmark (independent DADD chains on every SM):
+ * measured non-FMA FP64 ops/s, the roofline denominator of the MPC kernels. */
+int bs_fp64_peak(bs_ctx_t ctx, double* ops_per_s, double* ms);
+
+/* Validates structure (NdGrid::validate_structure, perfmodel.hpp:127-138)
+ * and uploads an immutable device copy. */
+int bs_models_upload(bs_ctx_t ctx, const bs_model_set* models, bs_models_t* out);
+void bs_models_free(bs_ctx_t ctx, bs_models_t models);
+
+/* --- model queries (parity probes for the interpolator) --------------------- */
+
+/* which: 0 latency_prefill, 1 latency_decode, 2 power_prefill, 3 power_decode.
+ * n queries of (features, tp, freq); out values and per-query status
+ * (ModelError on non-positive/non-finite, perfmodel.hpp:264,270, or unknown
+ * axis, perfmodel.hpp:254); clamp_events: per-query clamp count. */
+int bs_predict(bs_ctx_t ctx, bs_models_t models, int which, const bs_features* feats,
+               const int32_t* tp, const double* freq_mhz, int n, double* out,
+               int32_t* status, uint32_t* clamp_events);
+
+/* Raw NdGrid::interpolate over caller coordinates (no role mapping):
+ * coords is n x grid->rank, row-major.  clamp_events per query. */
+int bs_grid_interpolate(bs_ctx_t ctx, const bs_grid* grid, const double* coords, int n,
+                        double* out, uint32_t* clamp_events);
+
+/* --- prefill MPC ---------------------------------------------------------- */
+
+/* project_batches for each problem: out is n x BS_MAX_K, K per problem in
+ * out_K.  Per-problem status in out_status (SimulationError from
+ * form_prefill_batch, scheduler.hpp:47). */
+int bs_project_batches(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
+                       int n_cfgs, const bs_mpc_problem* problems, int n, bs_projected_batch* out,
+                       int32_t* out_K, int32_t* out_status);
+
+/* greedy_freq_select for n independent decisions (one CTA per decision). */
+int bs_mpc_greedy(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
+                  const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
+                  bs_mpc_result* out);
+
+/* Exhaustive MPC: every |cand|^K assignment, feasibility by meets_slo,
+ * objective by time_weighted_power; argmin over (objective, assignment in
+ * lexicographic frequency order, batch 0 most significant) -- the rule
+ * dvfs.hpp:243 applies to greedy.  Nothing feasible: all-max, feasible = 0.
+ * Requires |cand|^K < 2^62. */
+int bs_mpc_exhaustive(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
+                      const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems,
+                      int n, bs_mpc_result* out);
+
+/* Resident batches (the throughput path): upload a batch of problems once
+ * (one H2D copy), then enqueue its kernels any number of times on the
+ * context stream without host synchronisation, and copy results out.
+ * mode: 0 exhaustive, 1 greedy.  bs_mpc_plan_kernel_ms returns the number
+ * of phases and their durations from the last run with record_kernel_times
+ * (exhaustive: prepare, scan, prefix, leaf, finalize; greedy: greedy). */
+typedef struct bs_mpc_plan_s* bs_mpc_plan_t;
+int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
+                       const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
+                       int mode, bs_mpc_plan_t* out);
+int bs_mpc_plan_run(bs_ctx_t ctx, bs_mpc_plan_t plan, int record_kernel_times);
+int bs_mpc_plan_results(bs_ctx_t ctx, bs_mpc_plan_t plan, bs_mpc_result* out);
+int bs_mpc_plan_kernel_ms(bs_ctx_t ctx, bs_mpc_plan_t plan, float* ms, int n_ms);
+int bs_mpc_plan_info(bs_ctx_t ctx, bs_mpc_plan_t plan, uint64_t* h2d_bytes, uint64_t* work_capacity);
+void bs_mpc_plan_destroy(bs_ctx_t ctx, bs_mpc_plan_t plan);
+
+/* Per-trajectory probe for one problem: codes[i] encodes an assignment with
+ * batch 0 as the most significant base-|cand| digit.  out_feasible[i] =
+ * meets_slo, out_objective[i] = time_weighted_power. */
+int bs_mpc_eval_codes(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfg,
+                      const bs_scheduler_policy* policy, const bs_mpc_problem* problem,
+                      const uint64_t* codes, int n, int32_t* out_feasible, double* out_objective);
+
+/* The per-(k, f) tables of one problem: lat[k][f] = wf_k * L(k, f),
+ * pow[k][f] = P(k, f), energy[k][f] = lat * pow (W ms); each K x n_cand,
+ * row-major, with n_cand = |ladder.select(ladder_N)|. */
+int bs_mpc_tables(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfg,
+                  const bs_scheduler_policy* policy, const bs_mpc_problem* problem, int32_t* out_K,
+                  int32_t* out_n_cand, double* lat, double* pow, double* energy);
+
+/* --- decode pick -------------------------------------------------------- */
+
+int bs_decode_pick(bs_ctx_t ctx, bs_models_t models, const bs_decode_config* cfgs, int n_cfgs,
+                   const bs_decode_query* queries, int n, bs_decode_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BISCALE_GPU_H_ */

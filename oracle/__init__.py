@@ -1,0 +1,109 @@
+"""TEST INFRASTRUCTURE ONLY -- CPU checkers for the sm_100a path.
+
+* ``load_oracle()``: the plain-C restatement (``oracle/biscale_oracle.c``).
+* ``load_ref()``: the unmodified reference headers compiled by
+  ``oracle/Makefile`` into ``oracle/_ref/libpdsim_ref.so``.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+from paper_2602_18755_b200 import _abi as A
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libpdsim_ref.so"
+REFERENCE_ROOT = Path("/root/reference")
+
+_P = C.POINTER
+_dp = A.dp
+
+_COMMON = {
+    "interpolate": None,
+    "predict_batch": (C.c_int, [_P(A.bs_model_set), C.c_int, _P(A.bs_features), _P(C.c_int32), _dp, C.c_int, _dp,
+                                _P(C.c_int32)]),
+    "synth_model_set": (C.c_int, [C.c_int, _dp, C.c_int, _P(C.c_int32), C.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
+                                  _dp]),
+    "project": (C.c_int, [_P(A.bs_mpc_config), _P(A.bs_scheduler_policy), _P(A.bs_snapshot),
+                          _P(A.bs_projected_batch), _P(C.c_int32)]),
+    "greedy": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy), _P(A.bs_snapshot),
+                         _P(A.bs_mpc_result)]),
+    "exhaustive": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy),
+                             _P(A.bs_snapshot), _P(A.bs_mpc_result)]),
+    "eval_codes": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy),
+                             _P(A.bs_snapshot), _P(C.c_uint64), C.c_int, _P(C.c_int32), _dp]),
+    "decode_pick": (C.c_int, [_P(A.bs_model_set), _P(A.bs_decode_config), _P(A.bs_decode_query), C.c_int,
+                              _P(A.bs_decode_result)]),
+}
+
+
+def build(quiet: bool = True) -> None:
+    """Compile liboracle.so, and _ref/libpdsim_ref.so when /root/reference exists."""
+    targets = ["oracle"]
+    if (REFERENCE_ROOT / "proj" / "include").is_dir():
+        targets.append("ref")
+    res = subprocess.run(["make", "-C", str(HERE), *targets], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + res.stdout + res.stderr)
+
+
+def _bind(path: Path, prefix: str, extra: dict) -> C.CDLL:
+    if not path.exists():
+        raise FileNotFoundError(f"{path} not built (run oracle.build() where /root/reference is present)")
+    lib = C.CDLL(str(path))
+    for name, proto in {**_COMMON, **extra}.items():
+        if proto is None:
+            continue
+        fn = getattr(lib, prefix + name, None)
+        if fn is None:
+            continue
+        fn.restype, fn.argtypes = proto
+    lib.last_error = getattr(lib, prefix + "last_error")
+    lib.last_error.restype = C.c_char_p
+    return lib
+
+
+_oracle = None
+_ref = None
+
+
+def load_oracle() -> C.CDLL:
+    global _oracle
+    if _oracle is None:
+        _oracle = _bind(ORACLE_SO, "orc_", {
+            "interpolate_one": None,
+        })
+        _oracle.orc_interpolate.restype = C.c_int
+        _oracle.orc_interpolate.argtypes = [_P(A.bs_grid), _dp, _dp, _P(C.c_uint32)]
+        _oracle.orc_ladder_select.restype = C.c_int
+        _oracle.orc_ladder_select.argtypes = [_dp, C.c_int, C.c_int, _dp]
+    return _oracle
+
+
+def load_ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        _ref = _bind(REF_SO, "ref_", {
+            "predict": (C.c_int, [_P(A.bs_model_set), C.c_int, _P(A.bs_features), _P(C.c_int32), _dp, C.c_int, _dp,
+                                  _P(C.c_int32)]),
+            "greedy_batch": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy),
+                                       _P(A.bs_mpc_problem), C.c_int, _P(A.bs_mpc_result), C.c_int]),
+            "exhaustive_batch": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy),
+                                           _P(A.bs_mpc_problem), C.c_int, _P(A.bs_mpc_result), C.c_int]),
+            "tables": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy),
+                                 _P(A.bs_snapshot), _P(C.c_int32), _P(C.c_int32), _dp, _dp, _dp]),
+        })
+        _ref.ref_interpolate.restype = C.c_int
+        _ref.ref_interpolate.argtypes = [_P(A.bs_grid), _dp, C.c_int, _dp, _P(C.c_uint32)]
+        # the reference's predict has the batch signature under the name ref_predict
+        _ref.ref_predict_batch = _ref.ref_predict
+    return _ref
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()

@@ -1,0 +1,486 @@
+// ref_driver.cpp — TEST INFRASTRUCTURE ONLY (oracle).  Wraps the UNMODIFIED
+// reference headers (/root/reference/proj/include/pdsim, compiled where they
+// lie; nothing is copied) behind extern "C" entry points that take the same
+// POD structs as include/biscale_gpu.h, so the parity tests can run the real
+// reference on exactly the inputs the GPU path sees.  Built by
+// oracle/Makefile into oracle/_ref/libpdsim_ref.so.  Never linked into, or
+// called by, the product path.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "pdsim/dvfs.hpp"
+#include "pdsim/placement.hpp"
+#include "pdsim/runner.hpp"
+#include "pdsim/simulator.hpp"
+#include "pdsim/workload.hpp"
+
+#include "biscale_gpu.h"
+#include "ref_driver.h"
+
+using namespace pdsim;
+
+namespace {
+
+const char* role_name(int role) {
+  switch (role) {
+    case BS_AXIS_SUM_LEN: return kAxisSumLen;
+    case BS_AXIS_N_REQUESTS: return kAxisNumRequests;
+    case BS_AXIS_TP: return kAxisTp;
+    case BS_AXIS_FREQ: return kAxisFreq;
+    default: return "unknown";
+  }
+}
+
+NdGrid to_grid(const bs_grid& g) {
+  NdGrid out;
+  std::size_t total = 1;
+  for (int d = 0; d < g.rank; ++d) {
+    Axis a;
+    a.name = role_name(g.role[d]);
+    a.knots.assign(g.knots[d], g.knots[d] + g.n_knots[d]);
+    total *= static_cast<std::size_t>(g.n_knots[d]);
+    out.axes.push_back(std::move(a));
+  }
+  out.values.assign(g.values, g.values + total);
+  return out;
+}
+
+ModelSet to_models(const bs_model_set& m) {
+  ModelSet s;
+  s.latency_prefill.phase = Phase::prefill;
+  s.latency_prefill.grid = to_grid(m.latency_prefill);
+  s.latency_decode.phase = Phase::decode;
+  s.latency_decode.grid = to_grid(m.latency_decode);
+  s.power_prefill.phase = Phase::prefill;
+  s.power_prefill.grid = to_grid(m.power_prefill);
+  s.power_decode.phase = Phase::decode;
+  s.power_decode.grid = to_grid(m.power_decode);
+  for (int i = 0; i < m.n_idle; ++i) {
+    IdlePowerModel::TpEntry e;
+    e.tp = m.idle[i].tp;
+    e.freqs_mhz.assign(m.idle[i].freqs_mhz, m.idle[i].freqs_mhz + m.idle[i].n);
+    e.idle_w.assign(m.idle[i].idle_w, m.idle[i].idle_w + m.idle[i].n);
+    s.idle.entries.push_back(std::move(e));
+  }
+  return s;
+}
+
+MpcConfig to_mpc(const bs_mpc_config& c) {
+  MpcConfig m;
+  m.horizon_K = c.horizon_K;
+  m.ladder_N = c.ladder_N;
+  m.ladder.freqs_mhz.assign(c.ladder_mhz, c.ladder_mhz + c.n_ladder);
+  m.slo.ttft_ms = c.ttft_ms;
+  m.slo.tpot_ms = c.tpot_ms;
+  m.slo.percentile = c.percentile;
+  m.switch_latency_ms = c.switch_latency_ms;
+  m.margin = c.margin;
+  return m;
+}
+
+SchedulerPolicy to_policy(const bs_scheduler_policy& p) {
+  SchedulerPolicy s;
+  s.max_batch_tokens = p.max_batch_tokens;
+  s.max_batch_requests = p.max_batch_requests;
+  s.kv_capacity_tokens = p.kv_capacity_tokens;
+  s.chunking = p.chunking != 0;
+  return s;
+}
+
+QueueSnapshot to_snapshot(const bs_snapshot& s) {
+  QueueSnapshot q;
+  q.now_ms = s.now_ms;
+  q.phase = Phase::prefill;
+  q.tp = s.tp;
+  q.current_freq_mhz = s.current_freq_mhz;
+  q.target_freq_mhz = s.target_freq_mhz;
+  for (int i = 0; i < s.n_waiting; ++i) {
+    q.waiting.push_back(SnapshotWaiting{s.waiting[i].id, s.waiting[i].arrival_ms, s.waiting[i].total_len,
+                                        s.waiting[i].remaining_len});
+  }
+  if (s.running_active) {
+    q.running.active = true;
+    for (int i = 0; i < s.n_running; ++i) {
+      q.running.ids.push_back(i);
+      q.running.chunk_lens.push_back(0);
+      q.running.completes.push_back(s.running_completes[i] != 0);
+      q.running.arrivals_ms.push_back(s.running_arrivals_ms[i]);
+    }
+    q.running.work_remaining = s.running_work_remaining;
+    q.running.features.n_requests = s.running_features.n_requests;
+    q.running.features.sum_len = s.running_features.sum_len;
+  }
+  return q;
+}
+
+int status_of(const std::exception& e) {
+  if (dynamic_cast<const ParameterError*>(&e)) return BS_PARAMETER_ERROR;
+  if (dynamic_cast<const ModelError*>(&e)) return BS_MODEL_ERROR;
+  if (dynamic_cast<const SimulationError*>(&e)) return BS_SIMULATION_ERROR;
+  if (dynamic_cast<const ConfigError*>(&e)) return BS_CONFIG_ERROR;
+  if (dynamic_cast<const AccountingError*>(&e)) return BS_ACCOUNTING_ERROR;
+  if (dynamic_cast<const IoError*>(&e)) return BS_IO_ERROR;
+  if (dynamic_cast<const InfeasibleError*>(&e)) return BS_INFEASIBLE_ERROR;
+  return 99;
+}
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BS_OK;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+void fill_result(const GreedyResult& g, const std::vector<double>& cand, const QueueSnapshot& q, double max_mhz,
+                 bs_mpc_result* r) {
+  std::memset(r, 0, sizeof(*r));
+  r->K = static_cast<int32_t>(g.assignment.freqs.size());
+  r->feasible = g.feasible ? 1 : 0;
+  r->eval_count = g.eval_count;
+  r->objective_w = g.objective_w;
+  for (std::size_t k = 0; k < g.assignment.freqs.size() && k < BS_MAX_K; ++k) {
+    r->freqs_mhz[k] = g.assignment.freqs[k];
+    auto it = std::find(cand.begin(), cand.end(), g.assignment.freqs[k]);
+    r->freq_index[k] = it == cand.end() ? -1 : static_cast<int32_t>(it - cand.begin());
+  }
+  r->n_levels = static_cast<int32_t>(g.levels.size());
+  for (std::size_t l = 0; l < g.levels.size() && l < BS_MAX_LEVELS; ++l) {
+    r->levels[l].level = g.levels[l].level;
+    r->levels[l].k_prime = g.levels[l].k_prime;
+    r->levels[l].replaced_mhz = g.levels[l].replaced_mhz;
+    r->levels[l].mutations = g.levels[l].mutations;
+    r->levels[l].feasible_mutations = g.levels[l].feasible_mutations;
+    r->levels[l].accepted = g.levels[l].accepted ? 1 : 0;
+  }
+  // PrefillMpcController::run (dvfs.hpp:328-329)
+  r->decision_freq_mhz = g.assignment.freqs.empty() ? (q.target_freq_mhz > 0 ? q.target_freq_mhz : max_mhz)
+                                                    : g.assignment.freqs.front();
+}
+
+// tw_power exactly as the reference test oracle computes it
+// (tests/test_dvfs.cpp:58-67, tests/acceptance_main.cpp:150-160).
+double tw_power(const FrequencyAssignment& a, const std::vector<ProjectedBatch>& proj, const QueueSnapshot& q,
+                const ModelSet& m) {
+  double num = 0.0, den = 0.0;
+  for (std::size_t k = 0; k < a.freqs.size(); ++k) {
+    double lat = proj[k].work_fraction * predict_latency(m.latency_prefill, proj[k].features, q.tp, a.freqs[k]);
+    num += lat * predict_power(m.power_prefill, proj[k].features, q.tp, a.freqs[k]);
+    den += lat;
+  }
+  return den > 0.0 ? num / den : 0.0;
+}
+
+// Exhaustive MPC in the shape of the reference oracle loop
+// (tests/test_dvfs.cpp:74-94): odometer with digit 0 fastest, meets_slo then
+// tw_power per assignment.  The pinned tie-break (objective, then
+// lexicographic frequency vector -- dvfs.hpp:243's rule) replaces the
+// test's objective-only first-min; feasible assignments are counted.
+void exhaustive_one(const ModelSet& m, const MpcConfig& cfg, const SchedulerPolicy& policy, const QueueSnapshot& q,
+                    bs_mpc_result* r) {
+  cfg.validate();
+  std::vector<double> cand = cfg.candidates().freqs_mhz;
+  std::vector<ProjectedBatch> proj = project_batches(q, policy, cfg.horizon_K);
+  std::memset(r, 0, sizeof(*r));
+  const std::size_t K = proj.size();
+  r->K = static_cast<int32_t>(K);
+  double max_mhz = cand.back();
+  if (K == 0) {
+    r->feasible = 1;
+    r->decision_freq_mhz = q.target_freq_mhz > 0 ? q.target_freq_mhz : max_mhz;
+    return;
+  }
+  std::vector<std::size_t> idx(K, 0);
+  bool found = false;
+  double best_p = 0.0;
+  std::vector<double> best_f;
+  std::vector<std::size_t> best_idx;
+  std::uint64_t feasible_count = 0, total = 0;
+  FrequencyAssignment a;
+  a.freqs.resize(K);
+  while (true) {
+    for (std::size_t k = 0; k < K; ++k) a.freqs[k] = cand[idx[k]];
+    ++total;
+    if (meets_slo(a, proj, q, m, cfg)) {
+      ++feasible_count;
+      double p = tw_power(a, proj, q, m);
+      if (!found || p < best_p || (p == best_p && detail::lex_less(a.freqs, best_f))) {
+        found = true;
+        best_p = p;
+        best_f = a.freqs;
+        best_idx = idx;
+      }
+    }
+    std::size_t d = 0;
+    while (d < idx.size() && ++idx[d] == cand.size()) idx[d++] = 0;
+    if (d == idx.size()) break;
+  }
+  r->trajectories = total;
+  r->feasible_count = feasible_count;
+  r->eval_count = static_cast<int64_t>(total);
+  if (!found) {
+    best_f.assign(K, max_mhz);
+    best_idx.assign(K, cand.size() - 1);
+    a.freqs = best_f;
+    best_p = tw_power(a, proj, q, m);
+  }
+  r->feasible = found ? 1 : 0;
+  r->objective_w = best_p;
+  std::uint64_t code = 0;
+  for (std::size_t k = 0; k < K; ++k) {
+    r->freqs_mhz[k] = best_f[k];
+    r->freq_index[k] = static_cast<int32_t>(best_idx[k]);
+    code = code * cand.size() + best_idx[k];
+  }
+  r->best_code = code;
+  r->decision_freq_mhz = best_f.front();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_interpolate(const bs_grid* grid, const double* coords, int n, double* out, uint32_t* clamp_events) {
+  return guarded([&] {
+    NdGrid g = to_grid(*grid);
+    g.validate_structure();
+    for (int i = 0; i < n; ++i) {
+      std::vector<double> c(coords + static_cast<std::size_t>(i) * grid->rank,
+                            coords + static_cast<std::size_t>(i + 1) * grid->rank);
+      std::uint64_t before = g.clamp_events.value.load();
+      out[i] = g.interpolate(c);
+      if (clamp_events) clamp_events[i] = static_cast<uint32_t>(g.clamp_events.value.load() - before);
+    }
+  });
+}
+
+int ref_predict(const bs_model_set* models, int which, const bs_features* feats, const int32_t* tp,
+                const double* freq, int n, double* out, int32_t* status) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    for (int i = 0; i < n; ++i) {
+      BatchFeatures f;
+      f.n_requests = feats[i].n_requests;
+      f.sum_len = feats[i].sum_len;
+      status[i] = guarded([&] {
+        switch (which) {
+          case 0: out[i] = predict_latency(m.latency_prefill, f, tp[i], freq[i]); break;
+          case 1: out[i] = predict_latency(m.latency_decode, f, tp[i], freq[i]); break;
+          case 2: out[i] = predict_power(m.power_prefill, f, tp[i], freq[i]); break;
+          case 3: out[i] = predict_power(m.power_decode, f, tp[i], freq[i]); break;
+          default: out[i] = predict_idle_power(m.idle, tp[i], freq[i]); break;
+        }
+      });
+      if (status[i] != BS_OK) out[i] = 0.0;
+    }
+  });
+}
+
+int ref_synth_model_set(int family, const double* ladder, int n_ladder, const int32_t* tps, int n_tp,
+                        const double* prefill_opt, const double* decode_opt, double* lat_p, double* lat_d,
+                        double* pow_p, double* pow_d, double* idle_w) {
+  return guarded([&] {
+    FrequencyLadder l;
+    l.freqs_mhz.assign(ladder, ladder + n_ladder);
+    std::vector<int> tp_list(tps, tps + n_tp);
+    auto opts = [](const double* o) {
+      SynthOptions s;
+      s.lat_coef = o[0];
+      s.power_a = o[1];
+      s.power_b = o[2];
+      s.mem_knee_mhz = o[3];
+      s.idle_frac = o[4];
+      return s;
+    };
+    ModelSet m = synth_model_set(family == 0 ? SynthFamily::compute_bound : SynthFamily::memory_bound, l, tp_list,
+                                 opts(prefill_opt), opts(decode_opt));
+    std::copy(m.latency_prefill.grid.values.begin(), m.latency_prefill.grid.values.end(), lat_p);
+    std::copy(m.latency_decode.grid.values.begin(), m.latency_decode.grid.values.end(), lat_d);
+    std::copy(m.power_prefill.grid.values.begin(), m.power_prefill.grid.values.end(), pow_p);
+    std::copy(m.power_decode.grid.values.begin(), m.power_decode.grid.values.end(), pow_d);
+    std::size_t o = 0;
+    for (const auto& e : m.idle.entries) {
+      for (double w : e.idle_w) idle_w[o++] = w;
+    }
+  });
+}
+
+int ref_project(const bs_mpc_config* cfg, const bs_scheduler_policy* policy, const bs_snapshot* snap,
+                bs_projected_batch* out, int32_t* out_K) {
+  return guarded([&] {
+    QueueSnapshot q = to_snapshot(*snap);
+    std::vector<ProjectedBatch> proj = project_batches(q, to_policy(*policy), cfg->horizon_K);
+    *out_K = static_cast<int32_t>(proj.size());
+    for (std::size_t k = 0; k < proj.size() && k < BS_MAX_K; ++k) {
+      out[k].features.n_requests = proj[k].features.n_requests;
+      out[k].features.sum_len = proj[k].features.sum_len;
+      out[k].work_fraction = proj[k].work_fraction;
+      out[k].n_completing = static_cast<int32_t>(proj[k].completing_arrivals_ms.size());
+      double mn = std::numeric_limits<double>::infinity();
+      for (double a : proj[k].completing_arrivals_ms) mn = std::min(mn, a);
+      out[k].min_completing_arrival_ms = mn;
+    }
+  });
+}
+
+int ref_greedy(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+               const bs_snapshot* snap, bs_mpc_result* out) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    MpcConfig c = to_mpc(*cfg);
+    QueueSnapshot q = to_snapshot(*snap);
+    GreedyResult g = greedy_freq_select(q, c, m, to_policy(*policy));
+    std::vector<double> cand = c.candidates().freqs_mhz;
+    fill_result(g, cand, q, cand.back(), out);
+  });
+}
+
+// Many greedy decisions spread over host threads (each reference call stays
+// single-threaded, as the simulator uses it).  Returns the first failure.
+int ref_greedy_batch(const bs_model_set* models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
+                     const bs_mpc_problem* problems, int n, bs_mpc_result* out, int n_threads) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (;;) {
+        int i = next.fetch_add(1);
+        if (i >= n) return;
+        const bs_mpc_problem& p = problems[i];
+        out[i].status = guarded([&] {
+          MpcConfig c = to_mpc(cfgs[p.cfg_index]);
+          QueueSnapshot q = to_snapshot(p.snap);
+          GreedyResult g = greedy_freq_select(q, c, m, to_policy(policies[p.cfg_index]));
+          std::vector<double> cand = c.candidates().freqs_mhz;
+          fill_result(g, cand, q, cand.back(), &out[i]);
+        });
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, n_threads); ++t) pool.emplace_back(work);
+    for (auto& t : pool) t.join();
+  });
+}
+
+int ref_exhaustive(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+                   const bs_snapshot* snap, bs_mpc_result* out) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    exhaustive_one(m, to_mpc(*cfg), to_policy(*policy), to_snapshot(*snap), out);
+  });
+}
+
+int ref_exhaustive_batch(const bs_model_set* models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
+                         const bs_mpc_problem* problems, int n, bs_mpc_result* out, int n_threads) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (;;) {
+        int i = next.fetch_add(1);
+        if (i >= n) return;
+        const bs_mpc_problem& p = problems[i];
+        out[i].status = guarded([&] {
+          exhaustive_one(m, to_mpc(cfgs[p.cfg_index]), to_policy(policies[p.cfg_index]), to_snapshot(p.snap),
+                         &out[i]);
+        });
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, n_threads); ++t) pool.emplace_back(work);
+    for (auto& t : pool) t.join();
+  });
+}
+
+int ref_eval_codes(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+                   const bs_snapshot* snap, const uint64_t* codes, int n, int32_t* out_feasible,
+                   double* out_objective) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    MpcConfig c = to_mpc(*cfg);
+    QueueSnapshot q = to_snapshot(*snap);
+    std::vector<double> cand = c.candidates().freqs_mhz;
+    std::vector<ProjectedBatch> proj = project_batches(q, to_policy(*policy), c.horizon_K);
+    const std::size_t K = proj.size();
+    FrequencyAssignment a;
+    a.freqs.resize(K);
+    for (int i = 0; i < n; ++i) {
+      std::uint64_t code = codes[i];
+      for (std::size_t k = K; k-- > 0;) {
+        a.freqs[k] = cand[code % cand.size()];
+        code /= cand.size();
+      }
+      out_feasible[i] = meets_slo(a, proj, q, m, c) ? 1 : 0;
+      detail::MpcEvaluator ev{proj, q, m, c, {}};
+      out_objective[i] = ev.time_weighted_power(a);
+    }
+  });
+}
+
+int ref_tables(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+               const bs_snapshot* snap, int32_t* out_K, int32_t* out_n_cand, double* lat, double* pow,
+               double* energy) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    MpcConfig c = to_mpc(*cfg);
+    QueueSnapshot q = to_snapshot(*snap);
+    std::vector<double> cand = c.candidates().freqs_mhz;
+    std::vector<ProjectedBatch> proj = project_batches(q, to_policy(*policy), c.horizon_K);
+    detail::MpcEvaluator ev{proj, q, m, c, {}};
+    *out_K = static_cast<int32_t>(proj.size());
+    *out_n_cand = static_cast<int32_t>(cand.size());
+    for (std::size_t k = 0; k < proj.size(); ++k) {
+      for (std::size_t f = 0; f < cand.size(); ++f) {
+        auto [l, p] = ev.eval(k, cand[f]);
+        lat[k * cand.size() + f] = l;
+        pow[k * cand.size() + f] = p;
+        energy[k * cand.size() + f] = l * p;
+      }
+    }
+  });
+}
+
+int ref_decode_pick(const bs_model_set* models, const bs_decode_config* cfgs, const bs_decode_query* queries, int n,
+                    bs_decode_result* out) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    for (int i = 0; i < n; ++i) {
+      const bs_decode_query& qq = queries[i];
+      const bs_decode_config& c = cfgs[qq.cfg_index];
+      DecodePolicyConfig dc;
+      dc.tbt_slo_ms = c.tbt_slo_ms;
+      dc.kv_threshold = c.kv_threshold;
+      dc.margin = c.margin;
+      dc.ladder.freqs_mhz.assign(c.ladder_mhz, c.ladder_mhz + c.n_ladder);
+      BatchFeatures f;
+      f.n_requests = qq.batch.n_requests;
+      f.sum_len = qq.batch.sum_len;
+      KVCacheState kv;
+      kv.capacity_tokens = qq.kv_capacity_tokens;
+      kv.used_tokens = qq.kv_used_tokens;
+      std::memset(&out[i], 0, sizeof(out[i]));
+      out[i].status = guarded([&] {
+        DecodeDecision d = select_decode_freq_ex(f, kv, dc, m, qq.tp);
+        out[i].freq_mhz = d.freq_mhz;
+        out[i].eval_count = d.eval_count;
+        out[i].kv_override = d.kv_override ? 1 : 0;
+      });
+    }
+  });
+}
+
+}  // extern "C"

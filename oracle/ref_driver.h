@@ -1,0 +1,39 @@
+/* ref_driver.h -- TEST INFRASTRUCTURE ONLY.  extern "C" wrappers over the
+ * unmodified reference (see ref_driver.cpp).  Built into
+ * oracle/_ref/libpdsim_ref.so by oracle/Makefile; used by tests/ and by
+ * bench.py's cpu_baseline / --impl reference legs only. */
+#ifndef PDSIM_REF_DRIVER_H_
+#define PDSIM_REF_DRIVER_H_
+#include "biscale_gpu.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+const char* ref_last_error(void);
+int ref_interpolate(const bs_grid* grid, const double* coords, int n, double* out, uint32_t* clamp_events);
+int ref_predict(const bs_model_set* models, int which, const bs_features* feats, const int32_t* tp,
+                const double* freq, int n, double* out, int32_t* status);
+int ref_synth_model_set(int family, const double* ladder, int n_ladder, const int32_t* tps, int n_tp,
+                        const double* prefill_opt, const double* decode_opt, double* lat_p, double* lat_d,
+                        double* pow_p, double* pow_d, double* idle_w);
+int ref_project(const bs_mpc_config* cfg, const bs_scheduler_policy* policy, const bs_snapshot* snap,
+                bs_projected_batch* out, int32_t* out_K);
+int ref_greedy(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+               const bs_snapshot* snap, bs_mpc_result* out);
+int ref_greedy_batch(const bs_model_set* models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
+                     const bs_mpc_problem* problems, int n, bs_mpc_result* out, int n_threads);
+int ref_exhaustive(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+                   const bs_snapshot* snap, bs_mpc_result* out);
+int ref_exhaustive_batch(const bs_model_set* models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
+                         const bs_mpc_problem* problems, int n, bs_mpc_result* out, int n_threads);
+int ref_eval_codes(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+                   const bs_snapshot* snap, const uint64_t* codes, int n, int32_t* out_feasible,
+                   double* out_objective);
+int ref_tables(const bs_model_set* models, const bs_mpc_config* cfg, const bs_scheduler_policy* policy,
+               const bs_snapshot* snap, int32_t* out_K, int32_t* out_n_cand, double* lat, double* pow,
+               double* energy);
+int ref_decode_pick(const bs_model_set* models, const bs_decode_config* cfgs, const bs_decode_query* queries, int n,
+                    bs_decode_result* out);
+#ifdef __cplusplus
+}
+#endif
+#endif

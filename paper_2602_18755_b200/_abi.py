@@ -1,0 +1,217 @@
+"""ctypes mirror of ``include/biscale_gpu.h`` (the C ABI of the sm_100a path).
+
+The layouts below must match the header field for field; ``tests`` check the
+struct sizes against the C compiler's (``test_abi_layout``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+BS_MAX_RANK = 4
+BS_MAX_K = 16
+BS_MAX_CAND = 32
+BS_MAX_LEVELS = 32
+BS_MAX_LADDER = 64
+
+BS_OK = 0
+BS_PARAMETER_ERROR = 1
+BS_MODEL_ERROR = 2
+BS_SIMULATION_ERROR = 3
+BS_CONFIG_ERROR = 4
+BS_ACCOUNTING_ERROR = 5
+BS_IO_ERROR = 6
+BS_INFEASIBLE_ERROR = 7
+BS_CUDA_ERROR = 100
+
+AXIS_ROLE = {"sum_len": 0, "n_requests": 1, "tp": 2, "freq_mhz": 3}
+BS_AXIS_UNKNOWN = -1
+
+dp = C.POINTER(C.c_double)
+
+
+class bs_grid(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("role", C.c_int32 * BS_MAX_RANK),
+        ("n_knots", C.c_int32 * BS_MAX_RANK),
+        ("knots", dp * BS_MAX_RANK),
+        ("values", dp),
+    ]
+
+
+class bs_idle_entry(C.Structure):
+    _fields_ = [("tp", C.c_int32), ("n", C.c_int32), ("freqs_mhz", dp), ("idle_w", dp)]
+
+
+class bs_model_set(C.Structure):
+    _fields_ = [
+        ("latency_prefill", bs_grid),
+        ("latency_decode", bs_grid),
+        ("power_prefill", bs_grid),
+        ("power_decode", bs_grid),
+        ("n_idle", C.c_int32),
+        ("idle", C.POINTER(bs_idle_entry)),
+    ]
+
+
+class bs_features(C.Structure):
+    _fields_ = [("n_requests", C.c_int64), ("sum_len", C.c_int64)]
+
+
+class bs_scheduler_policy(C.Structure):
+    _fields_ = [
+        ("max_batch_tokens", C.c_int64),
+        ("max_batch_requests", C.c_int64),
+        ("kv_capacity_tokens", C.c_int64),
+        ("chunking", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class bs_mpc_config(C.Structure):
+    _fields_ = [
+        ("horizon_K", C.c_int32),
+        ("ladder_N", C.c_int32),
+        ("n_ladder", C.c_int32),
+        ("_pad", C.c_int32),
+        ("ladder_mhz", dp),
+        ("ttft_ms", C.c_double),
+        ("tpot_ms", C.c_double),
+        ("percentile", C.c_double),
+        ("switch_latency_ms", C.c_double),
+        ("margin", C.c_double),
+    ]
+
+
+class bs_waiting(C.Structure):
+    _fields_ = [("id", C.c_int64), ("arrival_ms", C.c_double), ("total_len", C.c_int64), ("remaining_len", C.c_int64)]
+
+
+class bs_snapshot(C.Structure):
+    _fields_ = [
+        ("now_ms", C.c_double),
+        ("current_freq_mhz", C.c_double),
+        ("target_freq_mhz", C.c_double),
+        ("running_work_remaining", C.c_double),
+        ("running_features", bs_features),
+        ("tp", C.c_int32),
+        ("running_active", C.c_int32),
+        ("n_waiting", C.c_int32),
+        ("n_running", C.c_int32),
+        ("waiting", C.POINTER(bs_waiting)),
+        ("running_completes", C.POINTER(C.c_uint8)),
+        ("running_arrivals_ms", dp),
+    ]
+
+
+class bs_mpc_problem(C.Structure):
+    _fields_ = [("snap", bs_snapshot), ("cfg_index", C.c_int32), ("_pad", C.c_int32)]
+
+
+class bs_level_stats(C.Structure):
+    _fields_ = [
+        ("level", C.c_int32),
+        ("k_prime", C.c_int32),
+        ("replaced_mhz", C.c_double),
+        ("mutations", C.c_int64),
+        ("feasible_mutations", C.c_int64),
+        ("accepted", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class bs_mpc_result(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("K", C.c_int32),
+        ("feasible", C.c_int32),
+        ("n_levels", C.c_int32),
+        ("eval_count", C.c_int64),
+        ("objective_w", C.c_double),
+        ("freqs_mhz", C.c_double * BS_MAX_K),
+        ("freq_index", C.c_int32 * BS_MAX_K),
+        ("decision_freq_mhz", C.c_double),
+        ("feasible_count", C.c_uint64),
+        ("trajectories", C.c_uint64),
+        ("best_code", C.c_uint64),
+        ("levels", bs_level_stats * BS_MAX_LEVELS),
+    ]
+
+
+class bs_projected_batch(C.Structure):
+    _fields_ = [
+        ("features", bs_features),
+        ("work_fraction", C.c_double),
+        ("min_completing_arrival_ms", C.c_double),
+        ("n_completing", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class bs_decode_config(C.Structure):
+    _fields_ = [
+        ("tbt_slo_ms", C.c_double),
+        ("kv_threshold", C.c_double),
+        ("margin", C.c_double),
+        ("n_ladder", C.c_int32),
+        ("_pad", C.c_int32),
+        ("ladder_mhz", dp),
+    ]
+
+
+class bs_decode_query(C.Structure):
+    _fields_ = [
+        ("batch", bs_features),
+        ("kv_capacity_tokens", C.c_int64),
+        ("kv_used_tokens", C.c_int64),
+        ("tp", C.c_int32),
+        ("cfg_index", C.c_int32),
+    ]
+
+
+class bs_decode_result(C.Structure):
+    _fields_ = [("freq_mhz", C.c_double), ("eval_count", C.c_int64), ("kv_override", C.c_int32), ("status", C.c_int32)]
+
+
+ctx_t = C.c_void_p
+models_t = C.c_void_p
+
+# (name, restype, argtypes) for every exported entry point of the header.
+PROTOTYPES = [
+    ("bs_abi_version", C.c_int, []),
+    ("bs_ctx_create", C.c_int, [C.c_int, C.POINTER(ctx_t)]),
+    ("bs_ctx_destroy", None, [ctx_t]),
+    ("bs_last_error", C.c_char_p, [ctx_t]),
+    ("bs_ctx_info", C.c_int, [ctx_t, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("bs_ctx_sync", C.c_int, [ctx_t]),
+    ("bs_ctx_kernel_launches", C.c_int64, [ctx_t]),
+    ("bs_ctx_stream", C.c_void_p, [ctx_t]),
+    ("bs_ctx_last_transfer", C.c_int, [ctx_t, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("bs_fp64_peak", C.c_int, [ctx_t, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("bs_models_upload", C.c_int, [ctx_t, C.POINTER(bs_model_set), C.POINTER(models_t)]),
+    ("bs_models_free", None, [ctx_t, models_t]),
+    ("bs_predict", C.c_int, [ctx_t, models_t, C.c_int, C.POINTER(bs_features), C.POINTER(C.c_int32), dp, C.c_int,
+                             dp, C.POINTER(C.c_int32), C.POINTER(C.c_uint32)]),
+    ("bs_grid_interpolate", C.c_int, [ctx_t, C.POINTER(bs_grid), dp, C.c_int, dp, C.POINTER(C.c_uint32)]),
+    ("bs_project_batches", C.c_int, [ctx_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy), C.c_int,
+                                     C.POINTER(bs_mpc_problem), C.c_int, C.POINTER(bs_projected_batch),
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    ("bs_mpc_greedy", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy), C.c_int,
+                                C.POINTER(bs_mpc_problem), C.c_int, C.POINTER(bs_mpc_result)]),
+    ("bs_mpc_exhaustive", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy),
+                                    C.c_int, C.POINTER(bs_mpc_problem), C.c_int, C.POINTER(bs_mpc_result)]),
+    ("bs_mpc_plan_create", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy),
+                                     C.c_int, C.POINTER(bs_mpc_problem), C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("bs_mpc_plan_run", C.c_int, [ctx_t, C.c_void_p, C.c_int]),
+    ("bs_mpc_plan_results", C.c_int, [ctx_t, C.c_void_p, C.POINTER(bs_mpc_result)]),
+    ("bs_mpc_plan_kernel_ms", C.c_int, [ctx_t, C.c_void_p, C.POINTER(C.c_float), C.c_int]),
+    ("bs_mpc_plan_info", C.c_int, [ctx_t, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("bs_mpc_plan_destroy", None, [ctx_t, C.c_void_p]),
+    ("bs_mpc_eval_codes", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy),
+                                    C.POINTER(bs_mpc_problem), C.POINTER(C.c_uint64), C.c_int,
+                                    C.POINTER(C.c_int32), dp]),
+    ("bs_mpc_tables", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy),
+                                C.POINTER(bs_mpc_problem), C.POINTER(C.c_int32), C.POINTER(C.c_int32), dp, dp, dp]),
+    ("bs_decode_pick", C.c_int, [ctx_t, models_t, C.POINTER(bs_decode_config), C.c_int, C.POINTER(bs_decode_query),
+                                 C.c_int, C.POINTER(bs_decode_result)]),
+]

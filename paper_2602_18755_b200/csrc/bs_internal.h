@@ -1,0 +1,116 @@
+// bs_internal.h — host-side runtime shared by the C-ABI translation units:
+// the context (stream, growable device/pinned scratch, last error), the
+// uploaded model set, and error helpers.
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "biscale_gpu.h"
+#include "bs_device.cuh"
+
+struct bs_ctx_s {
+  int device = 0;
+  uint64_t last_h2d = 0;  // bytes moved by the last entry point
+  uint64_t last_d2h = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  static constexpr int kSlots = 16;
+  Buf dev[kSlots];
+  Buf host[kSlots];
+
+  void* dev_buf(int slot, size_t bytes);   // grow-only device scratch
+  void* host_buf(int slot, size_t bytes);  // grow-only pinned host scratch
+  ~bs_ctx_s();
+};
+
+struct bs_models_s {
+  bs::DModels dm{};
+  void* dmem = nullptr;  // one allocation: knots, values, idle arrays
+  size_t bytes = 0;
+  bool grid_positive[4] = {false, false, false, false};  // every value > 0 and finite
+};
+
+namespace bs {
+
+// Scratch slot ids (each kernel family owns a few).
+enum Slot : int {
+  kSlotCfg = 0,
+  kSlotProblems = 1,
+  kSlotWaiting = 2,
+  kSlotRunning = 3,
+  kSlotTables = 4,
+  kSlotOut = 5,
+  kSlotLevels = 6,
+  kSlotBest = 7,
+  kSlotWork = 8,
+  kSlotCounts = 9,
+  kSlotMisc = 10,
+  kSlotMisc2 = 11,
+};
+
+int set_error(bs_ctx_t ctx, int code, const char* fmt, ...);
+
+#define BS_CUDA_TRY(ctx, expr)                                                                     \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return ::bs::set_error((ctx), BS_CUDA_ERROR, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                             __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define BS_LAUNCH_CHECK(ctx)                                                                         \
+  do {                                                                                               \
+    (ctx)->launches += 1;                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                             \
+    if (e_ != cudaSuccess)                                                                           \
+      return ::bs::set_error((ctx), BS_CUDA_ERROR, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                             __FILE__, __LINE__);                                                    \
+  } while (0)
+
+// FrequencyLadder::validate + select (perfmodel.hpp:56-91) on the host;
+// returns the candidate count or a negative status.
+int ladder_select(bs_ctx_t ctx, const double* ladder, int n_ladder, int n, double* out, int cap);
+
+// MpcConfig::validate (dvfs.hpp:25-31) and SchedulerPolicy::validate
+// (scheduler.hpp:17-21), then pack into the device layout.
+int pack_mpc_cfg(bs_ctx_t ctx, const bs_mpc_config& c, const bs_scheduler_policy& p, DMpcCfg* out);
+
+// Packs problems + configs into one pinned staging buffer and copies it to
+// HBM with a single cudaMemcpyAsync.  Device pointers returned in `dev`.
+struct PackedProblems {
+  DMpcCfg* cfgs = nullptr;
+  DProblem* problems = nullptr;
+  DWaiting* waiting = nullptr;
+  DRunning* running = nullptr;
+  char* base = nullptr;  // device blob holding all four arrays
+  size_t off_cfg = 0, off_prob = 0, off_wait = 0, off_run = 0;
+  int n = 0;
+  int n_cfgs = 0;
+  size_t h2d_bytes = 0;
+  int max_horizon = 0;
+  int max_nc = 0;
+  void rebase(char* b) {
+    base = b;
+    cfgs = reinterpret_cast<DMpcCfg*>(b + off_cfg);
+    problems = reinterpret_cast<DProblem*>(b + off_prob);
+    waiting = reinterpret_cast<DWaiting*>(b + off_wait);
+    running = reinterpret_cast<DRunning*>(b + off_run);
+  }
+};
+int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
+                  const bs_mpc_problem* problems, int n, PackedProblems* out);
+
+}  // namespace bs

@@ -1,0 +1,1014 @@
+"""Host-side mirror of the reference's ``pdsim`` interface for the decision path.
+
+Names, argument meanings and error behaviour follow
+``/root/reference/proj/include/pdsim/*.hpp`` so code (and tests) written
+against the reference read the same here.  The value types (ladders, grids,
+snapshots, configs) are plain Python; every computation on the decision path
+(prediction, projection, greedy/exhaustive MPC, decode pick) runs on the
+B200 through the C ABI of ``libbiscale_gpu.so`` -- there is no CPU fallback.
+
+Pure-Python pieces, which are input construction rather than decisions:
+``FrequencyLadder.select`` (host-side, as in the reference's controller
+constructor), ``BatchFeatures.from_lengths``, and ``synth_model`` /
+``synth_model_set`` (grid generation; bit-identical to the reference, see
+``tests/test_pdsim_host.py``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+from . import _abi
+from ._lib import lib
+
+# ---------------------------------------------------------------------------
+# errors.hpp:10-56
+# ---------------------------------------------------------------------------
+
+
+class PdsimError(Exception):
+    pass
+
+
+class ParameterError(PdsimError, ValueError):
+    pass
+
+
+class ModelError(PdsimError, RuntimeError):
+    pass
+
+
+class SimulationError(PdsimError, RuntimeError):
+    pass
+
+
+class ConfigError(PdsimError, RuntimeError):
+    pass
+
+
+class AccountingError(PdsimError, RuntimeError):
+    pass
+
+
+class IoError(PdsimError, RuntimeError):
+    pass
+
+
+class InfeasibleError(PdsimError, RuntimeError):
+    def __init__(self, constraint: str, what: str):
+        super().__init__(what)
+        self.constraint = constraint
+
+    def binding_constraint(self) -> str:
+        return self.constraint
+
+
+class CudaError(PdsimError, RuntimeError):
+    pass
+
+
+_STATUS_EXC = {
+    _abi.BS_PARAMETER_ERROR: ParameterError,
+    _abi.BS_MODEL_ERROR: ModelError,
+    _abi.BS_SIMULATION_ERROR: SimulationError,
+    _abi.BS_CONFIG_ERROR: ConfigError,
+    _abi.BS_ACCOUNTING_ERROR: AccountingError,
+    _abi.BS_IO_ERROR: IoError,
+    _abi.BS_CUDA_ERROR: CudaError,
+}
+
+
+def raise_status(code: int, message: str) -> None:
+    if code == _abi.BS_OK:
+        return
+    if code == _abi.BS_INFEASIBLE_ERROR:
+        constraint, _, what = message.partition("|")
+        raise InfeasibleError(constraint, what)
+    raise _STATUS_EXC.get(code, PdsimError)(message)
+
+
+# ---------------------------------------------------------------------------
+# perfmodel.hpp
+# ---------------------------------------------------------------------------
+
+
+class Phase(enum.IntEnum):
+    prefill = 0
+    decode = 1
+
+
+@dataclass
+class BatchFeatures:
+    """perfmodel.hpp:30-51."""
+
+    n_requests: int = 0
+    sum_len: int = 0
+    mean_len: float = 0.0
+    std_len: float = 0.0
+
+    @staticmethod
+    def from_lengths(lengths: Sequence[int]) -> "BatchFeatures":
+        f = BatchFeatures()
+        f.n_requests = len(lengths)
+        f.sum_len = int(sum(int(x) for x in lengths))
+        if f.n_requests > 0:
+            f.mean_len = float(f.sum_len) / float(f.n_requests)
+            ss = 0.0
+            for x in lengths:
+                d = float(x) - f.mean_len
+                ss += d * d
+            f.std_len = math.sqrt(ss / float(f.n_requests))
+        return f
+
+
+@dataclass
+class FrequencyLadder:
+    """perfmodel.hpp:53-92."""
+
+    freqs_mhz: list = field(default_factory=list)
+
+    def validate(self) -> None:
+        if not self.freqs_mhz:
+            raise ParameterError("frequency ladder: empty")
+        prev = 0.0
+        for f in self.freqs_mhz:
+            if not (f > prev):
+                raise ParameterError("frequency ladder: must be strictly increasing and > 0")
+            prev = f
+
+    def min_mhz(self) -> float:
+        return self.freqs_mhz[0]
+
+    def max_mhz(self) -> float:
+        return self.freqs_mhz[-1]
+
+    def contains(self, f: float) -> bool:
+        return any(g == f for g in self.freqs_mhz)
+
+    def select(self, n: int) -> "FrequencyLadder":
+        self.validate()
+        if n == 0:
+            raise ParameterError("frequency ladder: select(0)")
+        size = len(self.freqs_mhz)
+        if n >= size:
+            return FrequencyLadder(list(self.freqs_mhz))
+        if n == 1:
+            return FrequencyLadder([self.freqs_mhz[-1]])
+        out: list = []
+        for i in range(n):
+            idx = (i * (size - 1)) // (n - 1)
+            if not out or out[-1] != self.freqs_mhz[idx]:
+                out.append(self.freqs_mhz[idx])
+        return FrequencyLadder(out)
+
+
+kAxisSumLen = "sum_len"
+kAxisNumRequests = "n_requests"
+kAxisTp = "tp"
+kAxisFreq = "freq_mhz"
+
+
+@dataclass
+class Axis:
+    name: str
+    knots: list
+
+
+@dataclass
+class NdGrid:
+    """perfmodel.hpp:116-201 (values row-major, last axis fastest)."""
+
+    axes: list = field(default_factory=list)
+    values: list = field(default_factory=list)
+
+    def expected_size(self) -> int:
+        n = 1
+        for a in self.axes:
+            n *= len(a.knots)
+        return n
+
+    def validate_structure(self) -> None:
+        if not self.axes:
+            raise ModelError("grid: no axes")
+        for a in self.axes:
+            if not a.knots:
+                raise ModelError(f"grid: axis '{a.name}' has no knots")
+            for i in range(1, len(a.knots)):
+                if a.knots[i] <= a.knots[i - 1]:
+                    raise ModelError(f"grid: axis '{a.name}' knots not strictly increasing")
+        if len(self.values) != self.expected_size():
+            raise ModelError("grid: value count does not match axes")
+
+    def interpolate(self, coords: Sequence[float], device: "Device | None" = None) -> float:
+        """NdGrid::interpolate on the GPU (bs_grid_interpolate)."""
+        if len(coords) != len(self.axes):
+            raise ModelError("grid: coordinate rank mismatch")
+        return (device or default_device()).interpolate(self, [list(coords)])[0][0]
+
+
+@dataclass
+class LatencyTable:
+    phase: Phase = Phase.prefill
+    grid: NdGrid = field(default_factory=NdGrid)
+    synth: Optional[dict] = None
+
+
+@dataclass
+class PowerTable:
+    phase: Phase = Phase.prefill
+    grid: NdGrid = field(default_factory=NdGrid)
+    synth: Optional[dict] = None
+
+
+@dataclass
+class TpEntry:
+    tp: int = 1
+    freqs_mhz: list = field(default_factory=list)
+    idle_w: list = field(default_factory=list)
+
+
+@dataclass
+class IdlePowerModel:
+    entries: list = field(default_factory=list)
+
+
+@dataclass
+class ModelSet:
+    """perfmodel.hpp:494-503."""
+
+    latency_prefill: LatencyTable = field(default_factory=LatencyTable)
+    latency_decode: LatencyTable = field(default_factory=lambda: LatencyTable(Phase.decode))
+    power_prefill: PowerTable = field(default_factory=PowerTable)
+    power_decode: PowerTable = field(default_factory=lambda: PowerTable(Phase.decode))
+    idle: IdlePowerModel = field(default_factory=IdlePowerModel)
+
+    def latency(self, p: Phase) -> LatencyTable:
+        return self.latency_prefill if p == Phase.prefill else self.latency_decode
+
+    def power(self, p: Phase) -> PowerTable:
+        return self.power_prefill if p == Phase.prefill else self.power_decode
+
+
+class SynthFamily(enum.IntEnum):
+    compute_bound = 0
+    memory_bound = 1
+
+
+@dataclass
+class SynthOptions:
+    """perfmodel.hpp:379-387."""
+
+    lat_coef: float = 40.0
+    power_a: float = 1e-7
+    power_b: float = 10.0
+    mem_knee_mhz: float = 1200.0
+    idle_frac: float = 0.35
+    sum_len_knots: list = field(default_factory=lambda: [16.0, 64.0, 256.0, 1024.0, 4096.0, 16384.0])
+    n_request_knots: list = field(default_factory=lambda: [1.0, 2.0, 4.0, 8.0, 16.0, 32.0, 64.0, 128.0, 256.0])
+
+    def as_array(self) -> list:
+        return [self.lat_coef, self.power_a, self.power_b, self.mem_knee_mhz, self.idle_frac]
+
+
+def _synth_latency_ms(family, opt, sum_len, tp, freq):  # perfmodel.hpp:397-405
+    per_shard = sum_len / tp
+    if family == SynthFamily.compute_bound:
+        return opt.lat_coef * per_shard / freq
+    eff = min(freq, opt.mem_knee_mhz)
+    return opt.lat_coef * per_shard / eff
+
+
+def _synth_power_w(family, opt, tp, freq):  # perfmodel.hpp:407-412
+    if family == SynthFamily.compute_bound:
+        per_gpu = opt.power_a * freq * freq * freq + opt.power_b
+    else:
+        per_gpu = opt.power_a * freq + opt.power_b
+    return per_gpu * tp
+
+
+def synth_model(family: SynthFamily, phase: Phase, ladder: FrequencyLadder, tp_list: Sequence[int],
+                opt: SynthOptions | None = None) -> tuple:
+    """perfmodel.hpp:418-491; returns (latency, power, idle)."""
+    opt = opt or SynthOptions()
+    ladder.validate()
+    if not tp_list:
+        raise ParameterError("synth_model: tp_list empty")
+    for tp in tp_list:
+        if tp < 1:
+            raise ParameterError("synth_model: tp must be >= 1")
+    tpk = sorted(set(float(t) for t in tp_list))
+    meta = {"family": "compute-bound" if family == SynthFamily.compute_bound else "memory-bound",
+            "lat_coef": opt.lat_coef, "power_a": opt.power_a, "power_b": opt.power_b,
+            "mem_knee_mhz": opt.mem_knee_mhz if family == SynthFamily.memory_bound else 0.0,
+            "idle_frac": opt.idle_frac}
+    lat = LatencyTable(phase, NdGrid([Axis(kAxisSumLen, list(opt.sum_len_knots)),
+                                      Axis(kAxisNumRequests, list(opt.n_request_knots)),
+                                      Axis(kAxisTp, list(tpk)), Axis(kAxisFreq, list(ladder.freqs_mhz))], []), meta)
+    for s in opt.sum_len_knots:
+        for _ in opt.n_request_knots:
+            for tp in tpk:
+                for f in ladder.freqs_mhz:
+                    lat.grid.values.append(_synth_latency_ms(family, opt, s, tp, f))
+    if phase == Phase.prefill:
+        pw = PowerTable(phase, NdGrid([Axis(kAxisSumLen, list(opt.sum_len_knots)), Axis(kAxisTp, list(tpk)),
+                                       Axis(kAxisFreq, list(ladder.freqs_mhz))], []), meta)
+        for _ in opt.sum_len_knots:
+            for tp in tpk:
+                for f in ladder.freqs_mhz:
+                    pw.grid.values.append(_synth_power_w(family, opt, tp, f))
+    else:
+        pw = PowerTable(phase, NdGrid([Axis(kAxisSumLen, list(opt.sum_len_knots)),
+                                       Axis(kAxisNumRequests, list(opt.n_request_knots)), Axis(kAxisTp, list(tpk)),
+                                       Axis(kAxisFreq, list(ladder.freqs_mhz))], []), meta)
+        for _ in opt.sum_len_knots:
+            for _ in opt.n_request_knots:
+                for tp in tpk:
+                    for f in ladder.freqs_mhz:
+                        pw.grid.values.append(_synth_power_w(family, opt, tp, f))
+    idle = IdlePowerModel([TpEntry(int(tp), list(ladder.freqs_mhz),
+                                   [opt.idle_frac * _synth_power_w(family, opt, tp, f) for f in ladder.freqs_mhz])
+                           for tp in tpk])
+    lat.grid.validate_structure()
+    pw.grid.validate_structure()
+    return lat, pw, idle
+
+
+def synth_model_set(family: SynthFamily, ladder: FrequencyLadder, tp_list: Sequence[int],
+                    prefill_opt: SynthOptions | None = None, decode_opt: SynthOptions | None = None) -> ModelSet:
+    """perfmodel.hpp:505-516."""
+    pl, pp, pi = synth_model(family, Phase.prefill, ladder, tp_list, prefill_opt)
+    dl, dpw, _ = synth_model(family, Phase.decode, ladder, tp_list, decode_opt)
+    return ModelSet(pl, dl, pp, dpw, pi)
+
+
+# ---------------------------------------------------------------------------
+# slo.hpp, scheduler.hpp, controller.hpp, dvfs.hpp value types
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SLOSpec:
+    ttft_ms: float = 600.0
+    tpot_ms: float = 100.0
+    percentile: float = 0.99
+
+    def validate(self) -> None:
+        if self.ttft_ms <= 0.0 or self.tpot_ms <= 0.0:
+            raise ParameterError("slo: bounds must be > 0")
+        if self.percentile <= 0.0 or self.percentile > 1.0:
+            raise ParameterError("slo: percentile must be in (0,1]")
+
+
+@dataclass
+class SchedulerPolicy:
+    max_batch_tokens: int = 8192
+    max_batch_requests: int = 256
+    chunking: bool = True
+    kv_capacity_tokens: int = 1000000
+
+    def validate(self) -> None:
+        if self.max_batch_tokens < 1:
+            raise ParameterError("scheduler: max_batch_tokens must be >= 1")
+        if self.max_batch_requests < 1:
+            raise ParameterError("scheduler: max_batch_requests must be >= 1")
+        if self.kv_capacity_tokens < 1:
+            raise ParameterError("scheduler: kv_capacity_tokens must be >= 1")
+
+
+@dataclass
+class MpcConfig:
+    horizon_K: int = 8
+    ladder_N: int = 7
+    ladder: FrequencyLadder = field(default_factory=FrequencyLadder)
+    slo: SLOSpec = field(default_factory=SLOSpec)
+    switch_latency_ms: float = 30.0
+    margin: float = 0.05
+
+    def validate(self) -> None:
+        if self.horizon_K < 1:
+            raise ParameterError("mpc: horizon_K must be >= 1")
+        if self.ladder_N < 1:
+            raise ParameterError("mpc: ladder_N must be >= 1")
+        self.ladder.validate()
+        self.slo.validate()
+        if self.margin < 0.0:
+            raise ParameterError("mpc: margin must be >= 0")
+
+    def candidates(self) -> FrequencyLadder:
+        return self.ladder.select(self.ladder_N)
+
+
+@dataclass
+class DecodePolicyConfig:
+    tbt_slo_ms: float = 100.0
+    kv_threshold: float = 0.9
+    ladder: FrequencyLadder = field(default_factory=FrequencyLadder)
+    margin: float = 0.0
+
+    def validate(self) -> None:
+        if self.tbt_slo_ms <= 0.0:
+            raise ParameterError("decode policy: tbt_slo_ms must be > 0")
+        if self.kv_threshold <= 0.0 or self.kv_threshold >= 1.0:
+            raise ParameterError("decode policy: kv_threshold in (0,1)")
+        self.ladder.validate()
+        if self.margin < 0.0:
+            raise ParameterError("decode policy: margin must be >= 0")
+
+
+@dataclass
+class KVCacheState:
+    capacity_tokens: int = 0
+    used_tokens: int = 0
+    threshold: float = 0.9
+
+    def utilization(self) -> float:
+        return float(self.used_tokens) / float(self.capacity_tokens) if self.capacity_tokens > 0 else 0.0
+
+
+@dataclass
+class SnapshotWaiting:
+    id: int = -1
+    arrival_ms: float = 0.0
+    total_len: int = 0
+    remaining_len: int = 0
+
+
+@dataclass
+class SnapshotRunning:
+    active: bool = False
+    ids: list = field(default_factory=list)
+    chunk_lens: list = field(default_factory=list)
+    completes: list = field(default_factory=list)
+    arrivals_ms: list = field(default_factory=list)
+    work_remaining: float = 0.0
+    elapsed_ms: float = 0.0
+    features: BatchFeatures = field(default_factory=BatchFeatures)
+
+
+@dataclass
+class QueueSnapshot:
+    now_ms: float = 0.0
+    phase: Phase = Phase.prefill
+    tp: int = 1
+    current_freq_mhz: float = 0.0
+    target_freq_mhz: float = 0.0
+    waiting: list = field(default_factory=list)
+    running: SnapshotRunning = field(default_factory=SnapshotRunning)
+    decode_batch: BatchFeatures = field(default_factory=BatchFeatures)
+    kv: KVCacheState = field(default_factory=KVCacheState)
+
+
+@dataclass
+class FreqDecision:
+    freq_mhz: float = 0.0
+    feasible: bool = True
+    eval_count: int = 0
+
+
+@dataclass
+class ProjectedBatch:
+    features: BatchFeatures
+    work_fraction: float
+    n_completing: int
+    min_completing_arrival_ms: float
+
+
+@dataclass
+class FrequencyAssignment:
+    freqs: list = field(default_factory=list)
+
+
+@dataclass
+class GreedyLevelStats:
+    level: int = 0
+    replaced_mhz: float = 0.0
+    k_prime: int = 0
+    mutations: int = 0
+    feasible_mutations: int = 0
+    accepted: bool = False
+
+
+@dataclass
+class GreedyResult:
+    assignment: FrequencyAssignment = field(default_factory=FrequencyAssignment)
+    feasible: bool = True
+    eval_count: int = 0
+    objective_w: float = 0.0
+    levels: list = field(default_factory=list)
+    # exhaustive-only extras
+    feasible_count: int = 0
+    trajectories: int = 0
+    best_code: int = 0
+    decision_freq_mhz: float = 0.0
+    freq_index: list = field(default_factory=list)
+
+
+@dataclass
+class DecodeDecision:
+    freq_mhz: float = 0.0
+    eval_count: int = 0
+    kv_override: bool = False
+
+
+# ---------------------------------------------------------------------------
+# marshalling into the C ABI
+# ---------------------------------------------------------------------------
+
+
+def _darr(vals) -> C.Array:
+    return (C.c_double * max(1, len(vals)))(*[float(v) for v in vals])
+
+
+def c_grid(grid: NdGrid, keep: list) -> _abi.bs_grid:
+    g = _abi.bs_grid()
+    if len(grid.axes) > _abi.BS_MAX_RANK:
+        raise ParameterError(f"grid: rank {len(grid.axes)} exceeds {_abi.BS_MAX_RANK}")
+    g.rank = len(grid.axes)
+    for d, a in enumerate(grid.axes):
+        g.role[d] = _abi.AXIS_ROLE.get(a.name, _abi.BS_AXIS_UNKNOWN)
+        g.n_knots[d] = len(a.knots)
+        arr = _darr(a.knots)
+        keep.append(arr)
+        g.knots[d] = C.cast(arr, _abi.dp)
+    vals = _darr(grid.values)
+    keep.append(vals)
+    g.values = C.cast(vals, _abi.dp)
+    return g
+
+
+def c_model_set(m: ModelSet, keep: list) -> _abi.bs_model_set:
+    for t in (m.latency_prefill, m.latency_decode, m.power_prefill, m.power_decode):
+        t.grid.validate_structure()
+    s = _abi.bs_model_set()
+    s.latency_prefill = c_grid(m.latency_prefill.grid, keep)
+    s.latency_decode = c_grid(m.latency_decode.grid, keep)
+    s.power_prefill = c_grid(m.power_prefill.grid, keep)
+    s.power_decode = c_grid(m.power_decode.grid, keep)
+    n = len(m.idle.entries)
+    ents = (_abi.bs_idle_entry * max(1, n))()
+    for i, e in enumerate(m.idle.entries):
+        fa, wa = _darr(e.freqs_mhz), _darr(e.idle_w)
+        keep += [fa, wa]
+        ents[i].tp = e.tp
+        ents[i].n = len(e.freqs_mhz)
+        ents[i].freqs_mhz = C.cast(fa, _abi.dp)
+        ents[i].idle_w = C.cast(wa, _abi.dp)
+    keep.append(ents)
+    s.n_idle = n
+    s.idle = C.cast(ents, C.POINTER(_abi.bs_idle_entry))
+    return s
+
+
+def c_policy(p: SchedulerPolicy) -> _abi.bs_scheduler_policy:
+    c = _abi.bs_scheduler_policy()
+    c.max_batch_tokens = p.max_batch_tokens
+    c.max_batch_requests = p.max_batch_requests
+    c.kv_capacity_tokens = p.kv_capacity_tokens
+    c.chunking = 1 if p.chunking else 0
+    return c
+
+
+def c_mpc_config(cfg: MpcConfig, keep: list) -> _abi.bs_mpc_config:
+    c = _abi.bs_mpc_config()
+    c.horizon_K = cfg.horizon_K
+    c.ladder_N = cfg.ladder_N
+    lad = _darr(cfg.ladder.freqs_mhz)
+    keep.append(lad)
+    c.n_ladder = len(cfg.ladder.freqs_mhz)
+    c.ladder_mhz = C.cast(lad, _abi.dp)
+    c.ttft_ms = cfg.slo.ttft_ms
+    c.tpot_ms = cfg.slo.tpot_ms
+    c.percentile = cfg.slo.percentile
+    c.switch_latency_ms = cfg.switch_latency_ms
+    c.margin = cfg.margin
+    return c
+
+
+def c_decode_config(cfg: DecodePolicyConfig, keep: list) -> _abi.bs_decode_config:
+    c = _abi.bs_decode_config()
+    c.tbt_slo_ms = cfg.tbt_slo_ms
+    c.kv_threshold = cfg.kv_threshold
+    c.margin = cfg.margin
+    lad = _darr(cfg.ladder.freqs_mhz)
+    keep.append(lad)
+    c.n_ladder = len(cfg.ladder.freqs_mhz)
+    c.ladder_mhz = C.cast(lad, _abi.dp)
+    return c
+
+
+def c_snapshot(q: QueueSnapshot, keep: list) -> _abi.bs_snapshot:
+    s = _abi.bs_snapshot()
+    s.now_ms = q.now_ms
+    s.current_freq_mhz = q.current_freq_mhz
+    s.target_freq_mhz = q.target_freq_mhz
+    s.tp = q.tp
+    n = len(q.waiting)
+    w = (_abi.bs_waiting * max(1, n))()
+    for i, e in enumerate(q.waiting):
+        w[i].id = e.id
+        w[i].arrival_ms = e.arrival_ms
+        w[i].total_len = e.total_len
+        w[i].remaining_len = e.remaining_len
+    keep.append(w)
+    s.n_waiting = n
+    s.waiting = C.cast(w, C.POINTER(_abi.bs_waiting))
+    r = q.running
+    s.running_active = 1 if r.active else 0
+    if r.active:
+        nr = len(r.completes)
+        comp = (C.c_uint8 * max(1, nr))(*[1 if x else 0 for x in r.completes])
+        arr = _darr(r.arrivals_ms)
+        keep += [comp, arr]
+        s.n_running = nr
+        s.running_completes = C.cast(comp, C.POINTER(C.c_uint8))
+        s.running_arrivals_ms = C.cast(arr, _abi.dp)
+        s.running_work_remaining = r.work_remaining
+        s.running_features.n_requests = r.features.n_requests
+        s.running_features.sum_len = r.features.sum_len
+    return s
+
+
+def c_problems(snaps: Sequence[QueueSnapshot], cfg_index: Sequence[int] | None, keep: list):
+    n = len(snaps)
+    arr = (_abi.bs_mpc_problem * max(1, n))()
+    for i, q in enumerate(snaps):
+        arr[i].snap = c_snapshot(q, keep)
+        arr[i].cfg_index = 0 if cfg_index is None else cfg_index[i]
+    keep.append(arr)
+    return arr
+
+
+def greedy_from_c(r: _abi.bs_mpc_result) -> GreedyResult:
+    g = GreedyResult()
+    g.assignment = FrequencyAssignment([r.freqs_mhz[k] for k in range(r.K)])
+    g.freq_index = [r.freq_index[k] for k in range(r.K)]
+    g.feasible = bool(r.feasible)
+    g.eval_count = r.eval_count
+    g.objective_w = r.objective_w
+    g.levels = [GreedyLevelStats(r.levels[i].level, r.levels[i].replaced_mhz, r.levels[i].k_prime,
+                                 r.levels[i].mutations, r.levels[i].feasible_mutations, bool(r.levels[i].accepted))
+                for i in range(max(0, r.n_levels))]
+    g.feasible_count = r.feasible_count
+    g.trajectories = r.trajectories
+    g.best_code = r.best_code
+    g.decision_freq_mhz = r.decision_freq_mhz
+    return g
+
+
+# ---------------------------------------------------------------------------
+# device context
+# ---------------------------------------------------------------------------
+
+
+class Device:
+    """One C-ABI context (one CUDA stream) on one GPU.  Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = _abi.ctx_t()
+        rc = self._lib.bs_ctx_create(device, C.byref(h))
+        if rc != _abi.BS_OK:
+            raise CudaError(f"bs_ctx_create(device={device}) failed with status {rc}: no usable CUDA device "
+                            "(the decision path has no CPU fallback)")
+        self.handle = h
+        self.device = device
+        self._models: dict = {}
+
+    def close(self) -> None:
+        if self.handle:
+            for mh, _ in self._models.values():
+                self._lib.bs_models_free(self.handle, mh)
+            self._models.clear()
+            self._lib.bs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def error(self) -> str:
+        return (self._lib.bs_last_error(self.handle) or b"").decode()
+
+    def check(self, rc: int) -> None:
+        if rc != _abi.BS_OK:
+            raise_status(rc, self.error())
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.bs_ctx_kernel_launches(self.handle))
+
+    def sm_count(self) -> int:
+        d, s = C.c_int(), C.c_int()
+        self.check(self._lib.bs_ctx_info(self.handle, C.byref(d), C.byref(s)))
+        return s.value
+
+    def models(self, m: ModelSet) -> C.c_void_p:
+        """Device copy of a ModelSet (uploaded once per object, immutable)."""
+        key = id(m)
+        hit = self._models.get(key)
+        if hit is not None and hit[1] is m:
+            return hit[0]
+        keep: list = []
+        cm = c_model_set(m, keep)
+        mh = _abi.models_t()
+        self.check(self._lib.bs_models_upload(self.handle, C.byref(cm), C.byref(mh)))
+        self._models[key] = (mh, m)
+        return mh
+
+    def interpolate(self, grid: NdGrid, coords: Sequence[Sequence[float]]) -> tuple:
+        grid.validate_structure()
+        keep: list = []
+        g = c_grid(grid, keep)
+        n = len(coords)
+        flat = _darr([x for c in coords for x in c])
+        out = (C.c_double * max(1, n))()
+        cl = (C.c_uint32 * max(1, n))()
+        self.check(self._lib.bs_grid_interpolate(self.handle, C.byref(g), flat, n, out, cl))
+        return list(out[:n]), list(cl[:n])
+
+
+_default_lock = threading.Lock()
+_default: Device | None = None
+
+
+def default_device() -> Device:
+    global _default
+    with _default_lock:
+        if _default is None:
+            _default = Device(0)
+        return _default
+
+
+# ---------------------------------------------------------------------------
+# decision-path entry points (GPU)
+# ---------------------------------------------------------------------------
+
+_WHICH = {("latency", Phase.prefill): 0, ("latency", Phase.decode): 1,
+          ("power", Phase.prefill): 2, ("power", Phase.decode): 3}
+
+
+def _predict(kind: str, table, f: BatchFeatures, tp: int, freq_mhz: float, models: ModelSet,
+             device: Device | None) -> float:
+    dev = device or default_device()
+    which = _WHICH[(kind, table.phase)]
+    feats = (_abi.bs_features * 1)()
+    feats[0].n_requests = f.n_requests
+    feats[0].sum_len = f.sum_len
+    tpa = (C.c_int32 * 1)(tp)
+    fr = (C.c_double * 1)(freq_mhz)
+    out = (C.c_double * 1)()
+    st = (C.c_int32 * 1)()
+    dev.check(dev._lib.bs_predict(dev.handle, dev.models(models), which, feats, tpa, fr, 1, out, st, None))
+    if st[0] != _abi.BS_OK:
+        raise ModelError(f"{kind} model returned non-positive value")
+    return out[0]
+
+
+def predict_latency(models: ModelSet, phase: Phase, f: BatchFeatures, tp: int, freq_mhz: float,
+                    device: Device | None = None) -> float:
+    """predict_latency (perfmodel.hpp:262-266) on the GPU."""
+    return _predict("latency", models.latency(phase), f, tp, freq_mhz, models, device)
+
+
+def predict_power(models: ModelSet, phase: Phase, f: BatchFeatures, tp: int, freq_mhz: float,
+                  device: Device | None = None) -> float:
+    """predict_power (perfmodel.hpp:268-272) on the GPU."""
+    return _predict("power", models.power(phase), f, tp, freq_mhz, models, device)
+
+
+def project_batches(q: QueueSnapshot, policy: SchedulerPolicy, horizon_K: int,
+                    device: Device | None = None) -> list:
+    """project_batches (dvfs.hpp:63-100) on the GPU; ProjectedBatch summaries."""
+    if horizon_K < 1:
+        raise ParameterError("project_batches: horizon_K must be >= 1")
+    dev = device or default_device()
+    keep: list = []
+    cfg = MpcConfig(horizon_K=horizon_K, ladder_N=1, ladder=FrequencyLadder([1.0]))
+    cc = c_mpc_config(cfg, keep)
+    pc = c_policy(policy)
+    probs = c_problems([q], None, keep)
+    out = (_abi.bs_projected_batch * _abi.BS_MAX_K)()
+    K = (C.c_int32 * 1)()
+    st = (C.c_int32 * 1)()
+    dev.check(dev._lib.bs_project_batches(dev.handle, C.byref(cc), C.byref(pc), 1, probs, 1, out, K, st))
+    if st[0] != _abi.BS_OK:
+        raise_status(st[0], "scheduler: queued request with no remaining tokens")
+    res = []
+    for k in range(K[0]):
+        b = out[k]
+        res.append(ProjectedBatch(BatchFeatures(b.features.n_requests, b.features.sum_len), b.work_fraction,
+                                  b.n_completing, b.min_completing_arrival_ms))
+    return res
+
+
+def _mpc_batch(fn_name: str, snaps: Sequence[QueueSnapshot], cfgs: Sequence[MpcConfig],
+               policies: Sequence[SchedulerPolicy], cfg_index: Sequence[int] | None, models: ModelSet,
+               device: Device | None) -> list:
+    dev = device or default_device()
+    for c in cfgs:
+        c.validate()
+    keep: list = []
+    carr = (_abi.bs_mpc_config * len(cfgs))(*[c_mpc_config(c, keep) for c in cfgs])
+    parr = (_abi.bs_scheduler_policy * len(policies))(*[c_policy(p) for p in policies])
+    probs = c_problems(snaps, cfg_index, keep)
+    n = len(snaps)
+    out = (_abi.bs_mpc_result * max(1, n))()
+    fn = getattr(dev._lib, fn_name)
+    dev.check(fn(dev.handle, dev.models(models), carr, parr, len(cfgs), probs, n, out))
+    return [greedy_from_c(out[i]) for i in range(n)]
+
+
+def greedy_freq_select(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy,
+                       device: Device | None = None) -> GreedyResult:
+    """greedy_freq_select (dvfs.hpp:185-259), one CTA on the GPU."""
+    return _mpc_batch("bs_mpc_greedy", [q], [cfg], [policy], None, models, device)[0]
+
+
+def greedy_freq_select_batch(snaps: Sequence[QueueSnapshot], cfg: MpcConfig, models: ModelSet,
+                             policy: SchedulerPolicy, device: Device | None = None) -> list:
+    return _mpc_batch("bs_mpc_greedy", snaps, [cfg], [policy], None, models, device)
+
+
+def exhaustive_freq_select(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy,
+                           device: Device | None = None) -> GreedyResult:
+    """Exhaustive MPC (the reference's oracle loop, tests/test_dvfs.cpp:74-94),
+    argmin over (objective, lexicographic frequency vector)."""
+    return _mpc_batch("bs_mpc_exhaustive", [q], [cfg], [policy], None, models, device)[0]
+
+
+def exhaustive_freq_select_batch(snaps: Sequence[QueueSnapshot], cfg: MpcConfig, models: ModelSet,
+                                 policy: SchedulerPolicy, device: Device | None = None) -> list:
+    return _mpc_batch("bs_mpc_exhaustive", snaps, [cfg], [policy], None, models, device)
+
+
+def mpc_tables(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy,
+               device: Device | None = None) -> tuple:
+    """(lat, pow, energy) K x N tables of MpcEvaluator::eval (dvfs.hpp:150-160)."""
+    dev = device or default_device()
+    cfg.validate()
+    keep: list = []
+    cc = c_mpc_config(cfg, keep)
+    pc = c_policy(policy)
+    probs = c_problems([q], None, keep)
+    K, nc = C.c_int32(), C.c_int32()
+    size = _abi.BS_MAX_K * _abi.BS_MAX_CAND
+    lat, pw, en = (C.c_double * size)(), (C.c_double * size)(), (C.c_double * size)()
+    dev.check(dev._lib.bs_mpc_tables(dev.handle, dev.models(models), C.byref(cc), C.byref(pc), probs, C.byref(K),
+                                     C.byref(nc), lat, pw, en))
+    k, n = K.value, nc.value
+    rows = lambda a: [[a[i * n + j] for j in range(n)] for i in range(k)]  # noqa: E731
+    return rows(lat), rows(pw), rows(en)
+
+
+def mpc_eval_codes(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy,
+                   codes: Sequence[int], device: Device | None = None) -> tuple:
+    """meets_slo + time_weighted_power of given assignments (batch 0 most significant)."""
+    dev = device or default_device()
+    cfg.validate()
+    keep: list = []
+    cc = c_mpc_config(cfg, keep)
+    pc = c_policy(policy)
+    probs = c_problems([q], None, keep)
+    n = len(codes)
+    ca = (C.c_uint64 * max(1, n))(*codes)
+    feas = (C.c_int32 * max(1, n))()
+    obj = (C.c_double * max(1, n))()
+    dev.check(dev._lib.bs_mpc_eval_codes(dev.handle, dev.models(models), C.byref(cc), C.byref(pc), probs, ca, n,
+                                         feas, obj))
+    return [bool(x) for x in feas[:n]], list(obj[:n])
+
+
+def select_decode_freq_ex(batch: BatchFeatures, kv: KVCacheState, cfg: DecodePolicyConfig, models: ModelSet,
+                          tp: int, device: Device | None = None) -> DecodeDecision:
+    """select_decode_freq_ex (dvfs.hpp:274-293), one warp on the GPU."""
+    return select_decode_freq_batch([(batch, kv, tp)], cfg, models, device)[0]
+
+
+def select_decode_freq(batch: BatchFeatures, kv: KVCacheState, cfg: DecodePolicyConfig, models: ModelSet, tp: int,
+                       device: Device | None = None) -> float:
+    return select_decode_freq_ex(batch, kv, cfg, models, tp, device).freq_mhz
+
+
+def select_decode_freq_batch(queries: Sequence[tuple], cfg: DecodePolicyConfig, models: ModelSet,
+                             device: Device | None = None) -> list:
+    dev = device or default_device()
+    cfg.validate()
+    keep: list = []
+    cc = c_decode_config(cfg, keep)
+    n = len(queries)
+    qa = (_abi.bs_decode_query * max(1, n))()
+    for i, (b, kv, tp) in enumerate(queries):
+        qa[i].batch.n_requests = b.n_requests
+        qa[i].batch.sum_len = b.sum_len
+        qa[i].kv_capacity_tokens = kv.capacity_tokens
+        qa[i].kv_used_tokens = kv.used_tokens
+        qa[i].tp = tp
+        qa[i].cfg_index = 0
+    out = (_abi.bs_decode_result * max(1, n))()
+    dev.check(dev._lib.bs_decode_pick(dev.handle, dev.models(models), C.byref(cc), 1, qa, n, out))
+    return [DecodeDecision(out[i].freq_mhz, out[i].eval_count, bool(out[i].kv_override)) for i in range(n)]
+
+
+# ---------------------------------------------------------------------------
+# controllers (dvfs.hpp:302-390): the FreqController / ControllerFactory shape
+# ---------------------------------------------------------------------------
+
+
+class FreqController:
+    def decide(self, q: QueueSnapshot) -> FreqDecision:
+        raise NotImplementedError
+
+    def reacts_to_arrivals(self) -> bool:
+        return False
+
+    def on_arrival(self, q: QueueSnapshot) -> Optional[FreqDecision]:
+        return None
+
+    def predicted_latency_ms(self, f: BatchFeatures, phase: Phase, tp: int, freq_mhz: float) -> float:
+        raise NotImplementedError
+
+    def safety_margin(self) -> float:
+        return 0.05
+
+    def max_freq_mhz(self) -> float:
+        raise NotImplementedError
+
+
+class PrefillMpcController(FreqController):
+    """PrefillMpcController (dvfs.hpp:302-339) backed by bs_mpc_greedy."""
+
+    def __init__(self, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy, device: Device | None = None):
+        cfg.validate()
+        policy.validate()
+        self.cfg, self.models, self.policy = cfg, models, policy
+        self.device = device or default_device()
+        self._max = cfg.candidates().max_mhz()
+
+    def decide(self, q: QueueSnapshot) -> FreqDecision:
+        return self._run(q)
+
+    def reacts_to_arrivals(self) -> bool:
+        return True
+
+    def on_arrival(self, q: QueueSnapshot) -> Optional[FreqDecision]:
+        return self._run(q)
+
+    def predicted_latency_ms(self, f, phase, tp, freq_mhz):
+        return predict_latency(self.models, phase, f, tp, freq_mhz, self.device)
+
+    def safety_margin(self) -> float:
+        return self.cfg.margin
+
+    def max_freq_mhz(self) -> float:
+        return self._max
+
+    def _run(self, q: QueueSnapshot) -> FreqDecision:
+        g = greedy_freq_select(q, self.cfg, self.models, self.policy, self.device)
+        return FreqDecision(g.decision_freq_mhz, g.feasible, g.eval_count)
+
+
+class DecodePolicyController(FreqController):
+    """DecodePolicyController (dvfs.hpp:341-365) backed by bs_decode_pick."""
+
+    def __init__(self, cfg: DecodePolicyConfig, models: ModelSet, device: Device | None = None):
+        cfg.validate()
+        self.cfg, self.models = cfg, models
+        self.device = device or default_device()
+        self._safety = 0.05
+
+    def decide(self, q: QueueSnapshot) -> FreqDecision:
+        d = select_decode_freq_ex(q.decode_batch, q.kv, self.cfg, self.models, q.tp, self.device)
+        return FreqDecision(d.freq_mhz, True, d.eval_count)
+
+    def predicted_latency_ms(self, f, phase, tp, freq_mhz):
+        return predict_latency(self.models, phase, f, tp, freq_mhz, self.device)
+
+    def safety_margin(self) -> float:
+        return self._safety
+
+    def set_safety_margin(self, m: float) -> None:
+        self._safety = m
+
+    def max_freq_mhz(self) -> float:
+        return self.cfg.ladder.max_mhz()
+
+
+class TwoTierFactory:
+    """TwoTierFactory (dvfs.hpp:370-390): MPC on prefill, TBT policy on decode."""
+
+    def __init__(self, mpc: MpcConfig, decode: DecodePolicyConfig, controller_models: ModelSet,
+                 policy: SchedulerPolicy, device: Device | None = None):
+        self.mpc, self.decode, self.models, self.policy = mpc, decode, controller_models, policy
+        self.device = device
+
+    def make(self, phase: Phase, tp: int, base_freq_mhz: float) -> FreqController:
+        if phase == Phase.prefill:
+            return PrefillMpcController(self.mpc, self.models, self.policy, self.device)
+        ctl = DecodePolicyController(self.decode, self.models, self.device)
+        ctl.set_safety_margin(self.decode.margin if self.decode.margin > 0.0 else 0.05)
+        return ctl

@@ -1,0 +1,78 @@
+"""CPU-only checks of the drop-in boundary: the C-ABI library loads, exports
+every entry point include/biscale_gpu.h declares, its ctypes mirror has the
+C compiler's struct layouts, and with no GPU it fails loudly (no fallback)."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+import subprocess
+import tempfile
+from pathlib import Path
+
+import pytest
+
+from paper_2602_18755_b200 import _abi as A
+from paper_2602_18755_b200 import _lib
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "biscale_gpu.h"
+
+STRUCTS = ["bs_grid", "bs_idle_entry", "bs_model_set", "bs_features", "bs_scheduler_policy", "bs_mpc_config",
+           "bs_waiting", "bs_snapshot", "bs_mpc_problem", "bs_level_stats", "bs_mpc_result", "bs_projected_batch",
+           "bs_decode_config", "bs_decode_query", "bs_decode_result"]
+
+
+def declared_functions() -> set:
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(bs_[a-z0-9_]+)\s*\(", text))
+
+
+def test_header_and_prototypes_agree():
+    assert declared_functions() == set(_lib.exported_symbols())
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (bs_[a-z0-9_]+)", out))
+    assert declared_functions() <= exported
+
+
+def test_struct_layouts_match_c_compiler():
+    src = "#include <stdio.h>\n#include <stddef.h>\n#include \"biscale_gpu.h\"\nint main(void){\n"
+    for s in STRUCTS:
+        src += f'printf("{s} %zu\\n", sizeof({s}));\n'
+    src += 'printf("snap_waiting %zu\\n", offsetof(bs_snapshot, waiting));\n'
+    src += 'printf("result_levels %zu\\n", offsetof(bs_mpc_result, levels));\nreturn 0;}\n'
+    with tempfile.TemporaryDirectory() as d:
+        cpath = Path(d) / "l.c"
+        cpath.write_text(src)
+        exe = Path(d) / "l"
+        subprocess.run(["gcc", "-I", str(ROOT / "include"), str(cpath), "-o", str(exe)], check=True)
+        sizes = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True,
+                                                             text=True).stdout.splitlines())
+    for s in STRUCTS:
+        assert int(sizes[s]) == C.sizeof(getattr(A, s)), s
+    assert int(sizes["snap_waiting"]) == A.bs_snapshot.waiting.offset
+    assert int(sizes["result_levels"]) == A.bs_mpc_result.levels.offset
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2602_18755_b200 import pdsim as P
+    with pytest.raises(P.CudaError):
+        P.Device(0)
+
+
+def test_kernels_are_sm100a_fp64_without_fma():
+    """The shipped library carries sm_100a SASS, and the MPC kernels use
+    DADD/DMUL (no DFMA outside the IEEE division subroutine)."""
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "DADD" in sass and "DMUL" in sass
