@@ -324,13 +324,13 @@ def main():
             "decisions_per_s": world * D * args.steps / (total_ms * 1e-3),
             "feasible_fraction": feasible / max(1, trajectories),
             "phase_ms_avg": {k: statistics.mean(p[i] for p in phase_ms)
-                             for i, k in enumerate(["prepare", "scan", "prefix", "leaf", "finalize"])},
+                             for i, k in enumerate(["prepare", "seed", "bfs", "sweep", "finalize"])},
             "e2e": {"value": world * D * TRAJ_PER_DECISION / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
                     "matches_resident": bool(same)},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak.value, "traffic": traffic,
-                         "note": "W = 5H+2 = 32 FP64 ops per trajectory (SURVEY §8d) over the leaf kernel's event "
+                         "note": "W = 5H+2 = 32 FP64 ops per trajectory (SURVEY §8d) over the subtree kernel's event "
                                  "time; prefix sharing and infeasible-subtree pruning execute fewer ops, so frac may "
                                  "exceed 1; peak = measured non-FMA DADD issue rate (bs_fp64_peak)"},
             "gpu_launches": int(launches),

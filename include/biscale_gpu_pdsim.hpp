@@ -1,0 +1,337 @@
+// biscale_gpu_pdsim.hpp — header-only C++ drop-in for the reference's
+// controller interface, backed by the sm_100a C ABI (biscale_gpu.h).
+//
+// Include it from code that already includes the reference's pdsim headers
+// (proj/include/pdsim/dvfs.hpp).  It provides:
+//
+//   pdsim_gpu::Device                   RAII bs_ctx_t (one CUDA stream)
+//   pdsim_gpu::DeviceModels             bs_models_upload of a pdsim::ModelSet
+//   pdsim_gpu::GpuPrefillMpcController  : pdsim::FreqController
+//                                         (replaces PrefillMpcController,
+//                                          dvfs.hpp:302-339)
+//   pdsim_gpu::GpuDecodePolicyController: pdsim::FreqController
+//                                         (replaces DecodePolicyController,
+//                                          dvfs.hpp:341-365)
+//   pdsim_gpu::GpuTwoTierFactory        : pdsim::ControllerFactory
+//                                         (replaces TwoTierFactory,
+//                                          dvfs.hpp:370-390; drop-in for
+//                                          runner.hpp:118)
+//   pdsim_gpu::greedy_freq_select / exhaustive_freq_select /
+//   select_decode_freq_ex               batch-of-one wrappers
+//
+// Status codes are rethrown as the reference's exception types with the
+// library's message.  predicted_latency_ms is evaluated with the reference's
+// own predict_latency (the safety deadline relies on exact ties,
+// tests/test_simulator.cpp:609-617; the device interpolator is bit-identical
+// but a host call avoids a launch on the simulator's critical path).
+#pragma once
+
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "biscale_gpu.h"
+#include "pdsim/dvfs.hpp"
+#include "pdsim/errors.hpp"
+
+namespace pdsim_gpu {
+
+[[noreturn]] inline void rethrow(int status, const std::string& msg) {
+  switch (status) {
+    case BS_PARAMETER_ERROR: throw pdsim::ParameterError(msg);
+    case BS_MODEL_ERROR: throw pdsim::ModelError(msg);
+    case BS_SIMULATION_ERROR: throw pdsim::SimulationError(msg);
+    case BS_CONFIG_ERROR: throw pdsim::ConfigError(msg);
+    case BS_ACCOUNTING_ERROR: throw pdsim::AccountingError(msg);
+    case BS_IO_ERROR: throw pdsim::IoError(msg);
+    case BS_INFEASIBLE_ERROR: {
+      auto bar = msg.find('|');
+      if (bar == std::string::npos) throw pdsim::InfeasibleError("", msg);
+      throw pdsim::InfeasibleError(msg.substr(0, bar), msg.substr(bar + 1));
+    }
+    default: throw std::runtime_error("biscale_gpu: " + msg);
+  }
+}
+
+class Device {
+ public:
+  explicit Device(int device = 0) {
+    int rc = bs_ctx_create(device, &ctx_);
+    if (rc != BS_OK) rethrow(rc, "bs_ctx_create failed: no usable CUDA device (no CPU fallback)");
+  }
+  ~Device() { bs_ctx_destroy(ctx_); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  bs_ctx_t get() const { return ctx_; }
+  void check(int rc) const {
+    if (rc != BS_OK) rethrow(rc, bs_last_error(ctx_));
+  }
+
+ private:
+  bs_ctx_t ctx_ = nullptr;
+};
+
+namespace detail {
+
+inline int axis_role(const std::string& name) {
+  if (name == pdsim::kAxisSumLen) return BS_AXIS_SUM_LEN;
+  if (name == pdsim::kAxisNumRequests) return BS_AXIS_N_REQUESTS;
+  if (name == pdsim::kAxisTp) return BS_AXIS_TP;
+  if (name == pdsim::kAxisFreq) return BS_AXIS_FREQ;
+  return BS_AXIS_UNKNOWN;
+}
+
+inline bs_grid to_grid(const pdsim::NdGrid& g) {
+  bs_grid out{};
+  out.rank = static_cast<int32_t>(g.axes.size());
+  for (std::size_t d = 0; d < g.axes.size() && d < BS_MAX_RANK; ++d) {
+    out.role[d] = axis_role(g.axes[d].name);
+    out.n_knots[d] = static_cast<int32_t>(g.axes[d].knots.size());
+    out.knots[d] = g.axes[d].knots.data();
+  }
+  out.values = g.values.data();
+  return out;
+}
+
+// Owns the marshalled arrays of one QueueSnapshot.
+struct SnapshotView {
+  std::vector<bs_waiting> waiting;
+  std::vector<uint8_t> completes;
+  bs_snapshot snap{};
+
+  explicit SnapshotView(const pdsim::QueueSnapshot& q) {
+    waiting.reserve(q.waiting.size());
+    for (const auto& w : q.waiting) waiting.push_back(bs_waiting{w.id, w.arrival_ms, w.total_len, w.remaining_len});
+    snap.now_ms = q.now_ms;
+    snap.current_freq_mhz = q.current_freq_mhz;
+    snap.target_freq_mhz = q.target_freq_mhz;
+    snap.tp = q.tp;
+    snap.n_waiting = static_cast<int32_t>(waiting.size());
+    snap.waiting = waiting.data();
+    snap.running_active = q.running.active ? 1 : 0;
+    if (q.running.active) {
+      for (bool c : q.running.completes) completes.push_back(c ? 1 : 0);
+      snap.n_running = static_cast<int32_t>(completes.size());
+      snap.running_completes = completes.data();
+      snap.running_arrivals_ms = q.running.arrivals_ms.data();
+      snap.running_work_remaining = q.running.work_remaining;
+      snap.running_features = bs_features{q.running.features.n_requests, q.running.features.sum_len};
+    }
+  }
+};
+
+inline bs_mpc_config to_mpc(const pdsim::MpcConfig& c) {
+  bs_mpc_config o{};
+  o.horizon_K = c.horizon_K;
+  o.ladder_N = c.ladder_N;
+  o.n_ladder = static_cast<int32_t>(c.ladder.freqs_mhz.size());
+  o.ladder_mhz = c.ladder.freqs_mhz.data();
+  o.ttft_ms = c.slo.ttft_ms;
+  o.tpot_ms = c.slo.tpot_ms;
+  o.percentile = c.slo.percentile;
+  o.switch_latency_ms = c.switch_latency_ms;
+  o.margin = c.margin;
+  return o;
+}
+
+inline bs_scheduler_policy to_policy(const pdsim::SchedulerPolicy& p) {
+  bs_scheduler_policy o{};
+  o.max_batch_tokens = p.max_batch_tokens;
+  o.max_batch_requests = p.max_batch_requests;
+  o.kv_capacity_tokens = p.kv_capacity_tokens;
+  o.chunking = p.chunking ? 1 : 0;
+  return o;
+}
+
+inline pdsim::GreedyResult from_result(const bs_mpc_result& r) {
+  pdsim::GreedyResult g;
+  g.assignment.freqs.assign(r.freqs_mhz, r.freqs_mhz + r.K);
+  g.feasible = r.feasible != 0;
+  g.eval_count = r.eval_count;
+  g.objective_w = r.objective_w;
+  for (int l = 0; l < r.n_levels; ++l) {
+    pdsim::GreedyLevelStats s;
+    s.level = r.levels[l].level;
+    s.replaced_mhz = r.levels[l].replaced_mhz;
+    s.k_prime = r.levels[l].k_prime;
+    s.mutations = r.levels[l].mutations;
+    s.feasible_mutations = r.levels[l].feasible_mutations;
+    s.accepted = r.levels[l].accepted != 0;
+    g.levels.push_back(s);
+  }
+  return g;
+}
+
+}  // namespace detail
+
+// Immutable device copy of a pdsim::ModelSet (perfmodel.hpp:494-503).
+class DeviceModels {
+ public:
+  DeviceModels(const Device& dev, const pdsim::ModelSet& m) : dev_(&dev) {
+    bs_model_set s{};
+    s.latency_prefill = detail::to_grid(m.latency_prefill.grid);
+    s.latency_decode = detail::to_grid(m.latency_decode.grid);
+    s.power_prefill = detail::to_grid(m.power_prefill.grid);
+    s.power_decode = detail::to_grid(m.power_decode.grid);
+    std::vector<bs_idle_entry> idle;
+    for (const auto& e : m.idle.entries)
+      idle.push_back(bs_idle_entry{e.tp, static_cast<int32_t>(e.freqs_mhz.size()), e.freqs_mhz.data(),
+                                   e.idle_w.data()});
+    s.n_idle = static_cast<int32_t>(idle.size());
+    s.idle = idle.data();
+    dev.check(bs_models_upload(dev.get(), &s, &h_));
+  }
+  ~DeviceModels() { bs_models_free(dev_->get(), h_); }
+  DeviceModels(const DeviceModels&) = delete;
+  DeviceModels& operator=(const DeviceModels&) = delete;
+  bs_models_t get() const { return h_; }
+  const Device& device() const { return *dev_; }
+
+ private:
+  const Device* dev_;
+  bs_models_t h_ = nullptr;
+};
+
+// greedy_freq_select (dvfs.hpp:185-259) on the GPU.
+inline pdsim::GreedyResult greedy_freq_select(const DeviceModels& dm, const pdsim::QueueSnapshot& q,
+                                              const pdsim::MpcConfig& cfg, const pdsim::SchedulerPolicy& policy,
+                                              bs_mpc_result* raw = nullptr) {
+  detail::SnapshotView v(q);
+  bs_mpc_problem p{};
+  p.snap = v.snap;
+  const bs_mpc_config c = detail::to_mpc(cfg);
+  const bs_scheduler_policy pol = detail::to_policy(policy);
+  bs_mpc_result r{};
+  dm.device().check(bs_mpc_greedy(dm.device().get(), dm.get(), &c, &pol, 1, &p, 1, &r));
+  if (raw) *raw = r;
+  return detail::from_result(r);
+}
+
+// Exhaustive MPC (tests/test_dvfs.cpp:74-94 semantics, lexicographic ties).
+inline pdsim::GreedyResult exhaustive_freq_select(const DeviceModels& dm, const pdsim::QueueSnapshot& q,
+                                                  const pdsim::MpcConfig& cfg, const pdsim::SchedulerPolicy& policy,
+                                                  bs_mpc_result* raw = nullptr) {
+  detail::SnapshotView v(q);
+  bs_mpc_problem p{};
+  p.snap = v.snap;
+  const bs_mpc_config c = detail::to_mpc(cfg);
+  const bs_scheduler_policy pol = detail::to_policy(policy);
+  bs_mpc_result r{};
+  dm.device().check(bs_mpc_exhaustive(dm.device().get(), dm.get(), &c, &pol, 1, &p, 1, &r));
+  if (raw) *raw = r;
+  return detail::from_result(r);
+}
+
+// select_decode_freq_ex (dvfs.hpp:274-293) on the GPU.
+inline pdsim::DecodeDecision select_decode_freq_ex(const DeviceModels& dm, const pdsim::BatchFeatures& batch,
+                                                   const pdsim::KVCacheState& kv,
+                                                   const pdsim::DecodePolicyConfig& cfg, int tp) {
+  bs_decode_config c{};
+  c.tbt_slo_ms = cfg.tbt_slo_ms;
+  c.kv_threshold = cfg.kv_threshold;
+  c.margin = cfg.margin;
+  c.n_ladder = static_cast<int32_t>(cfg.ladder.freqs_mhz.size());
+  c.ladder_mhz = cfg.ladder.freqs_mhz.data();
+  bs_decode_query q{};
+  q.batch = bs_features{batch.n_requests, batch.sum_len};
+  q.kv_capacity_tokens = kv.capacity_tokens;
+  q.kv_used_tokens = kv.used_tokens;
+  q.tp = tp;
+  bs_decode_result r{};
+  dm.device().check(bs_decode_pick(dm.device().get(), dm.get(), &c, 1, &q, 1, &r));
+  pdsim::DecodeDecision d;
+  d.freq_mhz = r.freq_mhz;
+  d.eval_count = r.eval_count;
+  d.kv_override = r.kv_override != 0;
+  return d;
+}
+
+// PrefillMpcController (dvfs.hpp:302-339) backed by bs_mpc_greedy.
+class GpuPrefillMpcController : public pdsim::FreqController {
+ public:
+  GpuPrefillMpcController(pdsim::MpcConfig cfg, const pdsim::ModelSet& models, const DeviceModels& dm,
+                          pdsim::SchedulerPolicy policy)
+      : cfg_(std::move(cfg)), models_(&models), dm_(&dm), policy_(policy) {
+    cfg_.validate();
+    policy_.validate();
+    max_mhz_ = cfg_.candidates().max_mhz();
+  }
+
+  pdsim::FreqDecision decide(const pdsim::QueueSnapshot& q) override { return run(q); }
+  bool reacts_to_arrivals() const override { return true; }
+  std::optional<pdsim::FreqDecision> on_arrival(const pdsim::QueueSnapshot& q) override { return run(q); }
+  double predicted_latency_ms(const pdsim::BatchFeatures& f, pdsim::Phase phase, int tp,
+                              double freq_mhz) const override {
+    return pdsim::predict_latency(models_->latency(phase), f, tp, freq_mhz);
+  }
+  double safety_margin() const override { return cfg_.margin; }
+  double max_freq_mhz() const override { return max_mhz_; }
+
+ private:
+  pdsim::FreqDecision run(const pdsim::QueueSnapshot& q) const {
+    bs_mpc_result r{};
+    greedy_freq_select(*dm_, q, cfg_, policy_, &r);
+    return pdsim::FreqDecision{r.decision_freq_mhz, r.feasible != 0, r.eval_count};
+  }
+
+  pdsim::MpcConfig cfg_;
+  const pdsim::ModelSet* models_;
+  const DeviceModels* dm_;
+  pdsim::SchedulerPolicy policy_;
+  double max_mhz_ = 0.0;
+};
+
+// DecodePolicyController (dvfs.hpp:341-365) backed by bs_decode_pick.
+class GpuDecodePolicyController : public pdsim::FreqController {
+ public:
+  GpuDecodePolicyController(pdsim::DecodePolicyConfig cfg, const pdsim::ModelSet& models, const DeviceModels& dm)
+      : cfg_(std::move(cfg)), models_(&models), dm_(&dm) {
+    cfg_.validate();
+  }
+  pdsim::FreqDecision decide(const pdsim::QueueSnapshot& q) override {
+    pdsim::DecodeDecision d = select_decode_freq_ex(*dm_, q.decode_batch, q.kv, cfg_, q.tp);
+    return pdsim::FreqDecision{d.freq_mhz, true, d.eval_count};
+  }
+  double predicted_latency_ms(const pdsim::BatchFeatures& f, pdsim::Phase phase, int tp,
+                              double freq_mhz) const override {
+    return pdsim::predict_latency(models_->latency(phase), f, tp, freq_mhz);
+  }
+  double safety_margin() const override { return safety_margin_; }
+  double max_freq_mhz() const override { return cfg_.ladder.max_mhz(); }
+  void set_safety_margin(double m) { safety_margin_ = m; }
+
+ private:
+  pdsim::DecodePolicyConfig cfg_;
+  const pdsim::ModelSet* models_;
+  const DeviceModels* dm_;
+  double safety_margin_ = 0.05;
+};
+
+// TwoTierFactory (dvfs.hpp:370-390): drop-in ControllerFactory for
+// simulate_cluster / run_policy.
+class GpuTwoTierFactory : public pdsim::ControllerFactory {
+ public:
+  GpuTwoTierFactory(pdsim::MpcConfig mpc, pdsim::DecodePolicyConfig decode, const pdsim::ModelSet& controller_models,
+                    const DeviceModels& dm, pdsim::SchedulerPolicy policy)
+      : mpc_(std::move(mpc)), decode_(std::move(decode)), models_(&controller_models), dm_(&dm), policy_(policy) {}
+
+  std::unique_ptr<pdsim::FreqController> make(pdsim::Phase phase, int tp, double base_freq_mhz) override {
+    (void)tp;
+    (void)base_freq_mhz;
+    if (phase == pdsim::Phase::prefill)
+      return std::make_unique<GpuPrefillMpcController>(mpc_, *models_, *dm_, policy_);
+    auto ctl = std::make_unique<GpuDecodePolicyController>(decode_, *models_, *dm_);
+    ctl->set_safety_margin(decode_.margin > 0.0 ? decode_.margin : 0.05);
+    return ctl;
+  }
+
+ private:
+  pdsim::MpcConfig mpc_;
+  pdsim::DecodePolicyConfig decode_;
+  const pdsim::ModelSet* models_;
+  const DeviceModels* dm_;
+  pdsim::SchedulerPolicy policy_;
+};
+
+}  // namespace pdsim_gpu

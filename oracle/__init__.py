@@ -18,6 +18,7 @@ from paper_2602_18755_b200 import _abi as A
 HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libpdsim_ref.so"
+REPLAY_BIN = HERE / "_ref" / "replay_parity"
 REFERENCE_ROOT = Path("/root/reference")
 
 _P = C.POINTER
@@ -47,6 +48,8 @@ def build(quiet: bool = True) -> None:
     targets = ["oracle"]
     if (REFERENCE_ROOT / "proj" / "include").is_dir():
         targets.append("ref")
+        if (HERE.parent / "paper_2602_18755_b200" / "libbiscale_gpu.so").exists():
+            targets.append("replay")
     res = subprocess.run(["make", "-C", str(HERE), *targets], capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("oracle build failed:\n" + res.stdout + res.stderr)

@@ -222,6 +222,19 @@ struct DTables {
   double E[kMaxK][kMaxCand];
   double B0[kMaxK][kMaxCand];
   double B1[kMaxK][kMaxCand];
+  // Per level, the candidates sorted by their switched step (B1; T1 at level
+  // 0), ascending, ties by index.  fl(fl(t + b) - m) is monotone in b, so the
+  // children of any node that pass meets_slo's check at level k form a
+  // prefix of this order (the non-switching child f == last, whose step is
+  // B0, is tested on its own).  sorted_ok = every key finite.
+  double sb[kMaxK][kMaxCand];
+  unsigned char ord[kMaxK][kMaxCand];
+  unsigned char rank[kMaxK][kMaxCand];
+  int sorted_ok;
+  // Per-level bounds for the leaf-row skip: amax = max_f A, pmin_lo =
+  // fl(min_f P * (1 - 2^-50)) <= min_f P * (1 - u).
+  double amax[kMaxK];
+  double pmin_lo[kMaxK];
 };
 
 // Compact per-problem result written by the device; the host expands it

@@ -1,0 +1,533 @@
+// bs_exhaustive.cuh — exhaustive prefill-MPC rollout on sm_100a (included
+// by bs_mpc.cu inside its anonymous namespace).
+//
+// Semantics: every assignment of the |cand| candidate rungs to the K
+// projected batches; feasibility is meets_slo (dvfs.hpp:105-122), the
+// objective time_weighted_power (dvfs.hpp:163-171); argmin over (objective,
+// assignment in lexicographic frequency order) -- the tie rule dvfs.hpp:243
+// applies to greedy; the code of an assignment has batch 0 as its most
+// significant base-|cand| digit, so the rule is (objective, code).
+//
+// Search: level-synchronous breadth-first expansion over ALL decisions of
+// the batch.  meets_slo returns false at the first violated batch, so a
+// prefix that violates the deadline has no feasible completion: frontiers
+// only ever hold feasible prefixes, compacted with warp-aggregated appends.
+// Nodes at depth FD = K - I (I = 2 bottom levels, 3 for very wide trees) go
+// to the final list; the sweep kernel gives each final node one thread that
+// walks its I bottom levels (every leaf in increasing code order) with a
+// division-free objective filter and merges (objective, code) minima through
+// a 128-bit CAS.  Work is proportional to the feasible part of the tree, and
+// every level is spread over the whole GPU however uneven the decisions are.
+
+struct ExCtl {
+  unsigned long long level_count[kMaxK + 1];  // BFS list sizes per depth
+  unsigned long long final_count;
+  unsigned long long overflow;  // appends dropped for lack of capacity (must stay 0)
+};
+
+// Bottom levels swept per final node.
+__host__ __device__ inline int sweep_levels(int K, int nc) {
+  if (K <= 2) return K;
+  double np = 1.0;
+  for (int i = 0; i < K - 2; ++i) np *= nc;
+  return np > 16777216.0 ? 3 : 2;
+}
+
+__host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) {
+  unsigned long long r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+// Frontier lists in HBM, structure of arrays.
+struct Frontier {
+  int* d;                    // problem
+  unsigned long long* code;  // prefix code, batch 0 most significant
+  double* t;                 // meets_slo clock after the prefix
+  double* num;               // sum lat * pow
+  double* den;               // sum lat
+  int* last;                 // last digit (switch test of the next level)
+};
+
+__host__ __device__ inline size_t frontier_bytes(unsigned long long cap) { return 40ull * cap + 6 * 256; }
+
+__host__ __device__ inline Frontier frontier_at(void* base, unsigned long long cap) {
+  char* p = static_cast<char*>(base);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  Frontier f;
+  f.t = reinterpret_cast<double*>(take(8 * cap));
+  f.num = reinterpret_cast<double*>(take(8 * cap));
+  f.den = reinterpret_cast<double*>(take(8 * cap));
+  f.code = reinterpret_cast<unsigned long long*>(take(8 * cap));
+  f.d = reinterpret_cast<int*>(take(4 * cap));
+  f.last = reinterpret_cast<int*>(take(4 * cap));
+  return f;
+}
+
+// Final list: (problem, code) only; the sweep re-walks the prefix.
+struct FinalList {
+  int* d;
+  unsigned long long* code;
+};
+
+__host__ __device__ inline size_t final_bytes(unsigned long long cap) { return 12ull * cap + 2 * 256; }
+
+__host__ __device__ inline FinalList final_at(void* base, unsigned long long cap) {
+  char* p = static_cast<char*>(base);
+  FinalList f;
+  f.code = reinterpret_cast<unsigned long long*>(p);
+  f.d = reinterpret_cast<int*>(p + (8 * cap + 255) / 256 * 256);
+  return f;
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
+                                                               const DWaiting* W, const DRunning* R, DTables* tables,
+                                                               ExCtl* ctl, int n) {
+  __shared__ int s_status;
+  const int d = blockIdx.x;
+  if (d >= n) return;
+  if (d == 0 && threadIdx.x < kMaxK + 3) {  // counters of this run
+    if (threadIdx.x <= kMaxK)
+      ctl->level_count[threadIdx.x] = 0;
+    else if (threadIdx.x == kMaxK + 1)
+      ctl->final_count = 0;
+    else
+      ctl->overflow = 0;
+  }
+  const DProblem pr = probs[d];
+  const DMpcCfg& c = cfgs[pr.cfg];
+  DTables* T = &tables[d];
+  build_tables(m, pr, c, W + pr.wait_off, R + pr.run_off, T, &s_status);
+  if (threadIdx.x == 0) {
+    int st = s_status;
+    if (st == BS_OK) {
+      unsigned any = 0;
+      for (int k = 0; k < T->K; ++k) any |= T->bad_lat[k] | T->bad_pow[k];
+      if (any) st = BS_MODEL_ERROR;
+    }
+    T->status = st;
+  }
+}
+
+// One thread per problem: reset the argmin slots, seed the roots.
+__global__ void seed_kernel(const DTables* __restrict__ tables, int n, Key128* best, unsigned long long* feas,
+                            ExCtl* ctl, Frontier L0, FinalList fin, unsigned long long cap0,
+                            unsigned long long cap_final) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  best[d].obj = ~0ull;
+  best[d].code = ~0ull;
+  feas[d] = 0ull;
+  const DTables* T = &tables[d];
+  if (T->status != BS_OK || T->K == 0) return;
+  const int FD = T->K - sweep_levels(T->K, T->nc);
+  if (FD == 0) {
+    const unsigned long long s = atomicAdd(&ctl->final_count, 1ull);
+    if (s < cap_final) {
+      fin.d[s] = d;
+      fin.code[s] = 0;
+    } else {
+      atomicAdd(&ctl->overflow, 1ull);
+    }
+  } else {
+    const unsigned long long s = atomicAdd(&ctl->level_count[0], 1ull);
+    if (s < cap0) {
+      L0.d[s] = d;
+      L0.code[s] = 0;
+      L0.t[s] = 0.0;
+      L0.num[s] = 0.0;
+      L0.den[s] = 0.0;
+      L0.last[s] = -1;
+    } else {
+      atomicAdd(&ctl->overflow, 1ull);
+    }
+  }
+}
+
+// Child of node (t, num, den, last) at level k, digit f: meets_slo's step
+// (dvfs.hpp:111-118) and the time_weighted_power accumulation (167-168).
+// Returns feasibility at level k.
+__device__ __forceinline__ bool child_state(const DTables* __restrict__ T, int k, double t, double num, double den,
+                                            int last, int f, double& ct, double& cn, double& cd) {
+  if (k == 0) {
+    ct = T->T1[f];
+    cn = __dadd_rn(0.0, T->E[0][f]);
+    cd = __dadd_rn(0.0, T->A[0][f]);
+  } else {
+    ct = __dadd_rn(t, f == last ? T->B0[k][f] : T->B1[k][f]);
+    cn = __dadd_rn(num, T->E[k][f]);
+    cd = __dadd_rn(den, T->A[k][f]);
+  }
+  return !(__dsub_rn(ct, T->minarr[k]) > T->ttft);
+}
+
+// Warp-aggregated append of `want` entries (one per lane that wants one);
+// returns this lane's slot.
+__device__ __forceinline__ unsigned long long warp_append(unsigned long long* counter, bool want) {
+  const unsigned mask = __ballot_sync(0xffffffffu, want);
+  if (mask == 0u) return 0;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(mask)));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(mask & ((1u << lane) - 1u));
+}
+
+// Level k: every (depth-k node, digit) pair; feasible children at depth
+// k + 1 go to the next list, or to the final list at their problem's FD.
+__global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl, Frontier in,
+                                                  Frontier out, FinalList fin, int nc_max, unsigned long long cap_out,
+                                                  unsigned long long cap_final) {
+  const unsigned long long n_in = ctl->level_count[k];
+  const unsigned long long total = n_in * static_cast<unsigned long long>(nc_max);
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < total;
+       base += stride) {
+    const unsigned long long j = base + threadIdx.x;
+    bool ok = false, to_final = false;
+    int d = 0, f = 0;
+    double ct = 0.0, cn = 0.0, cd = 0.0;
+    unsigned long long cc = 0;
+    if (j < total) {
+      const unsigned long long node = j / static_cast<unsigned long long>(nc_max);
+      f = static_cast<int>(j - node * nc_max);
+      d = in.d[node];
+      const DTables* __restrict__ T = &tables[d];
+      const int nc = T->nc;
+      if (f < nc) {
+        ok = child_state(T, k, in.t[node], in.num[node], in.den[node], in.last[node], f, ct, cn, cd);
+        cc = in.code[node] * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
+        to_final = (k + 1) == T->K - sweep_levels(T->K, nc);
+      }
+    }
+    const unsigned long long sf = warp_append(&ctl->final_count, ok && to_final);
+    const unsigned long long so = warp_append(&ctl->level_count[k + 1], ok && !to_final);
+    if (ok && to_final) {
+      if (sf < cap_final) {
+        fin.d[sf] = d;
+        fin.code[sf] = cc;
+      } else {
+        atomicAdd(&ctl->overflow, 1ull);
+      }
+    } else if (ok) {
+      if (so < cap_out) {
+        out.d[so] = d;
+        out.code[so] = cc;
+        out.t[so] = ct;
+        out.num[so] = cn;
+        out.den[so] = cd;
+        out.last[so] = f;
+      } else {
+        atomicAdd(&ctl->overflow, 1ull);
+      }
+    }
+  }
+}
+
+// Per-thread accumulator of the sweep.
+struct LeafAcc {
+  double best;               // local minimum objective (+inf: none)
+  unsigned long long code;   // its code
+  double thr_scaled;         // fl(min(local, global hint) * C), +inf disables the filter
+  unsigned long long count;  // feasible leaves
+  // leaf-row skip ("row bound"): a row of leaves under a parent
+  // with (num, den) is provably worse than thr when
+  //   fl(num - fl(beta * den)) > s_last + num * 2^-40,
+  // beta = fl(thr * (1 + 2^-47)), s_last >= amax * (beta - pmin (1 - u))^+.
+  double amax_last;
+  double pmin_lo_last;
+  double beta;
+  double s_last;
+};
+
+__device__ __forceinline__ void set_threshold(LeafAcc& a, double hint) {
+  // hint is NaN while the slot still holds its (~0, ~0) reset value
+  const double thr = (a.best < hint || hint != hint) ? a.best : hint;
+  a.thr_scaled = thr >= kFilterMinBest ? __dmul_rn(thr, kFilterScale) : (thr == 0.0 ? 0.0 : INFINITY);
+  if (thr >= kFilterMinBest && thr < INFINITY) {
+    a.beta = __dmul_rn(thr, 1.0 + 0x1p-47);
+    const double gap = __dsub_rn(a.beta, a.pmin_lo_last);
+    a.s_last = gap > 0.0 ? __dmul_rn(__dmul_rn(gap, a.amax_last), 1.0 + 0x1p-40) : 0.0;
+  } else {
+    a.beta = INFINITY;
+    a.s_last = INFINITY;
+  }
+}
+
+// True when every leaf under a parent with (num, den) is provably worse than
+// the current threshold (requires the filter preconditions: A >= 0, finite,
+// den >= 2^-900).
+__device__ __forceinline__ bool row_dominated(const LeafAcc& a, double num, double den) {
+  return __dsub_rn(num, __dmul_rn(a.beta, den)) > __dadd_rn(a.s_last, __dmul_rn(num, 0x1p-40));
+}
+
+// Last level k = K-1 for one parent state: every f in 0..nc-1, in order.
+__device__ __forceinline__ void sweep_last(const DTables* __restrict__ T, int k, int nc, double t, double num,
+                                           double den, int last, unsigned long long code_base, bool filt,
+                                           double hint, LeafAcc& a) {
+  const double ttft = T->ttft;
+  const double m = T->minarr[k];
+  const double* __restrict__ B0 = T->B0[k];
+  const double* __restrict__ B1 = T->B1[k];
+  const double* __restrict__ E = T->E[k];
+  const double* __restrict__ A = T->A[k];
+#pragma unroll 4
+  for (int f = 0; f < nc; ++f) {
+    double tl;
+    if (k == 0)
+      tl = T->T1[f];
+    else
+      tl = __dadd_rn(t, f == last ? B0[f] : B1[f]);
+    if (__dsub_rn(tl, m) > ttft) continue;  // dvfs.hpp:117
+    a.count += 1;
+    const double nl = __dadd_rn(num, E[f]);
+    const double dl = __dadd_rn(den, A[f]);
+    if (filt && nl > __dmul_rn(a.thr_scaled, dl)) continue;  // provably worse than a known feasible key
+    const double obj = dl > 0.0 ? __ddiv_rn(nl, dl) : 0.0;  // dvfs.hpp:170
+    const unsigned long long code = code_base + static_cast<unsigned long long>(f);
+    if (obj < a.best || (obj == a.best && code < a.code)) {
+      a.best = obj;
+      a.code = code;
+      set_threshold(a, hint);
+    }
+  }
+}
+
+// Number of candidates at level k whose switched step passes meets_slo's
+// check from parent clock t (t unused at level 0, where the keys are T1):
+// by monotonicity of correctly rounded add/subtract in the step, the
+// passing candidates form a prefix of the sorted order ord[k].
+__device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, int k, int nc, double t) {
+  const double m = T->minarr[k], ttft = T->ttft;
+  const double* __restrict__ sb = T->sb[k];
+  int lo = 0, hi = nc;  // first failing position
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const double tl = k == 0 ? sb[mid] : __dadd_rn(t, sb[mid]);
+    if (__dsub_rn(tl, m) > ttft)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+// Calls fn(f, ct, cn, cd) for every child of (t, num, den, last) at level k
+// that passes the check: the sorted prefix (minus f == last, whose real step
+// is the non-switching B0) plus the non-switching child if it passes.
+// Returns the number of passing children.
+template <typename Fn>
+__device__ __forceinline__ int for_feasible_children(const DTables* __restrict__ T, int k, int nc, double t,
+                                                     double num, double den, int last, Fn&& fn) {
+  const int c = feasible_prefix(T, k, nc, t);
+  const unsigned char* __restrict__ ord = T->ord[k];
+  const double* __restrict__ sb = T->sb[k];
+  const double* __restrict__ E = T->E[k];
+  const double* __restrict__ A = T->A[k];
+  int passed = 0;
+  for (int j = 0; j < c; ++j) {
+    const int f = ord[j];
+    if (k > 0 && f == last) continue;
+    const double ct = k == 0 ? sb[j] : __dadd_rn(t, sb[j]);
+    fn(f, ct, __dadd_rn(num, E[f]), __dadd_rn(den, A[f]));
+    ++passed;
+  }
+  if (k > 0) {
+    const double ct = __dadd_rn(t, T->B0[k][last]);
+    if (!(__dsub_rn(ct, T->minarr[k]) > T->ttft)) {
+      fn(last, ct, __dadd_rn(num, E[last]), __dadd_rn(den, A[last]));
+      ++passed;
+    }
+  }
+  return passed;
+}
+
+// Leaves (level k = K-1) under a parent, sorted path: only passing leaves
+// are visited; each needs just its objective.
+__device__ __forceinline__ void leaves_sorted(const DTables* __restrict__ T, int k, int nc, double t, double num,
+                                              double den, int last, unsigned long long code_base, bool filt,
+                                              double hint, LeafAcc& a) {
+  const double m = T->minarr[k], ttft = T->ttft;
+  const double* __restrict__ sb = T->sb[k];
+  const double* __restrict__ E = T->E[k];
+  const double* __restrict__ A = T->A[k];
+  auto leaf = [&](int f, double nl, double dl) {
+    if (filt && nl > __dmul_rn(a.thr_scaled, dl)) return;  // provably worse than a known feasible key
+    const double obj = dl > 0.0 ? __ddiv_rn(nl, dl) : 0.0;  // dvfs.hpp:170
+    const unsigned long long code = code_base + static_cast<unsigned long long>(f);
+    if (obj < a.best || (obj == a.best && code < a.code)) {
+      a.best = obj;
+      a.code = code;
+      set_threshold(a, hint);
+    }
+  };
+  // all switched leaves pass when the largest step does (monotonicity)
+  const double tmax = k == 0 ? sb[nc - 1] : __dadd_rn(t, sb[nc - 1]);
+  if (!(__dsub_rn(tmax, m) > ttft)) {
+    int passed = nc;
+    bool diag = true;
+    if (k > 0) {  // the non-switching leaf f == last is re-tested with its own step
+      const double td = __dadd_rn(t, T->B0[k][last]);
+      diag = !(__dsub_rn(td, m) > ttft);
+      if (!diag) passed -= 1;
+    }
+    a.count += static_cast<unsigned long long>(passed);
+    if (filt && row_dominated(a, num, den)) return;
+#pragma unroll 4
+    for (int f = 0; f < nc; ++f) {
+      if (k > 0 && f == last && !diag) continue;
+      leaf(f, __dadd_rn(num, E[f]), __dadd_rn(den, A[f]));
+    }
+    return;
+  }
+  if (filt && row_dominated(a, num, den)) {  // count only
+    a.count += static_cast<unsigned long long>(
+        for_feasible_children(T, k, nc, t, num, den, last, [&](int, double, double, double) {}));
+    return;
+  }
+  a.count += static_cast<unsigned long long>(
+      for_feasible_children(T, k, nc, t, num, den, last, [&](int f, double, double nl, double dl) { leaf(f, nl, dl); }));
+}
+
+// Two bottom levels below a node at depth K-2, sorted path.
+__device__ __forceinline__ void two_sorted(const DTables* __restrict__ T, int k, int nc, double t, double num,
+                                           double den, int last, unsigned long long code_base, double hint,
+                                           LeafAcc& a) {
+  for_feasible_children(T, k, nc, t, num, den, last, [&](int g, double t2, double n2, double d2) {
+    const bool filt = T->filter_ok && d2 >= kFilterMinDen;
+    leaves_sorted(T, k + 1, nc, t2, n2, d2, g, (code_base + static_cast<unsigned long long>(g)) * nc, filt, hint, a);
+  });
+}
+
+// Two bottom levels (K-2, K-1) below a node at depth K-2.
+__device__ __forceinline__ void sweep_two(const DTables* __restrict__ T, int k, int nc, double t, double num,
+                                          double den, int last, unsigned long long code_base, double hint,
+                                          LeafAcc& a) {
+  for (int g = 0; g < nc; ++g) {
+    double t2, n2, d2;
+    if (!child_state(T, k, t, num, den, last, g, t2, n2, d2)) continue;
+    const bool filt = T->filter_ok && d2 >= kFilterMinDen;
+    sweep_last(T, k + 1, nc, t2, n2, d2, g, (code_base + static_cast<unsigned long long>(g)) * nc, filt, hint, a);
+  }
+}
+
+// State after the first P levels of code (digits MSD first), unchecked (the
+// BFS only emits feasible prefixes).
+__device__ __forceinline__ void walk(const DTables* __restrict__ T, int nc, int P, unsigned long long code,
+                                     double& t, double& num, double& den, int& last) {
+  t = 0.0;
+  num = 0.0;
+  den = 0.0;
+  last = -1;
+  unsigned long long div = ipow(static_cast<unsigned long long>(nc), P > 0 ? P - 1 : 0);
+  for (int k = 0; k < P; ++k) {
+    int f;
+    if (code < (1ull << 32)) {
+      const unsigned q = static_cast<unsigned>(code) / static_cast<unsigned>(div);
+      f = static_cast<int>(q);
+    } else {
+      f = static_cast<int>(code / div);
+    }
+    code -= static_cast<unsigned long long>(f) * div;
+    div /= static_cast<unsigned long long>(nc);
+    double ct, cn, cd;
+    child_state(T, k, t, num, den, last, f, ct, cn, cd);
+    t = ct;
+    num = cn;
+    den = cd;
+    last = f;
+  }
+}
+
+__device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsigned long long* feas) {
+  // warp-level merge when the whole warp holds one problem
+  const unsigned active = __activemask();
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(active) - 1;
+  const int d0 = __shfl_sync(active, d, leader);
+  unsigned long long bo = a.best < INFINITY ? static_cast<unsigned long long>(__double_as_longlong(a.best)) : ~0ull;
+  unsigned long long bc = a.code;
+  unsigned long long c = a.count;
+  if (active == 0xffffffffu && __all_sync(active, d == d0)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      const unsigned long long oo = __shfl_xor_sync(0xffffffffu, bo, o);
+      const unsigned long long oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (key_less(oo, oc, bo, bc)) {
+        bo = oo;
+        bc = oc;
+      }
+    }
+    if (lane == 0) {
+      if (c) atomicAdd(&feas[d0], c);
+      if (bo != ~0ull) atomic_min_key(&best[d0], bo, bc);
+    }
+  } else {
+    if (c) atomicAdd(&feas[d], c);
+    if (bo != ~0ull) atomic_min_key(&best[d], bo, bc);
+  }
+}
+
+// One thread per final node: the I bottom levels of its subtree.
+__global__ void __launch_bounds__(256) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
+                                                    FinalList fin, Key128* best, unsigned long long* feas) {
+  const unsigned long long n_fin = ctl->final_count;
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < n_fin;
+       base += stride) {
+    const unsigned long long j = base + threadIdx.x;
+    if (j >= n_fin) continue;  // only the last round is partial
+    const int d = fin.d[j];
+    const unsigned long long code = fin.code[j];
+    const DTables* __restrict__ T = &tables[d];
+    const int K = T->K, nc = T->nc;
+    const int I = sweep_levels(K, nc);
+    const int FD = K - I;
+    double t, num, den;
+    int last;
+    walk(T, nc, FD, code, t, num, den, last);
+    const double hint = __longlong_as_double(static_cast<long long>(
+        *reinterpret_cast<volatile unsigned long long*>(&best[d].obj)));
+    LeafAcc a;
+    a.best = INFINITY;
+    a.code = ~0ull;
+    a.count = 0;
+    a.amax_last = T->amax[K - 1];
+    a.pmin_lo_last = T->pmin_lo[K - 1];
+    set_threshold(a, hint);
+    const unsigned long long cb = code * static_cast<unsigned long long>(nc);
+    if (I == 1) {  // K == 1
+      sweep_last(T, FD, nc, t, num, den, last, cb, false, hint, a);
+    } else if (T->sorted_ok) {
+      if (I == 2) {
+        two_sorted(T, FD, nc, t, num, den, last, cb, hint, a);
+      } else {
+        for_feasible_children(T, FD, nc, t, num, den, last, [&](int e, double t3, double n3, double d3) {
+          two_sorted(T, FD + 1, nc, t3, n3, d3, e, (cb + static_cast<unsigned long long>(e)) * nc, hint, a);
+        });
+      }
+    } else {
+      // I == 3 adds one more level above the two swept ones
+      const int ne = I == 3 ? nc : 1;
+      for (int e = 0; e < ne; ++e) {
+        double t3 = t, n3 = num, d3 = den;
+        int l3 = last, k2 = FD;
+        unsigned long long cb2 = cb;
+        if (I == 3) {
+          if (!child_state(T, FD, t, num, den, last, e, t3, n3, d3)) continue;
+          l3 = e;
+          k2 = FD + 1;
+          cb2 = (cb + static_cast<unsigned long long>(e)) * nc;
+        }
+        sweep_two(T, k2, nc, t3, n3, d3, l3, cb2, hint, a);
+      }
+    }
+    flush_acc(d, a, best, feas);
+  }
+}

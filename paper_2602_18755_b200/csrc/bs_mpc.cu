@@ -7,17 +7,16 @@
 //   prepare_kernel   1 CTA / problem: project_batches (dvfs.hpp:63-100) by
 //                    one thread, then the K x N (lat, pow) tables by all
 //                    threads through the bit-exact interpolator.
-//   scan_kernel      1 CTA: exclusive scan of per-problem prefix counts,
-//                    reset of argmin slots and counters.
-//   prefix_kernel    grid-stride over every (problem, prefix of depth P):
-//                    walk P levels, drop infeasible prefixes (meets_slo
-//                    returns false at the first violation, so a violated
-//                    prefix has no feasible completion), append survivors.
-//   leaf_kernel      persistent, dynamically scheduled over the survivors:
-//                    each thread sweeps the N^I completions of its prefix
-//                    in increasing code order, with a division-free
-//                    objective filter, and merges its (objective, code)
-//                    minimum through a 128-bit CAS.
+//   seed_kernel      1 thread / problem: reset argmin slots, seed the roots.
+//   bfs_kernel       x (max depth of final nodes): level-synchronous
+//                    expansion of every feasible prefix of every decision,
+//                    compacted with warp-aggregated appends (meets_slo fails
+//                    at the first violated batch, so violated prefixes have
+//                    no feasible completion and are dropped for good).
+//   sweep_kernel     one thread per final node sweeps its bottom 2 (or 3)
+//                    levels in increasing code order with a division-free
+//                    objective filter; (objective, code) minima merge
+//                    through a 128-bit CAS.  See bs_exhaustive.cuh.
 //   finalize_kernel  1 thread / problem: decode the argmin code.
 #include <algorithm>
 #include <cmath>
@@ -30,12 +29,10 @@ using namespace bs;
 namespace {
 
 constexpr int kPrepThreads = 256;
-constexpr int kLeafThreads = 256;
 constexpr int kGreedyThreads = 256;
 constexpr double kFilterScale = 1.0 + 0x1p-50;  // C in the filter bound
 constexpr double kFilterMinBest = 0x1p-100;
 constexpr double kFilterMinDen = 0x1p-900;
-constexpr unsigned long long kItemPrefixBits = 44;
 
 // ---------------------------------------------------------------------------
 // projection: project_batches (dvfs.hpp:63-100) over form_prefill_batch
@@ -126,23 +123,6 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
   return BS_OK;
 }
 
-// Prefix depth of the exhaustive tree: the leaf sweep covers I = K - P
-// levels per thread.
-__host__ __device__ inline int prefix_depth(int K, int nc) {
-  if (K <= 2) return 0;
-  int P = K - 2;
-  double np = 1.0;
-  for (int i = 0; i < P; ++i) np *= nc;
-  if (np > 16777216.0) P = K - 3;
-  return P;
-}
-
-__host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) {
-  unsigned long long r = 1;
-  for (int i = 0; i < e; ++i) r *= b;
-  return r;
-}
-
 // Tables for one problem, written by a CTA.  Projection by thread 0.
 __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
                              const DRunning* R, DTables* T, int* s_status) {
@@ -177,6 +157,33 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     if (k == 0) T->T1[f] = __dadd_rn(pr.now, c.cand[f] != pr.cur_freq ? T->B1[0][f] : T->B0[0][f]);
   }
   __syncthreads();
+  // per-level sorted order of the switched steps: one thread per (k, f)
+  // computes its rank (ties by index), then scatters
+  int finite = 1;
+  for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
+    const int k = e / nc, f = e - k * nc;
+    const double* key = k == 0 ? T->T1 : T->B1[k];
+    const double v = key[f];
+    if (!isfinite(v) || !isfinite(T->B0[k][f])) finite = 0;
+    int r = 0;
+    for (int g = 0; g < nc; ++g) {
+      const double w = key[g];
+      r += (w < v || (w == v && g < f)) ? 1 : 0;
+    }
+    T->sb[k][r] = v;
+    T->ord[k][r] = static_cast<unsigned char>(f);
+    T->rank[k][f] = static_cast<unsigned char>(r);
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double amax = 0.0, pmin = INFINITY;
+    for (int f = 0; f < nc; ++f) {
+      amax = T->A[k][f] > amax ? T->A[k][f] : amax;
+      pmin = T->P[k][f] < pmin ? T->P[k][f] : pmin;
+    }
+    T->amax[k] = amax;
+    T->pmin_lo[k] = __dmul_rn(pmin, 1.0 - 0x1p-50);
+  }
+  const int all_finite = __syncthreads_and(finite);
   if (threadIdx.x == 0) {
     int ok = 1;
     for (int k = 0; k < K; ++k)
@@ -185,316 +192,12 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
         if (!(A >= 0.0) || !isfinite(A) || !isfinite(T->E[k][f])) ok = 0;
       }
     T->filter_ok = ok;
+    T->sorted_ok = all_finite && isfinite(T->ttft);
   }
   __syncthreads();
 }
 
-// ---------------------------------------------------------------------------
-// exhaustive: prepare / scan / prefix / leaf / finalize
-// ---------------------------------------------------------------------------
-struct ExCtl {
-  unsigned long long total_prefixes;
-  unsigned long long work_count;  // survivors appended
-  unsigned long long work_next;   // leaf scheduler cursor
-};
-
-__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
-                                                               const DWaiting* W, const DRunning* R, DTables* tables,
-                                                               unsigned long long* counts, int n) {
-  __shared__ int s_status;
-  const int d = blockIdx.x;
-  if (d >= n) return;
-  const DProblem pr = probs[d];
-  const DMpcCfg& c = cfgs[pr.cfg];
-  DTables* T = &tables[d];
-  build_tables(m, pr, c, W + pr.wait_off, R + pr.run_off, T, &s_status);
-  if (threadIdx.x == 0) {
-    int st = s_status;
-    if (st == BS_OK) {
-      unsigned any = 0;
-      for (int k = 0; k < T->K; ++k) any |= T->bad_lat[k] | T->bad_pow[k];
-      if (any) st = BS_MODEL_ERROR;
-    }
-    T->status = st;
-    unsigned long long np = 0;
-    if (st == BS_OK && T->K > 0) np = ipow(static_cast<unsigned long long>(c.nc), prefix_depth(T->K, c.nc));
-    counts[d] = np;
-  }
-}
-
-// Single CTA: exclusive scan of counts (in place -> offsets), slot reset.
-__global__ void __launch_bounds__(1024) scan_kernel(unsigned long long* counts, int n, Key128* best,
-                                                    unsigned long long* feas, ExCtl* ctl) {
-  __shared__ unsigned long long s_carry;
-  __shared__ unsigned long long s_warp[32];
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    unsigned long long v = i < n ? counts[i] : 0ull;
-    if (i < n) {
-      best[i].obj = ~0ull;
-      best[i].code = ~0ull;
-      feas[i] = 0ull;
-    }
-    // inclusive warp scan
-    unsigned long long x = v;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      unsigned long long w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      s_warp[lane] = w;
-    }
-    __syncthreads();
-    const unsigned long long excl = s_carry + (warp > 0 ? s_warp[warp - 1] : 0ull) + x - v;
-    if (i < n) counts[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    ctl->total_prefixes = s_carry;
-    ctl->work_count = 0;
-    ctl->work_next = 0;
-  }
-}
-
-// State after levels [0, P) of code prefix p (digits MSD first).
-struct PrefixState {
-  double t, num, den;
-  int last;
-  bool ok;
-};
-
-__device__ __forceinline__ PrefixState walk_prefix(const DTables* __restrict__ T, int nc, int P,
-                                                   unsigned long long p, bool check) {
-  PrefixState s;
-  s.t = 0.0;
-  s.num = 0.0;
-  s.den = 0.0;
-  s.last = -1;
-  s.ok = true;
-  unsigned long long div = ipow(static_cast<unsigned long long>(nc), P > 0 ? P - 1 : 0);
-  const double ttft = T->ttft;
-  for (int k = 0; k < P; ++k) {
-    const int f = static_cast<int>(p / div);
-    p -= static_cast<unsigned long long>(f) * div;
-    div /= static_cast<unsigned long long>(nc);
-    if (k == 0) {
-      s.t = T->T1[f];
-    } else {
-      s.t = __dadd_rn(s.t, f == s.last ? T->B0[k][f] : T->B1[k][f]);
-    }
-    s.num = __dadd_rn(s.num, T->E[k][f]);
-    s.den = __dadd_rn(s.den, T->A[k][f]);
-    s.last = f;
-    if (check && __dsub_rn(s.t, T->minarr[k]) > ttft) {
-      s.ok = false;
-      return s;
-    }
-  }
-  return s;
-}
-
-__device__ __forceinline__ int find_problem(const unsigned long long* offsets, int n, unsigned long long idx) {
-  int lo = 0, hi = n - 1;  // last d with offsets[d] <= idx
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (offsets[mid] <= idx)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
-}
-
-__global__ void __launch_bounds__(256) prefix_kernel(const DTables* __restrict__ tables,
-                                                     const unsigned long long* __restrict__ offsets, int n,
-                                                     ExCtl* ctl, unsigned long long* __restrict__ work,
-                                                     unsigned long long capacity) {
-  const unsigned long long total = ctl->total_prefixes;
-  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  const int lane = threadIdx.x & 31;
-  for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < total;
-       base += stride) {
-    const unsigned long long idx = base + threadIdx.x;
-    bool keep = false;
-    unsigned long long item = 0;
-    if (idx < total) {
-      const int d = find_problem(offsets, n, idx);
-      const unsigned long long p = idx - offsets[d];
-      const DTables* T = &tables[d];
-      const int P = prefix_depth(T->K, T->nc);
-      const PrefixState s = walk_prefix(T, T->nc, P, p, true);
-      keep = s.ok;
-      item = (static_cast<unsigned long long>(d) << kItemPrefixBits) | p;
-    }
-    // warp-aggregated append
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (mask == 0u) continue;
-    unsigned long long slot0 = 0;
-    if (lane == __ffs(mask) - 1) slot0 = atomicAdd(&ctl->work_count, static_cast<unsigned long long>(__popc(mask)));
-    slot0 = __shfl_sync(0xffffffffu, slot0, __ffs(mask) - 1);
-    if (keep) {
-      const unsigned long long slot = slot0 + __popc(mask & ((1u << lane) - 1u));
-      if (slot < capacity) work[slot] = item;
-    }
-  }
-}
-
-// Leaf sweep state per thread.
-struct LeafAcc {
-  double best;                // local minimum objective (+inf: none)
-  unsigned long long code;    // its code
-  double thr_scaled;          // fl(min(local, global hint) * C), +inf disables
-  unsigned long long count;   // feasible leaves
-};
-
-__device__ __forceinline__ void set_threshold(LeafAcc& a, double hint) {
-  // hint is NaN while the slot still holds its (~0, ~0) reset value
-  const double thr = (a.best < hint || hint != hint) ? a.best : hint;
-  a.thr_scaled = thr >= kFilterMinBest ? __dmul_rn(thr, kFilterScale) : (thr == 0.0 ? 0.0 : INFINITY);
-}
-
-// Last level (k = K - 1) for one state: sweep f = 0..nc-1.
-__device__ __forceinline__ void sweep_last(const DTables* __restrict__ T, int k, int nc, double t, double num,
-                                           double den, int last, unsigned long long code_base, bool filt,
-                                           double hint, LeafAcc& a) {
-  const double ttft = T->ttft;
-  const double m = T->minarr[k];
-  const double* __restrict__ B0 = T->B0[k];
-  const double* __restrict__ B1 = T->B1[k];
-  const double* __restrict__ E = T->E[k];
-  const double* __restrict__ A = T->A[k];
-#pragma unroll 4
-  for (int f = 0; f < nc; ++f) {
-    double tl;
-    if (k == 0)
-      tl = T->T1[f];
-    else
-      tl = __dadd_rn(t, f == last ? B0[f] : B1[f]);
-    if (__dsub_rn(tl, m) > ttft) continue;  // dvfs.hpp:117
-    a.count += 1;
-    const double nl = __dadd_rn(num, E[f]);
-    const double dl = __dadd_rn(den, A[f]);
-    if (filt && nl > __dmul_rn(a.thr_scaled, dl)) continue;  // provably > current best
-    const double obj = dl > 0.0 ? __ddiv_rn(nl, dl) : 0.0;  // dvfs.hpp:170
-    const unsigned long long code = code_base + static_cast<unsigned long long>(f);
-    if (obj < a.best || (obj == a.best && code < a.code)) {
-      a.best = obj;
-      a.code = code;
-      set_threshold(a, hint);
-    }
-  }
-}
-
-__device__ __forceinline__ void sweep_two(const DTables* __restrict__ T, int k, int nc, double t, double num,
-                                          double den, int last, unsigned long long code_base, double hint,
-                                          LeafAcc& a) {
-  const double ttft = T->ttft;
-  const double m = T->minarr[k];
-  for (int g = 0; g < nc; ++g) {
-    double t2;
-    if (k == 0)
-      t2 = T->T1[g];
-    else
-      t2 = __dadd_rn(t, g == last ? T->B0[k][g] : T->B1[k][g]);
-    if (__dsub_rn(t2, m) > ttft) continue;
-    const double n2 = __dadd_rn(num, T->E[k][g]);
-    const double d2 = __dadd_rn(den, T->A[k][g]);
-    const bool filt = T->filter_ok && d2 >= kFilterMinDen;
-    sweep_last(T, k + 1, nc, t2, n2, d2, g, (code_base + static_cast<unsigned long long>(g)) * nc, filt, hint, a);
-  }
-}
-
-__global__ void __launch_bounds__(kLeafThreads) leaf_kernel(const DTables* __restrict__ tables, ExCtl* ctl,
-                                                            const unsigned long long* __restrict__ work,
-                                                            Key128* best, unsigned long long* feas) {
-  __shared__ unsigned long long s_base;
-  const unsigned long long count = ctl->work_count;
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    if (threadIdx.x == 0) s_base = atomicAdd(&ctl->work_next, static_cast<unsigned long long>(blockDim.x));
-    __syncthreads();
-    const unsigned long long base = s_base;
-    __syncthreads();
-    if (base >= count) break;
-    const unsigned long long wi = base + threadIdx.x;
-    int d = -1;
-    LeafAcc a;
-    a.best = INFINITY;
-    a.code = ~0ull;
-    a.count = 0;
-    if (wi < count) {
-      const unsigned long long item = work[wi];
-      d = static_cast<int>(item >> kItemPrefixBits);
-      const unsigned long long p = item & ((1ull << kItemPrefixBits) - 1ull);
-      const DTables* T = &tables[d];
-      const int K = T->K, nc = T->nc;
-      const int P = prefix_depth(K, nc);
-      const PrefixState s = walk_prefix(T, nc, P, p, false);
-      const double hint = __longlong_as_double(static_cast<long long>(
-          *reinterpret_cast<volatile unsigned long long*>(&best[d].obj)));
-      set_threshold(a, hint);
-      const int I = K - P;
-      if (I == 1) {
-        const bool filt = T->filter_ok && (P == 0 || s.den >= kFilterMinDen);
-        sweep_last(T, P, nc, s.t, s.num, s.den, s.last, p * nc, filt, hint, a);
-      } else if (I == 2) {
-        sweep_two(T, P, nc, s.t, s.num, s.den, s.last, p * nc, hint, a);
-      } else {  // I == 3
-        const double ttft = T->ttft;
-        for (int e = 0; e < nc; ++e) {
-          double t3;
-          if (P == 0)
-            t3 = T->T1[e];
-          else
-            t3 = __dadd_rn(s.t, e == s.last ? T->B0[P][e] : T->B1[P][e]);
-          if (__dsub_rn(t3, T->minarr[P]) > ttft) continue;
-          sweep_two(T, P + 1, nc, t3, __dadd_rn(s.num, T->E[P][e]), __dadd_rn(s.den, T->A[P][e]), e,
-                    (p * nc + static_cast<unsigned long long>(e)) * nc, hint, a);
-        }
-      }
-    }
-    // Merge: warp-level when the whole warp works on one problem.
-    const int d0 = __shfl_sync(0xffffffffu, d, 0);
-    const bool uniform = __all_sync(0xffffffffu, d == d0) && d0 >= 0;
-    if (uniform) {
-      unsigned long long c = a.count;
-      unsigned long long bo = a.best < INFINITY ? static_cast<unsigned long long>(__double_as_longlong(a.best)) : ~0ull;
-      unsigned long long bc = a.code;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-        const unsigned long long oo = __shfl_xor_sync(0xffffffffu, bo, o);
-        const unsigned long long oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (key_less(oo, oc, bo, bc)) {
-          bo = oo;
-          bc = oc;
-        }
-      }
-      if (lane == 0) {
-        if (c) atomicAdd(&feas[d0], c);
-        if (bo != ~0ull) atomic_min_key(&best[d0], bo, bc);
-      }
-    } else if (d >= 0) {
-      if (a.count) atomicAdd(&feas[d], a.count);
-      if (a.best < INFINITY)
-        atomic_min_key(&best[d], static_cast<unsigned long long>(__double_as_longlong(a.best)), a.code);
-    }
-  }
-}
+#include "bs_exhaustive.cuh"
 
 __global__ void finalize_kernel(const DTables* __restrict__ tables, const DMpcCfg* cfgs, const DProblem* probs,
                                 const Key128* best, const unsigned long long* feas, DMpcOut* out, int n) {
@@ -865,7 +568,7 @@ int report_status(bs_ctx_t ctx, const bs_mpc_result* out, int n) {
 }
 
 enum Mode { kExhaustive = 0, kGreedy = 1 };
-constexpr int kNumEvents = 6;
+constexpr int kNumEvents = 6;  // exhaustive phases: prepare, seed, bfs, sweep, finalize
 
 // One batch of MPC decisions resident in HBM: packed problems, scratch, and
 // results.  Used by the one-shot entry points (buffers borrowed from the
@@ -877,30 +580,75 @@ struct MpcRun {
   std::vector<DMpcCfg> hc;          // host copy of configurations
   std::vector<int> cfg_of;          // per-problem configuration index
   std::vector<double> target;       // per-problem target_freq (controller fallback)
-  unsigned long long capacity = 0;  // exhaustive worklist capacity
+  int max_nc = 1;                   // largest candidate count in the batch
+  int bfs_levels = 0;               // deepest final-node depth over the batch
+  unsigned long long cap_level = 0;  // BFS list capacity (per ping-pong buffer)
+  unsigned long long cap_final = 0;  // final list capacity
   DTables* dT = nullptr;
-  unsigned long long* dCounts = nullptr;
   ExCtl* dCtl = nullptr;
   Key128* dBest = nullptr;
   unsigned long long* dFeas = nullptr;
-  unsigned long long* dWork = nullptr;
+  void* dLev[2] = {nullptr, nullptr};
+  void* dFin = nullptr;
   DMpcOut* dOut = nullptr;
   DLevel* dLv = nullptr;
+  int bfs_grid = 0, sweep_grid = 0;
   cudaEvent_t ev[kNumEvents] = {};
   bool have_events = false;
 };
 
+size_t up256(size_t x) { return (x + 255) / 256 * 256; }
 size_t tables_bytes(int n) { return sizeof(DTables) * static_cast<size_t>(n); }
-size_t counts_bytes(int n) { return ((8ull * n + 63) / 64) * 64 + sizeof(ExCtl) + 64; }
 size_t best_bytes(int n) { return (sizeof(Key128) + 8ull) * static_cast<size_t>(n); }
 size_t out_bytes(int n) { return sizeof(DMpcOut) * static_cast<size_t>(n); }
 size_t levels_bytes(int n) { return sizeof(DLevel) * BS_MAX_LEVELS * static_cast<size_t>(n); }
 
-// Packs the problems (one H2D copy) and validates configurations.
+// Device scratch layout of an exhaustive run (offsets from one base).
+struct ExLayout {
+  size_t tables = 0, ctl = 0, best = 0, lev0 = 0, lev1 = 0, fin = 0, out = 0, total = 0;
+};
+
+ExLayout ex_layout(const MpcRun& r, size_t start) {
+  ExLayout L;
+  size_t o = start;
+  L.tables = o;
+  o += up256(tables_bytes(r.n));
+  L.ctl = o;
+  o += up256(sizeof(ExCtl));
+  L.best = o;
+  o += up256(best_bytes(r.n));
+  L.lev0 = o;
+  o += up256(frontier_bytes(r.cap_level));
+  L.lev1 = o;
+  o += up256(frontier_bytes(r.cap_level));
+  L.fin = o;
+  o += up256(final_bytes(r.cap_final));
+  L.out = o;
+  o += up256(out_bytes(r.n));
+  L.total = o;
+  return L;
+}
+
+void bind_exhaustive(MpcRun* r, char* base, const ExLayout& L) {
+  r->dT = reinterpret_cast<DTables*>(base + L.tables);
+  r->dCtl = reinterpret_cast<ExCtl*>(base + L.ctl);
+  r->dBest = reinterpret_cast<Key128*>(base + L.best);
+  r->dFeas = reinterpret_cast<unsigned long long*>(r->dBest + r->n);
+  r->dLev[0] = base + L.lev0;
+  r->dLev[1] = base + L.lev1;
+  r->dFin = base + L.fin;
+  r->dOut = reinterpret_cast<DMpcOut*>(base + L.out);
+}
+
+constexpr size_t kMaxExhaustiveScratch = 24ull << 30;
+
+// Packs the problems (one H2D copy), validates configurations and sizes the
+// exhaustive frontiers from the horizons (K <= horizon_K).
 int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
              const bs_mpc_problem* problems, int n, int mode, MpcRun* run) {
   run->mode = mode;
   run->n = n;
+  if (n > (1 << 24)) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: at most 2^24 problems per call");
   int rc = pack_problems(ctx, cfgs, policies, n_cfgs, problems, n, &run->pk);
   if (rc) return rc;
   run->hc.resize(n_cfgs);
@@ -915,34 +663,45 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
                          run->hc[c].nc, run->hc[c].horizon);
     }
   }
+  run->max_nc = 1;
+  for (const DMpcCfg& c : run->hc) run->max_nc = std::max(run->max_nc, c.nc);
   run->cfg_of.resize(n);
   run->target.resize(n);
-  run->capacity = 0;
+  run->cap_level = 0;
+  run->cap_final = 0;
+  run->bfs_levels = 0;
   for (int i = 0; i < n; ++i) {
     run->cfg_of[i] = problems[i].cfg_index;
     run->target[i] = problems[i].snap.target_freq_mhz;
+    if (mode != kExhaustive) continue;
     const DMpcCfg& c = run->hc[problems[i].cfg_index];
-    if (mode == kExhaustive) run->capacity += ipow(static_cast<unsigned long long>(c.nc), prefix_depth(c.horizon, c.nc));
+    const int FD = c.horizon - sweep_levels(c.horizon, c.nc);
+    run->bfs_levels = std::max(run->bfs_levels, FD);
+    run->cap_final += ipow(static_cast<unsigned long long>(c.nc), FD);
+    run->cap_level += ipow(static_cast<unsigned long long>(c.nc), FD > 0 ? FD - 1 : 0);
   }
-  if (n > (1 << 19)) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: at most 2^19 problems per call");
+  if (mode == kExhaustive) {
+    run->cap_level = std::max<unsigned long long>(run->cap_level, static_cast<unsigned long long>(n));
+    run->cap_final = std::max<unsigned long long>(run->cap_final, static_cast<unsigned long long>(n));
+    const ExLayout L = ex_layout(*run, 0);
+    if (L.total > kMaxExhaustiveScratch)
+      return set_error(ctx, BS_PARAMETER_ERROR,
+                       "mpc exhaustive: batch needs %.1f GB of frontier scratch; split it into smaller calls",
+                       L.total / 1e9);
+  }
   return BS_OK;
-}
-
-void run_bind_exhaustive(MpcRun* run, void* tables, void* counts, void* best, void* work, void* out) {
-  const int n = run->n;
-  run->dT = static_cast<DTables*>(tables);
-  run->dCounts = static_cast<unsigned long long*>(counts);
-  run->dCtl = reinterpret_cast<ExCtl*>(static_cast<char*>(counts) + ((8ull * n + 63) / 64) * 64);
-  run->dBest = static_cast<Key128*>(best);
-  run->dFeas = reinterpret_cast<unsigned long long*>(run->dBest + n);
-  run->dWork = static_cast<unsigned long long*>(work);
-  run->dOut = static_cast<DMpcOut*>(out);
 }
 
 #define BS_REC(i)                                                         \
   do {                                                                    \
     if (timing) BS_CUDA_TRY(ctx, cudaEventRecord(run->ev[i], ctx->stream)); \
   } while (0)
+
+int grid_for(bs_ctx_t ctx, const void* kernel, int threads) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1) b = 1;
+  return ctx->sm_count * b;
+}
 
 // Enqueues the kernels of one run on the context stream (no host sync).
 int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
@@ -961,19 +720,27 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
     BS_REC(1);
     return BS_OK;
   }
+  if (!run->bfs_grid) {
+    run->bfs_grid = grid_for(ctx, reinterpret_cast<const void*>(bfs_kernel), 256);
+    run->sweep_grid = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel), 256);
+  }
+  const Frontier lev[2] = {frontier_at(run->dLev[0], run->cap_level), frontier_at(run->dLev[1], run->cap_level)};
+  const FinalList fin = final_at(run->dFin, run->cap_final);
   prepare_kernel<<<n, kPrepThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
-                                                      run->dT, run->dCounts, n);
+                                                      run->dT, run->dCtl, n);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
-  scan_kernel<<<1, 1024, 0, ctx->stream>>>(run->dCounts, n, run->dBest, run->dFeas, run->dCtl);
+  seed_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, n, run->dBest, run->dFeas, run->dCtl, lev[0], fin,
+                                                        run->cap_level, run->cap_final);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(2);
-  prefix_kernel<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(run->dT, run->dCounts, n, run->dCtl, run->dWork,
-                                                             run->capacity);
-  BS_LAUNCH_CHECK(ctx);
+  for (int k = 0; k < run->bfs_levels; ++k) {
+    bfs_kernel<<<run->bfs_grid, 256, 0, ctx->stream>>>(run->dT, k, run->dCtl, lev[k & 1], lev[(k + 1) & 1], fin,
+                                                       run->max_nc, run->cap_level, run->cap_final);
+    BS_LAUNCH_CHECK(ctx);
+  }
   BS_REC(3);
-  leaf_kernel<<<ctx->sm_count * 8, kLeafThreads, 0, ctx->stream>>>(run->dT, run->dCtl, run->dWork, run->dBest,
-                                                                   run->dFeas);
+  sweep_kernel<<<run->sweep_grid, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest, run->dFeas);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(4);
   finalize_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, pk.cfgs, pk.problems, run->dBest, run->dFeas,
@@ -987,9 +754,11 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
 int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   const int n = run->n;
   if (n == 0) return BS_OK;
-  DMpcOut* hOut = static_cast<DMpcOut*>(ctx->host_buf(kSlotOut, out_bytes(n)));
+  DMpcOut* hOut = static_cast<DMpcOut*>(ctx->host_buf(kSlotOut, out_bytes(n) + 64));
   DLevel* hLv = nullptr;
   if (!hOut) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
+  unsigned long long* hOverflow = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(hOut) + out_bytes(n));
+  *hOverflow = 0;
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut, run->dOut, out_bytes(n), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->last_d2h = out_bytes(n);
   if (run->mode == kGreedy) {
@@ -997,8 +766,14 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
     if (!hLv) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
     BS_CUDA_TRY(ctx, cudaMemcpyAsync(hLv, run->dLv, levels_bytes(n), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->last_d2h += levels_bytes(n);
+  } else {
+    BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOverflow, &run->dCtl->overflow, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->last_d2h += 8;
   }
   BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (*hOverflow)
+    return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: %llu frontier appends overflowed (capacity bug)",
+                     *hOverflow);
   for (int i = 0; i < n; ++i)
     expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
                   run->target[i], &out[i], run->mode == kExhaustive);
@@ -1015,15 +790,10 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
   ctx->last_d2h = 0;
   if (n == 0) return BS_OK;
   if (mode == kExhaustive) {
-    void* t = ctx->dev_buf(kSlotTables, tables_bytes(n));
-    void* c = ctx->dev_buf(kSlotCounts, counts_bytes(n));
-    void* b = ctx->dev_buf(kSlotBest, best_bytes(n));
-    void* w = ctx->dev_buf(kSlotWork, 8ull * run.capacity + 8);
-    void* o = ctx->dev_buf(kSlotOut, out_bytes(n));
-    if (!t || !c || !b || !w || !o)
-      return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: device allocation failed (%llu work items)",
-                       run.capacity);
-    run_bind_exhaustive(&run, t, c, b, w, o);
+    const ExLayout L = ex_layout(run, 0);
+    char* base = static_cast<char*>(ctx->dev_buf(kSlotWork, L.total));
+    if (!base) return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: device allocation of %zu bytes failed", L.total);
+    bind_exhaustive(&run, base, L);
   } else {
     run.dOut = static_cast<DMpcOut*>(ctx->dev_buf(kSlotOut, out_bytes(n)));
     run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n)));
@@ -1099,26 +869,18 @@ int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cf
     delete plan;
     return rc;
   }
-  const size_t a = 256;
-  auto up = [a](size_t x) { return (x + a - 1) / a * a; };
-  const size_t blob = up(run.pk.h2d_bytes);
-  size_t total = blob;
-  size_t o_t = 0, o_c = 0, o_b = 0, o_w = 0, o_o = 0, o_l = 0;
+  const size_t blob = up256(run.pk.h2d_bytes);
+  size_t total = blob, o_o = 0, o_l = 0;
+  ExLayout L;
   if (mode == kExhaustive) {
-    o_t = total;
-    total += up(tables_bytes(n));
-    o_c = total;
-    total += up(counts_bytes(n));
-    o_b = total;
-    total += up(best_bytes(n));
-    o_w = total;
-    total += up(8ull * run.capacity + 8);
+    L = ex_layout(run, blob);
+    total = L.total;
   } else {
     o_l = total;
-    total += up(levels_bytes(n));
+    total += up256(levels_bytes(n));
+    o_o = total;
+    total += up256(out_bytes(n));
   }
-  o_o = total;
-  total += up(out_bytes(n));
   if (cudaMalloc(&plan->mem, total) != cudaSuccess) {
     delete plan;
     return set_error(ctx, BS_CUDA_ERROR, "mpc plan: cudaMalloc(%zu) failed", total);
@@ -1132,7 +894,7 @@ int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cf
   }
   run.pk.rebase(m);
   if (mode == kExhaustive) {
-    run_bind_exhaustive(&run, m + o_t, m + o_c, m + o_b, m + o_w, m + o_o);
+    bind_exhaustive(&run, m, L);
   } else {
     run.dOut = reinterpret_cast<DMpcOut*>(m + o_o);
     run.dLv = reinterpret_cast<DLevel*>(m + o_l);
@@ -1167,7 +929,7 @@ int bs_mpc_plan_kernel_ms(bs_ctx_t ctx, bs_mpc_plan_t plan, float* ms, int n_ms)
 int bs_mpc_plan_info(bs_ctx_t ctx, bs_mpc_plan_t plan, uint64_t* h2d_bytes, uint64_t* work_capacity) {
   if (!ctx || !plan) return set_error(ctx, BS_PARAMETER_ERROR, "bs_mpc_plan_info: null argument");
   if (h2d_bytes) *h2d_bytes = plan->run.pk.h2d_bytes;
-  if (work_capacity) *work_capacity = plan->run.capacity;
+  if (work_capacity) *work_capacity = plan->run.cap_final;
   return BS_OK;
 }
 

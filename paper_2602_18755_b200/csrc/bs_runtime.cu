@@ -480,28 +480,29 @@ int bs_predict(bs_ctx_t ctx, bs_models_t models, int which, const bs_features* f
   if (!ctx || !models) return set_error(ctx, BS_PARAMETER_ERROR, "bs_predict: null context or models");
   if (which < 0 || which > 4) return set_error(ctx, BS_PARAMETER_ERROR, "bs_predict: which must be 0..4");
   if (n <= 0) return BS_OK;
-  const size_t in_bytes = sizeof(bs_features) * n + sizeof(int32_t) * n + sizeof(double) * n;
-  const size_t out_bytes = sizeof(double) * n + sizeof(int32_t) * n + sizeof(uint32_t) * n;
-  char* h = static_cast<char*>(ctx->host_buf(kSlotMisc, in_bytes + out_bytes));
-  char* d = static_cast<char*>(ctx->dev_buf(kSlotMisc, in_bytes + out_bytes));
+  // layout (every section 256-byte aligned): feats | freq | tp || out | status | clamps
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t o_f = 0, o_fr = up(sizeof(bs_features) * n), o_tp = o_fr + up(sizeof(double) * n);
+  const size_t in_bytes = o_tp + up(sizeof(int32_t) * n);
+  const size_t o_out = in_bytes, o_st = o_out + up(sizeof(double) * n), o_cl = o_st + up(sizeof(int32_t) * n);
+  const size_t total = o_cl + up(sizeof(uint32_t) * n);
+  char* h = static_cast<char*>(ctx->host_buf(kSlotMisc, total));
+  char* d = static_cast<char*>(ctx->dev_buf(kSlotMisc, total));
   if (!h || !d) return set_error(ctx, BS_CUDA_ERROR, "bs_predict: allocation failed");
-  std::memcpy(h, feats, sizeof(bs_features) * n);
-  std::memcpy(h + sizeof(bs_features) * n, tp, sizeof(int32_t) * n);
-  std::memcpy(h + sizeof(bs_features) * n + sizeof(int32_t) * n, freq, sizeof(double) * n);
+  std::memcpy(h + o_f, feats, sizeof(bs_features) * n);
+  std::memcpy(h + o_fr, freq, sizeof(double) * n);
+  std::memcpy(h + o_tp, tp, sizeof(int32_t) * n);
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
-  char* dout = d + in_bytes;
   predict_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
-      models->dm, which, reinterpret_cast<const bs_features*>(d),
-      reinterpret_cast<const int32_t*>(d + sizeof(bs_features) * n),
-      reinterpret_cast<const double*>(d + sizeof(bs_features) * n + sizeof(int32_t) * n), n,
-      reinterpret_cast<double*>(dout), reinterpret_cast<int32_t*>(dout + sizeof(double) * n),
-      reinterpret_cast<uint32_t*>(dout + sizeof(double) * n + sizeof(int32_t) * n));
+      models->dm, which, reinterpret_cast<const bs_features*>(d + o_f), reinterpret_cast<const int32_t*>(d + o_tp),
+      reinterpret_cast<const double*>(d + o_fr), n, reinterpret_cast<double*>(d + o_out),
+      reinterpret_cast<int32_t*>(d + o_st), reinterpret_cast<uint32_t*>(d + o_cl));
   BS_LAUNCH_CHECK(ctx);
-  BS_CUDA_TRY(ctx, cudaMemcpyAsync(h + in_bytes, dout, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(h + o_out, d + o_out, total - o_out, cudaMemcpyDeviceToHost, ctx->stream));
   BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  std::memcpy(out, h + in_bytes, sizeof(double) * n);
-  std::memcpy(status, h + in_bytes + sizeof(double) * n, sizeof(int32_t) * n);
-  if (clamp_events) std::memcpy(clamp_events, h + in_bytes + sizeof(double) * n + sizeof(int32_t) * n, sizeof(uint32_t) * n);
+  std::memcpy(out, h + o_out, sizeof(double) * n);
+  std::memcpy(status, h + o_st, sizeof(int32_t) * n);
+  if (clamp_events) std::memcpy(clamp_events, h + o_cl, sizeof(uint32_t) * n);
   for (int i = 0; i < n; ++i)
     if (status[i] != BS_OK) {
       set_error(ctx, status[i], "%s model returned non-positive value or has an unknown axis",

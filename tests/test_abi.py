@@ -76,3 +76,14 @@ def test_kernels_are_sm100a_fp64_without_fma():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "DADD" in sass and "DMUL" in sass
+
+
+def test_pdsim_shim_compiles_against_reference():
+    """include/biscale_gpu_pdsim.hpp compiles against the unmodified reference
+    headers (the C++ drop-in a pdsim maintainer would include)."""
+    import oracle
+    if not (oracle.REFERENCE_ROOT / "proj" / "include").is_dir():
+        pytest.skip("/root/reference absent")
+    res = subprocess.run(["make", "-C", str(oracle.HERE), "replay"], capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert oracle.REPLAY_BIN.exists()

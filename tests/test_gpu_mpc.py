@@ -110,12 +110,17 @@ def test_errors_map_to_reference_exceptions(gpu_device):
     q.waiting[0].remaining_len = 0  # scheduler.hpp:47
     with pytest.raises(P.SimulationError):
         P.greedy_freq_select(q, mpc_config([500.0, 1000.0], 600.0), m, P.SchedulerPolicy())
-    # a latency grid that goes non-positive at the low rung -> ModelError
+    # a latency grid that goes non-positive at the low rung raises ModelError
+    # exactly when the reference's search reaches that rung (dvfs.hpp:230-247)
     neg = dvfs_models()
     neg.latency_prefill.grid.values = [0.0, 0.0, 0.0, 0.0, -1.0, 24576.0, 20480.0, 16384.0]
     with pytest.raises(P.ModelError):
-        P.greedy_freq_select(waiting_snapshot([100], 1000.0), mpc_config([500.0, 750.0, 875.0, 1000.0], 1e6), neg,
+        P.greedy_freq_select(waiting_snapshot([100], 1000.0), mpc_config([500.0, 1000.0], 1e6), neg,
                              P.SchedulerPolicy())
+    # 4 rungs: level 1 settles on 750 and level 2 finds no 875 -> 500 never evaluated
+    g = P.greedy_freq_select(waiting_snapshot([100], 1000.0), mpc_config([500.0, 750.0, 875.0, 1000.0], 1e6), neg,
+                             P.SchedulerPolicy())
+    assert g.assignment.freqs == [750.0]
 
 
 def _instances(seed, n, **kw):

@@ -1,0 +1,31 @@
+"""Drop-in proof at the controller boundary: the reference's own, unmodified
+simulate_cluster (simulator.hpp:758-893) driven by the GPU controllers of
+include/biscale_gpu_pdsim.hpp must produce the same decision log, batch
+records and request records, bit for bit, as with the reference's
+TwoTierFactory (dvfs.hpp:370-390).  The binary is oracle/_ref/replay_parity
+(built where /root/reference exists; it travels with the repo snapshot)."""
+from __future__ import annotations
+
+import json
+import subprocess
+
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("args", [
+    ["--seed", "7", "--duration-s", "60", "--rps", "6"],
+    ["--seed", "11", "--duration-s", "60", "--rps", "10", "--shape", "0.5", "--ttft", "400"],
+    ["--seed", "3", "--duration-s", "40", "--rps", "12", "--prefill", "2", "--decode", "2", "--mpc-n", "5"],
+])
+def test_reference_simulator_with_gpu_controllers(args):
+    if not oracle.REPLAY_BIN.exists():
+        pytest.skip("replay_parity not built (needs /root/reference at build time)")
+    res = subprocess.run([str(oracle.REPLAY_BIN), *args], capture_output=True, text=True, timeout=600)
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["checked"] and line["decisions"] > 100
+    assert line["match"], line
+    assert res.returncode == 0
