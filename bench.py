@@ -245,7 +245,7 @@ def main():
         clocks.start()
         launches0 = dev.kernel_launches()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        leaf_ms, phase_ms = [], []
+        leaf_ms, phase_ms = [], []  # leaf_ms: the sweep kernel (dominant)
         for s in range(args.steps):
             step(evs[s], kernel_times=True)
             ms = (C.c_float * 5)()
@@ -255,7 +255,6 @@ def main():
             flush.zero_()  # untimed L2 flush between timed steps
         torch.cuda.synchronize()
         launches = dev.kernel_launches() - launches0
-        clk = clocks.stop()
         step_ms = [a.elapsed_time(b) for a, b in evs]
         total_ms = sum(step_ms)
         if world > 1:
@@ -277,6 +276,7 @@ def main():
         e2e_times.append(time.perf_counter() - t0)
         lib.bs_ctx_last_transfer(dev.handle, C.byref(h2d), C.byref(d2h))
     e2e_s = statistics.median(e2e_times)
+    clk = clocks.stop()  # sampled across the timed steps and the e2e calls (the device-timed region is ms-short)
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -330,7 +330,7 @@ def main():
                     "matches_resident": bool(same)},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak.value, "traffic": traffic,
-                         "note": "W = 5H+2 = 32 FP64 ops per trajectory (SURVEY §8d) over the subtree kernel's event "
+                         "note": "W = 5H+2 = 32 FP64 ops per trajectory (SURVEY §8d) over the sweep kernel's event "
                                  "time; prefix sharing and infeasible-subtree pruning execute fewer ops, so frac may "
                                  "exceed 1; peak = measured non-FMA DADD issue rate (bs_fp64_peak)"},
             "gpu_launches": int(launches),

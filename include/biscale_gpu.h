@@ -240,6 +240,71 @@ typedef struct bs_decode_result {
   int32_t status;
 } bs_decode_result;
 
+/* Request / Trace (workload.hpp:18-50): requests sorted by arrival. */
+typedef struct bs_request {
+  int64_t id;
+  double arrival_ms;
+  int64_t input_len;
+  int64_t output_len;
+} bs_request;
+
+typedef struct bs_trace {
+  int64_t n;
+  const bs_request* requests;
+  double duration_ms;
+} bs_trace;
+
+/* LengthDistribution (workload.hpp:54-85): an empirical pool (n_samples > 0)
+ * or the lognormal form. */
+typedef struct bs_length_dist {
+  int32_t lognormal;
+  int32_t n_samples;
+  double input_mu;
+  double input_sigma;
+  double output_mu;
+  double output_sigma;
+  const int64_t* sample_input;
+  const int64_t* sample_output;
+} bs_length_dist;
+
+/* SLOSpec (slo.hpp:7-16). */
+typedef struct bs_slo {
+  double ttft_ms;
+  double tpot_ms;
+  double percentile;
+} bs_slo;
+
+/* GoodputSearch (placement.hpp:107-111). */
+typedef struct bs_goodput_search {
+  double tolerance_rps;  /* default 0.25 */
+  int32_t probe_count;   /* default 1 */
+  int32_t _pad;
+  uint64_t seed;         /* default 0x9e3779b97f4a7c15 */
+} bs_goodput_search;
+
+/* InstanceConfig (simulator.hpp:22-31). */
+typedef struct bs_instance_config {
+  int32_t phase;         /* enum bs_phase */
+  int32_t tp;
+  double base_freq_mhz;
+} bs_instance_config;
+
+/* ConfigTableEntry (placement.hpp:25-34).  error_code: 0 none,
+ * BS_MODEL_ERROR (evaluate_candidate's caught ModelError, placement.hpp:233),
+ * -1 "no completed request at R_c" (placement.hpp:231); error holds the
+ * message. */
+typedef struct bs_table_entry {
+  bs_instance_config config;
+  double r_c;
+  double e_c;
+  int32_t has_e_c;
+  int32_t g_c;
+  int32_t saturated;
+  int32_t error_code;
+  int64_t k_star;
+  char error[96];
+} bs_table_entry;
+
 typedef struct bs_ctx_s* bs_ctx_t;
 typedef struct bs_models_s* bs_models_t;
 
@@ -248,6 +313,10 @@ typedef struct bs_models_s* bs_models_t;
 int bs_abi_version(void);
 int bs_ctx_create(int device, bs_ctx_t* out);
 void bs_ctx_destroy(bs_ctx_t ctx);
+/* Message of the last failing call on ctx.  The host-only entry points
+ * (bs_gen_gamma_trace, bs_placement_solve, bs_placement_max_throughput)
+ * accept ctx == NULL; their messages are then read with bs_last_error(NULL)
+ * (per calling thread). */
 const char* bs_last_error(bs_ctx_t ctx);
 /* Device the context runs on and its SM count (for host-side grid sizing). */
 int bs_ctx_info(bs_ctx_t ctx, int* device, int* sm_count);
@@ -340,6 +409,60 @@ int bs_mpc_tables(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfg,
 
 int bs_decode_pick(bs_ctx_t ctx, bs_models_t models, const bs_decode_config* cfgs, int n_cfgs,
                    const bs_decode_query* queries, int n, bs_decode_result* out);
+
+/* --- workload synthesis (host) -------------------------------------------- */
+
+/* gen_gamma_trace (workload.hpp:95-116), bit-identical to the reference's
+ * samplers (rng.hpp).  Writes min(n, capacity) requests (out may be NULL to
+ * count) and the total count in *n_out; BS_PARAMETER_ERROR if capacity is
+ * too small or an argument is invalid. */
+int bs_gen_gamma_trace(double mean_rps, double shape, double duration_ms, const bs_length_dist* lengths,
+                       uint64_t seed, bs_request* out, int64_t capacity, int64_t* n_out);
+
+/* --- coarse-tier placement ----------------------------------------------- */
+
+/* goodput_probe_trace (placement.hpp:145-149) = downsample_trace
+ * (workload.hpp:120-132) with probe_seed(k, replicate): the kept request
+ * indices (increasing) into trace->requests.  kept_idx holds trace->n. */
+int bs_downsample_keep(bs_ctx_t ctx, const bs_trace* trace, const bs_goodput_search* search, int64_t k,
+                       int replicate, int32_t* kept_idx, int64_t* n_kept);
+
+/* build_config_table (placement.hpp:240-260): for every candidate,
+ * max_goodput (154-199) and E_c (217-238).  Candidate order is the
+ * caller's (enumerate_candidates, placement.hpp:535-548, gives phase x tp x
+ * ladder). */
+int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, const bs_slo* slo,
+                     const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                     const bs_instance_config* cands, int n_cand, bs_table_entry* out);
+
+/* simulate_instance (simulator.hpp:667-739) at the instance's fixed
+ * frequency (no controller) + sim_meets_slo (placement.hpp:119-131) +
+ * energy sums, one device thread per trace: n traces share models, config,
+ * policy and SLO.  out[i] = {status, meets_slo, completed, busy_j, idle_j,
+ * horizon_ms}. */
+typedef struct bs_sim_summary {
+  int32_t status;
+  int32_t meets_slo;
+  int64_t completed;
+  double busy_energy_j;
+  double idle_energy_j;
+  double horizon_ms;
+} bs_sim_summary;
+int bs_simulate_instance(bs_ctx_t ctx, bs_models_t models, const bs_trace* traces, int n,
+                         const bs_instance_config* cfg, const bs_scheduler_policy* policy, const bs_slo* slo,
+                         bs_sim_summary* out);
+
+/* solve_placement (placement.hpp:357-416): counts[n] (lexicographically
+ * smallest among equal-cost optima), objective, GPUs used.
+ * BS_INFEASIBLE_ERROR: bs_last_error is "<binding constraint>|<message>". */
+int bs_placement_solve(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target_rps,
+                       double alpha, int64_t* counts, double* objective_w, int32_t* gpus_used);
+
+/* solve_max_throughput (placement.hpp:421-499), the DistServe-style
+ * max-frequency baseline. */
+int bs_placement_max_throughput(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus,
+                                double target_rps, double alpha, double max_freq_mhz, int64_t* counts,
+                                double* objective_w, int32_t* gpus_used);
 
 #ifdef __cplusplus
 }

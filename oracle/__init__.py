@@ -100,6 +100,19 @@ def load_ref() -> C.CDLL:
                                            _P(A.bs_mpc_problem), C.c_int, _P(A.bs_mpc_result), C.c_int]),
             "tables": (C.c_int, [_P(A.bs_model_set), _P(A.bs_mpc_config), _P(A.bs_scheduler_policy),
                                  _P(A.bs_snapshot), _P(C.c_int32), _P(C.c_int32), _dp, _dp, _dp]),
+            "gen_gamma_trace": (C.c_int, [C.c_double, C.c_double, C.c_double, _P(A.bs_length_dist), C.c_uint64,
+                                          _P(A.bs_request), C.c_int64, _P(C.c_int64)]),
+            "downsample_keep": (C.c_int, [_P(A.bs_trace), _P(A.bs_goodput_search), C.c_int64, C.c_int,
+                                          _P(C.c_int32), _P(C.c_int64)]),
+            "config_table": (C.c_int, [_P(A.bs_model_set), _P(A.bs_trace), _P(A.bs_slo), _P(A.bs_scheduler_policy),
+                                       _P(A.bs_goodput_search), _P(A.bs_instance_config), C.c_int,
+                                       _P(A.bs_table_entry)]),
+            "simulate": (C.c_int, [_P(A.bs_model_set), _P(A.bs_trace), C.c_int, _P(A.bs_instance_config),
+                                   _P(A.bs_scheduler_policy), _P(A.bs_slo), _P(A.bs_sim_summary)]),
+            "solve_placement": (C.c_int, [_P(A.bs_table_entry), C.c_int, C.c_int, C.c_double, C.c_double,
+                                          _P(C.c_int64), _dp, _P(C.c_int32)]),
+            "solve_max_throughput": (C.c_int, [_P(A.bs_table_entry), C.c_int, C.c_int, C.c_double, C.c_double,
+                                               C.c_double, _P(C.c_int64), _dp, _P(C.c_int32)]),
         })
         _ref.ref_interpolate.restype = C.c_int
         _ref.ref_interpolate.argtypes = [_P(A.bs_grid), _dp, C.c_int, _dp, _P(C.c_uint32)]

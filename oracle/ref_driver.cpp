@@ -484,3 +484,165 @@ int ref_decode_pick(const bs_model_set* models, const bs_decode_config* cfgs, co
 }
 
 }  // extern "C"
+
+namespace {
+
+Trace to_trace(const bs_trace& t) {
+  Trace out;
+  out.duration_ms = t.duration_ms;
+  for (int64_t i = 0; i < t.n; ++i)
+    out.requests.push_back(Request{t.requests[i].id, t.requests[i].arrival_ms, t.requests[i].input_len,
+                                   t.requests[i].output_len});
+  return out;
+}
+
+GoodputSearch to_search(const bs_goodput_search& s) {
+  GoodputSearch g;
+  g.tolerance_rps = s.tolerance_rps;
+  g.probe_count = s.probe_count;
+  g.seed = s.seed;
+  return g;
+}
+
+SLOSpec to_slo(const bs_slo& s) {
+  SLOSpec o;
+  o.ttft_ms = s.ttft_ms;
+  o.tpot_ms = s.tpot_ms;
+  o.percentile = s.percentile;
+  return o;
+}
+
+std::vector<ConfigTableEntry> to_table(const bs_table_entry* t, int n) {
+  std::vector<ConfigTableEntry> out(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    out[i].config = InstanceConfig{t[i].config.phase == BS_PHASE_PREFILL ? Phase::prefill : Phase::decode,
+                                   t[i].config.tp, t[i].config.base_freq_mhz};
+    out[i].r_c = t[i].r_c;
+    if (t[i].has_e_c) out[i].e_c = t[i].e_c;
+    out[i].g_c = t[i].g_c;
+    out[i].saturated = t[i].saturated != 0;
+    out[i].error = t[i].error_code ? std::string(t[i].error) : std::string();
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_gen_gamma_trace(double mean_rps, double shape, double duration_ms, const bs_length_dist* lengths,
+                        uint64_t seed, bs_request* out, int64_t capacity, int64_t* n_out) {
+  return guarded([&] {
+    LengthDistribution d;
+    if (lengths->n_samples > 0) {
+      for (int i = 0; i < lengths->n_samples; ++i)
+        d.samples.emplace_back(lengths->sample_input[i], lengths->sample_output[i]);
+    } else {
+      d.lognormal = LengthDistribution::Lognormal{lengths->input_mu, lengths->input_sigma, lengths->output_mu,
+                                                  lengths->output_sigma};
+    }
+    Trace t = gen_gamma_trace(mean_rps, shape, duration_ms, d, seed);
+    *n_out = static_cast<int64_t>(t.requests.size());
+    for (std::size_t i = 0; i < t.requests.size() && static_cast<int64_t>(i) < capacity; ++i)
+      if (out) out[i] = bs_request{t.requests[i].id, t.requests[i].arrival_ms, t.requests[i].input_len,
+                                   t.requests[i].output_len};
+  });
+}
+
+int ref_downsample_keep(const bs_trace* trace, const bs_goodput_search* search, int64_t k, int replicate,
+                        int32_t* kept_idx, int64_t* n_kept) {
+  return guarded([&] {
+    Trace base = to_trace(*trace);
+    Trace probe = goodput_probe_trace(base, to_search(*search), k, replicate);
+    std::size_t j = 0;
+    int64_t c = 0;
+    for (const Request& r : probe.requests) {
+      while (j < base.requests.size() && base.requests[j].id != r.id) ++j;
+      kept_idx[c++] = static_cast<int32_t>(j++);
+    }
+    *n_kept = c;
+  });
+}
+
+int ref_config_table(const bs_model_set* models, const bs_trace* trace, const bs_slo* slo,
+                     const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                     const bs_instance_config* cands, int n, bs_table_entry* out) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    std::vector<InstanceConfig> cs;
+    for (int i = 0; i < n; ++i)
+      cs.push_back(InstanceConfig{cands[i].phase == BS_PHASE_PREFILL ? Phase::prefill : Phase::decode, cands[i].tp,
+                                  cands[i].base_freq_mhz});
+    std::vector<ConfigTableEntry> t =
+        build_config_table(cs, to_trace(*trace), to_slo(*slo), m, to_policy(*policy), to_search(*search), true);
+    for (int i = 0; i < n; ++i) {
+      std::memset(&out[i], 0, sizeof(out[i]));
+      out[i].config = cands[i];
+      out[i].r_c = t[i].r_c;
+      out[i].has_e_c = t[i].e_c.has_value() ? 1 : 0;
+      out[i].e_c = t[i].e_c.value_or(0.0);
+      out[i].g_c = t[i].g_c;
+      out[i].saturated = t[i].saturated ? 1 : 0;
+      out[i].k_star = static_cast<int64_t>(std::llround(t[i].r_c / search->tolerance_rps));
+      out[i].error_code = t[i].error.empty() ? 0 : (t[i].error == "no completed request at R_c" ? -1 : BS_MODEL_ERROR);
+      std::snprintf(out[i].error, sizeof(out[i].error), "%s", t[i].error.c_str());
+    }
+  });
+}
+
+int ref_solve_placement(const bs_table_entry* table, int n, int total_gpus, double target_rps, double alpha,
+                        int64_t* counts, double* objective_w, int32_t* gpus_used) {
+  try {
+    PlacementProblem p{to_table(table, n), total_gpus, target_rps, alpha};
+    PlacementPlan plan = solve_placement(p);
+    for (int i = 0; i < n; ++i) counts[i] = plan.counts[i];
+    *objective_w = plan.objective_w;
+    *gpus_used = plan.gpus_used;
+    return BS_OK;
+  } catch (const InfeasibleError& e) {
+    g_err = e.binding_constraint() + "|" + e.what();
+    return BS_INFEASIBLE_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+int ref_solve_max_throughput(const bs_table_entry* table, int n, int total_gpus, double target_rps, double alpha,
+                             double max_freq_mhz, int64_t* counts, double* objective_w, int32_t* gpus_used) {
+  try {
+    PlacementProblem p{to_table(table, n), total_gpus, target_rps, alpha};
+    PlacementPlan plan = solve_max_throughput(p, max_freq_mhz);
+    for (int i = 0; i < n; ++i) counts[i] = plan.counts[i];
+    *objective_w = plan.objective_w;
+    *gpus_used = plan.gpus_used;
+    return BS_OK;
+  } catch (const InfeasibleError& e) {
+    g_err = e.binding_constraint() + "|" + e.what();
+    return BS_INFEASIBLE_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+}  // extern "C"
+
+extern "C" int ref_simulate(const bs_model_set* models, const bs_trace* traces, int n, const bs_instance_config* cfg,
+                            const bs_scheduler_policy* policy, const bs_slo* slo, bs_sim_summary* out) {
+  return guarded([&] {
+    ModelSet m = to_models(*models);
+    InstanceConfig ic{cfg->phase == BS_PHASE_PREFILL ? Phase::prefill : Phase::decode, cfg->tp, cfg->base_freq_mhz};
+    for (int i = 0; i < n; ++i) {
+      std::memset(&out[i], 0, sizeof(out[i]));
+      out[i].status = guarded([&] {
+        SimResult r = simulate_instance(to_trace(traces[i]), ic, to_policy(*policy), m);
+        out[i].meets_slo = sim_meets_slo(r, ic.phase, to_slo(*slo)) ? 1 : 0;
+        out[i].completed = r.completed_requests;
+        out[i].busy_energy_j = r.busy_energy_j();
+        out[i].idle_energy_j = r.idle_energy_j();
+        out[i].horizon_ms = r.horizon_ms;
+      });
+    }
+  });
+}

@@ -33,6 +33,19 @@ int ref_tables(const bs_model_set* models, const bs_mpc_config* cfg, const bs_sc
                double* energy);
 int ref_decode_pick(const bs_model_set* models, const bs_decode_config* cfgs, const bs_decode_query* queries, int n,
                     bs_decode_result* out);
+int ref_gen_gamma_trace(double mean_rps, double shape, double duration_ms, const bs_length_dist* lengths,
+                        uint64_t seed, bs_request* out, int64_t capacity, int64_t* n_out);
+int ref_downsample_keep(const bs_trace* trace, const bs_goodput_search* search, int64_t k, int replicate,
+                        int32_t* kept_idx, int64_t* n_kept);
+int ref_config_table(const bs_model_set* models, const bs_trace* trace, const bs_slo* slo,
+                     const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                     const bs_instance_config* cands, int n, bs_table_entry* out);
+int ref_solve_placement(const bs_table_entry* table, int n, int total_gpus, double target_rps, double alpha,
+                        int64_t* counts, double* objective_w, int32_t* gpus_used);
+int ref_simulate(const bs_model_set* models, const bs_trace* traces, int n, const bs_instance_config* cfg,
+                 const bs_scheduler_policy* policy, const bs_slo* slo, bs_sim_summary* out);
+int ref_solve_max_throughput(const bs_table_entry* table, int n, int total_gpus, double target_rps, double alpha,
+                             double max_freq_mhz, int64_t* counts, double* objective_w, int32_t* gpus_used);
 #ifdef __cplusplus
 }
 #endif

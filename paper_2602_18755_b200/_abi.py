@@ -173,6 +173,58 @@ class bs_decode_result(C.Structure):
     _fields_ = [("freq_mhz", C.c_double), ("eval_count", C.c_int64), ("kv_override", C.c_int32), ("status", C.c_int32)]
 
 
+class bs_request(C.Structure):
+    _fields_ = [("id", C.c_int64), ("arrival_ms", C.c_double), ("input_len", C.c_int64), ("output_len", C.c_int64)]
+
+
+class bs_trace(C.Structure):
+    _fields_ = [("n", C.c_int64), ("requests", C.POINTER(bs_request)), ("duration_ms", C.c_double)]
+
+
+class bs_length_dist(C.Structure):
+    _fields_ = [
+        ("lognormal", C.c_int32),
+        ("n_samples", C.c_int32),
+        ("input_mu", C.c_double),
+        ("input_sigma", C.c_double),
+        ("output_mu", C.c_double),
+        ("output_sigma", C.c_double),
+        ("sample_input", C.POINTER(C.c_int64)),
+        ("sample_output", C.POINTER(C.c_int64)),
+    ]
+
+
+class bs_slo(C.Structure):
+    _fields_ = [("ttft_ms", C.c_double), ("tpot_ms", C.c_double), ("percentile", C.c_double)]
+
+
+class bs_goodput_search(C.Structure):
+    _fields_ = [("tolerance_rps", C.c_double), ("probe_count", C.c_int32), ("_pad", C.c_int32), ("seed", C.c_uint64)]
+
+
+class bs_instance_config(C.Structure):
+    _fields_ = [("phase", C.c_int32), ("tp", C.c_int32), ("base_freq_mhz", C.c_double)]
+
+
+class bs_table_entry(C.Structure):
+    _fields_ = [
+        ("config", bs_instance_config),
+        ("r_c", C.c_double),
+        ("e_c", C.c_double),
+        ("has_e_c", C.c_int32),
+        ("g_c", C.c_int32),
+        ("saturated", C.c_int32),
+        ("error_code", C.c_int32),
+        ("k_star", C.c_int64),
+        ("error", C.c_char * 96),
+    ]
+
+
+class bs_sim_summary(C.Structure):
+    _fields_ = [("status", C.c_int32), ("meets_slo", C.c_int32), ("completed", C.c_int64),
+                ("busy_energy_j", C.c_double), ("idle_energy_j", C.c_double), ("horizon_ms", C.c_double)]
+
+
 ctx_t = C.c_void_p
 models_t = C.c_void_p
 
@@ -214,4 +266,18 @@ PROTOTYPES = [
                                 C.POINTER(bs_mpc_problem), C.POINTER(C.c_int32), C.POINTER(C.c_int32), dp, dp, dp]),
     ("bs_decode_pick", C.c_int, [ctx_t, models_t, C.POINTER(bs_decode_config), C.c_int, C.POINTER(bs_decode_query),
                                  C.c_int, C.POINTER(bs_decode_result)]),
+    ("bs_gen_gamma_trace", C.c_int, [C.c_double, C.c_double, C.c_double, C.POINTER(bs_length_dist), C.c_uint64,
+                                     C.POINTER(bs_request), C.c_int64, C.POINTER(C.c_int64)]),
+    ("bs_downsample_keep", C.c_int, [ctx_t, C.POINTER(bs_trace), C.POINTER(bs_goodput_search), C.c_int64, C.c_int,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    ("bs_goodput_table", C.c_int, [ctx_t, models_t, C.POINTER(bs_trace), C.POINTER(bs_slo),
+                                   C.POINTER(bs_scheduler_policy), C.POINTER(bs_goodput_search),
+                                   C.POINTER(bs_instance_config), C.c_int, C.POINTER(bs_table_entry)]),
+    ("bs_simulate_instance", C.c_int, [ctx_t, models_t, C.POINTER(bs_trace), C.c_int, C.POINTER(bs_instance_config),
+                                       C.POINTER(bs_scheduler_policy), C.POINTER(bs_slo), C.POINTER(bs_sim_summary)]),
+    ("bs_placement_solve", C.c_int, [ctx_t, C.POINTER(bs_table_entry), C.c_int, C.c_int, C.c_double, C.c_double,
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+    ("bs_placement_max_throughput", C.c_int, [ctx_t, C.POINTER(bs_table_entry), C.c_int, C.c_int, C.c_double,
+                                              C.c_double, C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                              C.POINTER(C.c_int32)]),
 ]

@@ -1,0 +1,835 @@
+// bs_placement.cu — coarse-tier placement search on sm_100a:
+// build_config_table (placement.hpp:240-260) = for every candidate,
+// max_goodput (154-199) + E_c (217-238); then solve_placement (357-416) and
+// solve_max_throughput (421-499).
+//
+//   mask_kernel    one warp per probe stream (rate step k, replicate j):
+//                  mt19937_64 seeded with probe_seed(k, j) (a warp-parallel
+//                  twist), keep request i iff uniform01 < min(1, k tol /
+//                  rate) (downsample_trace, workload.hpp:120-132); writes the
+//                  compacted kept-index list.  Streams depend only on (k, j),
+//                  so every candidate shares them.
+//   probe_kernel   one thread per (candidate, k, j): the instance event loop
+//                  at the candidate's fixed frequency (bs_sim.cuh), stopping
+//                  at the first SLO violation when no ModelError can occur
+//                  later in the run (all grid values positive, idle entry
+//                  present); otherwise the full run with exact error order.
+//   host replay    the reference's exact search path over the per-k results
+//                  (k_max, then 1, then lo + (hi - lo) / 2): feasibility is
+//                  not monotone in k (independent down-samples per k), so
+//                  "largest feasible k" would differ.
+//   energy_kernel  one thread per candidate with k* > 0: the full run at
+//                  (k*, replicate 0) -> busy (+ idle for prefill) / completed.
+//   ILP            exact branch and bound (host), reference fold order and
+//                  tie-breaks.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "bs_internal.h"
+#include "bs_rng.cuh"
+#include "bs_sim.cuh"
+
+using namespace bs;
+
+namespace {
+
+constexpr int kMaskWarps = 4;
+
+// --- keep masks ---------------------------------------------------------------
+
+struct MaskParams {
+  long long n;            // base requests
+  int k_max;
+  int reps;
+  double tol;
+  double base_rate;
+  unsigned long long seed;
+};
+
+// One warp per stream s = (k - 1) * reps + j.  The mt19937_64 twist in three
+// dependency phases (indices [0,156), [156,311), 311) so the warp computes it
+// in parallel; outputs are consumed in order, one per request.
+__global__ void __launch_bounds__(kMaskWarps * 32) mask_kernel(MaskParams mp, int* kept, long long* kept_count) {
+  __shared__ unsigned long long st[kMaskWarps][kMtN];
+  __shared__ unsigned long long tmp[kMaskWarps][kMtN];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = blockIdx.x * kMaskWarps + w;
+  if (s >= mp.k_max * mp.reps) return;
+  const long long k = s / mp.reps + 1;
+  const int j = s % mp.reps;
+  // keep = min(1, k * tol / base_rate)  (placement.hpp:146-147)
+  const double kk = __ddiv_rn(__dmul_rn(static_cast<double>(k), mp.tol), mp.base_rate);
+  const double keep = kk < 1.0 ? kk : 1.0;
+  unsigned long long* mt = st[w];
+  unsigned long long* tp = tmp[w];
+  if (lane == 0) {
+    const unsigned long long seed = probe_seed(mp.seed, k, j);
+    mt[0] = seed;
+    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+  }
+  __syncwarp();
+  int* out = kept + static_cast<size_t>(s) * mp.n;
+  long long count = 0;
+  for (long long base = 0; base < mp.n; base += kMtN) {
+    // twist
+    auto f = [&](unsigned long long a, unsigned long long b, unsigned long long c) {
+      const unsigned long long x = (a & kMtUpper) | (b & kMtLower);
+      unsigned long long xa = x >> 1;
+      if (x & 1ull) xa ^= kMtMatrix;
+      return c ^ xa;
+    };
+    for (int i = lane; i < kMtM; i += 32) tp[i] = f(mt[i], mt[i + 1], mt[i + kMtM]);
+    __syncwarp();
+    for (int i = lane; i < kMtM; i += 32) mt[i] = tp[i];
+    __syncwarp();
+    for (int i = kMtM + lane; i < kMtN - 1; i += 32) tp[i] = f(mt[i], mt[i + 1], mt[i - kMtM]);
+    __syncwarp();
+    for (int i = kMtM + lane; i < kMtN - 1; i += 32) mt[i] = tp[i];
+    __syncwarp();
+    if (lane == 0) mt[kMtN - 1] = f(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
+    __syncwarp();
+    // outputs in order, 32 at a time
+    const long long cnt = (mp.n - base) < kMtN ? (mp.n - base) : kMtN;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      bool keepit = false;
+      if (i < cnt) {
+        const double u = static_cast<double>(Mt64::temper(mt[i]) >> 11) * 0x1.0p-53;
+        keepit = u < keep;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, keepit);
+      if (keepit) out[count + __popc(mask & ((1u << lane) - 1u))] = static_cast<int>(base + i);
+      count += __popc(mask);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) kept_count[s] = count;
+}
+
+// --- probes ---------------------------------------------------------------------
+
+struct DCand {
+  int phase;
+  int tp;
+  double freq;
+  int safe;  // no ModelError possible: early exit allowed
+};
+
+struct ProbeOut {
+  int status;
+  int model_err;
+  int meets;
+  int empty;
+};
+
+struct TraceDev {
+  const double* arrival;
+  const long long* input;
+  const long long* output;
+  double duration_ms;
+};
+
+struct PolicyDev {
+  long long max_batch_tokens, max_batch_requests, kv_capacity;
+  int chunking;
+  double ttft, tpot;
+};
+
+__device__ __forceinline__ SimParams make_params(const DCand& c, const PolicyDev& pol, int early) {
+  SimParams p;
+  p.tp = c.tp;
+  p.freq = c.freq;
+  p.max_batch_tokens = pol.max_batch_tokens;
+  p.max_batch_requests = pol.max_batch_requests;
+  p.kv_capacity = pol.kv_capacity;
+  p.chunking = pol.chunking;
+  p.ttft_bound = pol.ttft;
+  p.tpot_bound = pol.tpot;
+  p.early_exit = early;
+  return p;
+}
+
+__global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_cand, int n_streams, long long n_base,
+                             const int* kept, const long long* kept_count, PolicyDev pol, Resident* heaps,
+                             int heap_cap, ProbeOut* out) {
+  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= static_cast<long long>(n_cand) * n_streams) return;
+  const int c = static_cast<int>(gid / n_streams);
+  const int s = static_cast<int>(gid % n_streams);
+  const DCand cd = cands[c];
+  ProbeOut o;
+  o.status = BS_OK;
+  o.model_err = 0;
+  o.meets = 1;
+  o.empty = 0;
+  const long long nk = kept_count[s];
+  if (nk == 0) {  // placement.hpp:169: an empty probe passes
+    o.empty = 1;
+    out[gid] = o;
+    return;
+  }
+  SimTrace st;
+  st.arrival = tr.arrival;
+  st.input = tr.input;
+  st.output = tr.output;
+  st.kept = kept + static_cast<size_t>(s) * n_base;
+  st.n = nk;
+  st.duration_ms = tr.duration_ms;
+  const SimParams p = make_params(cd, pol, cd.safe);
+  const SimOut r = cd.phase == BS_PHASE_PREFILL
+                       ? simulate_prefill(m, st, p)
+                       : simulate_decode(m, st, p, heaps + static_cast<size_t>(gid) * heap_cap, heap_cap);
+  o.status = r.status;
+  o.model_err = r.model_err;
+  o.meets = r.meets_slo;
+  out[gid] = o;
+}
+
+struct EnergyOut {
+  int status;
+  int model_err;
+  long long completed;
+  double busy_j;
+  double idle_j;
+};
+
+__global__ void energy_kernel(DModels m, TraceDev tr, const DCand* cands, const int* cand_stream, int n_cand,
+                              long long n_base, const int* kept, const long long* kept_count, PolicyDev pol,
+                              Resident* heaps, int heap_cap, EnergyOut* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cand) return;
+  const int s = cand_stream[c];
+  EnergyOut o;
+  o.status = BS_OK;
+  o.model_err = 0;
+  o.completed = 0;
+  o.busy_j = 0.0;
+  o.idle_j = 0.0;
+  if (s < 0) {
+    out[c] = o;
+    return;
+  }
+  SimTrace st;
+  st.arrival = tr.arrival;
+  st.input = tr.input;
+  st.output = tr.output;
+  st.kept = kept + static_cast<size_t>(s) * n_base;
+  st.n = kept_count[s];
+  st.duration_ms = tr.duration_ms;
+  const DCand cd = cands[c];
+  const SimParams p = make_params(cd, pol, 0);
+  const SimOut r = cd.phase == BS_PHASE_PREFILL
+                       ? simulate_prefill(m, st, p)
+                       : simulate_decode(m, st, p, heaps + static_cast<size_t>(c) * heap_cap, heap_cap);
+  o.status = r.status;
+  o.model_err = r.model_err;
+  o.completed = r.completed;
+  o.busy_j = r.busy_j;
+  o.idle_j = r.idle_j;
+  out[c] = o;
+}
+
+// Whole-trace simulations (bs_simulate_instance): thread i runs trace i.
+__global__ void sim_kernel(DModels m, const double* arrival, const long long* input, const long long* output,
+                           const int* identity, const long long* meta, const double* durations, int n, DCand cd,
+                           PolicyDev pol, Resident* heaps, int heap_cap, SimOut* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long off = meta[i];
+  SimTrace st;
+  st.arrival = arrival + off;
+  st.input = input + off;
+  st.output = output + off;
+  st.kept = identity;
+  st.n = meta[n + i];
+  st.duration_ms = durations[i];
+  const SimParams p = make_params(cd, pol, 0);
+  out[i] = cd.phase == BS_PHASE_PREFILL ? simulate_prefill(m, st, p)
+                                         : simulate_decode(m, st, p, heaps + static_cast<size_t>(i) * heap_cap, heap_cap);
+}
+
+// --- host helpers ---------------------------------------------------------------
+
+const char* model_err_msg(int kind) {
+  switch (kind) {
+    case 1: return "latency model returned non-positive value";
+    case 2: return "power model returned non-positive value";
+    default: return "idle model: tp not present";
+  }
+}
+
+int validate_trace(bs_ctx_t ctx, const bs_trace& t) {  // Trace::validate (workload.hpp:37-49)
+  double prev = 0.0;
+  for (int64_t i = 0; i < t.n; ++i) {
+    const bs_request& r = t.requests[i];
+    if (r.arrival_ms < 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "trace: negative arrival");
+    if (r.input_len < 1 || r.output_len < 1) return set_error(ctx, BS_PARAMETER_ERROR, "trace: lengths must be >= 1");
+    if (r.arrival_ms < prev) return set_error(ctx, BS_PARAMETER_ERROR, "trace: arrivals not sorted");
+    prev = r.arrival_ms;
+  }
+  if (t.n > 0 && t.duration_ms < t.requests[t.n - 1].arrival_ms)
+    return set_error(ctx, BS_PARAMETER_ERROR, "trace: duration shorter than last arrival");
+  return BS_OK;
+}
+
+
+
+// Replays the reference's binary search (placement.hpp:180-198) over the
+// per-k feasibility outcomes; err_k < 0 until a ModelError is met.
+struct SearchResult {
+  long long k_star = 0;
+  bool saturated = false;
+  int model_err = 0;  // nonzero: the ModelError kind the reference would raise
+};
+
+SearchResult replay_search(long long k_max, const std::function<int(long long)>& outcome) {
+  // outcome(k): 1 feasible, 0 infeasible, -kind ModelError
+  SearchResult r;
+  if (k_max < 1) return r;
+  int f = outcome(k_max);
+  if (f < 0) {
+    r.model_err = -f;
+    return r;
+  }
+  if (f == 1) {
+    r.k_star = k_max;
+    r.saturated = true;
+    return r;
+  }
+  f = outcome(1);
+  if (f < 0) {
+    r.model_err = -f;
+    return r;
+  }
+  if (f == 0) return r;
+  long long lo = 1, hi = k_max;
+  while (hi - lo > 1) {
+    const long long mid = lo + (hi - lo) / 2;
+    f = outcome(mid);
+    if (f < 0) {
+      r.model_err = -f;
+      r.k_star = 0;
+      return r;
+    }
+    if (f == 1)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  r.k_star = lo;
+  return r;
+}
+
+}  // namespace
+
+namespace bs {
+
+// --- ILP (placement.hpp:282-499), exact, host ---------------------------------------
+
+struct IlpEntry {
+  int phase;
+  int g;
+  double r;
+  double e;
+  bool usable;
+};
+
+static bool entry_usable(const bs_table_entry& e) { return e.error_code == 0 && e.r_c > 0.0 && e.has_e_c; }
+
+// SolverCtx::dfs (placement.hpp:297-334), same pruning, fold order, strict <.
+struct SolverCtx {
+  const std::vector<IlpEntry>* t;
+  double need;
+  std::vector<long long> counts, best_counts;
+  double best_cost = INFINITY;
+  bool found = false;
+  std::vector<double> min_e_p, min_e_d, max_rpg_p, max_rpg_d;
+
+  void dfs(size_t i, int gpus_left, double cost, double rp, double rd) {
+    const double def_p = std::max(0.0, need - rp);
+    const double def_d = std::max(0.0, need - rd);
+    if (def_p > 0.0 && min_e_p[i] == INFINITY) return;
+    if (def_d > 0.0 && min_e_d[i] == INFINITY) return;
+    double lb = cost;
+    if (def_p > 0.0) lb += def_p * min_e_p[i];
+    if (def_d > 0.0) lb += def_d * min_e_d[i];
+    if (lb >= best_cost && found) return;
+    double gpus_needed = 0.0;
+    if (def_p > 0.0) gpus_needed += def_p / max_rpg_p[i];
+    if (def_d > 0.0) gpus_needed += def_d / max_rpg_d[i];
+    if (gpus_needed > static_cast<double>(gpus_left) + 1e-9) return;
+    if (i == t->size()) {
+      if (def_p > 1e-9 || def_d > 1e-9) return;
+      if (!found || cost < best_cost) {
+        found = true;
+        best_cost = cost;
+        best_counts = counts;
+      }
+      return;
+    }
+    const IlpEntry& e = (*t)[i];
+    const long long max_n = e.usable ? gpus_left / e.g : 0;
+    const double ec = e.e;
+    for (long long n = 0; n <= max_n; ++n) {
+      counts[i] = n;
+      const double add_r = static_cast<double>(n) * e.r;
+      const double add_cost = static_cast<double>(n) * ec * e.r;
+      dfs(i + 1, gpus_left - static_cast<int>(n) * e.g, cost + add_cost, rp + (e.phase == BS_PHASE_PREFILL ? add_r : 0.0),
+          rd + (e.phase == BS_PHASE_DECODE ? add_r : 0.0));
+    }
+    counts[i] = 0;
+  }
+};
+
+// min_gpus_for_phase (placement.hpp:339-351)
+static int min_gpus_for_phase(const std::vector<IlpEntry>& t, int phase, double need, int budget) {
+  std::vector<double> best(static_cast<size_t>(budget) + 1, 0.0);
+  for (int g = 1; g <= budget; ++g) {
+    double v = 0.0;
+    for (const auto& e : t) {
+      if (e.phase != phase || !e.usable || e.g > g) continue;
+      v = std::max(v, best[static_cast<size_t>(g - e.g)] + e.r);
+    }
+    best[static_cast<size_t>(g)] = std::max(best[static_cast<size_t>(g - 1)], v);
+    if (best[static_cast<size_t>(g)] >= need - 1e-9) return g;
+  }
+  return -1;
+}
+
+static std::string capacity_msg(const std::vector<IlpEntry>& t, double need, int total) {
+  const int gp = min_gpus_for_phase(t, BS_PHASE_PREFILL, need, total);
+  const int gd = min_gpus_for_phase(t, BS_PHASE_DECODE, need, total);
+  auto s = [&](int g) { return g < 0 ? std::string(">" + std::to_string(total)) : std::to_string(g); };
+  return "prefill needs " + s(gp) + " GPUs, decode needs " + s(gd) + ", available " + std::to_string(total);
+}
+
+static int validate_problem(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target,
+                            double alpha) {  // PlacementProblem::validate (placement.hpp:42-51)
+  if (total_gpus < 1) return set_error(ctx, BS_PARAMETER_ERROR, "placement: total_gpus must be >= 1");
+  if (target <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: target_rps must be > 0");
+  if (alpha < 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: alpha must be >= 0");
+  for (int i = 0; i < n; ++i) {
+    const bs_table_entry& e = table[i];
+    if (e.g_c != e.config.tp) return set_error(ctx, BS_PARAMETER_ERROR, "placement: G_c must equal tp");
+    if (e.r_c < 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: R_c must be >= 0");
+    if (e.r_c > 0.0 && e.has_e_c && e.e_c <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: E_c must be > 0");
+  }
+  return BS_OK;
+}
+
+}  // namespace bs
+
+extern "C" {
+
+int bs_downsample_keep(bs_ctx_t ctx, const bs_trace* trace, const bs_goodput_search* search, int64_t k,
+                       int replicate, int32_t* kept_idx, int64_t* n_kept) {
+  if (!ctx || !trace || !search) return set_error(ctx, BS_PARAMETER_ERROR, "bs_downsample_keep: null argument");
+  if (trace->n <= 0) {
+    *n_kept = 0;
+    return BS_OK;
+  }
+  const double base_rate = trace->duration_ms <= 0.0 ? 0.0
+                               : static_cast<double>(trace->n) / (trace->duration_ms / 1000.0);
+  // one stream: k' = k, reps = replicate + 1, take stream (k, replicate) by
+  // running the kernel over [k, k] via k_max = k and reading stream index.
+  MaskParams mp;
+  mp.n = trace->n;
+  mp.k_max = static_cast<int>(k);
+  mp.reps = replicate + 1;
+  mp.tol = search->tolerance_rps;
+  mp.base_rate = base_rate;
+  mp.seed = search->seed;
+  const long long streams = static_cast<long long>(mp.k_max) * mp.reps;
+  int* dk = static_cast<int*>(ctx->dev_buf(kSlotMisc, 4ull * streams * mp.n + 8ull * streams + 256));
+  if (!dk) return set_error(ctx, BS_CUDA_ERROR, "downsample: allocation failed");
+  long long* dc = reinterpret_cast<long long*>(reinterpret_cast<char*>(dk) + ((4ull * streams * mp.n + 255) / 256) * 256);
+  mask_kernel<<<static_cast<unsigned>((streams + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, ctx->stream>>>(
+      mp, dk, dc);
+  BS_LAUNCH_CHECK(ctx);
+  const long long s = (k - 1) * mp.reps + replicate;
+  long long cnt = 0;
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(&cnt, dc + s, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  BS_CUDA_TRY(ctx, cudaMemcpy(kept_idx, dk + s * mp.n, 4ull * cnt, cudaMemcpyDeviceToHost));
+  *n_kept = cnt;
+  return BS_OK;
+}
+
+int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, const bs_slo* slo,
+                     const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                     const bs_instance_config* cands, int n_cand, bs_table_entry* out) {
+  if (!ctx || !models || !base || !slo || !policy || !search || (!cands && n_cand > 0))
+    return set_error(ctx, BS_PARAMETER_ERROR, "bs_goodput_table: null argument");
+  if (n_cand < 1) return set_error(ctx, BS_PARAMETER_ERROR, "config table: no candidates");
+  int rc = validate_trace(ctx, *base);
+  if (rc) return rc;
+  if (slo->ttft_ms <= 0.0 || slo->tpot_ms <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "slo: bounds must be > 0");
+  if (slo->percentile <= 0.0 || slo->percentile > 1.0)
+    return set_error(ctx, BS_PARAMETER_ERROR, "slo: percentile must be in (0,1]");
+  if (search->tolerance_rps <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "goodput: tolerance must be > 0");
+  if (search->probe_count < 1) return set_error(ctx, BS_PARAMETER_ERROR, "goodput: probe_count must be >= 1");
+  for (int c = 0; c < n_cand; ++c) {  // InstanceConfig::validate via InstanceSim (simulator.hpp:27-30)
+    if (cands[c].tp < 1) return set_error(ctx, BS_PARAMETER_ERROR, "instance: tp must be >= 1");
+    if (cands[c].base_freq_mhz <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "instance: base_freq_mhz must be > 0");
+  }
+  if (policy->max_batch_tokens < 1) return set_error(ctx, BS_PARAMETER_ERROR, "scheduler: max_batch_tokens must be >= 1");
+  if (policy->max_batch_requests < 1)
+    return set_error(ctx, BS_PARAMETER_ERROR, "scheduler: max_batch_requests must be >= 1");
+  if (policy->kv_capacity_tokens < 1)
+    return set_error(ctx, BS_PARAMETER_ERROR, "scheduler: kv_capacity_tokens must be >= 1");
+
+  const long long n = base->n;
+  // Trace::mean_rps (workload.hpp:32-35) and k_max (placement.hpp:161-162)
+  const double base_rate = base->duration_ms <= 0.0 ? 0.0 : static_cast<double>(n) / (base->duration_ms / 1000.0);
+  const long long k_max = static_cast<long long>(std::floor(base_rate / search->tolerance_rps));
+  const int reps = search->probe_count;
+  for (int c = 0; c < n_cand; ++c) {
+    std::memset(&out[c], 0, sizeof(bs_table_entry));
+    out[c].config = cands[c];
+    out[c].g_c = cands[c].tp;
+  }
+  ctx->last_h2d = 0;
+  ctx->last_d2h = 0;
+  if (k_max < 1 || n == 0) return BS_OK;  // r_c = 0 everywhere
+
+  // per-candidate safety (no ModelError reachable): grids positive, axes
+  // known, idle entry for tp present with at least one point
+  std::vector<DCand> hc(n_cand);
+  std::vector<int> idle_tp_ok(n_cand, 0);
+  {
+    std::vector<int> ids(models->dm.idle.n_entries), ns(models->dm.idle.n_entries);
+    if (models->dm.idle.n_entries > 0) {
+      BS_CUDA_TRY(ctx, cudaMemcpy(ids.data(), models->dm.idle.tp, 4ull * ids.size(), cudaMemcpyDeviceToHost));
+      BS_CUDA_TRY(ctx, cudaMemcpy(ns.data(), models->dm.idle.n, 4ull * ns.size(), cudaMemcpyDeviceToHost));
+    }
+    for (int c = 0; c < n_cand; ++c) {
+      for (size_t e = 0; e < ids.size(); ++e)
+        if (ids[e] == cands[c].tp) {
+          idle_tp_ok[c] = ns[e] >= 1;
+          break;
+        }
+      const int gl = cands[c].phase == BS_PHASE_PREFILL ? 0 : 1;
+      const int gp = cands[c].phase == BS_PHASE_PREFILL ? 2 : 3;
+      hc[c].phase = cands[c].phase;
+      hc[c].tp = cands[c].tp;
+      hc[c].freq = cands[c].base_freq_mhz;
+      hc[c].safe = models->grid_positive[gl] && models->grid_positive[gp] && !models->dm.grid[gl].bad_axis &&
+                   !models->dm.grid[gp].bad_axis && idle_tp_ok[c];
+    }
+  }
+  // decode scratch: at most min(max_batch_requests, n, kv / min_need) residents
+  long long min_need = INT64_MAX;
+  for (long long i = 0; i < n; ++i)
+    min_need = std::min<long long>(min_need, base->requests[i].input_len + base->requests[i].output_len);
+  long long heap_cap = std::min<long long>(policy->max_batch_requests, n);
+  heap_cap = std::min<long long>(heap_cap, std::max<long long>(1, policy->kv_capacity_tokens / std::max(1LL, min_need)));
+  bool any_decode = false;
+  for (int c = 0; c < n_cand; ++c) any_decode |= cands[c].phase == BS_PHASE_DECODE;
+
+  const long long n_streams = k_max * reps;
+  const long long n_probes = n_streams * n_cand;
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t o_arr = 0, o_in = up(8ull * n), o_out = o_in + up(8ull * n), o_cand = o_out + up(8ull * n);
+  const size_t in_bytes = o_cand + up(sizeof(DCand) * n_cand) + up(4ull * n_cand);
+  const size_t o_kept = in_bytes, o_kc = o_kept + up(4ull * n_streams * n), o_probe = o_kc + up(8ull * n_streams);
+  const size_t o_heap = o_probe + up(sizeof(ProbeOut) * n_probes);
+  const size_t heap_rows = any_decode ? static_cast<size_t>(std::max<long long>(n_probes, n_cand)) : 0;
+  const size_t o_en = o_heap + up(sizeof(Resident) * heap_rows * heap_cap);
+  const size_t total = o_en + up(sizeof(EnergyOut) * n_cand);
+  char* d = static_cast<char*>(ctx->dev_buf(kSlotWork, total));
+  char* h = static_cast<char*>(ctx->host_buf(kSlotWork, in_bytes + sizeof(ProbeOut) * n_probes + sizeof(EnergyOut) * n_cand + 256));
+  if (!d || !h) return set_error(ctx, BS_CUDA_ERROR, "config table: allocation of %zu bytes failed", total);
+  double* ha = reinterpret_cast<double*>(h + o_arr);
+  long long* hi = reinterpret_cast<long long*>(h + o_in);
+  long long* ho = reinterpret_cast<long long*>(h + o_out);
+  for (long long i = 0; i < n; ++i) {
+    ha[i] = base->requests[i].arrival_ms;
+    hi[i] = base->requests[i].input_len;
+    ho[i] = base->requests[i].output_len;
+  }
+  std::memcpy(h + o_cand, hc.data(), sizeof(DCand) * n_cand);
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->last_h2d = in_bytes;
+  TraceDev tr{reinterpret_cast<const double*>(d + o_arr), reinterpret_cast<const long long*>(d + o_in),
+              reinterpret_cast<const long long*>(d + o_out), base->duration_ms};
+  MaskParams mp{n, static_cast<int>(k_max), reps, search->tolerance_rps, base_rate, search->seed};
+  int* dkept = reinterpret_cast<int*>(d + o_kept);
+  long long* dkc = reinterpret_cast<long long*>(d + o_kc);
+  mask_kernel<<<static_cast<unsigned>((n_streams + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, ctx->stream>>>(
+      mp, dkept, dkc);
+  BS_LAUNCH_CHECK(ctx);
+  PolicyDev pol{policy->max_batch_tokens, policy->max_batch_requests, policy->kv_capacity_tokens, policy->chunking,
+                slo->ttft_ms, slo->tpot_ms};
+  ProbeOut* dprobe = reinterpret_cast<ProbeOut*>(d + o_probe);
+  Resident* dheap = reinterpret_cast<Resident*>(d + o_heap);
+  const DCand* dc = reinterpret_cast<const DCand*>(d + o_cand);
+  probe_kernel<<<static_cast<unsigned>((n_probes + 127) / 128), 128, 0, ctx->stream>>>(
+      models->dm, tr, dc, n_cand, static_cast<int>(n_streams), n, dkept, dkc, pol, dheap, static_cast<int>(heap_cap),
+      dprobe);
+  BS_LAUNCH_CHECK(ctx);
+  ProbeOut* hp = reinterpret_cast<ProbeOut*>(h + in_bytes);
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(hp, dprobe, sizeof(ProbeOut) * n_probes, cudaMemcpyDeviceToHost, ctx->stream));
+  BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->last_d2h = sizeof(ProbeOut) * n_probes;
+
+  // replay each candidate's search; feasible(k) = every replicate passes
+  // (empty probes pass, SimulationError fails, ModelError propagates)
+  std::vector<int> cand_stream(n_cand, -1);
+  std::vector<SearchResult> sr(n_cand);
+  for (int c = 0; c < n_cand; ++c) {
+    auto outcome = [&](long long k) -> int {
+      for (int j = 0; j < reps; ++j) {
+        const ProbeOut& p = hp[static_cast<size_t>(c) * n_streams + (k - 1) * reps + j];
+        if (p.empty) continue;
+        if (p.status == BS_MODEL_ERROR) return -p.model_err;
+        if (p.status == BS_PARAMETER_ERROR) return -100;
+        if (p.status != BS_OK || !p.meets) return 0;
+      }
+      return 1;
+    };
+    sr[c] = replay_search(k_max, outcome);
+    if (sr[c].model_err == 100) return set_error(ctx, BS_CUDA_ERROR, "config table: device resident scratch too small");
+    if (sr[c].model_err) {
+      out[c].error_code = BS_MODEL_ERROR;
+      std::snprintf(out[c].error, sizeof out[c].error, "%s", model_err_msg(sr[c].model_err));
+      if (sr[c].model_err == 3)
+        std::snprintf(out[c].error, sizeof out[c].error, "idle model: tp %d not present", cands[c].tp);
+      continue;
+    }
+    out[c].k_star = sr[c].k_star;
+    out[c].r_c = static_cast<double>(sr[c].k_star) * search->tolerance_rps;  // placement.hpp:182, 197
+    out[c].saturated = sr[c].saturated ? 1 : 0;
+    if (out[c].r_c > 0.0) cand_stream[c] = static_cast<int>((sr[c].k_star - 1) * reps + 0);
+  }
+  // E_c at (k*, replicate 0): a full run (placement.hpp:227-231)
+  int* dstream = reinterpret_cast<int*>(d + o_cand + up(sizeof(DCand) * n_cand));
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(dstream, cand_stream.data(), 4ull * n_cand, cudaMemcpyHostToDevice, ctx->stream));
+  EnergyOut* den = reinterpret_cast<EnergyOut*>(d + o_en);
+  energy_kernel<<<(n_cand + 63) / 64, 64, 0, ctx->stream>>>(models->dm, tr, dc, dstream, n_cand, n, dkept, dkc, pol,
+                                                            dheap, static_cast<int>(heap_cap), den);
+  BS_LAUNCH_CHECK(ctx);
+  EnergyOut* he = reinterpret_cast<EnergyOut*>(h + in_bytes + sizeof(ProbeOut) * n_probes);
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(he, den, sizeof(EnergyOut) * n_cand, cudaMemcpyDeviceToHost, ctx->stream));
+  BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->last_d2h += sizeof(EnergyOut) * n_cand;
+  for (int c = 0; c < n_cand; ++c) {
+    if (cand_stream[c] < 0) continue;
+    const EnergyOut& e = he[c];
+    if (e.status == BS_MODEL_ERROR) {
+      out[c].error_code = BS_MODEL_ERROR;
+      out[c].r_c = 0.0;
+      out[c].k_star = 0;
+      if (e.model_err == 3)
+        std::snprintf(out[c].error, sizeof out[c].error, "idle model: tp %d not present", cands[c].tp);
+      else
+        std::snprintf(out[c].error, sizeof out[c].error, "%s", model_err_msg(e.model_err));
+      continue;
+    }
+    if (e.status == BS_SIMULATION_ERROR)  // not caught by evaluate_candidate: propagates
+      return set_error(ctx, BS_SIMULATION_ERROR, "simulation error while measuring E_c");
+    if (e.status != BS_OK) return set_error(ctx, BS_CUDA_ERROR, "config table: device resident scratch too small");
+    // energy_per_request (placement.hpp:205-213)
+    if (e.completed < 1) {
+      out[c].error_code = -1;
+      std::snprintf(out[c].error, sizeof out[c].error, "no completed request at R_c");
+      continue;
+    }
+    double en = e.busy_j;
+    if (cands[c].phase == BS_PHASE_PREFILL) en += e.idle_j;
+    out[c].e_c = en / static_cast<double>(e.completed);
+    out[c].has_e_c = 1;
+  }
+  return BS_OK;
+}
+
+int bs_simulate_instance(bs_ctx_t ctx, bs_models_t models, const bs_trace* traces, int n,
+                         const bs_instance_config* cfg, const bs_scheduler_policy* policy, const bs_slo* slo,
+                         bs_sim_summary* out) {
+  if (!ctx || !models || (!traces && n > 0) || !cfg || !policy || !slo || !out)
+    return set_error(ctx, BS_PARAMETER_ERROR, "bs_simulate_instance: null argument");
+  if (n <= 0) return BS_OK;
+  if (cfg->tp < 1) return set_error(ctx, BS_PARAMETER_ERROR, "instance: tp must be >= 1");
+  if (cfg->base_freq_mhz <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "instance: base_freq_mhz must be > 0");
+  long long total = 0, max_n = 1, min_need = INT64_MAX;
+  for (int i = 0; i < n; ++i) {
+    int rc = validate_trace(ctx, traces[i]);
+    if (rc) return rc;
+    total += traces[i].n;
+    max_n = std::max<long long>(max_n, traces[i].n);
+    for (int64_t r = 0; r < traces[i].n; ++r)
+      min_need = std::min<long long>(min_need, traces[i].requests[r].input_len + traces[i].requests[r].output_len);
+  }
+  long long heap_cap = std::min<long long>(policy->max_batch_requests, max_n);
+  if (min_need != INT64_MAX)
+    heap_cap = std::min<long long>(heap_cap, std::max<long long>(1, policy->kv_capacity_tokens / std::max(1LL, min_need)));
+  heap_cap = std::max<long long>(heap_cap, 1);
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t o_arr = 0, o_in = up(8ull * total + 8), o_out = o_in + up(8ull * total + 8);
+  const size_t o_idx = o_out + up(8ull * total + 8), o_meta = o_idx + up(4ull * max_n);
+  const size_t in_bytes = o_meta + up(sizeof(long long) * 2 * n + sizeof(double) * n);
+  const size_t o_heap = in_bytes, o_res = o_heap + up(sizeof(Resident) * heap_cap * n);
+  const size_t all = o_res + up(sizeof(SimOut) * n);
+  char* d = static_cast<char*>(ctx->dev_buf(kSlotWork, all));
+  char* h = static_cast<char*>(ctx->host_buf(kSlotWork, all));
+  if (!d || !h) return set_error(ctx, BS_CUDA_ERROR, "simulate_instance: allocation failed");
+  double* ha = reinterpret_cast<double*>(h + o_arr);
+  long long* hi = reinterpret_cast<long long*>(h + o_in);
+  long long* ho = reinterpret_cast<long long*>(h + o_out);
+  int* hx = reinterpret_cast<int*>(h + o_idx);
+  long long* hm = reinterpret_cast<long long*>(h + o_meta);  // offsets[n], counts[n]
+  double* hd = reinterpret_cast<double*>(h + o_meta + sizeof(long long) * 2 * n);
+  long long off = 0;
+  for (int i = 0; i < n; ++i) {
+    hm[i] = off;
+    hm[n + i] = traces[i].n;
+    hd[i] = traces[i].duration_ms;
+    for (int64_t r = 0; r < traces[i].n; ++r) {
+      ha[off + r] = traces[i].requests[r].arrival_ms;
+      hi[off + r] = traces[i].requests[r].input_len;
+      ho[off + r] = traces[i].requests[r].output_len;
+    }
+    off += traces[i].n;
+  }
+  for (long long r = 0; r < max_n; ++r) hx[r] = static_cast<int>(r);
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  DCand cd{cfg->phase, cfg->tp, cfg->base_freq_mhz, 0};
+  PolicyDev pol{policy->max_batch_tokens, policy->max_batch_requests, policy->kv_capacity_tokens, policy->chunking,
+                slo->ttft_ms, slo->tpot_ms};
+  sim_kernel<<<(n + 63) / 64, 64, 0, ctx->stream>>>(
+      models->dm, reinterpret_cast<const double*>(d + o_arr), reinterpret_cast<const long long*>(d + o_in),
+      reinterpret_cast<const long long*>(d + o_out), reinterpret_cast<const int*>(d + o_idx),
+      reinterpret_cast<const long long*>(d + o_meta), reinterpret_cast<const double*>(d + o_meta + sizeof(long long) * 2 * n),
+      n, cd, pol, reinterpret_cast<Resident*>(d + o_heap), static_cast<int>(heap_cap),
+      reinterpret_cast<SimOut*>(d + o_res));
+  BS_LAUNCH_CHECK(ctx);
+  const SimOut* hr = reinterpret_cast<const SimOut*>(h + o_res);
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(h + o_res, d + o_res, sizeof(SimOut) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; ++i) {
+    out[i].status = hr[i].status;
+    out[i].meets_slo = hr[i].status == BS_OK ? hr[i].meets_slo : 0;
+    out[i].completed = hr[i].completed;
+    out[i].busy_energy_j = hr[i].busy_j;
+    out[i].idle_energy_j = hr[i].idle_j;
+    out[i].horizon_ms = hr[i].horizon_ms;
+  }
+  return BS_OK;
+}
+
+int bs_placement_solve(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target_rps,
+                       double alpha, int64_t* counts, double* objective_w, int32_t* gpus_used) {
+  if ((!table && n > 0) || !counts) return set_error(ctx, BS_PARAMETER_ERROR, "bs_placement_solve: null argument");
+  int rc = validate_problem(ctx, table, n, total_gpus, target_rps, alpha);
+  if (rc) return rc;
+  std::vector<IlpEntry> t(n);
+  bool has_p = false, has_d = false;
+  for (int i = 0; i < n; ++i) {
+    t[i] = IlpEntry{table[i].config.phase, table[i].g_c, table[i].r_c, table[i].has_e_c ? table[i].e_c : 0.0,
+                    entry_usable(table[i])};
+    if (t[i].usable) (t[i].phase == BS_PHASE_PREFILL ? has_p : has_d) = true;
+  }
+  if (!has_p) return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-prefill|no usable prefill configuration in the table");
+  if (!has_d) return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-decode|no usable decode configuration in the table");
+  SolverCtx s;
+  s.t = &t;
+  s.need = (1.0 + alpha) * target_rps;
+  s.counts.assign(n, 0);
+  s.min_e_p.assign(n + 1, INFINITY);
+  s.min_e_d.assign(n + 1, INFINITY);
+  s.max_rpg_p.assign(n + 1, 0.0);
+  s.max_rpg_d.assign(n + 1, 0.0);
+  for (int i = n; i-- > 0;) {  // placement.hpp:376-390
+    s.min_e_p[i] = s.min_e_p[i + 1];
+    s.min_e_d[i] = s.min_e_d[i + 1];
+    s.max_rpg_p[i] = s.max_rpg_p[i + 1];
+    s.max_rpg_d[i] = s.max_rpg_d[i + 1];
+    if (!t[i].usable) continue;
+    if (t[i].phase == BS_PHASE_PREFILL) {
+      s.min_e_p[i] = std::min(s.min_e_p[i], t[i].e);
+      s.max_rpg_p[i] = std::max(s.max_rpg_p[i], t[i].r / t[i].g);
+    } else {
+      s.min_e_d[i] = std::min(s.min_e_d[i], t[i].e);
+      s.max_rpg_d[i] = std::max(s.max_rpg_d[i], t[i].r / t[i].g);
+    }
+  }
+  s.dfs(0, total_gpus, 0.0, 0.0, 0.0);
+  if (!s.found) return set_error(ctx, BS_INFEASIBLE_ERROR, "capacity|%s", capacity_msg(t, s.need, total_gpus).c_str());
+  int used = 0;
+  for (int i = 0; i < n; ++i) {
+    counts[i] = s.best_counts[i];
+    used += static_cast<int>(s.best_counts[i]) * t[i].g;
+  }
+  if (objective_w) *objective_w = s.best_cost;
+  if (gpus_used) *gpus_used = used;
+  return BS_OK;
+}
+
+int bs_placement_max_throughput(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target_rps,
+                                double alpha, double max_freq_mhz, int64_t* counts, double* objective_w,
+                                int32_t* gpus_used) {
+  if ((!table && n > 0) || !counts)
+    return set_error(ctx, BS_PARAMETER_ERROR, "bs_placement_max_throughput: null argument");
+  int rc = validate_problem(ctx, table, n, total_gpus, target_rps, alpha);
+  if (rc) return rc;
+  std::vector<IlpEntry> t(n);
+  bool has_p = false, has_d = false;
+  for (int i = 0; i < n; ++i) {  // restricted table (placement.hpp:423-430)
+    const bool keep = table[i].config.base_freq_mhz == max_freq_mhz;
+    t[i] = IlpEntry{table[i].config.phase, table[i].g_c, keep ? table[i].r_c : 0.0,
+                    keep && table[i].has_e_c ? table[i].e_c : 0.0, keep && entry_usable(table[i])};
+    if (t[i].usable) (t[i].phase == BS_PHASE_PREFILL ? has_p : has_d) = true;
+  }
+  if (!has_p)
+    return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-prefill|no usable max-frequency prefill configuration");
+  if (!has_d)
+    return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-decode|no usable max-frequency decode configuration");
+  const double need = (1.0 + alpha) * target_rps;
+  std::vector<long long> cur(n, 0), best;
+  bool found = false;
+  double best_score = -1.0;
+  int best_gpus = 0;
+  std::function<void(size_t, int, double, double)> rec = [&](size_t i, int left, double rp, double rd) {
+    if (i == static_cast<size_t>(n)) {  // placement.hpp:448-461
+      if (rp < need - 1e-9 || rd < need - 1e-9) return;
+      const int used = total_gpus - left;
+      if (used <= 0) return;
+      const double score = std::min(rp, rd) / static_cast<double>(used);
+      const bool better = !found || score > best_score + 1e-12 || (std::abs(score - best_score) <= 1e-12 && used < best_gpus);
+      if (better) {
+        found = true;
+        best_score = score;
+        best_gpus = used;
+        best = cur;
+      }
+      return;
+    }
+    const IlpEntry& e = t[i];
+    const long long max_n = e.usable ? left / e.g : 0;
+    for (long long c = 0; c <= max_n; ++c) {
+      cur[i] = c;
+      rec(i + 1, left - static_cast<int>(c) * e.g,
+          rp + (e.phase == BS_PHASE_PREFILL ? static_cast<double>(c) * e.r : 0.0),
+          rd + (e.phase == BS_PHASE_DECODE ? static_cast<double>(c) * e.r : 0.0));
+    }
+    cur[i] = 0;
+  };
+  rec(0, total_gpus, 0.0, 0.0);
+  if (!found) return set_error(ctx, BS_INFEASIBLE_ERROR, "capacity|%s", capacity_msg(t, need, total_gpus).c_str());
+  int used = 0;
+  double obj = 0.0;
+  for (int i = 0; i < n; ++i) {  // placement.hpp:490-495
+    counts[i] = best[i];
+    used += static_cast<int>(best[i]) * t[i].g;
+    if (table[i].config.base_freq_mhz == max_freq_mhz && table[i].has_e_c)
+      obj += static_cast<double>(best[i]) * table[i].e_c * table[i].r_c;
+  }
+  if (objective_w) *objective_w = obj;
+  if (gpus_used) *gpus_used = used;
+  return BS_OK;
+}
+
+}  // extern "C"

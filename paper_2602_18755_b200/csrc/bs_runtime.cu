@@ -55,13 +55,18 @@ bs_ctx_s::~bs_ctx_s() {
 
 namespace bs {
 
+thread_local std::string g_host_err;
+
 int set_error(bs_ctx_t ctx, int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
-  if (ctx) ctx->err = buf;
+  if (ctx)
+    ctx->err = buf;
+  else
+    g_host_err = buf;  // host-only entry points called without a context
   return code;
 }
 
@@ -318,7 +323,7 @@ void bs_ctx_destroy(bs_ctx_t ctx) {
   delete ctx;
 }
 
-const char* bs_last_error(bs_ctx_t ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* bs_last_error(bs_ctx_t ctx) { return ctx ? ctx->err.c_str() : bs::g_host_err.c_str(); }
 
 int bs_ctx_info(bs_ctx_t ctx, int* device, int* sm_count) {
   if (!ctx) return BS_PARAMETER_ERROR;

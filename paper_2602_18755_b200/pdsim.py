@@ -1012,3 +1012,412 @@ class TwoTierFactory:
         ctl = DecodePolicyController(self.decode, self.models, self.device)
         ctl.set_safety_margin(self.decode.margin if self.decode.margin > 0.0 else 0.05)
         return ctl
+
+
+# ---------------------------------------------------------------------------
+# workload.hpp: requests, traces, windows
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Request:
+    id: int = 0
+    arrival_ms: float = 0.0
+    input_len: int = 1
+    output_len: int = 1
+
+
+@dataclass
+class Trace:
+    """workload.hpp:26-50."""
+
+    requests: list = field(default_factory=list)
+    duration_ms: float = 0.0
+    seed: Optional[int] = None
+
+    def duration_s(self) -> float:
+        return self.duration_ms / 1000.0
+
+    def mean_rps(self) -> float:
+        if self.duration_ms <= 0.0:
+            return 0.0
+        return float(len(self.requests)) / self.duration_s()
+
+    def validate(self) -> None:
+        prev = 0.0
+        for r in self.requests:
+            if r.arrival_ms < 0.0:
+                raise ParameterError("trace: negative arrival")
+            if r.input_len < 1 or r.output_len < 1:
+                raise ParameterError("trace: lengths must be >= 1")
+            if r.arrival_ms < prev:
+                raise ParameterError("trace: arrivals not sorted")
+            prev = r.arrival_ms
+        if self.requests and self.duration_ms < self.requests[-1].arrival_ms:
+            raise ParameterError("trace: duration shorter than last arrival")
+
+
+@dataclass
+class Lognormal:
+    input_mu: float = 6.0
+    input_sigma: float = 0.5
+    output_mu: float = 4.5
+    output_sigma: float = 0.5
+
+
+@dataclass
+class LengthDistribution:
+    """workload.hpp:54-85."""
+
+    samples: list = field(default_factory=list)
+    lognormal: Optional[Lognormal] = None
+
+    @staticmethod
+    def fixed(input_len: int, output_len: int) -> "LengthDistribution":
+        return LengthDistribution([(input_len, output_len)])
+
+
+def c_trace(t: Trace, keep: list) -> _abi.bs_trace:
+    n = len(t.requests)
+    arr = (_abi.bs_request * max(1, n))()
+    for i, r in enumerate(t.requests):
+        arr[i].id, arr[i].arrival_ms, arr[i].input_len, arr[i].output_len = r.id, r.arrival_ms, r.input_len, r.output_len
+    keep.append(arr)
+    ct = _abi.bs_trace()
+    ct.n = n
+    ct.requests = C.cast(arr, C.POINTER(_abi.bs_request))
+    ct.duration_ms = t.duration_ms
+    return ct
+
+
+def c_lengths(d: LengthDistribution, keep: list) -> _abi.bs_length_dist:
+    c = _abi.bs_length_dist()
+    if d.samples:
+        ins = (C.c_int64 * len(d.samples))(*[a for a, _ in d.samples])
+        outs = (C.c_int64 * len(d.samples))(*[b for _, b in d.samples])
+        keep += [ins, outs]
+        c.n_samples = len(d.samples)
+        c.sample_input = C.cast(ins, C.POINTER(C.c_int64))
+        c.sample_output = C.cast(outs, C.POINTER(C.c_int64))
+    elif d.lognormal is not None:
+        c.lognormal = 1
+        ln = d.lognormal
+        c.input_mu, c.input_sigma, c.output_mu, c.output_sigma = ln.input_mu, ln.input_sigma, ln.output_mu, ln.output_sigma
+    else:
+        raise ParameterError("length distribution: no samples and no parametric form")
+    return c
+
+
+def gen_gamma_trace(mean_rps: float, shape: float, duration_ms: float, lengths: LengthDistribution,
+                    seed: int) -> Trace:
+    """gen_gamma_trace (workload.hpp:95-116): native host synthesis with the
+    reference's own samplers (bit-identical)."""
+    if mean_rps <= 0.0:
+        raise ParameterError("gen_gamma_trace: mean_rps must be > 0")
+    if shape <= 0.0:
+        raise ParameterError("gen_gamma_trace: shape must be > 0")
+    if duration_ms <= 0.0:
+        raise ParameterError("gen_gamma_trace: duration_ms must be > 0")
+    L = lib()
+    keep: list = []
+    cl = c_lengths(lengths, keep)
+    n = C.c_int64()
+    rc = L.bs_gen_gamma_trace(mean_rps, shape, duration_ms, C.byref(cl), seed, None, 0, C.byref(n))
+    raise_status(rc, "gen_gamma_trace failed")
+    out = (_abi.bs_request * max(1, n.value))()
+    rc = L.bs_gen_gamma_trace(mean_rps, shape, duration_ms, C.byref(cl), seed, out, n.value, C.byref(n))
+    raise_status(rc, "gen_gamma_trace failed")
+    return Trace([Request(out[i].id, out[i].arrival_ms, out[i].input_len, out[i].output_len) for i in range(n.value)],
+                 duration_ms, seed)
+
+
+def split_windows(t: Trace, window_ms: float) -> list:
+    """split_windows (workload.hpp:184-201)."""
+    if window_ms <= 0.0:
+        raise ParameterError("split_windows: window_ms must be > 0")
+    n = max(1, int(math.ceil(t.duration_ms / window_ms)))
+    wins = [Trace([], min(window_ms, t.duration_ms - float(i) * window_ms), t.seed) for i in range(n)]
+    for r in t.requests:
+        idx = int(r.arrival_ms / window_ms)
+        if idx >= n:
+            idx = n - 1
+        wins[idx].requests.append(Request(r.id, r.arrival_ms - float(idx) * window_ms, r.input_len, r.output_len))
+    return wins
+
+
+def predict_next_window(history: Trace) -> Trace:
+    """predict_next_window (workload.hpp:205-208): identity."""
+    if not history.requests:
+        raise ParameterError("predict_next_window: empty history")
+    return history
+
+
+# ---------------------------------------------------------------------------
+# placement.hpp: config table, goodput search, ILP, window planning
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class InstanceConfig:
+    phase: Phase = Phase.prefill
+    tp: int = 1
+    base_freq_mhz: float = 0.0
+
+
+@dataclass
+class ConfigTableEntry:
+    """placement.hpp:25-34."""
+
+    config: InstanceConfig = field(default_factory=InstanceConfig)
+    r_c: float = 0.0
+    e_c: Optional[float] = None
+    g_c: int = 0
+    saturated: bool = False
+    error: str = ""
+    k_star: int = 0
+
+    def usable(self) -> bool:
+        return not self.error and self.r_c > 0.0 and self.e_c is not None
+
+
+@dataclass
+class GoodputSearch:
+    tolerance_rps: float = 0.25
+    probe_count: int = 1
+    seed: int = 0x9e3779b97f4a7c15
+
+
+@dataclass
+class GoodputResult:
+    r_c: float = 0.0
+    k_star: int = 0
+    saturated: bool = False
+
+
+@dataclass
+class ClusterInstance:
+    config: InstanceConfig = field(default_factory=InstanceConfig)
+    weight: float = 0.0
+
+
+@dataclass
+class PlacementProblem:
+    table: list = field(default_factory=list)
+    total_gpus: int = 0
+    target_rps: float = 0.0
+    alpha: float = 0.05
+
+
+@dataclass
+class PlacementPlan:
+    counts: list = field(default_factory=list)
+    table: list = field(default_factory=list)
+    objective_w: float = 0.0
+    target_rps: float = 0.0
+    alpha: float = 0.0
+    total_gpus: int = 0
+    gpus_used: int = 0
+    instances: list = field(default_factory=list)
+
+
+def c_slo(s: SLOSpec) -> _abi.bs_slo:
+    c = _abi.bs_slo()
+    c.ttft_ms, c.tpot_ms, c.percentile = s.ttft_ms, s.tpot_ms, s.percentile
+    return c
+
+
+def c_search(s: GoodputSearch) -> _abi.bs_goodput_search:
+    c = _abi.bs_goodput_search()
+    c.tolerance_rps, c.probe_count, c.seed = s.tolerance_rps, s.probe_count, s.seed
+    return c
+
+
+def c_candidates(cands) -> C.Array:
+    arr = (_abi.bs_instance_config * max(1, len(cands)))()
+    for i, c in enumerate(cands):
+        arr[i].phase, arr[i].tp, arr[i].base_freq_mhz = int(c.phase), c.tp, c.base_freq_mhz
+    return arr
+
+
+def entry_from_c(e: _abi.bs_table_entry) -> ConfigTableEntry:
+    return ConfigTableEntry(InstanceConfig(Phase(e.config.phase), e.config.tp, e.config.base_freq_mhz), e.r_c,
+                            e.e_c if e.has_e_c else None, e.g_c, bool(e.saturated),
+                            e.error.decode() if e.error_code else "", e.k_star)
+
+
+def c_table(table) -> C.Array:
+    arr = (_abi.bs_table_entry * max(1, len(table)))()
+    for i, e in enumerate(table):
+        arr[i].config.phase, arr[i].config.tp, arr[i].config.base_freq_mhz = int(e.config.phase), e.config.tp, \
+            e.config.base_freq_mhz
+        arr[i].r_c = e.r_c
+        arr[i].has_e_c = 1 if e.e_c is not None else 0
+        arr[i].e_c = e.e_c if e.e_c is not None else 0.0
+        arr[i].g_c = e.g_c
+        arr[i].saturated = 1 if e.saturated else 0
+        arr[i].error_code = 2 if e.error else 0
+        arr[i].error = e.error.encode()[:95]
+        arr[i].k_star = e.k_star
+    return arr
+
+
+def enumerate_candidates(ladder: FrequencyLadder, tp_options) -> list:
+    """enumerate_candidates (placement.hpp:535-548): phase x tp x ladder."""
+    ladder.validate()
+    if not tp_options:
+        raise ParameterError("candidates: tp_options empty")
+    return [InstanceConfig(ph, tp, f) for ph in (Phase.prefill, Phase.decode) for tp in tp_options
+            for f in ladder.freqs_mhz]
+
+
+def build_config_table(candidates, base: Trace, slo: SLOSpec, models: ModelSet, policy: SchedulerPolicy,
+                       search: GoodputSearch, parallel: bool = True, device: Device | None = None) -> list:
+    """build_config_table (placement.hpp:240-260) on the GPU: every candidate's
+    goodput probes in one grid, then the E_c runs."""
+    if not candidates:
+        raise ParameterError("config table: no candidates")
+    dev = device or default_device()
+    keep: list = []
+    ct = c_trace(base, keep)
+    cs, cp, cg = c_slo(slo), c_policy(policy), c_search(search)
+    cands = c_candidates(candidates)
+    out = (_abi.bs_table_entry * len(candidates))()
+    dev.check(dev._lib.bs_goodput_table(dev.handle, dev.models(models), C.byref(ct), C.byref(cs), C.byref(cp),
+                                        C.byref(cg), cands, len(candidates), out))
+    return [entry_from_c(out[i]) for i in range(len(candidates))]
+
+
+def evaluate_candidate(cfg: InstanceConfig, base: Trace, slo: SLOSpec, models: ModelSet, policy: SchedulerPolicy,
+                       search: GoodputSearch, device: Device | None = None) -> ConfigTableEntry:
+    """evaluate_candidate (placement.hpp:217-238)."""
+    return build_config_table([cfg], base, slo, models, policy, search, device=device)[0]
+
+
+def max_goodput(cfg: InstanceConfig, base: Trace, slo: SLOSpec, models: ModelSet, policy: SchedulerPolicy,
+                search: GoodputSearch, device: Device | None = None) -> GoodputResult:
+    """max_goodput (placement.hpp:154-199); ModelError propagates."""
+    e = evaluate_candidate(cfg, base, slo, models, policy, search, device)
+    if e.error and e.error != "no completed request at R_c":
+        raise ModelError(e.error)
+    return GoodputResult(e.r_c, e.k_star, e.saturated)
+
+
+def downsample_keep(base: Trace, search: GoodputSearch, k: int, replicate: int = 0,
+                    device: Device | None = None) -> list:
+    """Indices kept by goodput_probe_trace (placement.hpp:145-149) on the GPU."""
+    dev = device or default_device()
+    keep: list = []
+    ct = c_trace(base, keep)
+    cg = c_search(search)
+    idx = (C.c_int32 * max(1, len(base.requests)))()
+    n = C.c_int64()
+    dev.check(dev._lib.bs_downsample_keep(dev.handle, C.byref(ct), C.byref(cg), k, replicate, idx, C.byref(n)))
+    return list(idx[:n.value])
+
+
+def goodput_probe_trace(base: Trace, search: GoodputSearch, k: int, replicate: int = 0,
+                        device: Device | None = None) -> Trace:
+    idx = downsample_keep(base, search, k, replicate, device)
+    return Trace([base.requests[i] for i in idx], base.duration_ms, None)
+
+
+def derive_routing_weights(counts, table) -> list:
+    """derive_routing_weights (placement.hpp:264-280)."""
+    if len(counts) != len(table):
+        raise ParameterError("weights: count/table size mismatch")
+    phase_r = [0.0, 0.0]
+    for n, e in zip(counts, table):
+        phase_r[0 if e.config.phase == Phase.prefill else 1] += float(n) * e.r_c
+    out = []
+    for n, e in zip(counts, table):
+        p = 0 if e.config.phase == Phase.prefill else 1
+        for _ in range(n):
+            out.append(ClusterInstance(e.config, e.r_c / phase_r[p]))
+    return out
+
+
+def _solve(fn_name: str, p: PlacementProblem, extra: tuple, device: Device | None) -> PlacementPlan:
+    dev = device or default_device()
+    n = len(p.table)
+    tab = c_table(p.table)
+    counts = (C.c_int64 * max(1, n))()
+    obj = C.c_double()
+    used = C.c_int32()
+    rc = getattr(dev._lib, fn_name)(dev.handle, tab, n, p.total_gpus, p.target_rps, p.alpha, *extra, counts,
+                                    C.byref(obj), C.byref(used))
+    if rc != _abi.BS_OK:
+        raise_status(rc, dev.error())
+    plan = PlacementPlan(list(counts[:n]), list(p.table), obj.value, p.target_rps, p.alpha, p.total_gpus, used.value)
+    if fn_name == "bs_placement_max_throughput":
+        # the baseline plan carries the restricted table (placement.hpp:423-430, 486)
+        restricted = []
+        for e in p.table:
+            if e.config.base_freq_mhz != extra[0]:
+                e = ConfigTableEntry(e.config, 0.0, None, e.g_c, e.saturated, "below maximum frequency", e.k_star)
+            restricted.append(e)
+        plan.table = restricted
+    plan.instances = derive_routing_weights(plan.counts, plan.table)
+    return plan
+
+
+def solve_placement(p: PlacementProblem, device: Device | None = None) -> PlacementPlan:
+    """solve_placement (placement.hpp:357-416): exact branch and bound."""
+    return _solve("bs_placement_solve", p, (), device)
+
+
+def solve_max_throughput(p: PlacementProblem, max_freq_mhz: float, device: Device | None = None) -> PlacementPlan:
+    """solve_max_throughput (placement.hpp:421-499)."""
+    return _solve("bs_placement_max_throughput", p, (max_freq_mhz,), device)
+
+
+@dataclass
+class PlanOptions:
+    alpha: float = 0.05
+    peak_subwindow_s: float = 10.0
+    search: GoodputSearch = field(default_factory=GoodputSearch)
+    policy: SchedulerPolicy = field(default_factory=SchedulerPolicy)
+    probe_trace: Optional[Trace] = None
+    parallel_table: bool = True
+
+
+@dataclass
+class WindowPlanResult:
+    plan: PlacementPlan = field(default_factory=PlacementPlan)
+    predicted_peak_rps: float = 0.0
+    table: list = field(default_factory=list)
+
+
+def peak_rps(t: Trace, subwindow_s: float) -> float:
+    """peak_rps (placement.hpp:513-527)."""
+    if not t.requests:
+        raise ParameterError("peak_rps: empty trace")
+    if subwindow_s <= 0.0:
+        raise ParameterError("peak_rps: subwindow must be > 0")
+    w_ms = subwindow_s * 1000.0
+    n_windows = int(t.duration_ms / w_ms)
+    if n_windows < 1:
+        return t.mean_rps()
+    counts = [0] * n_windows
+    for r in t.requests:
+        idx = int(r.arrival_ms / w_ms)
+        if idx >= n_windows:
+            continue
+        counts[idx] += 1
+    return float(max(counts)) / subwindow_s
+
+
+def plan_window(history: Trace, total_gpus: int, slo: SLOSpec, models: ModelSet, ladder: FrequencyLadder,
+                tp_options, opts: PlanOptions | None = None, device: Device | None = None) -> WindowPlanResult:
+    """plan_window (placement.hpp:558-582) without the table cache file."""
+    opts = opts or PlanOptions()
+    history.validate()
+    if not history.requests:
+        raise ParameterError("plan_window: empty history")
+    predicted = predict_next_window(history)
+    res = WindowPlanResult()
+    res.predicted_peak_rps = peak_rps(predicted, opts.peak_subwindow_s)
+    probe = opts.probe_trace if opts.probe_trace is not None else predicted
+    candidates = enumerate_candidates(ladder, tp_options)
+    res.table = build_config_table(candidates, probe, slo, models, opts.policy, opts.search, opts.parallel_table, device)
+    res.plan = solve_placement(PlacementProblem(res.table, total_gpus, res.predicted_peak_rps, opts.alpha), device)
+    return res
