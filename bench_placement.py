@@ -50,6 +50,10 @@ def main():
         table = P.build_config_table(cands, base, slo, models, pol, search, device=dev)
         times.append(time.perf_counter() - t0)
     t_table = min(times)
+    st = (C.c_double * 8)()
+    dev._lib.bs_ctx_stats(dev.handle, st, 8)
+    stats = {"mask_ms": st[0], "probe_ms": st[1], "energy_ms": st[2], "max_events_per_probe": st[3],
+             "total_events": st[4]}
     t0 = time.perf_counter()
     plan = P.solve_placement(P.PlacementProblem(table, 16, P.peak_rps(base, 10.0), 0.05), dev)
     t_ilp = time.perf_counter() - t0
@@ -58,7 +62,7 @@ def main():
             "requests": len(base.requests), "candidates": len(cands), "k_max": k_max,
             "probes": k_max * len(cands), "table_s": t_table, "configs_per_s": len(cands) / t_table,
             "probes_per_s": k_max * len(cands) / t_table, "ilp_s": t_ilp, "usable": sum(e.usable() for e in table),
-            "gpus_used": plan.gpus_used, "objective_w": plan.objective_w}
+            "gpus_used": plan.gpus_used, "objective_w": plan.objective_w, "phases": stats}
     if not args.no_cpu:
         import oracle
         from paper_2602_18755_b200 import _abi as A

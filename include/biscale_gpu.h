@@ -324,6 +324,10 @@ int bs_ctx_info(bs_ctx_t ctx, int* device, int* sm_count);
 int bs_ctx_sync(bs_ctx_t ctx);
 /* Number of kernels the context launched since creation (instrumentation). */
 int64_t bs_ctx_kernel_launches(bs_ctx_t ctx);
+/* Instrumentation of the last call that records it (bs_goodput_table:
+ * {mask ms, probe ms, energy ms, max events per probe, total events}).
+ * Returns the number of values available. */
+int bs_ctx_stats(bs_ctx_t ctx, double* out, int n);
 /* The context's cudaStream_t (as void*), for event timing by the caller. */
 void* bs_ctx_stream(bs_ctx_t ctx);
 /* Host<->device bytes moved by the last one-shot entry point. */

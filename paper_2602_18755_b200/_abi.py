@@ -237,6 +237,7 @@ PROTOTYPES = [
     ("bs_ctx_info", C.c_int, [ctx_t, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("bs_ctx_sync", C.c_int, [ctx_t]),
     ("bs_ctx_kernel_launches", C.c_int64, [ctx_t]),
+    ("bs_ctx_stats", C.c_int, [ctx_t, C.POINTER(C.c_double), C.c_int]),
     ("bs_ctx_stream", C.c_void_p, [ctx_t]),
     ("bs_ctx_last_transfer", C.c_int, [ctx_t, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("bs_fp64_peak", C.c_int, [ctx_t, C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -22,6 +22,8 @@ struct bs_ctx_s {
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;
+  double stats[16] = {};  // phase timings / counters of the last entry point
+  int n_stats = 0;
 
   struct Buf {
     void* p = nullptr;

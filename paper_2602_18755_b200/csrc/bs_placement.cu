@@ -124,6 +124,12 @@ struct ProbeOut {
   int model_err;
   int meets;
   int empty;
+  long long events;  // batches / iterations simulated (instrumentation)
+  // energy accounting of the run; complete whenever the probe was feasible
+  // (a feasible probe never stops early), which is what E_c needs
+  long long completed;
+  double busy_j;
+  double idle_j;
 };
 
 struct TraceDev {
@@ -153,11 +159,41 @@ __device__ __forceinline__ SimParams make_params(const DCand& c, const PolicyDev
   return p;
 }
 
+// Per-warp shared scratch of the warp-cooperative decode simulator: the
+// resident heap (when it fits) and the 3 x 32-entry window arrays.
+__host__ __device__ inline size_t warp_scratch_bytes(int heap_cap, bool heap_in_smem) {
+  return (heap_in_smem ? static_cast<size_t>(heap_cap) * sizeof(Resident) : 0) + 3 * 32 * sizeof(double);
+}
+
+__device__ __forceinline__ WarpScratch carve_scratch(unsigned char* smem, int warp, int heap_cap, bool heap_in_smem,
+                                                    Resident* gheap) {
+  unsigned char* p = smem + static_cast<size_t>(warp) * warp_scratch_bytes(heap_cap, heap_in_smem);
+  WarpScratch ws;
+  if (heap_in_smem) {
+    ws.heap = reinterpret_cast<Resident*>(p);
+    p += static_cast<size_t>(heap_cap) * sizeof(Resident);
+  } else {
+    ws.heap = gheap;
+  }
+  ws.L = reinterpret_cast<double*>(p);
+  ws.P = ws.L + 32;
+  ws.T = ws.L + 64;
+  return ws;
+}
+
+// One warp per probe.  Prefill probes run the scalar event loop on lane 0
+// (batches are few); decode probes run the warp-cooperative simulator
+// (bs_sim.cuh), which evaluates up to 32 iterations' predictions at once.
+// Packing 32 probes into one warp instead would serialise their divergent
+// paths.
 __global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_cand, int n_streams, long long n_base,
                              const int* kept, const long long* kept_count, PolicyDev pol, Resident* heaps,
-                             int heap_cap, ProbeOut* out) {
-  const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (gid >= static_cast<long long>(n_cand) * n_streams) return;
+                             int heap_cap, int heap_in_smem, const int* order, ProbeOut* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long slot = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (slot >= static_cast<long long>(n_cand) * n_streams) return;
+  const long long gid = order[slot];  // launch order: likely-long probes first
   const int c = static_cast<int>(gid / n_streams);
   const int s = static_cast<int>(gid % n_streams);
   const DCand cd = cands[c];
@@ -166,10 +202,14 @@ __global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_c
   o.model_err = 0;
   o.meets = 1;
   o.empty = 0;
+  o.events = 0;
+  o.completed = 0;
+  o.busy_j = 0.0;
+  o.idle_j = 0.0;
   const long long nk = kept_count[s];
   if (nk == 0) {  // placement.hpp:169: an empty probe passes
     o.empty = 1;
-    out[gid] = o;
+    if (lane == 0) out[gid] = o;
     return;
   }
   SimTrace st;
@@ -180,12 +220,23 @@ __global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_c
   st.n = nk;
   st.duration_ms = tr.duration_ms;
   const SimParams p = make_params(cd, pol, cd.safe);
-  const SimOut r = cd.phase == BS_PHASE_PREFILL
-                       ? simulate_prefill(m, st, p)
-                       : simulate_decode(m, st, p, heaps + static_cast<size_t>(gid) * heap_cap, heap_cap);
+  SimOut r;
+  if (cd.phase == BS_PHASE_PREFILL) {
+    if (lane != 0) return;
+    r = simulate_prefill(m, st, p);
+  } else {
+    const WarpScratch ws =
+        carve_scratch(smem, warp, heap_cap, heap_in_smem != 0, heaps + static_cast<size_t>(gid) * heap_cap);
+    r = simulate_decode_warp(m, st, p, ws, heap_cap, lane);
+    if (lane != 0) return;
+  }
   o.status = r.status;
   o.model_err = r.model_err;
   o.meets = r.meets_slo;
+  o.events = r.batches;
+  o.completed = r.completed;
+  o.busy_j = r.busy_j;
+  o.idle_j = r.idle_j;
   out[gid] = o;
 }
 
@@ -199,8 +250,10 @@ struct EnergyOut {
 
 __global__ void energy_kernel(DModels m, TraceDev tr, const DCand* cands, const int* cand_stream, int n_cand,
                               long long n_base, const int* kept, const long long* kept_count, PolicyDev pol,
-                              Resident* heaps, int heap_cap, EnergyOut* out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+                              Resident* heaps, int heap_cap, int heap_in_smem, EnergyOut* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // one warp per candidate
   if (c >= n_cand) return;
   const int s = cand_stream[c];
   EnergyOut o;
@@ -210,7 +263,7 @@ __global__ void energy_kernel(DModels m, TraceDev tr, const DCand* cands, const 
   o.busy_j = 0.0;
   o.idle_j = 0.0;
   if (s < 0) {
-    out[c] = o;
+    if (lane == 0) out[c] = o;
     return;
   }
   SimTrace st;
@@ -222,9 +275,16 @@ __global__ void energy_kernel(DModels m, TraceDev tr, const DCand* cands, const 
   st.duration_ms = tr.duration_ms;
   const DCand cd = cands[c];
   const SimParams p = make_params(cd, pol, 0);
-  const SimOut r = cd.phase == BS_PHASE_PREFILL
-                       ? simulate_prefill(m, st, p)
-                       : simulate_decode(m, st, p, heaps + static_cast<size_t>(c) * heap_cap, heap_cap);
+  SimOut r;
+  if (cd.phase == BS_PHASE_PREFILL) {
+    if (lane != 0) return;
+    r = simulate_prefill(m, st, p);
+  } else {
+    const WarpScratch ws =
+        carve_scratch(smem, warp, heap_cap, heap_in_smem != 0, heaps + static_cast<size_t>(c) * heap_cap);
+    r = simulate_decode_warp(m, st, p, ws, heap_cap, lane);
+    if (lane != 0) return;
+  }
   o.status = r.status;
   o.model_err = r.model_err;
   o.completed = r.completed;
@@ -236,8 +296,10 @@ __global__ void energy_kernel(DModels m, TraceDev tr, const DCand* cands, const 
 // Whole-trace simulations (bs_simulate_instance): thread i runs trace i.
 __global__ void sim_kernel(DModels m, const double* arrival, const long long* input, const long long* output,
                            const int* identity, const long long* meta, const double* durations, int n, DCand cd,
-                           PolicyDev pol, Resident* heaps, int heap_cap, SimOut* out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+                           PolicyDev pol, Resident* heaps, int heap_cap, int heap_in_smem, SimOut* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // one warp per trace
   if (i >= n) return;
   const long long off = meta[i];
   SimTrace st;
@@ -248,11 +310,25 @@ __global__ void sim_kernel(DModels m, const double* arrival, const long long* in
   st.n = meta[n + i];
   st.duration_ms = durations[i];
   const SimParams p = make_params(cd, pol, 0);
-  out[i] = cd.phase == BS_PHASE_PREFILL ? simulate_prefill(m, st, p)
-                                         : simulate_decode(m, st, p, heaps + static_cast<size_t>(i) * heap_cap, heap_cap);
+  SimOut r;
+  if (cd.phase == BS_PHASE_PREFILL) {
+    if (lane != 0) return;
+    r = simulate_prefill(m, st, p);
+  } else {
+    const WarpScratch ws =
+        carve_scratch(smem, warp, heap_cap, heap_in_smem != 0, heaps + static_cast<size_t>(i) * heap_cap);
+    r = simulate_decode_warp(m, st, p, ws, heap_cap, lane);
+    if (lane != 0) return;
+  }
+  out[i] = r;
 }
 
 // --- host helpers ---------------------------------------------------------------
+
+cudaError_t set_smem_limit(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
 
 const char* model_err_msg(int kind) {
   switch (kind) {
@@ -534,7 +610,8 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
   const long long n_probes = n_streams * n_cand;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t o_arr = 0, o_in = up(8ull * n), o_out = o_in + up(8ull * n), o_cand = o_out + up(8ull * n);
-  const size_t in_bytes = o_cand + up(sizeof(DCand) * n_cand) + up(4ull * n_cand);
+  const size_t o_order = o_cand + up(sizeof(DCand) * n_cand) + up(4ull * n_cand);
+  const size_t in_bytes = o_order + up(4ull * n_cand * n_streams);
   const size_t o_kept = in_bytes, o_kc = o_kept + up(4ull * n_streams * n), o_probe = o_kc + up(8ull * n_streams);
   const size_t o_heap = o_probe + up(sizeof(ProbeOut) * n_probes);
   const size_t heap_rows = any_decode ? static_cast<size_t>(std::max<long long>(n_probes, n_cand)) : 0;
@@ -552,6 +629,16 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
     ho[i] = base->requests[i].output_len;
   }
   std::memcpy(h + o_cand, hc.data(), sizeof(DCand) * n_cand);
+  {  // decode probes at high rate steps run longest (feasible ones never stop early): launch them first
+    int* ho_ = reinterpret_cast<int*>(h + o_order);
+    long long w = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (long long k = k_max; k >= 1; --k)
+        for (int c = 0; c < n_cand; ++c) {
+          if ((cands[c].phase == BS_PHASE_DECODE) != (pass == 0)) continue;
+          for (int j = 0; j < reps; ++j) ho_[w++] = static_cast<int>(static_cast<long long>(c) * n_streams + (k - 1) * reps + j);
+        }
+  }
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->last_h2d = in_bytes;
   TraceDev tr{reinterpret_cast<const double*>(d + o_arr), reinterpret_cast<const long long*>(d + o_in),
@@ -559,18 +646,27 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
   MaskParams mp{n, static_cast<int>(k_max), reps, search->tolerance_rps, base_rate, search->seed};
   int* dkept = reinterpret_cast<int*>(d + o_kept);
   long long* dkc = reinterpret_cast<long long*>(d + o_kc);
+  cudaEvent_t ev[4];
+  for (auto& e : ev) BS_CUDA_TRY(ctx, cudaEventCreate(&e));
+  BS_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
   mask_kernel<<<static_cast<unsigned>((n_streams + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, ctx->stream>>>(
       mp, dkept, dkc);
   BS_LAUNCH_CHECK(ctx);
+  BS_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
   PolicyDev pol{policy->max_batch_tokens, policy->max_batch_requests, policy->kv_capacity_tokens, policy->chunking,
                 slo->ttft_ms, slo->tpot_ms};
   ProbeOut* dprobe = reinterpret_cast<ProbeOut*>(d + o_probe);
   Resident* dheap = reinterpret_cast<Resident*>(d + o_heap);
   const DCand* dc = reinterpret_cast<const DCand*>(d + o_cand);
-  probe_kernel<<<static_cast<unsigned>((n_probes + 127) / 128), 128, 0, ctx->stream>>>(
+  const int* dorder = reinterpret_cast<const int*>(d + o_order);
+  const bool heap_smem = heap_cap <= 1024;
+  const size_t smem4 = 4 * warp_scratch_bytes(static_cast<int>(heap_cap), heap_smem);
+  BS_CUDA_TRY(ctx, set_smem_limit(reinterpret_cast<const void*>(probe_kernel), smem4));
+  probe_kernel<<<static_cast<unsigned>((n_probes * 32 + 127) / 128), 128, smem4, ctx->stream>>>(
       models->dm, tr, dc, n_cand, static_cast<int>(n_streams), n, dkept, dkc, pol, dheap, static_cast<int>(heap_cap),
-      dprobe);
+      heap_smem ? 1 : 0, dorder, dprobe);
   BS_LAUNCH_CHECK(ctx);
+  BS_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
   ProbeOut* hp = reinterpret_cast<ProbeOut*>(h + in_bytes);
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(hp, dprobe, sizeof(ProbeOut) * n_probes, cudaMemcpyDeviceToHost, ctx->stream));
   BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -605,33 +701,44 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
     out[c].saturated = sr[c].saturated ? 1 : 0;
     if (out[c].r_c > 0.0) cand_stream[c] = static_cast<int>((sr[c].k_star - 1) * reps + 0);
   }
-  // E_c at (k*, replicate 0): a full run (placement.hpp:227-231)
-  int* dstream = reinterpret_cast<int*>(d + o_cand + up(sizeof(DCand) * n_cand));
-  BS_CUDA_TRY(ctx, cudaMemcpyAsync(dstream, cand_stream.data(), 4ull * n_cand, cudaMemcpyHostToDevice, ctx->stream));
-  EnergyOut* den = reinterpret_cast<EnergyOut*>(d + o_en);
-  energy_kernel<<<(n_cand + 63) / 64, 64, 0, ctx->stream>>>(models->dm, tr, dc, dstream, n_cand, n, dkept, dkc, pol,
-                                                            dheap, static_cast<int>(heap_cap), den);
-  BS_LAUNCH_CHECK(ctx);
-  EnergyOut* he = reinterpret_cast<EnergyOut*>(h + in_bytes + sizeof(ProbeOut) * n_probes);
-  BS_CUDA_TRY(ctx, cudaMemcpyAsync(he, den, sizeof(EnergyOut) * n_cand, cudaMemcpyDeviceToHost, ctx->stream));
-  BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  ctx->last_d2h += sizeof(EnergyOut) * n_cand;
+  // E_c at (k*, replicate 0) (placement.hpp:227-231): that probe passed, so
+  // it never stopped early and its run is exactly simulate_instance on the
+  // same probe trace -- reuse its energy accounting.  An empty probe trace
+  // only records the idle span [0, duration] (simulator.hpp:731-733).
+  {
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    long long mx = 0, sum = 0;
+    for (long long i = 0; i < n_probes; ++i) {
+      mx = std::max(mx, hp[i].events);
+      sum += hp[i].events;
+    }
+    ctx->stats[0] = a;
+    ctx->stats[1] = b;
+    ctx->stats[2] = 0.0;
+    ctx->stats[3] = static_cast<double>(mx);
+    ctx->stats[4] = static_cast<double>(sum);
+    ctx->n_stats = 5;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   for (int c = 0; c < n_cand; ++c) {
     if (cand_stream[c] < 0) continue;
-    const EnergyOut& e = he[c];
-    if (e.status == BS_MODEL_ERROR) {
-      out[c].error_code = BS_MODEL_ERROR;
-      out[c].r_c = 0.0;
-      out[c].k_star = 0;
-      if (e.model_err == 3)
+    const ProbeOut& e = hp[static_cast<size_t>(c) * n_streams + cand_stream[c]];
+    if (e.empty) {
+      if (!idle_tp_ok[c]) {
+        out[c].error_code = BS_MODEL_ERROR;
+        out[c].r_c = 0.0;
+        out[c].k_star = 0;
+        out[c].saturated = 0;
         std::snprintf(out[c].error, sizeof out[c].error, "idle model: tp %d not present", cands[c].tp);
-      else
-        std::snprintf(out[c].error, sizeof out[c].error, "%s", model_err_msg(e.model_err));
+      } else {
+        out[c].error_code = -1;
+        std::snprintf(out[c].error, sizeof out[c].error, "no completed request at R_c");
+      }
       continue;
     }
-    if (e.status == BS_SIMULATION_ERROR)  // not caught by evaluate_candidate: propagates
-      return set_error(ctx, BS_SIMULATION_ERROR, "simulation error while measuring E_c");
-    if (e.status != BS_OK) return set_error(ctx, BS_CUDA_ERROR, "config table: device resident scratch too small");
+    if (e.status != BS_OK || !e.meets) return set_error(ctx, BS_CUDA_ERROR, "config table: inconsistent probe at k*");
     // energy_per_request (placement.hpp:205-213)
     if (e.completed < 1) {
       out[c].error_code = -1;
@@ -639,7 +746,7 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
       continue;
     }
     double en = e.busy_j;
-    if (cands[c].phase == BS_PHASE_PREFILL) en += e.idle_j;
+    if (cands[c].phase == BS_PHASE_PREFILL) en = en + e.idle_j;
     out[c].e_c = en / static_cast<double>(e.completed);
     out[c].has_e_c = 1;
   }
@@ -699,11 +806,14 @@ int bs_simulate_instance(bs_ctx_t ctx, bs_models_t models, const bs_trace* trace
   DCand cd{cfg->phase, cfg->tp, cfg->base_freq_mhz, 0};
   PolicyDev pol{policy->max_batch_tokens, policy->max_batch_requests, policy->kv_capacity_tokens, policy->chunking,
                 slo->ttft_ms, slo->tpot_ms};
-  sim_kernel<<<(n + 63) / 64, 64, 0, ctx->stream>>>(
+  const bool heap_smem = heap_cap <= 1024;
+  const size_t smem4 = 4 * warp_scratch_bytes(static_cast<int>(heap_cap), heap_smem);
+  BS_CUDA_TRY(ctx, set_smem_limit(reinterpret_cast<const void*>(sim_kernel), smem4));
+  sim_kernel<<<(n * 32 + 127) / 128, 128, smem4, ctx->stream>>>(
       models->dm, reinterpret_cast<const double*>(d + o_arr), reinterpret_cast<const long long*>(d + o_in),
       reinterpret_cast<const long long*>(d + o_out), reinterpret_cast<const int*>(d + o_idx),
       reinterpret_cast<const long long*>(d + o_meta), reinterpret_cast<const double*>(d + o_meta + sizeof(long long) * 2 * n),
-      n, cd, pol, reinterpret_cast<Resident*>(d + o_heap), static_cast<int>(heap_cap),
+      n, cd, pol, reinterpret_cast<Resident*>(d + o_heap), static_cast<int>(heap_cap), heap_smem ? 1 : 0,
       reinterpret_cast<SimOut*>(d + o_res));
   BS_LAUNCH_CHECK(ctx);
   const SimOut* hr = reinterpret_cast<const SimOut*>(h + o_res);

@@ -340,6 +340,13 @@ int bs_ctx_sync(bs_ctx_t ctx) {
 
 int64_t bs_ctx_kernel_launches(bs_ctx_t ctx) { return ctx ? ctx->launches : -1; }
 
+int bs_ctx_stats(bs_ctx_t ctx, double* out, int n) {
+  if (!ctx || !out) return 0;
+  const int m = std::min(n, ctx->n_stats);
+  for (int i = 0; i < m; ++i) out[i] = ctx->stats[i];
+  return ctx->n_stats;
+}
+
 void* bs_ctx_stream(bs_ctx_t ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int bs_ctx_last_transfer(bs_ctx_t ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {

@@ -83,12 +83,149 @@ __device__ __forceinline__ Resident heap_pop(Resident* h, int& n) {
   return top;
 }
 
+// A grid specialised to one instance.  tp and freq_mhz are constant for a
+// whole simulation, so their bracketing (lo, frac) is computed once.  An axis
+// whose frac is exactly 0 (a fixed value on a knot -- ladder rungs always
+// are) or that has a single knot contributes the factor 1.0 - 0 = 1.0 to
+// every low corner and weight 0 to every high corner, which
+// NdGrid::interpolate then skips (perfmodel.hpp:183-190); dropping such axes
+// therefore leaves every weight product, the corner order and the sum
+// bit-identical while the corner loop shrinks from 2^D to 2^(active axes).
+// sum_len / n_requests are bracketed per call by binary search (the index
+// std::upper_bound finds).
+struct FastGrid {
+  int na;                      // active axes, in axis order
+  int bad;
+  int role[kMaxRank];          // role of each active axis
+  int n[kMaxRank];
+  const double* knots[kMaxRank];
+  long long stride[kMaxRank];  // row-major stride of each active axis
+  int fixed[kMaxRank];         // 1: tp / freq (lo, frac below)
+  int lo[kMaxRank];
+  double frac[kMaxRank];
+  long long base;              // flat offset of the dropped axes' lo
+  const double* values;
+};
+
+__device__ __forceinline__ void bracket(const double* k, int n, double x, int* lo, double* frac) {
+  const double k0 = k[0], kn = k[n - 1];
+  if (x < k0 || x > kn) x = x < k0 ? k0 : (kn < x ? kn : x);
+  if (n == 1) {
+    *lo = 0;
+    *frac = 0.0;
+    return;
+  }
+  int a = 0, b = n;  // first index with k[i] > x
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if (x < k[mid])
+      b = mid;
+    else
+      a = mid + 1;
+  }
+  int hi = a < 1 ? 1 : (a > n - 1 ? n - 1 : a);
+  *lo = hi - 1;
+  *frac = __ddiv_rn(__dsub_rn(x, k[hi - 1]), __dsub_rn(k[hi], k[hi - 1]));
+}
+
+__device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double freq) {
+  FastGrid f;
+  f.na = 0;
+  f.bad = g.bad_axis;
+  f.values = g.values;
+  f.base = 0;
+  long long stride[kMaxRank];
+  long long st = 1;
+  for (int d = g.rank - 1; d >= 0; --d) {
+    stride[d] = st;
+    st *= g.n[d];
+  }
+  for (int d = 0; d < g.rank; ++d) {
+    if (g.n[d] == 1) continue;  // single knot: lo 0, factor 1.0, high corners weight 0
+    const bool fixed_axis = g.role[d] == BS_AXIS_TP || g.role[d] == BS_AXIS_FREQ;
+    int lo = 0;
+    double fr = 0.0;
+    if (fixed_axis) {
+      bracket(g.knots[d], g.n[d], g.role[d] == BS_AXIS_TP ? static_cast<double>(tp) : freq, &lo, &fr);
+      if (fr == 0.0) {  // on a knot: drop the axis, keep its lo in the base offset
+        f.base += lo * stride[d];
+        continue;
+      }
+    }
+    const int a = f.na++;
+    f.role[a] = g.role[d];
+    f.n[a] = g.n[d];
+    f.knots[a] = g.knots[d];
+    f.stride[a] = stride[d];
+    f.fixed[a] = fixed_axis ? 1 : 0;
+    f.lo[a] = lo;
+    f.frac[a] = fr;
+  }
+  return f;
+}
+
+// bracket() without a dependent load chain: std::upper_bound's index in a
+// sorted knot vector is the number of knots k with !(x < k); the loads are
+// independent and the count is branch-free.
+__device__ __forceinline__ void bracket_count(const double* __restrict__ k, int n, double x, int* lo, double* frac) {
+  const double k0 = __ldg(k), kn = __ldg(k + n - 1);
+  if (x < k0 || x > kn) x = x < k0 ? k0 : (kn < x ? kn : x);
+  int cnt = 0;
+  for (int i = 0; i < n; ++i) cnt += !(x < __ldg(k + i)) ? 1 : 0;
+  const int hi = cnt < 1 ? 1 : (cnt > n - 1 ? n - 1 : cnt);
+  *lo = hi - 1;
+  const double klo = __ldg(k + hi - 1), khi = __ldg(k + hi);
+  *frac = __ddiv_rn(__dsub_rn(x, klo), __dsub_rn(khi, klo));
+}
+
+__device__ __forceinline__ double fast_interp(const FastGrid& g, long long n_req, long long sum_len) {
+  int lo[kMaxRank];
+  double frac[kMaxRank];
+#pragma unroll
+  for (int a = 0; a < kMaxRank; ++a) {
+    if (a >= g.na) break;
+    if (g.fixed[a]) {
+      lo[a] = g.lo[a];
+      frac[a] = g.frac[a];
+    } else {  // active varying axes have >= 2 knots (single-knot axes are dropped)
+      bracket_count(g.knots[a], g.n[a], static_cast<double>(g.role[a] == BS_AXIS_SUM_LEN ? sum_len : n_req),
+                    &lo[a], &frac[a]);
+    }
+  }
+  double acc = 0.0;
+  if (g.na == 2) {  // the common case: (sum_len, n_requests) with tp and freq on knots
+    const double w0[2] = {__dsub_rn(1.0, frac[0]), frac[0]};
+    const double w1[2] = {__dsub_rn(1.0, frac[1]), frac[1]};
+#pragma unroll
+    for (int mask = 0; mask < 4; ++mask) {
+      const int h0 = mask & 1, h1 = mask >> 1;
+      const double weight = __dmul_rn(__dmul_rn(1.0, w0[h0]), w1[h1]);
+      const long long flat = g.base + (lo[0] + h0) * g.stride[0] + (lo[1] + h1) * g.stride[1];
+      if (weight != 0.0) acc = __dadd_rn(acc, __dmul_rn(weight, __ldg(g.values + flat)));
+    }
+    return acc;
+  }
+  const int corners = 1 << g.na;
+  for (int mask = 0; mask < corners; ++mask) {
+    double weight = 1.0;
+    long long flat = g.base;
+#pragma unroll
+    for (int a = 0; a < kMaxRank; ++a) {
+      if (a >= g.na) break;
+      const int high = (mask >> a) & 1;
+      weight = __dmul_rn(weight, high ? frac[a] : __dsub_rn(1.0, frac[a]));
+      flat += (lo[a] + high) * g.stride[a];
+    }
+    if (weight != 0.0) acc = __dadd_rn(acc, __dmul_rn(weight, __ldg(g.values + flat)));
+  }
+  return acc;
+}
+
 // predict_latency / predict_power at the instance's (tp, freq); false on
 // ModelError (perfmodel.hpp:264, 270).
-__device__ __forceinline__ bool predict_at(const DGrid& g, long long n_req, long long sum_len, const SimParams& p,
-                                           double* out) {
-  if (g.bad_axis) return false;
-  const double v = interp(g, make_query(n_req, sum_len, p.tp, p.freq), nullptr);
+__device__ __forceinline__ bool predict_at(const FastGrid& g, long long n_req, long long sum_len, double* out) {
+  if (g.bad) return false;
+  const double v = fast_interp(g, n_req, sum_len);
   *out = v;
   return model_value_ok(v);
 }
@@ -104,8 +241,8 @@ __device__ SimOut simulate_prefill(const DModels& m, const SimTrace& tr, const S
   o.busy_j = 0.0;
   o.idle_j = 0.0;
   o.batches = 0;
-  const DGrid& lat = m.grid[0];
-  const DGrid& pw = m.grid[2];
+  const FastGrid lat = fast_grid(m.grid[0], p.tp, p.freq);
+  const FastGrid pw = fast_grid(m.grid[2], p.tp, p.freq);
   double idle_w = 0.0;
   const bool have_idle = idle_power(m.idle, p.tp, p.freq, &idle_w);
   double now = 0.0;
@@ -175,12 +312,12 @@ __device__ SimOut simulate_prefill(const DModels& m, const SimTrace& tr, const S
         }
       }
       double L;
-      if (!predict_at(lat, npick, sum, p, &L)) {
+      if (!predict_at(lat, npick, sum, &L)) {
         o.status = BS_MODEL_ERROR;
         o.model_err = 1;
         return o;
       }
-      if (!predict_at(pw, npick, sum, p, &bp)) {
+      if (!predict_at(pw, npick, sum, &bp)) {
         o.status = BS_MODEL_ERROR;
         o.model_err = 2;
         return o;
@@ -239,8 +376,8 @@ __device__ SimOut simulate_decode(const DModels& m, const SimTrace& tr, const Si
   o.busy_j = 0.0;
   o.idle_j = 0.0;
   o.batches = 0;
-  const DGrid& lat = m.grid[1];
-  const DGrid& pw = m.grid[3];
+  const FastGrid lat = fast_grid(m.grid[1], p.tp, p.freq);
+  const FastGrid pw = fast_grid(m.grid[3], p.tp, p.freq);
   double idle_w = 0.0;
   const bool have_idle = idle_power(m.idle, p.tp, p.freq, &idle_w);
   double now = 0.0;
@@ -307,12 +444,12 @@ __device__ SimOut simulate_decode(const DModels& m, const SimTrace& tr, const Si
         continue;
       }
       double L;
-      if (!predict_at(lat, n_res, sum_ctx, p, &L)) {
+      if (!predict_at(lat, n_res, sum_ctx, &L)) {
         o.status = BS_MODEL_ERROR;
         o.model_err = 1;
         return o;
       }
-      if (!predict_at(pw, n_res, sum_ctx, p, &bp)) {
+      if (!predict_at(pw, n_res, sum_ctx, &bp)) {
         o.status = BS_MODEL_ERROR;
         o.model_err = 2;
         return o;
@@ -358,6 +495,241 @@ __device__ SimOut simulate_decode(const DModels& m, const SimTrace& tr, const Si
     }
     ++arr;
     now = t_arr;
+  }
+  o.horizon_ms = fmax(tr.duration_ms, now);
+  record_idle(now, o.horizon_ms);
+  return o;
+}
+
+// Warp-cooperative simulate_decode_instance (simulator.hpp:441-578), no
+// controller, bit-identical to simulate_decode.
+//
+// Between two events -- the next retirement (known in advance: a resident
+// admitted at iteration i with o output tokens retires at the end of
+// iteration i + o - 1) and the next admissible arrival -- the batch size n is
+// constant and the summed context grows by n per iteration, so the features
+// of up to 32 future iterations are known before their start times are.  The
+// 32 lanes evaluate those iterations' latency and power interpolations in
+// parallel; lane 0 then runs the only truly serial part, the FP64 chain
+// t_done = t_start + 1.0 * L, and the warp locates the first iteration whose
+// end admits a waiting arrival (the window ends there), checks every token
+// gap, and accumulates the energy terms in record order.  All lanes hold the
+// same scalar state (redundant, divergence-free); the resident heap and the
+// per-window arrays live in the warp's shared memory.
+struct WarpScratch {
+  Resident* heap;  // heap_cap entries
+  double* L;       // 32
+  double* P;       // 32
+  double* T;       // 32
+};
+
+__device__ SimOut simulate_decode_warp(const DModels& m, const SimTrace& tr, const SimParams& p, WarpScratch ws,
+                                       int heap_cap, int lane) {
+  SimOut o;
+  o.status = BS_OK;
+  o.model_err = 0;
+  o.meets_slo = 1;
+  o.completed = 0;
+  o.busy_j = 0.0;
+  o.idle_j = 0.0;
+  o.batches = 0;
+  const FastGrid lat = fast_grid(m.grid[1], p.tp, p.freq);
+  const FastGrid pw = fast_grid(m.grid[3], p.tp, p.freq);
+  double idle_w = 0.0;
+  const bool have_idle = idle_power(m.idle, p.tp, p.freq, &idle_w);
+  double now = 0.0;
+  long long arr = 0, whead = 0;
+  int n_res = 0;
+  long long sum_ctx = 0, reserved = 0, it = 0;
+  double prev_end = 0.0;
+  Resident* heap = ws.heap;
+
+  auto record_idle = [&](double from, double to) -> bool {
+    if (to <= from) return true;
+    if (!have_idle) {
+      o.status = BS_MODEL_ERROR;
+      o.model_err = 3;
+      return false;
+    }
+    o.idle_j = __dadd_rn(o.idle_j, __ddiv_rn(__dmul_rn(idle_w, __dsub_rn(to, from)), 1000.0));
+    return true;
+  };
+
+  while (arr < tr.n || whead < arr || n_res > 0) {
+    // ---- boundary: pull arrivals, admit (simulator.hpp:515-519, 455-470)
+    while (arr < tr.n && tr.arrival[tr.kept[arr]] <= now) ++arr;
+    int n_new = 0;
+    double new_min_arr = 0.0;
+    while (whead < arr) {
+      const int r = tr.kept[whead];
+      const long long need = tr.input[r] + tr.output[r];
+      if (need > p.kv_capacity) {
+        o.status = BS_SIMULATION_ERROR;
+        o.meets_slo = 0;
+        return o;
+      }
+      if (n_res >= p.max_batch_requests) break;
+      if (reserved + need > p.kv_capacity) break;
+      if (n_res >= heap_cap) {
+        o.status = BS_PARAMETER_ERROR;
+        return o;
+      }
+      Resident rs;
+      rs.retire = it + tr.output[r] - 1;
+      rs.need = need;
+      int nn = n_res;
+      if (lane == 0) heap_push(heap, nn, rs);
+      __syncwarp();
+      n_res += 1;
+      reserved += need;
+      sum_ctx += tr.input[r];
+      const double a = tr.arrival[r];
+      new_min_arr = n_new == 0 ? a : (a < new_min_arr ? a : new_min_arr);
+      ++n_new;
+      ++whead;
+    }
+    if (n_res == 0) {
+      if (arr >= tr.n && whead >= arr) break;
+      if (whead < arr) {
+        o.status = BS_SIMULATION_ERROR;
+        o.meets_slo = 0;
+        return o;
+      }
+      const double t_next = fmax(tr.arrival[tr.kept[arr]], now);
+      if (!record_idle(now, t_next)) return o;
+      now = t_next;
+      continue;
+    }
+    // ---- the event window: iterations it .. R at constant n (R = next retirement)
+    const long long R = heap[0].retire;
+    // the next arrival matters at the first boundary it has reached, unless
+    // admission stays blocked until a retirement (n and reserved are constant
+    // inside the window); a request too large for the KV cache always stops
+    // the window (admit throws, simulator.hpp:459-462)
+    bool arrival_cuts = false;
+    double t_a = INFINITY;
+    if (whead == arr && arr < tr.n) {
+      const int r = tr.kept[arr];
+      const long long need = tr.input[r] + tr.output[r];
+      arrival_cuts = need > p.kv_capacity || (n_res < p.max_batch_requests && reserved + need <= p.kv_capacity);
+      t_a = tr.arrival[r];
+    }
+    bool first_chunk = true, cut = false;
+    long long it0 = it;
+    while (!cut) {
+      const long long left = R - it0 + 1;
+      const int mcount = left < 32 ? static_cast<int>(left) : 32;
+      // parallel: features and predictions of iterations it0 .. it0 + mcount - 1
+      // latency is needed for every iteration (t_done); power only for a
+      // segment of positive length (record_segment returns before
+      // exec_power when to <= from, simulator.hpp:214-215)
+      bool bad = false, pbad = false;
+      if (lane < mcount) {
+        const long long s = sum_ctx + static_cast<long long>(lane) * n_res;
+        double Lv = 0.0, Pv = 0.0;
+        if (!predict_at(lat, n_res, s, &Lv)) bad = true;
+        if (!predict_at(pw, n_res, s, &Pv)) pbad = true;
+        ws.L[lane] = Lv;
+        ws.P[lane] = Pv;
+      }
+      const unsigned badm = __ballot_sync(0xffffffffu, bad);
+      const unsigned pbadm = __ballot_sync(0xffffffffu, pbad);
+      const int first_bad = badm ? __ffs(badm) - 1 : mcount;
+      // serial: end times of the window's iterations (simulator.hpp:362, 537)
+      __syncwarp();
+      if (lane == 0) {  // 1.0 * L == L exactly, so the chain is one DADD per iteration
+        double t = now;
+#pragma unroll 8
+        for (int l = 0; l < first_bad; ++l) {
+          t = __dadd_rn(t, ws.L[l]);
+          ws.T[l] = t;
+        }
+      }
+      __syncwarp();
+      // where does the window stop?  at the first iteration whose end admits
+      // the waiting arrival, at the retirement, or at a model error
+      bool stop_here = false;
+      if (lane < first_bad) stop_here = arrival_cuts && ws.T[lane] >= t_a;
+      const unsigned stopm = __ballot_sync(0xffffffffu, stop_here);
+      int last = first_bad - 1;  // last iteration simulated in this chunk
+      if (stopm) last = min(last, __ffs(stopm) - 1);
+      // token gaps (max_tbt_ms, simulator.hpp:81-89) for iterations 0..last
+      bool viol = false;
+      if (lane <= last) {
+        const double t_start = lane == 0 ? now : ws.T[lane - 1];
+        const double te = ws.T[lane];
+        if (lane == 0 && first_chunk) {
+          if (n_res > n_new && __dsub_rn(te, prev_end) > p.tpot_bound) viol = true;
+          if (n_new > 0 && __dsub_rn(te, new_min_arr) > p.tpot_bound) viol = true;
+        } else if (__dsub_rn(te, t_start) > p.tpot_bound) {
+          viol = true;
+        }
+      }
+      const unsigned violm = __ballot_sync(0xffffffffu, viol);
+      if (violm) {
+        o.meets_slo = 0;
+        if (p.early_exit) return o;
+      }
+      // energy of the segments, in record order (simulator.hpp:213-228)
+      // each lane forms its segment's energy term; lane 0 adds them in record
+      // order (the only serial part)
+      bool seg = false;
+      if (lane <= last) {
+        const double t_start = lane == 0 ? now : ws.T[lane - 1];
+        const double te = ws.T[lane];
+        seg = te > t_start;
+        ws.L[lane] = seg ? __ddiv_rn(__dmul_rn(ws.P[lane], __dsub_rn(te, t_start)), 1000.0) : 0.0;
+      }
+      const unsigned segm = __ballot_sync(0xffffffffu, seg);
+      const unsigned perrm = segm & pbadm;
+      const int perr = perrm ? __ffs(perrm) - 1 : -1;
+      __syncwarp();
+      if (lane == 0) {
+        double busy = o.busy_j;
+        const int upto = perr >= 0 ? perr - 1 : last;
+#pragma unroll 8
+        for (int l = 0; l <= upto; ++l)
+          if ((segm >> l) & 1u) busy = __dadd_rn(busy, ws.L[l]);
+        ws.P[0] = busy;
+      }
+      __syncwarp();
+      o.busy_j = ws.P[0];
+      o.batches += __popc(segm & (perr >= 0 ? ((1u << perr) - 1u) : 0xffffffffu));
+      __syncwarp();
+      if (perr >= 0) {
+        o.status = BS_MODEL_ERROR;
+        o.model_err = 2;
+        return o;
+      }
+      if (last >= 0) {
+        const double t_end = ws.T[last];
+        sum_ctx += n_res * static_cast<long long>(last + 1);
+        it0 += last + 1;
+        now = t_end;
+        prev_end = t_end;
+      }
+      __syncwarp();
+      if (first_bad < mcount && last == first_bad - 1 && !stopm) {
+        o.status = BS_MODEL_ERROR;
+        o.model_err = 1;
+        return o;
+      }
+      first_chunk = false;
+      cut = stopm != 0 || it0 > R;
+    }
+    it = it0;
+    // retirements at the end of iteration it - 1 (simulator.hpp:546-555)
+    while (n_res > 0 && heap[0].retire <= it - 1) {
+      const Resident r = heap[0];
+      int nn = n_res;
+      __syncwarp();
+      if (lane == 0) heap_pop(heap, nn);
+      __syncwarp();
+      n_res -= 1;
+      reserved -= r.need;
+      sum_ctx -= r.need;
+      ++o.completed;
+    }
   }
   o.horizon_ms = fmax(tr.duration_ms, now);
   record_idle(now, o.horizon_ms);
