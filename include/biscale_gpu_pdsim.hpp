@@ -18,6 +18,11 @@
 //                                          runner.hpp:118)
 //   pdsim_gpu::greedy_freq_select / exhaustive_freq_select /
 //   select_decode_freq_ex               batch-of-one wrappers
+//   pdsim_gpu::build_config_table       replaces build_config_table
+//                                         (placement.hpp:240-260), the call
+//                                         in plan_window (placement.hpp:576)
+//   pdsim_gpu::solve_placement /        replace solve_placement (357-416) and
+//   solve_max_throughput                  solve_max_throughput (421-499)
 //
 // Status codes are rethrown as the reference's exception types with the
 // library's message.  predicted_latency_ms is evaluated with the reference's
@@ -26,6 +31,7 @@
 // but a host call avoids a launch on the simulator's critical path).
 #pragma once
 
+#include <cstdio>
 #include <memory>
 #include <optional>
 #include <string>
@@ -34,6 +40,7 @@
 #include "biscale_gpu.h"
 #include "pdsim/dvfs.hpp"
 #include "pdsim/errors.hpp"
+#include "pdsim/placement.hpp"
 
 namespace pdsim_gpu {
 
@@ -307,6 +314,118 @@ class GpuDecodePolicyController : public pdsim::FreqController {
   const DeviceModels* dm_;
   double safety_margin_ = 0.05;
 };
+
+// --- coarse-tier placement ------------------------------------------------------
+
+namespace detail {
+
+struct TraceView {
+  std::vector<bs_request> reqs;
+  bs_trace t{};
+  explicit TraceView(const pdsim::Trace& tr) {
+    reqs.reserve(tr.requests.size());
+    for (const auto& r : tr.requests) reqs.push_back(bs_request{r.id, r.arrival_ms, r.input_len, r.output_len});
+    t.n = static_cast<int64_t>(reqs.size());
+    t.requests = reqs.data();
+    t.duration_ms = tr.duration_ms;
+  }
+};
+
+inline bs_table_entry to_entry(const pdsim::ConfigTableEntry& e) {
+  bs_table_entry o{};
+  o.config = bs_instance_config{e.config.phase == pdsim::Phase::prefill ? BS_PHASE_PREFILL : BS_PHASE_DECODE,
+                                e.config.tp, e.config.base_freq_mhz};
+  o.r_c = e.r_c;
+  o.has_e_c = e.e_c ? 1 : 0;
+  o.e_c = e.e_c ? *e.e_c : 0.0;
+  o.g_c = e.g_c;
+  o.saturated = e.saturated ? 1 : 0;
+  o.error_code = e.error.empty() ? 0 : BS_MODEL_ERROR;
+  std::snprintf(o.error, sizeof(o.error), "%s", e.error.c_str());
+  return o;
+}
+
+inline pdsim::ConfigTableEntry from_entry(const bs_table_entry& e) {
+  pdsim::ConfigTableEntry o;
+  o.config = pdsim::InstanceConfig{e.config.phase == BS_PHASE_PREFILL ? pdsim::Phase::prefill : pdsim::Phase::decode,
+                                   e.config.tp, e.config.base_freq_mhz};
+  o.r_c = e.r_c;
+  if (e.has_e_c) o.e_c = e.e_c;
+  o.g_c = e.g_c;
+  o.saturated = e.saturated != 0;
+  if (e.error_code != 0) o.error = e.error;
+  return o;
+}
+
+template <class Solve>
+pdsim::PlacementPlan solve_with(const pdsim::PlacementProblem& p, Solve&& solve) {
+  p.validate();
+  std::vector<bs_table_entry> t;
+  t.reserve(p.table.size());
+  for (const auto& e : p.table) t.push_back(to_entry(e));
+  std::vector<int64_t> counts(p.table.size(), 0);
+  double obj = 0.0;
+  int32_t used = 0;
+  int rc = solve(t.data(), static_cast<int>(t.size()), counts.data(), &obj, &used);
+  if (rc != BS_OK) rethrow(rc, bs_last_error(nullptr));
+  pdsim::PlacementPlan plan;
+  plan.counts.assign(counts.begin(), counts.end());
+  plan.table = p.table;
+  plan.objective_w = obj;
+  plan.target_rps = p.target_rps;
+  plan.alpha = p.alpha;
+  plan.total_gpus = p.total_gpus;
+  plan.gpus_used = used;
+  plan.instances = pdsim::derive_routing_weights(plan.counts, plan.table);
+  return plan;
+}
+
+}  // namespace detail
+
+// build_config_table (placement.hpp:240-260) on the GPU: the goodput probes
+// of every candidate in one grid, the exact binary-search replay, then E_c.
+// Drop-in for the call in plan_window (placement.hpp:576).
+inline std::vector<pdsim::ConfigTableEntry> build_config_table(const DeviceModels& dm,
+                                                               const std::vector<pdsim::InstanceConfig>& candidates,
+                                                               const pdsim::Trace& base, const pdsim::SLOSpec& slo,
+                                                               const pdsim::SchedulerPolicy& policy,
+                                                               const pdsim::GoodputSearch& search) {
+  if (candidates.empty()) throw pdsim::ParameterError("config table: no candidates");
+  detail::TraceView tv(base);
+  const bs_slo s{slo.ttft_ms, slo.tpot_ms, slo.percentile};
+  const bs_scheduler_policy pol = detail::to_policy(policy);
+  bs_goodput_search g{};
+  g.tolerance_rps = search.tolerance_rps;
+  g.probe_count = search.probe_count;
+  g.seed = search.seed;
+  std::vector<bs_instance_config> cands;
+  for (const auto& c : candidates)
+    cands.push_back(bs_instance_config{c.phase == pdsim::Phase::prefill ? BS_PHASE_PREFILL : BS_PHASE_DECODE, c.tp,
+                                       c.base_freq_mhz});
+  std::vector<bs_table_entry> out(candidates.size());
+  dm.device().check(bs_goodput_table(dm.device().get(), dm.get(), &tv.t, &s, &pol, &g, cands.data(),
+                                     static_cast<int>(cands.size()), out.data()));
+  std::vector<pdsim::ConfigTableEntry> table;
+  table.reserve(out.size());
+  for (const auto& e : out) table.push_back(detail::from_entry(e));
+  return table;
+}
+
+// solve_placement (placement.hpp:357-416), same fold order and tie-breaks;
+// InfeasibleError with the reference's constraint and message.
+inline pdsim::PlacementPlan solve_placement(const pdsim::PlacementProblem& p) {
+  return detail::solve_with(p, [&](const bs_table_entry* t, int n, int64_t* counts, double* obj, int32_t* used) {
+    return bs_placement_solve(nullptr, t, n, p.total_gpus, p.target_rps, p.alpha, counts, obj, used);
+  });
+}
+
+// solve_max_throughput (placement.hpp:421-499).
+inline pdsim::PlacementPlan solve_max_throughput(const pdsim::PlacementProblem& p, double max_freq_mhz) {
+  return detail::solve_with(p, [&](const bs_table_entry* t, int n, int64_t* counts, double* obj, int32_t* used) {
+    return bs_placement_max_throughput(nullptr, t, n, p.total_gpus, p.target_rps, p.alpha, max_freq_mhz, counts,
+                                       obj, used);
+  });
+}
 
 // TwoTierFactory (dvfs.hpp:370-390): drop-in ControllerFactory for
 // simulate_cluster / run_policy.

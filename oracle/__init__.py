@@ -19,6 +19,7 @@ HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libpdsim_ref.so"
 REPLAY_BIN = HERE / "_ref" / "replay_parity"
+PLACEMENT_BIN = HERE / "_ref" / "placement_parity"
 REFERENCE_ROOT = Path("/root/reference")
 
 _P = C.POINTER

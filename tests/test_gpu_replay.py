@@ -29,3 +29,20 @@ def test_reference_simulator_with_gpu_controllers(args):
     assert line["checked"] and line["decisions"] > 100
     assert line["match"], line
     assert res.returncode == 0
+
+
+@pytest.mark.parametrize("args", [
+    ["--seed", "7", "--duration-s", "600", "--rps", "12", "--levels", "8"],
+    ["--seed", "9", "--duration-s", "300", "--rps", "20", "--levels", "16", "--gpus", "8"],
+    ["--seed", "5", "--duration-s", "300", "--rps", "6", "--levels", "5", "--ttft", "300", "--tpot", "60"],
+])
+def test_reference_planner_with_gpu_config_table(args):
+    """build_config_table / solve_placement / solve_max_throughput through the
+    C++ shim (pdsim_gpu::*) against the reference's own functions."""
+    if not oracle.PLACEMENT_BIN.exists():
+        pytest.skip("placement_parity not built (needs /root/reference at build time)")
+    res = subprocess.run([str(oracle.PLACEMENT_BIN), *args], capture_output=True, text=True, timeout=900)
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["table_mismatch"] == 0, line
+    assert line["match"], line
+    assert res.returncode == 0
