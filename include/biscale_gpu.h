@@ -468,6 +468,149 @@ int bs_placement_max_throughput(bs_ctx_t ctx, const bs_table_entry* table, int n
                                 double target_rps, double alpha, double max_freq_mhz, int64_t* counts,
                                 double* objective_w, int32_t* gpus_used);
 
+/* --- cluster replay ---------------------------------------------------------- */
+
+/* ClusterInstance (simulator.hpp:741-744). */
+typedef struct bs_cluster_instance {
+  bs_instance_config config;
+  double weight; /* routing weight within its phase (RouterState, simulator.hpp:582-598) */
+} bs_cluster_instance;
+
+/* What run_policy / run_window_policy (runner.hpp:112-136) fix for one
+ * replay: the controllers TwoTierFactory (dvfs.hpp:370-390) builds, the
+ * simulator options and the report's SLO and ramp-up. */
+typedef struct bs_replay_config {
+  bs_mpc_config mpc;           /* PrefillMpcController configuration */
+  bs_decode_config decode;     /* DecodePolicyController configuration */
+  bs_scheduler_policy policy;  /* every instance's SchedulerPolicy (and the MPC projection's) */
+  bs_slo slo;                  /* make_report's SLO (metrics.hpp:121) */
+  double switch_latency_ms;    /* SimOptions::switch_latency_ms (simulator.hpp:127) */
+  double horizon_ms;           /* SimOptions::horizon_ms; < 0: max(duration, last event) */
+  double rampup_s;             /* trim_steady_state ramp-up (metrics.hpp:71) */
+  int32_t controlled;          /* 1: TwoTierFactory controllers; 0: nullptr factory (base frequencies) */
+  int32_t _pad;
+} bs_replay_config;
+
+/* One simulate_cluster call (simulator.hpp:758-893). */
+typedef struct bs_scenario {
+  bs_trace trace;                       /* requests sorted by arrival */
+  const bs_cluster_instance* instances; /* index = instance id */
+  int32_t n_instances;
+  int32_t config;                       /* index into the bs_replay_config array */
+} bs_scenario;
+
+/* SimResult counters and the MetricsReport of
+ * make_report(trim_steady_state(sim, rampup_s), slo) (metrics.hpp:71-156).
+ * status: BS_OK or the exception class simulate_cluster would throw
+ * (message through bs_last_error for the first failing scenario). */
+typedef struct bs_replay_summary {
+  int32_t status;
+  int32_t has_p99_ttft;
+  int32_t has_p99_tpot;
+  int32_t has_e_first;
+  int32_t has_e_output;
+  int32_t _pad;
+  double horizon_ms;
+  int64_t completed_requests;      /* SimResult::completed_requests */
+  int64_t generated_tokens;        /* SimResult::generated_tokens */
+  int64_t n_batches;
+  int64_t n_idles;
+  int64_t n_decisions;
+  int64_t decisions_by_trigger[3]; /* boundary, arrival, safety */
+  /* MetricsReport */
+  double p99_ttft_ms;
+  double p99_mean_tpot_ms;
+  double energy_per_first_token_j;
+  double energy_per_output_token_j;
+  double avg_power_prefill_w;
+  double avg_power_decode_w;
+  double prefill_energy_j;
+  double decode_energy_j;
+  double span_ms;
+  int64_t report_completed;
+  int64_t report_generated;
+  int64_t ttft_violations;
+  int64_t tpot_violations;
+} bs_replay_summary;
+
+/* RequestRecord (simulator.hpp:59-101), with the token times reduced to
+ * what the metrics read.  Absent optionals are NaN. */
+typedef struct bs_replay_request {
+  int64_t id;
+  int32_t prefill_instance;
+  int32_t decode_instance;
+  double prefill_done_ms;         /* = decode_join_ms */
+  double decode_first_start_ms;
+  double first_token_ms;          /* token_times_ms.front() */
+  double last_token_ms;           /* token_times_ms.back() */
+  double max_tbt_ms;              /* RequestRecord::max_tbt_ms */
+  int64_t n_tokens;               /* token_times_ms.size() */
+  int32_t completed;
+  int32_t _pad;
+} bs_replay_request;
+
+/* BatchRecord / IdleRecord / DecisionRecord (simulator.hpp:33-57,
+ * controller.hpp:100-107) in SimResult order (stable by start, instance). */
+typedef struct bs_batch_record {
+  int32_t instance;
+  int32_t phase;
+  int64_t batch_seq;
+  double start_ms;
+  double end_ms;
+  int64_t n_requests;
+  int64_t sum_len;
+  double freq_mhz;
+  double power_w;
+  double energy_j;
+} bs_batch_record;
+
+typedef struct bs_idle_record {
+  int32_t instance;
+  int32_t phase;
+  double start_ms;
+  double end_ms;
+  double freq_mhz;
+  double power_w;
+  double energy_j;
+} bs_idle_record;
+
+typedef struct bs_decision_record {
+  double time_ms;
+  int32_t instance;
+  int32_t trigger; /* 0 boundary, 1 arrival, 2 safety */
+  double chosen_freq_mhz;
+  int32_t feasible;
+  int32_t _pad;
+  int64_t eval_count;
+} bs_decision_record;
+
+/* Optional full logs of one scenario: caller arrays and capacities; the
+ * counts are written back (records beyond a capacity are dropped and the
+ * count still reports the total). */
+typedef struct bs_replay_logs {
+  bs_batch_record* batches;
+  int64_t batch_cap;
+  int64_t n_batches;
+  bs_idle_record* idles;
+  int64_t idle_cap;
+  int64_t n_idles;
+  bs_decision_record* decisions;
+  int64_t decision_cap;
+  int64_t n_decisions;
+} bs_replay_logs;
+
+/* simulate_cluster (simulator.hpp:758-893) + trim_steady_state + make_report
+ * for n independent scenarios, on the device: prefill instances one CTA each
+ * (event loop + block-cooperative greedy MPC per decision), decode instances
+ * one warp each (event loop + warp ladder walk per iteration).  sim_models
+ * is the simulator's ground truth, ctl_models the controllers' model set
+ * (TwoTierFactory's controller_models; may be the same handle).  requests
+ * (optional) receives sum(trace.n) records in trace order; logs (optional)
+ * one entry per scenario. */
+int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_models, const bs_replay_config* cfgs, int n_cfgs,
+              const bs_scenario* scenarios, int n, bs_replay_summary* out, bs_replay_request* requests,
+              bs_replay_logs* logs);
+
 #ifdef __cplusplus
 }
 #endif

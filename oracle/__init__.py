@@ -114,6 +114,9 @@ def load_ref() -> C.CDLL:
                                           _P(C.c_int64), _dp, _P(C.c_int32)]),
             "solve_max_throughput": (C.c_int, [_P(A.bs_table_entry), C.c_int, C.c_int, C.c_double, C.c_double,
                                                C.c_double, _P(C.c_int64), _dp, _P(C.c_int32)]),
+            "replay": (C.c_int, [_P(A.bs_model_set), _P(A.bs_model_set), _P(A.bs_replay_config), _P(A.bs_scenario),
+                                 C.c_int, _P(A.bs_replay_summary), _P(A.bs_replay_request), _P(A.bs_replay_logs),
+                                 C.c_int]),
         })
         _ref.ref_interpolate.restype = C.c_int
         _ref.ref_interpolate.argtypes = [_P(A.bs_grid), _dp, C.c_int, _dp, _P(C.c_uint32)]

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "pdsim/dvfs.hpp"
+#include "pdsim/metrics.hpp"
 #include "pdsim/placement.hpp"
 #include "pdsim/runner.hpp"
 #include "pdsim/simulator.hpp"
@@ -644,5 +645,129 @@ extern "C" int ref_simulate(const bs_model_set* models, const bs_trace* traces, 
         out[i].horizon_ms = r.horizon_ms;
       });
     }
+  });
+}
+
+// --- cluster replay: simulate_cluster + trim_steady_state + make_report -------
+
+namespace {
+
+void replay_one(const ModelSet& sim_m, const ModelSet& ctl_m, const bs_replay_config& rc, const bs_scenario& sc,
+                bs_replay_summary* o, bs_replay_request* req, bs_replay_logs* logs) {
+  Trace tr = to_trace(sc.trace);
+  ClusterSpec cl;
+  for (int i = 0; i < sc.n_instances; ++i) {
+    const bs_cluster_instance& ci = sc.instances[i];
+    cl.instances.push_back(ClusterInstance{
+        InstanceConfig{ci.config.phase == BS_PHASE_PREFILL ? Phase::prefill : Phase::decode, ci.config.tp,
+                       ci.config.base_freq_mhz},
+        ci.weight});
+  }
+  SchedulerPolicy pol = to_policy(rc.policy);
+  SimOptions opts;
+  opts.switch_latency_ms = rc.switch_latency_ms;
+  opts.horizon_ms = rc.horizon_ms;
+  MpcConfig mpc = to_mpc(rc.mpc);
+  DecodePolicyConfig dc;
+  dc.tbt_slo_ms = rc.decode.tbt_slo_ms;
+  dc.kv_threshold = rc.decode.kv_threshold;
+  dc.margin = rc.decode.margin;
+  dc.ladder.freqs_mhz.assign(rc.decode.ladder_mhz, rc.decode.ladder_mhz + rc.decode.n_ladder);
+  TwoTierFactory factory(mpc, dc, ctl_m, pol);
+  SimResult r = simulate_cluster(tr, cl, pol, sim_m, rc.controlled ? &factory : nullptr, opts);
+  TrimmedResult view = trim_steady_state(r, rc.rampup_s);
+  MetricsReport rep = make_report(view, to_slo(rc.slo), "w", "two-tier");
+  o->horizon_ms = r.horizon_ms;
+  o->completed_requests = r.completed_requests;
+  o->generated_tokens = r.generated_tokens;
+  o->n_batches = static_cast<int64_t>(r.batches.size());
+  o->n_idles = static_cast<int64_t>(r.idles.size());
+  o->n_decisions = static_cast<int64_t>(r.decisions.records.size());
+  for (const auto& d : r.decisions.records) o->decisions_by_trigger[static_cast<int>(d.trigger)] += 1;
+  o->has_p99_ttft = rep.p99_ttft_ms.has_value();
+  o->p99_ttft_ms = rep.p99_ttft_ms.value_or(NAN);
+  o->has_p99_tpot = rep.p99_mean_tpot_ms.has_value();
+  o->p99_mean_tpot_ms = rep.p99_mean_tpot_ms.value_or(NAN);
+  o->has_e_first = rep.energy_per_first_token_j.has_value();
+  o->energy_per_first_token_j = rep.energy_per_first_token_j.value_or(NAN);
+  o->has_e_output = rep.energy_per_output_token_j.has_value();
+  o->energy_per_output_token_j = rep.energy_per_output_token_j.value_or(NAN);
+  o->avg_power_prefill_w = rep.avg_power_prefill_w;
+  o->avg_power_decode_w = rep.avg_power_decode_w;
+  o->prefill_energy_j = rep.prefill_energy_j;
+  o->decode_energy_j = rep.decode_energy_j;
+  o->span_ms = rep.span_ms;
+  o->report_completed = rep.completed_requests;
+  o->report_generated = rep.generated_tokens;
+  o->ttft_violations = rep.ttft_violations;
+  o->tpot_violations = rep.tpot_violations;
+  if (req) {
+    // SimResult::requests is ordered by id; emit in trace order
+    for (int64_t i = 0; i < sc.trace.n; ++i) {
+      const int64_t id = sc.trace.requests[i].id;
+      auto it = std::lower_bound(r.requests.begin(), r.requests.end(), id,
+                                 [](const RequestRecord& a, int64_t v) { return a.id < v; });
+      bs_replay_request& q = req[i];
+      std::memset(&q, 0, sizeof q);
+      q.id = id;
+      q.prefill_instance = it->prefill_instance;
+      q.decode_instance = it->decode_instance;
+      q.prefill_done_ms = it->prefill_done_ms.value_or(NAN);
+      q.decode_first_start_ms = it->decode_first_start_ms.value_or(NAN);
+      q.first_token_ms = it->token_times_ms.empty() ? NAN : it->token_times_ms.front();
+      q.last_token_ms = it->token_times_ms.empty() ? NAN : it->token_times_ms.back();
+      q.max_tbt_ms = it->max_tbt_ms().value_or(NAN);
+      q.n_tokens = static_cast<int64_t>(it->token_times_ms.size());
+      q.completed = it->completed ? 1 : 0;
+    }
+  }
+  if (logs) {
+    logs->n_batches = static_cast<int64_t>(r.batches.size());
+    for (int64_t k = 0; k < logs->n_batches && k < logs->batch_cap; ++k) {
+      const BatchRecord& b = r.batches[k];
+      logs->batches[k] = bs_batch_record{b.instance, b.phase == Phase::prefill ? 0 : 1, b.batch_seq, b.start_ms,
+                                         b.end_ms, b.features.n_requests, b.features.sum_len, b.freq_mhz, b.power_w,
+                                         b.energy_j};
+    }
+    logs->n_idles = static_cast<int64_t>(r.idles.size());
+    for (int64_t k = 0; k < logs->n_idles && k < logs->idle_cap; ++k) {
+      const IdleRecord& b = r.idles[k];
+      logs->idles[k] = bs_idle_record{b.instance, b.phase == Phase::prefill ? 0 : 1, b.start_ms, b.end_ms,
+                                      b.freq_mhz, b.power_w, b.energy_j};
+    }
+    logs->n_decisions = static_cast<int64_t>(r.decisions.records.size());
+    for (int64_t k = 0; k < logs->n_decisions && k < logs->decision_cap; ++k) {
+      const DecisionRecord& d = r.decisions.records[k];
+      logs->decisions[k] = bs_decision_record{d.time_ms, d.instance, static_cast<int32_t>(d.trigger),
+                                              d.chosen_freq_mhz, d.feasible ? 1 : 0, 0, d.eval_count};
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int ref_replay(const bs_model_set* sim_models, const bs_model_set* ctl_models, const bs_replay_config* cfgs,
+                          const bs_scenario* sc, int n, bs_replay_summary* out, bs_replay_request* requests,
+                          bs_replay_logs* logs, int n_threads) {
+  return guarded([&] {
+    const ModelSet sim_m = to_models(*sim_models);
+    const ModelSet ctl_m = to_models(ctl_models ? *ctl_models : *sim_models);
+    std::vector<int64_t> req_off(static_cast<std::size_t>(n) + 1, 0);
+    for (int i = 0; i < n; ++i) req_off[i + 1] = req_off[i] + sc[i].trace.n;
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (int i = next++; i < n; i = next++) {
+        std::memset(&out[i], 0, sizeof out[i]);
+        out[i].status = guarded([&] {
+          replay_one(sim_m, ctl_m, cfgs[sc[i].config], sc[i], &out[i], requests ? requests + req_off[i] : nullptr,
+                     logs ? &logs[i] : nullptr);
+        });
+      }
+    };
+    const int t = std::max(1, std::min(n_threads, n));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < t; ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
   });
 }

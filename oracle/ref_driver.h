@@ -46,6 +46,9 @@ int ref_simulate(const bs_model_set* models, const bs_trace* traces, int n, cons
                  const bs_scheduler_policy* policy, const bs_slo* slo, bs_sim_summary* out);
 int ref_solve_max_throughput(const bs_table_entry* table, int n, int total_gpus, double target_rps, double alpha,
                              double max_freq_mhz, int64_t* counts, double* objective_w, int32_t* gpus_used);
+int ref_replay(const bs_model_set* sim_models, const bs_model_set* ctl_models, const bs_replay_config* cfgs,
+               const bs_scenario* sc, int n, bs_replay_summary* out, bs_replay_request* requests,
+               bs_replay_logs* logs, int n_threads);
 #ifdef __cplusplus
 }
 #endif

@@ -225,6 +225,101 @@ class bs_sim_summary(C.Structure):
                 ("busy_energy_j", C.c_double), ("idle_energy_j", C.c_double), ("horizon_ms", C.c_double)]
 
 
+class bs_cluster_instance(C.Structure):
+    _fields_ = [("config", bs_instance_config), ("weight", C.c_double)]
+
+
+class bs_replay_config(C.Structure):
+    _fields_ = [
+        ("mpc", bs_mpc_config),
+        ("decode", bs_decode_config),
+        ("policy", bs_scheduler_policy),
+        ("slo", bs_slo),
+        ("switch_latency_ms", C.c_double),
+        ("horizon_ms", C.c_double),
+        ("rampup_s", C.c_double),
+        ("controlled", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class bs_scenario(C.Structure):
+    _fields_ = [("trace", bs_trace), ("instances", C.POINTER(bs_cluster_instance)), ("n_instances", C.c_int32),
+                ("config", C.c_int32)]
+
+
+class bs_replay_summary(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("has_p99_ttft", C.c_int32),
+        ("has_p99_tpot", C.c_int32),
+        ("has_e_first", C.c_int32),
+        ("has_e_output", C.c_int32),
+        ("_pad", C.c_int32),
+        ("horizon_ms", C.c_double),
+        ("completed_requests", C.c_int64),
+        ("generated_tokens", C.c_int64),
+        ("n_batches", C.c_int64),
+        ("n_idles", C.c_int64),
+        ("n_decisions", C.c_int64),
+        ("decisions_by_trigger", C.c_int64 * 3),
+        ("p99_ttft_ms", C.c_double),
+        ("p99_mean_tpot_ms", C.c_double),
+        ("energy_per_first_token_j", C.c_double),
+        ("energy_per_output_token_j", C.c_double),
+        ("avg_power_prefill_w", C.c_double),
+        ("avg_power_decode_w", C.c_double),
+        ("prefill_energy_j", C.c_double),
+        ("decode_energy_j", C.c_double),
+        ("span_ms", C.c_double),
+        ("report_completed", C.c_int64),
+        ("report_generated", C.c_int64),
+        ("ttft_violations", C.c_int64),
+        ("tpot_violations", C.c_int64),
+    ]
+
+
+class bs_replay_request(C.Structure):
+    _fields_ = [
+        ("id", C.c_int64),
+        ("prefill_instance", C.c_int32),
+        ("decode_instance", C.c_int32),
+        ("prefill_done_ms", C.c_double),
+        ("decode_first_start_ms", C.c_double),
+        ("first_token_ms", C.c_double),
+        ("last_token_ms", C.c_double),
+        ("max_tbt_ms", C.c_double),
+        ("n_tokens", C.c_int64),
+        ("completed", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class bs_batch_record(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("phase", C.c_int32), ("batch_seq", C.c_int64), ("start_ms", C.c_double),
+                ("end_ms", C.c_double), ("n_requests", C.c_int64), ("sum_len", C.c_int64), ("freq_mhz", C.c_double),
+                ("power_w", C.c_double), ("energy_j", C.c_double)]
+
+
+class bs_idle_record(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("phase", C.c_int32), ("start_ms", C.c_double), ("end_ms", C.c_double),
+                ("freq_mhz", C.c_double), ("power_w", C.c_double), ("energy_j", C.c_double)]
+
+
+class bs_decision_record(C.Structure):
+    _fields_ = [("time_ms", C.c_double), ("instance", C.c_int32), ("trigger", C.c_int32),
+                ("chosen_freq_mhz", C.c_double), ("feasible", C.c_int32), ("_pad", C.c_int32),
+                ("eval_count", C.c_int64)]
+
+
+class bs_replay_logs(C.Structure):
+    _fields_ = [
+        ("batches", C.POINTER(bs_batch_record)), ("batch_cap", C.c_int64), ("n_batches", C.c_int64),
+        ("idles", C.POINTER(bs_idle_record)), ("idle_cap", C.c_int64), ("n_idles", C.c_int64),
+        ("decisions", C.POINTER(bs_decision_record)), ("decision_cap", C.c_int64), ("n_decisions", C.c_int64),
+    ]
+
+
 ctx_t = C.c_void_p
 models_t = C.c_void_p
 
@@ -281,4 +376,7 @@ PROTOTYPES = [
     ("bs_placement_max_throughput", C.c_int, [ctx_t, C.POINTER(bs_table_entry), C.c_int, C.c_int, C.c_double,
                                               C.c_double, C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                               C.POINTER(C.c_int32)]),
+    ("bs_replay", C.c_int, [ctx_t, models_t, models_t, C.POINTER(bs_replay_config), C.c_int, C.POINTER(bs_scenario),
+                            C.c_int, C.POINTER(bs_replay_summary), C.POINTER(bs_replay_request),
+                            C.POINTER(bs_replay_logs)]),
 ]

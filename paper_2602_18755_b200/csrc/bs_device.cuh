@@ -189,9 +189,10 @@ struct DProblem {
   int tp;
   int run_active;
   int n_wait;
-  int n_run;
+  int n_run;  // < 0: the running batch is summarised by run_minarr / run_ncomp
   int cfg;
-  int _pad;
+  int run_ncomp;      // completing members of the running batch (when n_run < 0)
+  double run_minarr;  // their smallest arrival, +inf if none (when n_run < 0)
 };
 
 // Per-problem projection + (k, f) tables, built on device.

@@ -33,12 +33,6 @@ __host__ __device__ inline int sweep_levels(int K, int nc) {
   return np > 16777216.0 ? 3 : 2;
 }
 
-__host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) {
-  unsigned long long r = 1;
-  for (int i = 0; i < e; ++i) r *= b;
-  return r;
-}
-
 // Frontier lists in HBM, structure of arrays.
 struct Frontier {
   int* d;                    // problem

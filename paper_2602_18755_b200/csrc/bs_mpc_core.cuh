@@ -1,0 +1,418 @@
+// bs_mpc_core.cuh — prefill-MPC building blocks shared by the MPC kernels
+// (bs_mpc.cu) and the cluster replay (bs_replay.cu): project_batches on the
+// device, the per-decision (k, f) tables, the assignment evaluator and the
+// block-cooperative greedy search.  Included inside each translation unit's
+// anonymous namespace.  Reference: proj/include/pdsim/dvfs.hpp.
+#pragma once
+
+constexpr int kGreedyThreads = 256;
+
+__host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) {
+  unsigned long long r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// projection: project_batches (dvfs.hpp:63-100) over form_prefill_batch
+// (scheduler.hpp:40-66).  Only the queue head can be partially consumed (a
+// partial chunk ends a batch), so the state is (head, head_remaining).
+// ---------------------------------------------------------------------------
+__device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting* W, const DRunning* R, DTables* T) {
+  int K = 0;
+  if (pr.run_active) {
+    T->n_req[0] = pr.run_n;
+    T->sum_len[0] = pr.run_sum;
+    T->wf[0] = pr.run_wr;
+    double mn = INFINITY;
+    int nc = 0;
+    if (pr.n_run < 0) {  // summarised by the caller (the cluster replay)
+      mn = pr.run_minarr;
+      nc = pr.run_ncomp;
+    }
+    for (int i = 0; i < pr.n_run; ++i) {
+      if (R[i].completes) {
+        const double a = R[i].arrival;
+        mn = a < mn ? a : mn;
+        ++nc;
+      }
+    }
+    T->minarr[0] = mn;
+    T->ncomp[0] = nc;
+    K = 1;
+  }
+  int head = 0;
+  long long head_rem = pr.n_wait > 0 ? W[0].remaining : 0;
+  while (head < pr.n_wait && K < c.horizon) {
+    long long tokens = 0, npick = 0, sum = 0;
+    int consumed = 0, ncomp = 0;
+    double mn = INFINITY;
+    long long partial_rem = -1;
+    for (int i = head; i < pr.n_wait; ++i) {
+      if (npick >= c.max_batch_requests) break;
+      const long long rem = i == head ? head_rem : W[i].remaining;
+      if (rem <= 0) {
+        T->K = K;
+        return BS_SIMULATION_ERROR;  // scheduler.hpp:47
+      }
+      long long take;
+      if (c.chunking) {
+        const long long room = c.max_batch_tokens - tokens;
+        if (room <= 0) break;
+        take = rem < room ? rem : room;
+        tokens += take;
+      } else {
+        if (rem > c.max_batch_tokens) {
+          if (npick == 0) {
+            ++npick;
+            sum += rem;
+            ++ncomp;
+            const double a = W[i].arrival;
+            mn = a < mn ? a : mn;
+            ++consumed;
+          }
+          break;
+        }
+        if (tokens + rem > c.max_batch_tokens) break;
+        take = rem;
+        tokens += rem;
+      }
+      ++npick;
+      sum += take;
+      if (take == rem) {
+        ++ncomp;
+        const double a = W[i].arrival;
+        mn = a < mn ? a : mn;
+        ++consumed;
+      } else {
+        partial_rem = rem - take;
+        break;
+      }
+    }
+    T->n_req[K] = npick;
+    T->sum_len[K] = sum;
+    T->wf[K] = 1.0;
+    T->minarr[K] = mn;
+    T->ncomp[K] = ncomp;
+    ++K;
+    head += consumed;
+    if (partial_rem >= 0) {
+      head_rem = partial_rem;
+    } else if (head < pr.n_wait) {
+      head_rem = W[head].remaining;
+    }
+  }
+  T->K = K;
+  return BS_OK;
+}
+
+// Tables for one problem, written by a CTA.  Projection by thread 0.
+__device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
+                             const DRunning* R, DTables* T, int* s_status) {
+  if (threadIdx.x == 0) {
+    T->nc = c.nc;
+    T->ttft = c.ttft;
+    int st = project_dev(pr, c, W, R, T);
+    if (st == BS_OK && (m.grid[0].bad_axis || m.grid[2].bad_axis) && T->K > 0) st = BS_MODEL_ERROR;
+    *s_status = st;
+    for (int k = 0; k < kMaxK; ++k) {
+      T->bad_lat[k] = 0u;
+      T->bad_pow[k] = 0u;
+    }
+  }
+  __syncthreads();
+  const int K = T->K;
+  const int nc = c.nc;
+  if (*s_status != BS_OK) return;
+  for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
+    const int k = e / nc, f = e - k * nc;
+    const Query q = make_query(T->n_req[k], T->sum_len[k], pr.tp, c.cand[f]);
+    const double L = interp(m.grid[0], q, nullptr);
+    const double P = interp(m.grid[2], q, nullptr);
+    if (!model_value_ok(L)) atomicOr(&T->bad_lat[k], 1u << f);
+    if (!model_value_ok(P)) atomicOr(&T->bad_pow[k], 1u << f);
+    const double A = __dmul_rn(T->wf[k], L);                               // dvfs.hpp:112-113, 154-155
+    T->A[k][f] = A;
+    T->P[k][f] = P;
+    T->E[k][f] = __dmul_rn(A, P);                                          // dvfs.hpp:167
+    T->B0[k][f] = __dmul_rn(A, c.one_plus_margin);                         // dvfs.hpp:115
+    T->B1[k][f] = __dmul_rn(__dadd_rn(A, c.switch_ms), c.one_plus_margin);  // dvfs.hpp:114-115
+    if (k == 0) T->T1[f] = __dadd_rn(pr.now, c.cand[f] != pr.cur_freq ? T->B1[0][f] : T->B0[0][f]);
+  }
+  __syncthreads();
+  // per-level sorted order of the switched steps: one thread per (k, f)
+  // computes its rank (ties by index), then scatters
+  int finite = 1;
+  for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
+    const int k = e / nc, f = e - k * nc;
+    const double* key = k == 0 ? T->T1 : T->B1[k];
+    const double v = key[f];
+    if (!isfinite(v) || !isfinite(T->B0[k][f])) finite = 0;
+    int r = 0;
+    for (int g = 0; g < nc; ++g) {
+      const double w = key[g];
+      r += (w < v || (w == v && g < f)) ? 1 : 0;
+    }
+    T->sb[k][r] = v;
+    T->ord[k][r] = static_cast<unsigned char>(f);
+    T->rank[k][f] = static_cast<unsigned char>(r);
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double amax = 0.0, pmin = INFINITY;
+    for (int f = 0; f < nc; ++f) {
+      amax = T->A[k][f] > amax ? T->A[k][f] : amax;
+      pmin = T->P[k][f] < pmin ? T->P[k][f] : pmin;
+    }
+    T->amax[k] = amax;
+    T->pmin_lo[k] = __dmul_rn(pmin, 1.0 - 0x1p-50);
+  }
+  const int all_finite = __syncthreads_and(finite);
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    for (int k = 0; k < K; ++k)
+      for (int f = 0; f < nc; ++f) {
+        const double A = T->A[k][f];
+        if (!(A >= 0.0) || !isfinite(A) || !isfinite(T->E[k][f])) ok = 0;
+      }
+    T->filter_ok = ok;
+    T->sorted_ok = all_finite && isfinite(T->ttft);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// greedy_freq_select (dvfs.hpp:185-259): one CTA per decision.
+// ---------------------------------------------------------------------------
+
+// Evaluates one assignment (ascending candidate indices).  Returns
+// 0 infeasible, 1 feasible; *err = 0 none, 1 latency, 2 power -- the first
+// ModelError the reference would raise (meets_slo's predict_latency calls
+// in k order up to the first violation, then time_weighted_power's
+// predict_latency/predict_power pairs in k order).
+__device__ int eval_assignment(const DTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* idx,
+                               double* obj, int* err) {
+  *err = 0;
+  double t = pr.now;
+  const int K = T.K;
+  bool feas = true;
+  for (int k = 0; k < K; ++k) {
+    const int f = idx[k];
+    if ((T.bad_lat[k] >> f) & 1u) {
+      *err = 1;
+      return 0;
+    }
+    const bool sw = k == 0 ? (c.cand[f] != pr.cur_freq) : (f != idx[k - 1]);
+    t = __dadd_rn(t, sw ? T.B1[k][f] : T.B0[k][f]);
+    if (__dsub_rn(t, T.minarr[k]) > T.ttft) {
+      feas = false;
+      break;
+    }
+  }
+  if (!feas) return 0;
+  double num = 0.0, den = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const int f = idx[k];
+    if ((T.bad_lat[k] >> f) & 1u) {
+      *err = 1;
+      return 1;
+    }
+    if ((T.bad_pow[k] >> f) & 1u) {
+      *err = 2;
+      return 1;
+    }
+    num = __dadd_rn(num, T.E[k][f]);
+    den = __dadd_rn(den, T.A[k][f]);
+  }
+  *obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+  return 1;
+}
+
+// objective only (tw_power of an assignment, errors ignored)
+__device__ double tw_objective(const DTables& T, const unsigned char* idx) {
+  double num = 0.0, den = 0.0;
+  for (int k = 0; k < T.K; ++k) {
+    num = __dadd_rn(num, T.E[k][idx[k]]);
+    den = __dadd_rn(den, T.A[k][idx[k]]);
+  }
+  return den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+}
+
+// Shared state of one block-cooperative greedy decision.
+struct GreedyShared {
+  DTables T;
+  int status;
+  int np;
+  int init_feas;
+  int accepted;
+  double obj;
+  unsigned long long feas;
+  unsigned long long err;  // min over (code << 2 | type) of erroring mutations
+  unsigned long long wbo[kGreedyThreads / 32], wbc[kGreedyThreads / 32];
+  int pos[kMaxK];
+  unsigned char cur[kMaxK];
+};
+
+// greedy_freq_select (dvfs.hpp:185-259) for one decision by the whole CTA
+// (blockDim.x <= kGreedyThreads, a multiple of 32); every thread must call
+// it.  Results in *o (and per-level stats in lv when non-null); o may live
+// in shared or global memory.  Returns with the block synchronised.
+__device__ void greedy_block(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
+                             const DRunning* R, GreedyShared& S, DMpcOut* o, DLevel* lv) {
+  build_tables(m, pr, c, W, R, &S.T, &S.status);
+  const int K = S.T.K, nc = c.nc;
+  if (threadIdx.x == 0) {
+    memset(o, 0, sizeof *o);
+    o->status = S.status;
+    o->K = K;
+  }
+  if (S.status != BS_OK) return;
+  if (K == 0) {  // dvfs.hpp:194-197
+    if (threadIdx.x == 0) o->feasible = 1;
+    return;
+  }
+  // all-max initialization (dvfs.hpp:201-205)
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < K; ++k) S.cur[k] = static_cast<unsigned char>(nc - 1);
+    double obj = 0.0;
+    int err;
+    const int feas = eval_assignment(S.T, pr, c, S.cur, &obj, &err);
+    if (!feas && !err) {
+      // infeasible: objective still computed (dvfs.hpp:204), may raise
+      for (int k = 0; k < K && !err; ++k) {
+        if ((S.T.bad_lat[k] >> (nc - 1)) & 1u) err = 1;
+        else if ((S.T.bad_pow[k] >> (nc - 1)) & 1u) err = 2;
+      }
+      obj = tw_objective(S.T, S.cur);
+    }
+    if (err) o->status = BS_MODEL_ERROR;
+    S.init_feas = feas;
+    S.obj = obj;
+    o->feasible = feas;
+    o->eval_count = 1;
+    o->objective = obj;
+  }
+  __syncthreads();
+  if (o->status != BS_OK) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (S.init_feas && nc > 1) {
+    const int last_level = nc >= 3 ? nc - 2 : 1;
+    // avail (descending) position j <-> ascending index nc - 1 - j
+    for (int l = 1; l <= last_level; ++l) {
+      const int target = nc - l;  // avail[l-1]
+      const int r1 = nc - 1 - l;  // avail[l]
+      const int r2 = l + 1 < nc ? nc - 2 - l : -1;
+      const unsigned long long base = r2 >= 0 ? 3ull : 2ull;
+      if (threadIdx.x == 0) {
+        int np = 0;
+        for (int k = 0; k < K; ++k)
+          if (S.cur[k] == target) S.pos[np++] = k;
+        S.np = np;
+        S.feas = 0;
+        S.err = ~0ull;
+      }
+      __syncthreads();
+      const int np = S.np;
+      if (np == 0) break;  // dvfs.hpp:222
+      const unsigned long long combos = ipow(base, np);
+      unsigned char mut[kMaxK];
+      for (int k = 0; k < K; ++k) mut[k] = S.cur[k];
+      unsigned long long bo = ~0ull, bc = ~0ull, feas = 0, errkey = ~0ull;
+      for (unsigned long long code = 1 + threadIdx.x; code < combos; code += blockDim.x) {
+        unsigned long long cc = code, lex = 0;
+        for (int i = 0; i < np; ++i) {  // digit i -> S.pos[i], least significant first (dvfs.hpp:233-237)
+          const unsigned long long digit = cc % base;
+          cc /= base;
+          mut[S.pos[i]] = static_cast<unsigned char>(digit == 0 ? target : (digit == 1 ? r1 : r2));
+        }
+        // lexicographic key of the frequency vector: positions in batch
+        // order, smaller frequency (larger digit) first
+        for (int i = 0; i < np; ++i) {
+          const unsigned char v = mut[S.pos[i]];
+          const unsigned long long digit = v == target ? 0 : (v == r1 ? 1 : 2);
+          lex = lex * base + (base - 1 - digit);
+        }
+        double obj = 0.0;
+        int err;
+        const int ok = eval_assignment(S.T, pr, c, mut, &obj, &err);
+        if (err) {
+          const unsigned long long ek = (code << 2) | static_cast<unsigned long long>(err);
+          errkey = ek < errkey ? ek : errkey;
+          continue;
+        }
+        if (!ok) continue;
+        ++feas;
+        const unsigned long long ob = static_cast<unsigned long long>(__double_as_longlong(obj));
+        if (key_less(ob, lex, bo, bc)) {
+          bo = ob;
+          bc = lex;
+        }
+      }
+      // block reduction of (obj, lex), feasible count, first error
+#pragma unroll
+      for (int of = 16; of > 0; of >>= 1) {
+        const unsigned long long oo = __shfl_xor_sync(0xffffffffu, bo, of);
+        const unsigned long long oc = __shfl_xor_sync(0xffffffffu, bc, of);
+        if (key_less(oo, oc, bo, bc)) {
+          bo = oo;
+          bc = oc;
+        }
+        feas += __shfl_xor_sync(0xffffffffu, feas, of);
+        const unsigned long long oe = __shfl_xor_sync(0xffffffffu, errkey, of);
+        errkey = oe < errkey ? oe : errkey;
+      }
+      if (lane == 0) {
+        S.wbo[warp] = bo;
+        S.wbc[warp] = bc;
+        atomicAdd(&S.feas, feas);
+        atomicMin(&S.err, errkey);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+          if (key_less(S.wbo[w], S.wbc[w], bo, bc)) {
+            bo = S.wbo[w];
+            bc = S.wbc[w];
+          }
+        // every mutation of the level is evaluated before acceptance
+        o->eval_count += static_cast<long long>(combos - 1);
+        DLevel L;
+        L.k_prime = np;
+        L.replaced_mhz = c.cand[target];
+        L.mutations = static_cast<long long>(combos - 1);
+        L.feasible_mutations = static_cast<long long>(S.feas);
+        L.accepted = 0;
+        if (S.err != ~0ull) {
+          o->status = BS_MODEL_ERROR;
+          o->n_levels = -static_cast<int>(S.err & 3ull);  // error type for the message
+        } else {
+          // improved iff best_p < cur or (== and lex_less(best, cur)); every
+          // mutation is lexicographically below the current assignment
+          const double bp = __longlong_as_double(static_cast<long long>(bo));
+          if (bo != ~0ull && bp <= S.obj) {
+            // decode the lex key back into digits
+            unsigned long long lx = bc;
+            for (int i = np - 1; i >= 0; --i) {
+              const unsigned long long digit = base - 1 - (lx % base);
+              lx /= base;
+              S.cur[S.pos[i]] = static_cast<unsigned char>(digit == 0 ? target : (digit == 1 ? r1 : r2));
+            }
+            S.obj = bp;
+            o->objective = bp;
+            L.accepted = 1;
+          }
+          if (lv) lv[o->n_levels] = L;
+          o->n_levels += 1;
+        }
+        S.accepted = L.accepted;  // broadcast acceptance (not S.feas: thread 0 resets that at the
+                                  // next level while slower warps may still be testing this flag)
+      }
+      __syncthreads();
+      if (o->status != BS_OK || S.accepted == 0) break;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && o->status == BS_OK) {
+    for (int k = 0; k < K; ++k) o->idx[k] = S.cur[k];
+  }
+  __syncthreads();
+}

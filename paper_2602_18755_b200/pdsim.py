@@ -1421,3 +1421,188 @@ def plan_window(history: Trace, total_gpus: int, slo: SLOSpec, models: ModelSet,
     res.table = build_config_table(candidates, probe, slo, models, opts.policy, opts.search, opts.parallel_table, device)
     res.plan = solve_placement(PlacementProblem(res.table, total_gpus, res.predicted_peak_rps, opts.alpha), device)
     return res
+
+
+# ---------------------------------------------------------------------------
+# simulator.hpp:741-893 + metrics.hpp:71-156: cluster replay on the device
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ClusterSpec:
+    """ClusterSpec (simulator.hpp:746-756): index = instance id."""
+
+    instances: list = field(default_factory=list)
+
+
+@dataclass
+class SimOptions:
+    """SimOptions (simulator.hpp:126-130)."""
+
+    switch_latency_ms: float = 30.0
+    horizon_ms: float = -1.0
+
+
+@dataclass
+class MetricsReport:
+    """MetricsReport (metrics.hpp:104-119); absent optionals are None."""
+
+    p99_ttft_ms: Optional[float] = None
+    p99_mean_tpot_ms: Optional[float] = None
+    energy_per_first_token_j: Optional[float] = None
+    energy_per_output_token_j: Optional[float] = None
+    avg_power_prefill_w: float = 0.0
+    avg_power_decode_w: float = 0.0
+    prefill_energy_j: float = 0.0
+    decode_energy_j: float = 0.0
+    span_ms: float = 0.0
+    completed_requests: int = 0
+    generated_tokens: int = 0
+    ttft_violations: int = 0
+    tpot_violations: int = 0
+
+
+@dataclass
+class ReplayScenario:
+    """One simulate_cluster call (run_policy, runner.hpp:112-122) followed by
+    make_report(trim_steady_state(sim, rampup_s), slo)."""
+
+    trace: Trace
+    cluster: ClusterSpec
+    policy: SchedulerPolicy = field(default_factory=SchedulerPolicy)
+    controllers: Optional[TwoTierFactory] = None  # None: fixed base frequencies
+    opts: SimOptions = field(default_factory=SimOptions)
+    slo: SLOSpec = field(default_factory=SLOSpec)
+    rampup_s: float = 30.0
+
+
+@dataclass
+class ReplayResult:
+    status: int = 0
+    horizon_ms: float = 0.0
+    completed_requests: int = 0
+    generated_tokens: int = 0
+    n_batches: int = 0
+    n_idles: int = 0
+    n_decisions: int = 0
+    decisions_by_trigger: tuple = (0, 0, 0)
+    report: MetricsReport = field(default_factory=MetricsReport)
+    requests: Optional[list] = None   # bs_replay_request per trace request (trace order)
+    batches: Optional[list] = None    # bs_batch_record, SimResult order
+    idles: Optional[list] = None
+    decisions: Optional[list] = None
+
+
+def _opt(has: int, v: float) -> Optional[float]:
+    return float(v) if has else None
+
+
+def c_replay_config(s: ReplayScenario, keep: list) -> _abi.bs_replay_config:
+    c = _abi.bs_replay_config()
+    f = s.controllers
+    if f is not None:
+        c.mpc = c_mpc_config(f.mpc, keep)
+        c.decode = c_decode_config(f.decode, keep)
+        c.controlled = 1
+    c.policy = c_policy(s.policy)
+    c.slo = c_slo(s.slo)
+    c.switch_latency_ms = s.opts.switch_latency_ms
+    c.horizon_ms = s.opts.horizon_ms
+    c.rampup_s = s.rampup_s
+    return c
+
+
+def summary_from_c(o: _abi.bs_replay_summary) -> ReplayResult:
+    rep = MetricsReport(_opt(o.has_p99_ttft, o.p99_ttft_ms), _opt(o.has_p99_tpot, o.p99_mean_tpot_ms),
+                        _opt(o.has_e_first, o.energy_per_first_token_j),
+                        _opt(o.has_e_output, o.energy_per_output_token_j), o.avg_power_prefill_w,
+                        o.avg_power_decode_w, o.prefill_energy_j, o.decode_energy_j, o.span_ms, o.report_completed,
+                        o.report_generated, o.ttft_violations, o.tpot_violations)
+    return ReplayResult(o.status, o.horizon_ms, o.completed_requests, o.generated_tokens, o.n_batches, o.n_idles,
+                        o.n_decisions, tuple(o.decisions_by_trigger), rep)
+
+
+def c_replay_inputs(scenarios: Sequence[ReplayScenario], keep: list) -> tuple:
+    """(bs_replay_config[n], bs_scenario[n], total requests): one configuration per scenario."""
+    n = len(scenarios)
+    cfgs = (_abi.bs_replay_config * n)()
+    scs = (_abi.bs_scenario * n)()
+    total = 0
+    for i, s in enumerate(scenarios):
+        cfgs[i] = c_replay_config(s, keep)
+        scs[i].trace = c_trace(s.trace, keep)
+        inst = (_abi.bs_cluster_instance * max(1, len(s.cluster.instances)))()
+        for j, ci in enumerate(s.cluster.instances):
+            inst[j].config.phase, inst[j].config.tp = int(ci.config.phase), ci.config.tp
+            inst[j].config.base_freq_mhz, inst[j].weight = ci.config.base_freq_mhz, ci.weight
+        keep.append(inst)
+        scs[i].instances = C.cast(inst, C.POINTER(_abi.bs_cluster_instance))
+        scs[i].n_instances = len(s.cluster.instances)
+        scs[i].config = i
+        total += len(s.trace.requests)
+    return cfgs, scs, total
+
+
+def c_replay_logs(scenarios: Sequence[ReplayScenario], keep: list) -> C.Array:
+    lg = (_abi.bs_replay_logs * len(scenarios))()
+    for i, s in enumerate(scenarios):
+        cap = sum(r.output_len for r in s.trace.requests) + 4 * len(s.trace.requests) + 1024
+        for name, typ, cap_name in (("batches", _abi.bs_batch_record, "batch_cap"),
+                                    ("idles", _abi.bs_idle_record, "idle_cap"),
+                                    ("decisions", _abi.bs_decision_record, "decision_cap")):
+            arr = (typ * cap)()
+            keep.append(arr)
+            setattr(lg[i], name, C.cast(arr, C.POINTER(typ)))
+            setattr(lg[i], cap_name, cap)
+    return lg
+
+
+def replay(scenarios: Sequence[ReplayScenario], models: ModelSet, device: Device | None = None,
+           requests: bool = False, logs: bool = False, raise_errors: bool = True) -> list:
+    """simulate_cluster + trim_steady_state + make_report for every scenario
+    in one device call (bs_replay).  All scenarios share the simulator's
+    ModelSet and the controllers' ModelSet (TwoTierFactory.models)."""
+    dev = device or default_device()
+    n = len(scenarios)
+    if n == 0:
+        return []
+    ctl = None
+    for s in scenarios:
+        if s.controllers is not None:
+            if ctl is not None and s.controllers.models is not ctl:
+                raise ParameterError("replay: one controller ModelSet per call")
+            ctl = s.controllers.models
+    keep: list = []
+    cfgs, scs, total = c_replay_inputs(scenarios, keep)
+    out = (_abi.bs_replay_summary * n)()
+    reqs = (_abi.bs_replay_request * max(1, total))() if requests else None
+    lg = c_replay_logs(scenarios, keep) if logs else None
+    mh = dev.models(models)
+    ch = dev.models(ctl) if ctl is not None else mh
+    rc = dev._lib.bs_replay(dev.handle, mh, ch, cfgs, n, scs, n, out, reqs, lg)
+    if rc != _abi.BS_OK and (raise_errors or rc == _abi.BS_CUDA_ERROR):
+        raise_status(rc, dev.error())
+    res = [summary_from_c(out[i]) for i in range(n)]
+    q = 0
+    for i, s in enumerate(scenarios):
+        if requests:
+            res[i].requests = [reqs[q + k] for k in range(len(s.trace.requests))]
+            q += len(s.trace.requests)
+        if logs:
+            L = lg[i]
+            if L.n_batches > L.batch_cap or L.n_idles > L.idle_cap or L.n_decisions > L.decision_cap:
+                raise SimulationError("replay: log capacity exceeded")
+            res[i].batches = [L.batches[k] for k in range(L.n_batches)]
+            res[i].idles = [L.idles[k] for k in range(L.n_idles)]
+            res[i].decisions = [L.decisions[k] for k in range(L.n_decisions)]
+    return res
+
+
+def simulate_cluster_report(trace: Trace, cluster: ClusterSpec, policy: SchedulerPolicy, models: ModelSet,
+                            controllers: Optional[TwoTierFactory] = None, opts: SimOptions | None = None,
+                            slo: SLOSpec | None = None, rampup_s: float = 30.0,
+                            device: Device | None = None) -> ReplayResult:
+    """One scenario of replay(): run_policy (runner.hpp:112-122) + the
+    window report (runner.hpp:131-133)."""
+    return replay([ReplayScenario(trace, cluster, policy, controllers, opts or SimOptions(), slo or SLOSpec(),
+                                  rampup_s)], models, device, requests=True)[0]

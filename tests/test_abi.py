@@ -20,7 +20,9 @@ HEADER = ROOT / "include" / "biscale_gpu.h"
 STRUCTS = ["bs_grid", "bs_idle_entry", "bs_model_set", "bs_features", "bs_scheduler_policy", "bs_mpc_config",
            "bs_waiting", "bs_snapshot", "bs_mpc_problem", "bs_level_stats", "bs_mpc_result", "bs_projected_batch",
            "bs_decode_config", "bs_decode_query", "bs_decode_result", "bs_request", "bs_trace", "bs_length_dist",
-           "bs_slo", "bs_goodput_search", "bs_instance_config", "bs_table_entry", "bs_sim_summary"]
+           "bs_slo", "bs_goodput_search", "bs_instance_config", "bs_table_entry", "bs_sim_summary",
+           "bs_cluster_instance", "bs_replay_config", "bs_scenario", "bs_replay_summary", "bs_replay_request",
+           "bs_batch_record", "bs_idle_record", "bs_decision_record", "bs_replay_logs"]
 
 
 def declared_functions() -> set:
