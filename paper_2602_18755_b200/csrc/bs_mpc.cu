@@ -23,6 +23,7 @@
 #include <cstring>
 
 #include "bs_internal.h"
+#include "bs_sim.cuh"
 
 using namespace bs;
 

@@ -107,8 +107,12 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
 }
 
 // Tables for one problem, written by a CTA.  Projection by thread 0.
+// fl / fp (optional): the latency / power grids reduced to (pr.tp, cand[f])
+// for every candidate f (FastGrid, bs_sim.cuh) -- bit-identical values with
+// 2^(active axes) corners instead of 2^rank.
 __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
-                             const DRunning* R, DTables* T, int* s_status) {
+                             const DRunning* R, DTables* T, int* s_status, const FastGrid* fl = nullptr,
+                             const FastGrid* fp = nullptr) {
   if (threadIdx.x == 0) {
     T->nc = c.nc;
     T->ttft = c.ttft;
@@ -126,9 +130,15 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
   if (*s_status != BS_OK) return;
   for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
     const int k = e / nc, f = e - k * nc;
-    const Query q = make_query(T->n_req[k], T->sum_len[k], pr.tp, c.cand[f]);
-    const double L = interp(m.grid[0], q, nullptr);
-    const double P = interp(m.grid[2], q, nullptr);
+    double L, P;
+    if (fl) {
+      L = fast_interp(fl[f], T->n_req[k], T->sum_len[k]);
+      P = fast_interp(fp[f], T->n_req[k], T->sum_len[k]);
+    } else {
+      const Query q = make_query(T->n_req[k], T->sum_len[k], pr.tp, c.cand[f]);
+      L = interp(m.grid[0], q, nullptr);
+      P = interp(m.grid[2], q, nullptr);
+    }
     if (!model_value_ok(L)) atomicOr(&T->bad_lat[k], 1u << f);
     if (!model_value_ok(P)) atomicOr(&T->bad_pow[k], 1u << f);
     const double A = __dmul_rn(T->wf[k], L);                               // dvfs.hpp:112-113, 154-155
@@ -257,8 +267,9 @@ struct GreedyShared {
 // it.  Results in *o (and per-level stats in lv when non-null); o may live
 // in shared or global memory.  Returns with the block synchronised.
 __device__ void greedy_block(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
-                             const DRunning* R, GreedyShared& S, DMpcOut* o, DLevel* lv) {
-  build_tables(m, pr, c, W, R, &S.T, &S.status);
+                             const DRunning* R, GreedyShared& S, DMpcOut* o, DLevel* lv,
+                             const FastGrid* fl = nullptr, const FastGrid* fp = nullptr) {
+  build_tables(m, pr, c, W, R, &S.T, &S.status, fl, fp);
   const int K = S.T.K, nc = c.nc;
   if (threadIdx.x == 0) {
     memset(o, 0, sizeof *o);

@@ -35,6 +35,7 @@
 #include <vector>
 
 #include "bs_internal.h"
+#include "bs_sim.cuh"
 
 using namespace bs;
 
@@ -209,6 +210,21 @@ __device__ __forceinline__ bool predict(const DGrid& g, long long n, long long s
   return true;
 }
 
+__device__ __forceinline__ bool predict_fast(const FastGrid& g, long long n, long long sum, double* out, int* err,
+                                             int kind) {
+  if (g.bad) {
+    *err = kErrAxis;
+    return false;
+  }
+  const double v = fast_interp(g, n, sum);
+  if (!model_value_ok(v)) {
+    *err = kind;
+    return false;
+  }
+  *out = v;
+  return true;
+}
+
 // predict_idle_power (perfmodel.hpp:274-288) with its two ModelErrors.
 __device__ __forceinline__ bool idle_w(const DIdle& m, int tp, double f, double* out, int* err) {
   for (int i = 0; i < m.n_entries; ++i) {
@@ -285,12 +301,20 @@ __device__ __forceinline__ double energy_j(double p, double from, double to) {  
   return __ddiv_rn(__dmul_rn(p, __dsub_rn(to, from)), 1000.0);
 }
 
+// Idle power at a frequency: the generic lookup, or a per-slot cache.
+struct IdleDirect {
+  const DIdle* m;
+  int tp;
+  __device__ bool operator()(double f, double* p, int* err) const { return idle_w(*m, tp, f, p, err); }
+};
+
 // InstanceSim::record_idle (simulator.hpp:205-209).
-__device__ bool record_idle(Writer& w, const DModels& m, int tp, const FreqBook& fb, double from, double to) {
+template <class IdleFn>
+__device__ bool record_idle(Writer& w, const IdleFn& idle, const FreqBook& fb, double from, double to) {
   if (to <= from) return true;
   double p;
   int err = 0;
-  if (!idle_w(m.idle, tp, fb.in_force, &p, &err)) {
+  if (!idle(fb.in_force, &p, &err)) {
     w.fail(BS_MODEL_ERROR, err);
     return false;
   }
@@ -299,16 +323,60 @@ __device__ bool record_idle(Writer& w, const DModels& m, int tp, const FreqBook&
 }
 
 // InstanceSim::idle_until (simulator.hpp:258-267).
-__device__ bool idle_until(Writer& w, const DModels& m, int tp, FreqBook& fb, double& now, double to) {
+template <class IdleFn>
+__device__ bool idle_until(Writer& w, const IdleFn& idle, FreqBook& fb, double& now, double to) {
   while (fb.next() < to) {
     const double t = fb.next();
-    if (!record_idle(w, m, tp, fb, now, t)) return false;
+    if (!record_idle(w, idle, fb, now, t)) return false;
     fb.activate();
     now = t;
   }
-  if (!record_idle(w, m, tp, fb, now, to)) return false;
+  if (!record_idle(w, idle, fb, now, to)) return false;
   now = to;
   return true;
+}
+
+// Per-frequency model caches of one instance: every grid the instance
+// queries reduced to its (tp, f) (FastGrid: bit-identical, 2^(active axes)
+// corners, independent knot loads) plus the idle power, for the frequencies
+// the instance can run at or the controller can pick.
+struct PreCache {  // views into the prefill CTA's dynamic shared memory (ns slots each)
+  int ns;
+  double* f;
+  double* idle;
+  int* idle_err;
+  FastGrid *lat, *pw;    // simulator: prefill latency / power
+  FastGrid *clat, *cpw;  // controller: prefill latency / power
+};
+
+__host__ __device__ inline size_t pre_cache_bytes(int ns) {
+  return static_cast<size_t>(ns) * (4 * sizeof(FastGrid) + 2 * sizeof(double) + sizeof(int)) + 16;
+}
+
+__device__ inline PreCache pre_cache_at(unsigned char* base, int ns) {
+  PreCache c;
+  c.ns = ns;
+  c.lat = reinterpret_cast<FastGrid*>(base);
+  c.pw = c.lat + ns;
+  c.clat = c.pw + ns;
+  c.cpw = c.clat + ns;
+  c.f = reinterpret_cast<double*>(c.cpw + ns);
+  c.idle = c.f + ns;
+  c.idle_err = reinterpret_cast<int*>(c.idle + ns);
+  return c;
+}
+
+struct DecSlot {
+  double f;
+  double idle;
+  int idle_err;
+  FastGrid lat, pw, clat;  // simulator latency / power, controller latency (decode)
+};
+
+__device__ __forceinline__ int find_slot(const double* fs, int ns, double f) {
+  for (int i = 0; i < ns; ++i)
+    if (fs[i] == f) return i;
+  return -1;
 }
 
 __device__ void save_state(DInstState* s, const Writer& w, double now, const FreqBook& fb) {
@@ -337,6 +405,8 @@ struct PrefillSim {
   const DReplay* R;
   const DInst* I;
   const DRCfg* C;
+  const PreCache* gc;
+  int slot;  // cache slot of the in-force frequency
   Writer w;
   FreqBook fb;
   double now;
@@ -356,10 +426,12 @@ struct PrefillSim {
   __device__ double arrival_of(long long i) const { return R->arrival[R->plist[I->list0 + i]]; }
   __device__ long long input_of(long long i) const { return R->input[R->plist[I->list0 + i]]; }
 
-  __device__ void init(const DReplay* r, const DInst* i, const DRCfg* c) {
+  __device__ void init(const DReplay* r, const DInst* i, const DRCfg* c, const PreCache* cache) {
     R = r;
     I = i;
     C = c;
+    gc = cache;
+    slot = find_slot(gc->f, gc->ns, i->base_freq);
     w.init(r, i);
     fb.in_force = i->base_freq;
     fb.pend = 0;
@@ -377,9 +449,27 @@ struct PrefillSim {
     resume = 0;
   }
 
+  __device__ bool idle(double f, double* p, int* err) const {
+    const int k = find_slot(gc->f, gc->ns, f);
+    if (k < 0) return idle_w(R->sim.idle, I->tp, f, p, err);
+    *p = gc->idle[k];
+    *err = gc->idle_err[k];
+    return gc->idle_err[k] == 0;
+  }
+  struct IdleCached {
+    const PrefillSim* s;
+    __device__ bool operator()(double f, double* p, int* err) const { return s->idle(f, p, err); }
+  };
+
+  __device__ void activate() {
+    fb.activate();
+    slot = find_slot(gc->f, gc->ns, fb.in_force);
+  }
+
   __device__ bool exec_latency() {  // InstanceSim::exec_latency at the in-force frequency
     int err = 0;
-    if (!predict(R->sim.grid[0], fn, fsum, I->tp, fb.in_force, &L, &err, kErrLatency)) {
+    if (slot >= 0 ? !predict_fast(gc->lat[slot], fn, fsum, &L, &err, kErrLatency)
+                  : !predict(R->sim.grid[0], fn, fsum, I->tp, fb.in_force, &L, &err, kErrLatency)) {
       w.fail(BS_MODEL_ERROR, err);
       return false;
     }
@@ -391,7 +481,9 @@ struct PrefillSim {
     if (!C->controlled) return true;
     double pl;
     int err = 0;
-    if (!predict(R->ctl.grid[0], fn, fsum, I->tp, f, &pl, &err, kErrLatency)) {
+    const int k = find_slot(gc->f, gc->ns, f);
+    if (k >= 0 ? !predict_fast(gc->clat[k], fn, fsum, &pl, &err, kErrLatency)
+               : !predict(R->ctl.grid[0], fn, fsum, I->tp, f, &pl, &err, kErrLatency)) {
       w.fail(BS_MODEL_ERROR, err);
       return false;
     }
@@ -406,7 +498,8 @@ struct PrefillSim {
     if (to > seg_start) {
       double p;
       int err = 0;
-      if (!predict(R->sim.grid[2], fn, fsum, I->tp, fb.in_force, &p, &err, kErrPower)) {
+      if (slot >= 0 ? !predict_fast(gc->pw[slot], fn, fsum, &p, &err, kErrPower)
+                    : !predict(R->sim.grid[2], fn, fsum, I->tp, fb.in_force, &p, &err, kErrPower)) {
         w.fail(BS_MODEL_ERROR, err);
         return false;
       }
@@ -603,10 +696,10 @@ struct PrefillSim {
       if (t_sw <= t_safety && t_sw <= t_arr) {
         if (active) {
           if (!close_segment(t_sw)) return 0;
-        } else if (!record_idle(w, R->sim, I->tp, fb, now, t_sw)) {
+        } else if (!record_idle(w, IdleCached{this}, fb, now, t_sw)) {
           return 0;
         }
-        fb.activate();
+        activate();
         now = t_sw;
         if (active && !exec_latency()) return 0;
         continue;
@@ -628,7 +721,7 @@ struct PrefillSim {
         continue;
       }
       if (t_arr == INFINITY) return 0;
-      if (!active && !record_idle(w, R->sim, I->tp, fb, now, t_arr)) return 0;
+      if (!active && !record_idle(w, IdleCached{this}, fb, now, t_arr)) return 0;
       now = fmax(now, t_arr);
       push_arrival();
       if (active && C->controlled && !fired) {
@@ -642,6 +735,7 @@ struct PrefillSim {
 
 __global__ void __launch_bounds__(kPrefillThreads) prefill_kernel(DReplay R, const int* pre_ids, int n_pre) {
   __shared__ GreedyShared S;
+  extern __shared__ __align__(16) unsigned char pre_dsm[];
   __shared__ DProblem s_pr;
   __shared__ DMpcOut s_out;
   __shared__ int s_cmd;
@@ -649,13 +743,32 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_kernel(DReplay R, con
   const int gi = pre_ids[blockIdx.x];
   const DInst I = R.inst[gi];
   const DRCfg* C = &R.cfgs[R.scen[I.scen].cfg];
+  // slots [0, nc): the MPC candidates (indexed like DTables' f); slot nc: base
+  const int nc = C->controlled ? C->mpc.nc : 0;
+  const int ns = nc + 1;
+  const PreCache G = pre_cache_at(pre_dsm, ns);
+  for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+    const double f = t < nc ? C->mpc.cand[t] : I.base_freq;
+    G.f[t] = f;
+    int err = 0;
+    double p = 0.0;
+    G.idle_err[t] = idle_w(R.sim.idle, I.tp, f, &p, &err) ? 0 : err;
+    G.idle[t] = p;
+  }
+  for (int t = threadIdx.x; t < 4 * ns; t += blockDim.x) {
+    const int g = t / ns, k = t - g * ns;
+    const double f = k < nc ? C->mpc.cand[k] : I.base_freq;
+    const FastGrid fg = fast_grid(g < 2 ? R.sim.grid[g == 0 ? 0 : 2] : R.ctl.grid[g == 2 ? 0 : 2], I.tp, f);
+    (g == 0 ? G.lat : g == 1 ? G.pw : g == 2 ? G.clat : G.cpw)[k] = fg;
+  }
+  __syncthreads();
   PrefillSim sim;
-  if (threadIdx.x == 0) sim.init(&R, &I, C);
+  if (threadIdx.x == 0) sim.init(&R, &I, C, &G);  // G: views, valid for the block's lifetime
   for (;;) {
     if (threadIdx.x == 0) s_cmd = sim.advance(&s_out, &s_pr);
     __syncthreads();
     if (s_cmd == 0) break;
-    greedy_block(R.ctl, s_pr, C->mpc, R.W + s_pr.wait_off, nullptr, S, &s_out, nullptr);
+    greedy_block(R.ctl, s_pr, C->mpc, R.W + s_pr.wait_off, nullptr, S, &s_out, nullptr, G.clat, G.cpw);
     __syncthreads();
   }
   if (threadIdx.x == 0) {
@@ -757,8 +870,8 @@ __global__ void route_kernel(DReplay R, int n_scen) {
 // select_decode_freq_ex (dvfs.hpp:274-293) as a warp ladder walk (lane j
 // evaluates rung j of each 32-rung chunk; a ballot finds where the
 // reference's ascending walk stops).  Warp-uniform; false on ModelError.
-__device__ bool decode_pick(const DReplay& R, const DRCfg* C, long long n, long long sum, int tp, long long cap,
-                            long long used, double* f, long long* eval, int* err) {
+__device__ bool decode_pick(const DReplay& R, const DRCfg* C, const DecSlot* slots, long long n, long long sum, int tp,
+                            long long cap, long long used, double* f, long long* eval, int* err) {
   const int lane = threadIdx.x & 31;
   const double util = cap > 0 ? __ddiv_rn(static_cast<double>(used), static_cast<double>(cap)) : 0.0;
   *f = C->ladder[C->n_ladder - 1];
@@ -774,7 +887,7 @@ __device__ bool decode_pick(const DReplay& R, const DRCfg* C, long long n, long 
     const int j = j0 + lane;
     bool fits = false, bad = false;
     if (j < C->n_ladder) {
-      const double v = interp(g, make_query(n, sum, tp, C->ladder[j]), nullptr);
+      const double v = fast_interp(slots[j].clat, n, sum);  // slot j = rung j
       bad = !model_value_ok(v);
       fits = !bad && __dmul_rn(v, C->dec_one_plus_margin) <= C->dec_tbt;  // dvfs.hpp:285-286
     }
@@ -807,7 +920,8 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 // over lanes for the per-iteration emissions (every resident emits one token
 // at every iteration end, simulator.hpp:544-557), whose per-request
 // reductions (first/last token, worst gap) are kept in the resident entry.
-__global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_ids, int n_dec) {
+__global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_ids, int n_dec, int max_slots) {
+  extern __shared__ __align__(16) unsigned char dsm[];
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= n_dec) return;
@@ -822,6 +936,48 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
   DResident* res = R.res + I.res0;
   const DGrid& lat_g = R.sim.grid[1];
   const DGrid& pow_g = R.sim.grid[3];
+  // per-frequency caches: slots [0, n_ladder) = the decode ladder, slot n_ladder = base
+  DecSlot* slots = reinterpret_cast<DecSlot*>(dsm) + (threadIdx.x >> 5) * max_slots;
+  const int nl = C->controlled ? C->n_ladder : 0;
+  const int ns = nl + 1;
+  for (int t = lane; t < ns; t += 32) {
+    const double f = t < nl ? C->ladder[t] : I.base_freq;
+    slots[t].f = f;
+    int err = 0;
+    double p = 0.0;
+    slots[t].idle_err = idle_w(R.sim.idle, I.tp, f, &p, &err) ? 0 : err;
+    slots[t].idle = p;
+  }
+  for (int t = lane; t < 3 * ns; t += 32) {
+    const int g = t / ns, k = t - g * ns;
+    const double f = k < nl ? C->ladder[k] : I.base_freq;
+    const FastGrid fg = fast_grid(g == 0 ? R.sim.grid[1] : g == 1 ? R.sim.grid[3] : R.ctl.grid[1], I.tp, f);
+    if (g == 0) slots[k].lat = fg;
+    else if (g == 1) slots[k].pw = fg;
+    else slots[k].clat = fg;
+  }
+  __syncwarp();
+  auto slot_of = [&](double f) {
+    for (int i = 0; i < ns; ++i)
+      if (slots[i].f == f) return i;
+    return -1;
+  };
+  struct IdleSlots {
+    const DecSlot* sl;
+    int ns;
+    const DIdle* m;
+    int tp;
+    __device__ bool operator()(double f, double* p, int* err) const {
+      for (int i = 0; i < ns; ++i)
+        if (sl[i].f == f) {
+          *p = sl[i].idle;
+          *err = sl[i].idle_err;
+          return sl[i].idle_err == 0;
+        }
+      return idle_w(*m, tp, f, p, err);
+    }
+  };
+  const IdleSlots idle_fn{slots, ns, &R.sim.idle, I.tp};
 
   Writer w;
   w.init(&R, &I, lane == 0);
@@ -834,9 +990,11 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
   int n_res = 0, active = 0, fired = 0;
   double last_end = 0.0;
 
+  int slot = slot_of(fb.in_force);
   auto exec_latency = [&]() -> bool {
     int err = 0;
-    if (!predict(lat_g, fn, fsum, I.tp, fb.in_force, &L, &err, kErrLatency)) {
+    if (slot >= 0 ? !predict_fast(slots[slot].lat, fn, fsum, &L, &err, kErrLatency)
+                  : !predict(lat_g, fn, fsum, I.tp, fb.in_force, &L, &err, kErrLatency)) {
       w.fail(BS_MODEL_ERROR, err);
       return false;
     }
@@ -846,7 +1004,8 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
     if (to > seg_start) {
       double p;
       int err = 0;
-      if (!predict(pow_g, fn, fsum, I.tp, fb.in_force, &p, &err, kErrPower)) {
+      if (slot >= 0 ? !predict_fast(slots[slot].pw, fn, fsum, &p, &err, kErrPower)
+                    : !predict(pow_g, fn, fsum, I.tp, fb.in_force, &p, &err, kErrPower)) {
         w.fail(BS_MODEL_ERROR, err);
         return false;
       }
@@ -897,7 +1056,8 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
           break;
         }
         const double t_next = fmax(R.djoin[base + arr], now);
-        if (!idle_until(w, R.sim, I.tp, fb, now, t_next)) break;
+        if (!idle_until(w, idle_fn, fb, now, t_next)) { slot = slot_of(fb.in_force); break; }
+        slot = slot_of(fb.in_force);
         continue;
       }
       // start_iteration (simulator.hpp:472-492)
@@ -912,7 +1072,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
         double f;
         long long eval;
         int err = 0;
-        if (!decode_pick(R, C, fn, fsum, I.tp, C->kv_cap, sum_ctx, &f, &eval, &err)) {
+        if (!decode_pick(R, C, slots, fn, fsum, I.tp, C->kv_cap, sum_ctx, &f, &eval, &err)) {
           w.fail(BS_MODEL_ERROR, err);
           break;
         }
@@ -925,7 +1085,9 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
       if (C->controlled) {  // arm_safety (simulator.hpp:230-235)
         double pl;
         int err = 0;
-        if (!predict(R.ctl.grid[1], fn, fsum, I.tp, decided, &pl, &err, kErrLatency)) {
+        const int ks = slot_of(decided);
+        if (ks >= 0 ? !predict_fast(slots[ks].clat, fn, fsum, &pl, &err, kErrLatency)
+                    : !predict(R.ctl.grid[1], fn, fsum, I.tp, decided, &pl, &err, kErrLatency)) {
           w.fail(BS_MODEL_ERROR, err);
           break;
         }
@@ -988,6 +1150,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_i
     if (t_sw <= t_safety && t_sw <= t_arr) {
       if (!close_segment(t_sw)) break;
       fb.activate();
+      slot = slot_of(fb.in_force);
       now = t_sw;
       if (!exec_latency()) break;
       continue;
@@ -1146,7 +1309,7 @@ __global__ void __launch_bounds__(kReportThreads) report_kernel(DReplay R, bs_re
     fb.at = st->pend_at;
     fb.to = st->pend_f;
     double now = st->now;
-    idle_until(w, R.sim, I.tp, fb, now, s_horizon);
+    idle_until(w, IdleDirect{&R.sim.idle, I.tp}, fb, now, s_horizon);
     st->n_idl = w.n_idl;
     st->fill_status = w.status;
     st->fill_err = w.err;
@@ -1723,8 +1886,13 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
     for (auto& e : ev) BS_CUDA_TRY(ctx, cudaEventCreate(&e));
     BS_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
     if (!pre_ids.empty()) {
-      prefill_kernel<<<static_cast<int>(pre_ids.size()), kPrefillThreads, 0, ctx->stream>>>(R, dpre,
-                                                                                          static_cast<int>(pre_ids.size()));
+      int max_ns = 1;
+      for (const DRCfg& c : hcfg) max_ns = std::max(max_ns, (c.controlled ? c.mpc.nc : 0) + 1);
+      const size_t psmem = pre_cache_bytes(max_ns);
+      BS_CUDA_TRY(ctx, cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(psmem)));
+      prefill_kernel<<<static_cast<int>(pre_ids.size()), kPrefillThreads, psmem, ctx->stream>>>(
+          R, dpre, static_cast<int>(pre_ids.size()));
       BS_LAUNCH_CHECK(ctx);
     }
     BS_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
@@ -1733,7 +1901,13 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
     BS_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
     if (!dec_ids.empty()) {
       const int nd = static_cast<int>(dec_ids.size());
-      decode_kernel<<<(nd + 3) / 4, 128, 0, ctx->stream>>>(R, ddec, nd);
+      int max_slots = 1;
+      for (const DRCfg& c : hcfg) max_slots = std::max(max_slots, (c.controlled ? c.n_ladder : 0) + 1);
+      const size_t smem = sizeof(DecSlot) * static_cast<size_t>(max_slots) * 4;
+      if (smem > 48 * 1024)
+        BS_CUDA_TRY(ctx, cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem)));
+      decode_kernel<<<(nd + 3) / 4, 128, smem, ctx->stream>>>(R, ddec, nd, max_slots);
       BS_LAUNCH_CHECK(ctx);
     }
     BS_CUDA_TRY(ctx, cudaEventRecord(ev[3], ctx->stream));

@@ -232,7 +232,7 @@ __device__ __forceinline__ bool predict_at(const FastGrid& g, long long n_req, l
 
 // simulate_prefill_instance (simulator.hpp:278-409) without a controller,
 // followed by simulate_instance's accounting (667-739).
-__device__ SimOut simulate_prefill(const DModels& m, const SimTrace& tr, const SimParams& p) {
+__device__ inline SimOut simulate_prefill(const DModels& m, const SimTrace& tr, const SimParams& p) {
   SimOut o;
   o.status = BS_OK;
   o.model_err = 0;
@@ -366,7 +366,7 @@ __device__ SimOut simulate_prefill(const DModels& m, const SimTrace& tr, const S
 
 // simulate_decode_instance (simulator.hpp:441-578) without a controller.
 // `heap` is per-thread scratch with room for max_batch_requests residents.
-__device__ SimOut simulate_decode(const DModels& m, const SimTrace& tr, const SimParams& p, Resident* heap,
+__device__ inline SimOut simulate_decode(const DModels& m, const SimTrace& tr, const SimParams& p, Resident* heap,
                                   int heap_cap) {
   SimOut o;
   o.status = BS_OK;
@@ -523,7 +523,7 @@ struct WarpScratch {
   double* T;       // 32
 };
 
-__device__ SimOut simulate_decode_warp(const DModels& m, const SimTrace& tr, const SimParams& p, WarpScratch ws,
+__device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& tr, const SimParams& p, WarpScratch ws,
                                        int heap_cap, int lane) {
   SimOut o;
   o.status = BS_OK;
