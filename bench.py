@@ -18,8 +18,17 @@ per-decision argmin.
          exhaustive loop over meets_slo + time_weighted_power,
          tests/test_dvfs.cpp:74-94) on the host cores, bounded sample
 
+Extra keys, one object per other BASELINE.json configuration (each with its
+own device timing, the reference on the host cores and a parity check):
+  c3_placement   configs[2]: config table + ILP, placement configs/s
+  c4_replay      configs[3]-shaped what-if replay sweep, scenarios/s
+  c5_greedy      configs[4] greedy MPC (H8 x 24 levels), decisions/s
+  c5_exhaustive  configs[4] exhaustive MPC (24^8 per decision), decisions/s
+(`--only c3|c4|c5g|c5x` runs one alone; `--no-extras` skips them.)
+
 Multi-GPU (torchrun): weak scaling, every rank evaluates its own corpus
-(independent decisions), no data-path collective; max-over-ranks time.
+(independent decisions), no data-path collective; max-over-ranks time.  The
+C4/C5 extras split their fixed scenario sets across ranks.
 `--impl reference` times the reference CPU implementation instead.
 """
 from __future__ import annotations
@@ -56,6 +65,11 @@ def parse():
     ap.add_argument("--ttft", type=float, default=600.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU baseline sample duration")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C3/C4/C5 sub-benchmarks")
+    ap.add_argument("--only", choices=["c3", "c4", "c5g", "c5x"], default=None,
+                    help="run one sub-benchmark alone and print its JSON object")
+    ap.add_argument("--c4-scenarios", type=int, default=1024)
+    ap.add_argument("--c5x-decisions", type=int, default=256)
     return ap.parse_args()
 
 
@@ -187,6 +201,264 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# Sub-benchmarks of the other BASELINE.json configurations (extra keys of the
+# JSON line; the headline `value` stays C2).  Each times the device path,
+# times the reference on the host cores on a bounded sample of the same
+# work, and checks the device results against the reference's.
+# ---------------------------------------------------------------------------
+
+def _dist_max(x: float, world: int, local: int) -> float:
+    if world == 1:
+        return x
+    from paper_2602_18755_b200 import sharding as S
+
+    return S.max_over_ranks(x, device=f"cuda:{local}")
+
+
+def _barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def bench_c3(dev, with_cpu: bool, repeats: int = 3) -> dict:
+    """configs[2]: coarse-tier placement for a 16-GPU cluster over a bursty
+    1-hour window: the config table (goodput search + E_c of every
+    candidate, build_config_table placement.hpp:240-260) + the ILP."""
+    import ctypes as C
+
+    from paper_2602_18755_b200 import _abi as A
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import workloads as Wk
+
+    lad = Wk.ladder(16)
+    models = Wk.llama_models(lad)
+    base = P.gen_gamma_trace(12.0, 0.5, 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), 7)
+    cands = P.enumerate_candidates(lad, [1, 2, 4, 8])
+    pol, slo, search = P.SchedulerPolicy(max_batch_tokens=2048), P.SLOSpec(600.0, 100.0), P.GoodputSearch()
+    P.build_config_table(cands, base, slo, models, pol, search, device=dev)  # warm-up
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        table = P.build_config_table(cands, base, slo, models, pol, search, device=dev)
+        times.append(time.perf_counter() - t0)
+    st = (C.c_double * 8)()
+    dev._lib.bs_ctx_stats(dev.handle, st, 8)
+    t0 = time.perf_counter()
+    plan = P.solve_placement(P.PlacementProblem(table, 16, P.peak_rps(base, 10.0), 0.05), dev)
+    t_ilp = time.perf_counter() - t0
+    t_table = statistics.median(times)
+    k_max = int(base.mean_rps() // search.tolerance_rps)
+    out = {"workload": "C3: 1-hour gamma(0.5) window at 12 rps, 128 candidates (2 phases x TP{1,2,4,8} x 16 "
+                       "rungs), max_batch_tokens 2048, G = 16", "requests": len(base.requests),
+           "value": len(cands) / t_table, "unit": "placement configs/s", "table_s": t_table,
+           "probes_per_s": k_max * len(cands) / t_table, "ilp_s": t_ilp, "gpus_used": plan.gpus_used,
+           "objective_w": plan.objective_w, "phase_ms": {"mask": st[0], "probe": st[1], "energy": st[2]},
+           "events_simulated": st[4], "e2e_note": "value is end to end through pdsim.build_config_table "
+                                                 "(host trace in, table out)"}
+    if with_cpu:
+        import oracle
+
+        ref = oracle.load_ref()
+        keep: list = []
+        cm, ct = P.c_model_set(models, keep), P.c_trace(base, keep)
+        outc = (A.bs_table_entry * len(cands))()
+        t0 = time.perf_counter()
+        rc = ref.ref_config_table(C.byref(cm), C.byref(ct), C.byref(P.c_slo(slo)), C.byref(P.c_policy(pol)),
+                                  C.byref(P.c_search(search)), P.c_candidates(cands), len(cands), outc)
+        t_cpu = time.perf_counter() - t0
+        same = rc == 0 and all((e.r_c, e.e_c, e.saturated, e.error) == (o.r_c, o.e_c, o.saturated, o.error)
+                               for e, o in zip(table, [P.entry_from_c(outc[i]) for i in range(len(cands))]))
+        out["cpu_baseline"] = {"value": len(cands) / t_cpu, "unit": "placement configs/s", "cores": cpu_threads(),
+                               "kind": "reference", "seconds": t_cpu,
+                               "sample": "the whole table: build_config_table (std::async per candidate)"}
+        out["identical_to_reference"] = bool(same)
+    return out
+
+
+def bench_c4(dev, rank: int, world: int, local: int, n_scen: int, with_cpu: bool) -> dict:
+    """configs[3]-shaped: what-if replay sweep (trace seeds x SLO pairs) of
+    simulate_cluster with per-iteration two-tier decisions + the report,
+    scenarios sharded across ranks."""
+    import ctypes as C
+
+    from paper_2602_18755_b200 import _abi as A
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import sharding as S
+    from paper_2602_18755_b200 import workloads as Wk
+
+    models, scs_all = Wk.c4_scenarios(n_scen)
+    lo, hi = S.shard_bounds(len(scs_all), rank, world)
+    scs = scs_all[lo:hi]
+    lib = dev._lib
+    keep: list = []
+    cfgs, cscs, _ = P.c_replay_inputs(scs, keep)
+    n = len(scs)
+    outs = (A.bs_replay_summary * max(1, n))()
+    mh = dev.models(models)
+    dev.check(lib.bs_replay(dev.handle, mh, mh, cfgs, n, cscs, n, outs, None, None))  # warm-up
+    st = (C.c_double * 8)()
+    times, kern = [], []
+    for _ in range(3):
+        _barrier(world)
+        t0 = time.perf_counter()
+        dev.check(lib.bs_replay(dev.handle, mh, mh, cfgs, n, cscs, n, outs, None, None))
+        times.append(time.perf_counter() - t0)
+        lib.bs_ctx_stats(dev.handle, st, 8)
+        kern.append([st[i] for i in range(4)])
+    e2e = _dist_max(statistics.median(times), world, local)
+    kms = _dist_max(statistics.median(sum(k) for k in kern), world, local)
+    dec = sum(outs[i].n_decisions for i in range(n))
+    h2d, d2h = C.c_uint64(), C.c_uint64()
+    lib.bs_ctx_last_transfer(dev.handle, C.byref(h2d), C.byref(d2h))
+    out = {"workload": f"C4-shaped: {len(scs_all)} what-if scenarios (8 trace seeds x (TTFT, TPOT) pairs), 5-min "
+                       "gamma(0.5) windows at 12 rps, 2P(tp2)+2D(tp4), greedy MPC K=8 N=7 + decode slack DVFS",
+           "value": len(scs_all) / (kms / 1e3), "unit": "scenarios/s", "kernel_ms": kms,
+           "decisions_per_s_rank0": dec / (kms / 1e3),
+           "phase_ms_rank0": dict(zip(["prefill", "route", "decode", "report"],
+                                      [statistics.median(k[i] for k in kern) for i in range(4)])),
+           "e2e": {"value": len(scs_all) / e2e, "unit": "scenarios/s", "h2d_bytes_per_step": int(h2d.value),
+                   "d2h_bytes_per_step": int(d2h.value)},
+           "all_ok": all(outs[i].status == 0 for i in range(n))}
+    if with_cpu and rank == 0:
+        import oracle
+
+        ref = oracle.load_ref()
+        m = min(32, n)
+        k2: list = []
+        rc_cfgs, rc_scs, _ = P.c_replay_inputs(scs[:m], k2)
+        rout = (A.bs_replay_summary * m)()
+        cm = P.c_model_set(models, k2)
+        t0 = time.perf_counter()
+        rc = ref.ref_replay(C.byref(cm), C.byref(cm), rc_cfgs, rc_scs, m, rout, None, None, cpu_threads())
+        t_cpu = time.perf_counter() - t0
+        names = [f for f, _ in A.bs_replay_summary._fields_ if f not in ("_pad", "decisions_by_trigger")]
+        same = rc == 0 and all(all(getattr(outs[i], f) == getattr(rout[i], f) or
+                                   (getattr(outs[i], f) != getattr(outs[i], f) and getattr(rout[i], f) !=
+                                    getattr(rout[i], f)) for f in names) for i in range(m))
+        out["cpu_baseline"] = {"value": m / t_cpu, "unit": "scenarios/s", "cores": cpu_threads(),
+                               "kind": "reference", "seconds": t_cpu,
+                               "sample": f"first {m} scenarios: pdsim::simulate_cluster + trim_steady_state + "
+                                         "make_report, one scenario per thread"}
+        out["identical_on_sample"] = bool(same)
+    return out
+
+
+def bench_c5(dev, mode: str, rank: int, world: int, local: int, n_dec: int, with_cpu: bool) -> dict:
+    """configs[4]: horizon-8 MPC on a 24-level grid, greedy or exhaustive,
+    decisions sharded across ranks."""
+    import ctypes as C
+    import random
+
+    from paper_2602_18755_b200 import _abi as A
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import sharding as S
+    from paper_2602_18755_b200 import workloads as Wk
+
+    models, cfg, pol, snaps_all = Wk.c5_corpus(0xC5, n_dec)
+    lo, hi = S.shard_bounds(len(snaps_all), rank, world)
+    snaps = snaps_all[lo:hi]
+    lib = dev._lib
+    keep: list = []
+    cc = (A.bs_mpc_config * 1)(P.c_mpc_config(cfg, keep))
+    cp = (A.bs_scheduler_policy * 1)(P.c_policy(pol))
+    probs = P.c_problems(snaps, None, keep)
+    n = len(snaps)
+    res = (A.bs_mpc_result * max(1, n))()
+    mh = dev.models(models)
+    fn = lib.bs_mpc_greedy if mode == "greedy" else lib.bs_mpc_exhaustive
+    dev.check(fn(dev.handle, mh, cc, cp, 1, probs, n, res))
+    times = []
+    for _ in range(3):
+        _barrier(world)
+        t0 = time.perf_counter()
+        dev.check(fn(dev.handle, mh, cc, cp, 1, probs, n, res))
+        times.append(time.perf_counter() - t0)
+    t = _dist_max(statistics.median(times), world, local)
+    out = {"workload": f"C5: {len(snaps_all)} scenarios, horizon 8 on a 24-level ladder, {mode} MPC",
+           "value": len(snaps_all) / t, "unit": "decisions/s", "seconds": t,
+           "timing": "end to end through the C ABI with host buffers (pack + H2D + kernels + D2H)",
+           "feasible_decisions_rank0": sum(res[i].feasible for i in range(n))}
+    if mode == "greedy":
+        out["mutations_per_s_rank0"] = sum(res[i].eval_count for i in range(n)) / t
+    else:
+        traj = sum(res[i].trajectories for i in range(n))
+        out["trajectories_per_s"] = traj * world / t
+        out["roofline_note"] = "24^8 = 1.1e11 trajectories per decision, W = 5*8+2 = 42 FP64 ops each: " \
+                               f"{traj * world * 42 / t / 1e12:.0f} TFLOP/s-equivalent algorithmic (pruned search)"
+    if not with_cpu or rank != 0:
+        return out
+    import oracle
+
+    ref = oracle.load_ref()
+    cm = P.c_model_set(models, keep)
+    threads = cpu_threads()
+    if mode == "greedy":
+        m = min(64, n)
+        rout = (A.bs_mpc_result * m)()
+        t0 = time.perf_counter()
+        rc = ref.ref_greedy_batch(C.byref(cm), cc, cp, probs, m, rout, threads)
+        tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": m / tc, "unit": "decisions/s", "cores": threads, "kind": "reference",
+                               "sample": f"first {m} decisions, greedy_freq_select, one per thread"}
+        out["identical_on_sample"] = rc == 0 and all(
+            (rout[i].objective_w, rout[i].eval_count, rout[i].feasible, list(rout[i].freqs_mhz)) ==
+            (res[i].objective_w, res[i].eval_count, res[i].feasible, list(res[i].freqs_mhz)) for i in range(m))
+        return out
+    # exhaustive: property checks at full size + the reference's per-trajectory cost
+    rng = random.Random(5)
+    ok, checked = True, 0
+    for i in range(min(4, n)):
+        r = res[i]
+        if not r.feasible:
+            continue
+        checked += 1
+        snap = P.c_snapshot(snaps[i], keep)
+        codes = [r.best_code] + [rng.randrange(24 ** r.K) for _ in range(20000)]
+        cd = (C.c_uint64 * len(codes))(*codes)
+        fe, ob = (C.c_int32 * len(codes))(), (C.c_double * len(codes))()
+        ok &= ref.ref_eval_codes(C.byref(cm), cc, cp, C.byref(snap), cd, len(codes), fe, ob) == 0
+        ok &= bool(fe[0]) and ob[0] == r.objective_w
+        ok &= all(not fe[j] or ob[j] >= r.objective_w for j in range(1, len(codes)))
+        g = A.bs_mpc_result()
+        ok &= ref.ref_greedy(C.byref(cm), cc, cp, C.byref(snap), C.byref(g)) == 0
+        ok &= (not g.feasible) or g.objective_w >= r.objective_w
+    out["property_checks"] = {"decisions": checked, "passed": bool(ok),
+                              "what": "GPU argmin re-evaluated by the reference (feasible, objective bit-equal); "
+                                      "20k random feasible codes never better; reference greedy sandwich"}
+    m = 400_000
+    snap = P.c_snapshot(snaps[0], keep)
+    cd = (C.c_uint64 * m)(*[rng.randrange(24 ** max(1, res[0].K)) for _ in range(m)])
+    fe, ob = (C.c_int32 * m)(), (C.c_double * m)()
+    t0 = time.perf_counter()
+    ref.ref_eval_codes(C.byref(cm), cc, cp, C.byref(snap), cd, m, fe, ob)
+    per = (time.perf_counter() - t0) / m
+    out["cpu_baseline"] = {"value": threads / per, "unit": "trajectories/s", "cores": threads, "kind": "reference",
+                           "sample": f"{m} random trajectories of decision 0 through the reference's meets_slo + "
+                                     f"time_weighted_power on one core ({per * 1e9:.0f} ns each) x {threads} cores "
+                                     f"(extrapolated: one 24^8 decision = {24 ** 8 * per / threads / 3600:.1f} h)"}
+    return out
+
+
+def run_extras(args, dev, rank, world, local) -> dict:
+    with_cpu = world == 1 and not args.no_cpu_baseline
+    todo = [args.only] if args.only else ["c3", "c4", "c5g", "c5x"]
+    out = {}
+    for k in todo:
+        if k == "c3":
+            if world == 1:
+                out["c3_placement"] = bench_c3(dev, with_cpu)
+        elif k == "c4":
+            out["c4_replay"] = bench_c4(dev, rank, world, local, args.c4_scenarios, with_cpu)
+        elif k == "c5g":
+            out["c5_greedy"] = bench_c5(dev, "greedy", rank, world, local, 4096, with_cpu)
+        else:
+            out["c5_exhaustive"] = bench_c5(dev, "exhaustive", rank, world, local, args.c5x_decisions, with_cpu)
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -205,6 +477,13 @@ def main():
     from paper_2602_18755_b200 import workloads as Wk
 
     dev = P.Device(local)
+    if args.only:
+        extra = run_extras(args, dev, rank, world, local)
+        if rank == 0:
+            print(json.dumps(extra), flush=True)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
     lib = dev._lib
     torch.cuda.set_device(local)
     stream = torch.cuda.ExternalStream(lib.bs_ctx_stream(dev.handle), device=f"cuda:{local}")
@@ -312,6 +591,7 @@ def main():
         except Exception as e:  # the reference driver is optional on a box without it
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    extras = {} if args.no_extras else run_extras(args, dev, rank, world, local)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -337,6 +617,7 @@ def main():
             "clocks": clk,
             "cpu_baseline": cpu,
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

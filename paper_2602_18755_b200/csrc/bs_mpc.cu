@@ -467,7 +467,46 @@ int bs_project_batches(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_schedul
 int bs_mpc_exhaustive(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
                       const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
                       bs_mpc_result* out) {
-  return one_shot(ctx, models, cfgs, policies, n_cfgs, problems, n, out, kExhaustive);
+  if (!ctx || !models) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: null context or models");
+  if (n_cfgs < 1 || !cfgs || !policies || n <= 0)
+    return one_shot(ctx, models, cfgs, policies, n_cfgs, problems, n, out, kExhaustive);
+  // Frontier scratch is sized for the worst case (every prefix feasible), so
+  // wide trees (e.g. 24^8) are run in consecutive chunks of decisions whose
+  // worst case fits the scratch budget; results are independent per decision.
+  std::vector<double> per_cfg(n_cfgs, 0.0);
+  for (int c = 0; c < n_cfgs; ++c) {
+    DMpcCfg hc;
+    if (pack_mpc_cfg(ctx, cfgs[c], policies[c], &hc) != BS_OK) {
+      per_cfg[c] = 0.0;  // reported by the chunk that contains it
+      continue;
+    }
+    const int FD = hc.horizon - sweep_levels(hc.horizon, hc.nc);
+    per_cfg[c] = 12.0 * static_cast<double>(ipow(hc.nc, FD)) +
+                 80.0 * static_cast<double>(ipow(hc.nc, FD > 0 ? FD - 1 : 0)) + sizeof(DTables) + 256.0;
+  }
+  ctx->err.clear();
+  const double budget = 0.66 * static_cast<double>(kMaxExhaustiveScratch);
+  uint64_t h2d = 0, d2h = 0;
+  int a = 0;
+  while (a < n) {
+    double need = 0.0;
+    int b = a;
+    while (b < n) {
+      const int ci = problems[b].cfg_index;
+      const double w = (ci >= 0 && ci < n_cfgs) ? per_cfg[ci] : 0.0;
+      if (b > a && need + w > budget) break;
+      need += w;
+      ++b;
+    }
+    const int rc = one_shot(ctx, models, cfgs, policies, n_cfgs, problems + a, b - a, out + a, kExhaustive);
+    h2d += ctx->last_h2d;
+    d2h += ctx->last_d2h;
+    if (rc != BS_OK) return rc;
+    a = b;
+  }
+  ctx->last_h2d = h2d;
+  ctx->last_d2h = d2h;
+  return BS_OK;
 }
 
 int bs_mpc_greedy(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,

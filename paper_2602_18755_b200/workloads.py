@@ -66,3 +66,45 @@ def c1_corpus(seed: int = 0xC1, n: int = 256):
     rng = random.Random(seed)
     snaps = [synthetic_snapshot(rng, lad, n_lo=8, n_hi=32, arrival_window_ms=100.0) for _ in range(n)]
     return models, cfg, pol, snaps
+
+
+def c5_corpus(seed: int = 0xC5, n: int = 4096, ttft_ms: float = 600.0):
+    """C5 problems: horizon 8 on a 24-level grid (24^8 = 1.1e11 trajectories
+    per decision exhaustively; greedy <= 22 levels x 6560 mutations)."""
+    lad = ladder(24)
+    models = llama_models(lad)
+    cfg = P.MpcConfig(horizon_K=8, ladder_N=24, ladder=lad, slo=P.SLOSpec(ttft_ms=ttft_ms))
+    pol = P.SchedulerPolicy(max_batch_tokens=512)
+    rng = random.Random(seed)
+    snaps = [synthetic_snapshot(rng, lad, n_lo=8, n_hi=32, arrival_window_ms=200.0) for _ in range(n)]
+    return models, cfg, pol, snaps
+
+
+def c4_scenarios(n_scen: int = 1024, window_s: float = 300.0, rps: float = 12.0, seeds: int = 8, n_pre: int = 2,
+                 n_dec: int = 2, levels: int = 8):
+    """C4-shaped what-if sweep: scenario k replays trace seed k % seeds with
+    the (TTFT, TPOT) pair (k // seeds) % 128 of {400..900} x {60..140} ms
+    (16 x 8), on a fixed nP(tp2) + nD(tp4) cluster at max frequency with the
+    two-tier controllers (greedy MPC K=8, N=7; decode slack policy), report
+    after a 30 s ramp-up."""
+    lad = ladder(levels)
+    models = llama_models(lad)
+    fmax = lad.freqs_mhz[-1]
+    pol = P.SchedulerPolicy(max_batch_tokens=512)
+    ttfts = [400.0 + 500.0 * i / 15 for i in range(16)]
+    tpots = [60.0 + 80.0 * i / 7 for i in range(8)]
+    traces = [P.gen_gamma_trace(rps, 0.5, window_s * 1000.0,
+                                P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), 1000 + s)
+              for s in range(seeds)]
+    inst = [P.ClusterInstance(P.InstanceConfig(P.Phase.prefill, 2, fmax), 1.0 / n_pre) for _ in range(n_pre)]
+    inst += [P.ClusterInstance(P.InstanceConfig(P.Phase.decode, 4, fmax), 1.0 / n_dec) for _ in range(n_dec)]
+    scs = []
+    for k in range(n_scen):
+        slo_i = (k // seeds) % 128
+        slo = P.SLOSpec(ttfts[slo_i % 16], tpots[slo_i // 16])
+        mpc = P.MpcConfig(horizon_K=8, ladder_N=7, ladder=lad, slo=slo)
+        dec = P.DecodePolicyConfig(tbt_slo_ms=slo.tpot_ms, kv_threshold=0.9, ladder=lad, margin=0.05)
+        fac = P.TwoTierFactory(mpc, dec, models, pol)
+        scs.append(P.ReplayScenario(traces[k % seeds], P.ClusterSpec(list(inst)), pol, fac, P.SimOptions(30.0, -1.0),
+                                    slo, 30.0))
+    return models, scs
