@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
-    ap.add_argument("--decisions", type=int, default=256, help="decisions per step per GPU")
+    ap.add_argument("--decisions", type=int, default=1024, help="decisions per step per GPU")
     ap.add_argument("--ttft", type=float, default=600.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU baseline sample duration")

@@ -49,7 +49,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if (not force and obj.exists() and obj.stat().st_mtime >= src.stat().st_mtime
                 and obj.stat().st_mtime >= newest_header):
             continue
-        cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("BS_NVCC_EXTRA", "").split()
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

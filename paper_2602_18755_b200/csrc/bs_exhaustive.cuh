@@ -223,6 +223,10 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
   }
 }
 
+#ifndef BS_SWEEP_MINB
+#define BS_SWEEP_MINB 3  // resident CTAs per SM the sweep is register-budgeted for
+#endif
+
 // Per-thread accumulator of the sweep.
 struct LeafAcc {
   double best;               // local minimum objective (+inf: none)
@@ -469,7 +473,7 @@ __device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsig
 }
 
 // One thread per final node: the I bottom levels of its subtree.
-__global__ void __launch_bounds__(256) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
+__global__ void __launch_bounds__(256, BS_SWEEP_MINB) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
                                                     FinalList fin, Key128* best, unsigned long long* feas) {
   const unsigned long long n_fin = ctl->final_count;
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;

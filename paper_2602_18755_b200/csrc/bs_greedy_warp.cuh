@@ -1,0 +1,391 @@
+// bs_greedy_warp.cuh — greedy_freq_select (dvfs.hpp:185-259) for one
+// decision by ONE warp (included after bs_mpc_core.cuh inside a translation
+// unit's anonymous namespace).
+//
+// Same decision, counters and errors as greedy_block, organised for many
+// concurrent decisions per SM (the cluster replay runs one prefill instance
+// per warp):
+//   * compact per-warp tables in shared memory, row stride = |cand|;
+//   * positions of a level by a ballot over batches;
+//   * a level's mutations by an exact prefix-sharing depth-first walk:
+//     lanes own prefixes of the first J mutated positions (digit 0 = the
+//     earliest position, as in the reference's code), and walk the rest in
+//     batch order keeping (t, num, den) per depth.  A step that violates
+//     meets_slo ends every mutation below it (meets_slo returns false at the
+//     first violation, dvfs.hpp:117), so the subtree is skipped.  Each
+//     surviving mutation's clock and sums are built by the same additions in
+//     the same k order as eval_assignment, so objectives are bit-identical.
+//     Used only when no (k, f) prediction of the decision is bad; otherwise
+//     every mutation is evaluated in full (exact ModelError order).
+#pragma once
+
+struct WTables {
+  int K, nc, status, anybad;
+  double ttft;
+  unsigned bad_lat[kMaxK];
+  unsigned bad_pow[kMaxK];
+  long long n_req[kMaxK];
+  long long sum_len[kMaxK];
+  double wf[kMaxK];
+  double minarr[kMaxK];
+  int ncomp[kMaxK];
+  // views into the warp's table scratch: [k * nc + f]
+  double *A, *P, *E, *B0, *B1;
+  double* T1;
+};
+
+struct WGreedyShared {
+  WTables T;
+  int np;
+  int accepted;
+  double obj;
+  unsigned char cur[kMaxK];
+  int pos[kMaxK];
+};
+
+__host__ __device__ inline size_t wtable_doubles(int horizon, int nc) { return 5ull * horizon * nc + nc; }
+
+__device__ inline void wtables_bind(WTables& T, double* scratch, int horizon, int nc) {
+  const size_t kn = static_cast<size_t>(horizon) * nc;
+  T.A = scratch;
+  T.P = T.A + kn;
+  T.E = T.P + kn;
+  T.B0 = T.E + kn;
+  T.B1 = T.B0 + kn;
+  T.T1 = T.B1 + kn;
+}
+
+// eval_assignment on the compact tables (see bs_mpc_core.cuh).
+__device__ inline int weval(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* idx,
+                            double* obj, int* err) {
+  *err = 0;
+  const int K = T.K, nc = T.nc;
+  double t = pr.now;
+  for (int k = 0; k < K; ++k) {
+    const int f = idx[k];
+    if ((T.bad_lat[k] >> f) & 1u) {
+      *err = 1;
+      return 0;
+    }
+    const bool sw = k == 0 ? (c.cand[f] != pr.cur_freq) : (f != idx[k - 1]);
+    t = __dadd_rn(t, sw ? T.B1[k * nc + f] : T.B0[k * nc + f]);
+    if (__dsub_rn(t, T.minarr[k]) > T.ttft) return 0;
+  }
+  double num = 0.0, den = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const int f = idx[k];
+    if ((T.bad_lat[k] >> f) & 1u) {
+      *err = 1;
+      return 1;
+    }
+    if ((T.bad_pow[k] >> f) & 1u) {
+      *err = 2;
+      return 1;
+    }
+    num = __dadd_rn(num, T.E[k * nc + f]);
+    den = __dadd_rn(den, T.A[k * nc + f]);
+  }
+  *obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+  return 1;
+}
+
+// One meets_slo step plus the objective sums (no bad predictions).
+__device__ __forceinline__ bool wstep(const WTables& T, const DProblem& pr, const DMpcCfg& c, int k, int f,
+                                      double& t, double& num, double& den, int& last) {
+  const int nc = T.nc;
+  const bool sw = k == 0 ? (c.cand[f] != pr.cur_freq) : (f != last);
+  t = __dadd_rn(t, sw ? T.B1[k * nc + f] : T.B0[k * nc + f]);
+  if (__dsub_rn(t, T.minarr[k]) > T.ttft) return false;
+  num = __dadd_rn(num, T.E[k * nc + f]);
+  den = __dadd_rn(den, T.A[k * nc + f]);
+  last = f;
+  return true;
+}
+
+// All mutations of one level with a common prefix (digits 0..J-1 fixed =
+// `prefix`, digit i <-> position pos[i]); folds feasible ones into
+// (bo, bc, feas).  digit -> candidate: 0 target, 1 r1, 2 r2.
+__device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* cur,
+                           const int* pos, int np, int base, int target, int r1, int r2, int J,
+                           unsigned long long prefix, unsigned long long& bo, unsigned long long& bc,
+                           unsigned long long& feas) {
+  const int K = T.K;
+  auto cand_of = [&](int d) { return d == 0 ? target : (d == 1 ? r1 : r2); };
+  // prefix digits (least significant = earliest position)
+  int dig[kMaxK];
+  unsigned long long pw[kMaxK + 1];
+  pw[0] = 1;
+  for (int i = 0; i < np; ++i) pw[i + 1] = pw[i] * static_cast<unsigned long long>(base);
+  unsigned long long rem = prefix;
+  for (int i = 0; i < J; ++i) {
+    dig[i] = static_cast<int>(rem % base);
+    rem /= base;
+  }
+  // walk k = 0 .. (J < np ? pos[J] - 1 : K - 1) with the prefix applied
+  double t = pr.now, num = 0.0, den = 0.0;
+  int last = -1;
+  const int stop0 = J < np ? pos[J] : K;
+  int pi = 0;
+  for (int k = 0; k < stop0; ++k) {
+    int f = cur[k];
+    if (pi < J && pos[pi] == k) f = cand_of(dig[pi++]);
+    if (!wstep(T, pr, c, k, f, t, num, den, last)) return;
+  }
+  unsigned long long lexp = 0;  // lex key of the prefix digits
+  for (int i = 0; i < J; ++i) lexp = lexp * base + static_cast<unsigned long long>(base - 1 - dig[i]);
+  auto leaf = [&](double n, double d, unsigned long long code, unsigned long long lex) {
+    if (code == 0) return;  // the unmutated assignment is not a mutation
+    ++feas;
+    const double obj = d > 0.0 ? __ddiv_rn(n, d) : 0.0;
+    const unsigned long long ob = static_cast<unsigned long long>(__double_as_longlong(obj));
+    if (key_less(ob, lex, bo, bc)) {
+      bo = ob;
+      bc = lex;
+    }
+  };
+  if (J == np) {
+    leaf(num, den, prefix, lexp);
+    return;
+  }
+  // iterative DFS over digits J..np-1
+  double st_t[kMaxK + 1], st_n[kMaxK + 1], st_d[kMaxK + 1];
+  int st_l[kMaxK + 1];
+  unsigned long long st_code[kMaxK + 1], st_lex[kMaxK + 1];
+  st_t[J] = t;
+  st_n[J] = num;
+  st_d[J] = den;
+  st_l[J] = last;
+  st_code[J] = prefix;
+  st_lex[J] = lexp;
+  int i = J;
+  dig[J] = 0;
+  for (;;) {
+    if (dig[i] == base) {
+      if (i == J) break;
+      --i;
+      ++dig[i];
+      continue;
+    }
+    double tt = st_t[i], nn = st_n[i], dd = st_d[i];
+    int ll = st_l[i];
+    const int end = i + 1 < np ? pos[i + 1] : K;
+    bool ok = wstep(T, pr, c, pos[i], cand_of(dig[i]), tt, nn, dd, ll);
+    for (int k = pos[i] + 1; ok && k < end; ++k) ok = wstep(T, pr, c, k, cur[k], tt, nn, dd, ll);
+    if (!ok) {  // meets_slo fails below this digit: no feasible mutation in the subtree
+      ++dig[i];
+      continue;
+    }
+    const unsigned long long code = st_code[i] + static_cast<unsigned long long>(dig[i]) * pw[i];
+    const unsigned long long lex = st_lex[i] * base + static_cast<unsigned long long>(base - 1 - dig[i]);
+    if (i + 1 == np) {
+      leaf(nn, dd, code, lex);
+      ++dig[i];
+      continue;
+    }
+    st_t[i + 1] = tt;
+    st_n[i + 1] = nn;
+    st_d[i + 1] = dd;
+    st_l[i + 1] = ll;
+    st_code[i + 1] = code;
+    st_lex[i + 1] = lex;
+    ++i;
+    dig[i] = 0;
+  }
+}
+
+// greedy_freq_select for one decision by the calling warp (all 32 lanes).
+// fl / fp: the controller's latency / power grids reduced per candidate
+// (FastGrid), or null for the generic interpolator.  lv (optional): level
+// stats.  Results in *o (lane 0 writes; the warp is synchronised on return).
+__device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
+                            const DRunning* R, WGreedyShared& S, DMpcOut* o, DLevel* lv, const FastGrid* fl,
+                            const FastGrid* fp) {
+  const int lane = threadIdx.x & 31;
+  WTables& T = S.T;
+  if (lane == 0) {
+    T.nc = c.nc;
+    T.ttft = c.ttft;
+    int st = project_dev(pr, c, W, R, &T);
+    if (st == BS_OK && (m.grid[0].bad_axis || m.grid[2].bad_axis) && T.K > 0) st = BS_MODEL_ERROR;
+    T.status = st;
+    for (int k = 0; k < kMaxK; ++k) T.bad_lat[k] = T.bad_pow[k] = 0u;
+    memset(o, 0, sizeof *o);
+    o->status = st;
+    o->K = T.K;
+  }
+  __syncwarp();
+  if (T.status != BS_OK) return;
+  const int K = T.K, nc = c.nc;
+  if (K == 0) {  // dvfs.hpp:194-197
+    if (lane == 0) o->feasible = 1;
+    __syncwarp();
+    return;
+  }
+  unsigned anybad = 0;
+  for (int e = lane; e < K * nc; e += 32) {
+    const int k = e / nc, f = e - k * nc;
+    double L, P;
+    if (fl) {
+      L = fast_interp(fl[f], T.n_req[k], T.sum_len[k]);
+      P = fast_interp(fp[f], T.n_req[k], T.sum_len[k]);
+    } else {
+      const Query q = make_query(T.n_req[k], T.sum_len[k], pr.tp, c.cand[f]);
+      L = interp(m.grid[0], q, nullptr);
+      P = interp(m.grid[2], q, nullptr);
+    }
+    if (!model_value_ok(L)) {
+      atomicOr(&T.bad_lat[k], 1u << f);
+      anybad = 1;
+    }
+    if (!model_value_ok(P)) {
+      atomicOr(&T.bad_pow[k], 1u << f);
+      anybad = 1;
+    }
+    const double A = __dmul_rn(T.wf[k], L);                                  // dvfs.hpp:112-113, 154-155
+    T.A[e] = A;
+    T.P[e] = P;
+    T.E[e] = __dmul_rn(A, P);                                               // dvfs.hpp:167
+    T.B0[e] = __dmul_rn(A, c.one_plus_margin);                              // dvfs.hpp:115
+    T.B1[e] = __dmul_rn(__dadd_rn(A, c.switch_ms), c.one_plus_margin);      // dvfs.hpp:114-115
+    if (k == 0) T.T1[f] = __dadd_rn(pr.now, c.cand[f] != pr.cur_freq ? T.B1[e] : T.B0[e]);
+  }
+  const bool bad = __any_sync(0xffffffffu, anybad);
+  __syncwarp();
+  // all-max initialization (dvfs.hpp:201-205)
+  if (lane == 0) {
+    for (int k = 0; k < K; ++k) S.cur[k] = static_cast<unsigned char>(nc - 1);
+    double obj = 0.0;
+    int err;
+    const int feas = weval(T, pr, c, S.cur, &obj, &err);
+    if (!feas && !err) {
+      for (int k = 0; k < K && !err; ++k) {
+        if ((T.bad_lat[k] >> (nc - 1)) & 1u) err = 1;
+        else if ((T.bad_pow[k] >> (nc - 1)) & 1u) err = 2;
+      }
+      double num = 0.0, den = 0.0;
+      for (int k = 0; k < K; ++k) {
+        num = __dadd_rn(num, T.E[k * nc + nc - 1]);
+        den = __dadd_rn(den, T.A[k * nc + nc - 1]);
+      }
+      obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+    }
+    if (err) o->status = BS_MODEL_ERROR;
+    S.accepted = feas;  // broadcast the initial feasibility
+    S.obj = obj;
+    o->feasible = feas;
+    o->eval_count = 1;
+    o->objective = obj;
+  }
+  __syncwarp();
+  if (o->status != BS_OK) return;
+  if (S.accepted && nc > 1) {
+    const int last_level = nc >= 3 ? nc - 2 : 1;
+    for (int l = 1; l <= last_level; ++l) {
+      const int target = nc - l;  // avail[l-1] (ascending index)
+      const int r1 = nc - 1 - l;  // avail[l]
+      const int r2 = l + 1 < nc ? nc - 2 - l : -1;
+      const int base = r2 >= 0 ? 3 : 2;
+      const unsigned pm = __ballot_sync(0xffffffffu, lane < K && S.cur[lane] == target);
+      const int np = __popc(pm);
+      if (np == 0) break;  // dvfs.hpp:222
+      if (lane == 0) {
+        unsigned mm = pm;
+        for (int i = 0; i < np; ++i) {
+          S.pos[i] = __ffs(mm) - 1;
+          mm &= mm - 1;
+        }
+      }
+      __syncwarp();
+      const unsigned long long combos = ipow(static_cast<unsigned long long>(base), np);
+      unsigned long long bo = ~0ull, bc = ~0ull, feas = 0, errkey = ~0ull;
+      if (!bad) {
+        // prefixes of the first J digits spread over lanes
+        int J = 0;
+        unsigned long long tasks = 1;
+        while (J < np && tasks < 64) {
+          tasks *= base;
+          ++J;
+        }
+        for (unsigned long long p = lane; p < tasks; p += 32)
+          wlevel_dfs(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, p, bo, bc, feas);
+      } else {
+        unsigned char mut[kMaxK];
+        for (int k = 0; k < K; ++k) mut[k] = S.cur[k];
+        for (unsigned long long code = 1 + lane; code < combos; code += 32) {
+          unsigned long long cc = code, lex = 0;
+          for (int i = 0; i < np; ++i) {  // digit i -> pos[i], least significant first (dvfs.hpp:233-237)
+            const unsigned long long digit = cc % base;
+            cc /= base;
+            mut[S.pos[i]] = static_cast<unsigned char>(digit == 0 ? target : (digit == 1 ? r1 : r2));
+          }
+          for (int i = 0; i < np; ++i) {
+            const unsigned char v = mut[S.pos[i]];
+            const unsigned long long digit = v == target ? 0 : (v == r1 ? 1 : 2);
+            lex = lex * base + (base - 1 - digit);
+          }
+          double obj = 0.0;
+          int err;
+          const int ok = weval(T, pr, c, mut, &obj, &err);
+          if (err) {
+            const unsigned long long ek = (code << 2) | static_cast<unsigned long long>(err);
+            errkey = ek < errkey ? ek : errkey;
+            continue;
+          }
+          if (!ok) continue;
+          ++feas;
+          const unsigned long long ob = static_cast<unsigned long long>(__double_as_longlong(obj));
+          if (key_less(ob, lex, bo, bc)) {
+            bo = ob;
+            bc = lex;
+          }
+        }
+      }
+#pragma unroll
+      for (int of = 16; of > 0; of >>= 1) {
+        const unsigned long long oo = __shfl_xor_sync(0xffffffffu, bo, of);
+        const unsigned long long oc = __shfl_xor_sync(0xffffffffu, bc, of);
+        if (key_less(oo, oc, bo, bc)) {
+          bo = oo;
+          bc = oc;
+        }
+        feas += __shfl_xor_sync(0xffffffffu, feas, of);
+        const unsigned long long oe = __shfl_xor_sync(0xffffffffu, errkey, of);
+        errkey = oe < errkey ? oe : errkey;
+      }
+      if (lane == 0) {
+        o->eval_count += static_cast<long long>(combos - 1);  // every mutation counts (dvfs.hpp:238)
+        DLevel Lv;
+        Lv.k_prime = np;
+        Lv.replaced_mhz = c.cand[target];
+        Lv.mutations = static_cast<long long>(combos - 1);
+        Lv.feasible_mutations = static_cast<long long>(feas);
+        Lv.accepted = 0;
+        if (errkey != ~0ull) {
+          o->status = BS_MODEL_ERROR;
+          o->n_levels = -static_cast<int>(errkey & 3ull);
+        } else {
+          const double bp = __longlong_as_double(static_cast<long long>(bo));
+          if (bo != ~0ull && bp <= S.obj) {
+            unsigned long long lx = bc;
+            for (int i = np - 1; i >= 0; --i) {
+              const unsigned long long digit = base - 1 - (lx % base);
+              lx /= base;
+              S.cur[S.pos[i]] = static_cast<unsigned char>(digit == 0 ? target : (digit == 1 ? r1 : r2));
+            }
+            S.obj = bp;
+            o->objective = bp;
+            Lv.accepted = 1;
+          }
+          if (lv) lv[o->n_levels] = Lv;
+          o->n_levels += 1;
+        }
+        S.accepted = Lv.accepted;
+      }
+      __syncwarp();
+      if (o->status != BS_OK || S.accepted == 0) break;
+    }
+  }
+  if (lane == 0 && o->status == BS_OK)
+    for (int k = 0; k < K; ++k) o->idx[k] = S.cur[k];
+  __syncwarp();
+}

@@ -18,7 +18,8 @@ __host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) 
 // (scheduler.hpp:40-66).  Only the queue head can be partially consumed (a
 // partial chunk ends a batch), so the state is (head, head_remaining).
 // ---------------------------------------------------------------------------
-__device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting* W, const DRunning* R, DTables* T) {
+template <class Tab>
+__device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting* W, const DRunning* R, Tab* T) {
   int K = 0;
   if (pr.run_active) {
     T->n_req[0] = pr.run_n;

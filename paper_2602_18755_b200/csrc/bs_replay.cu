@@ -42,8 +42,8 @@ using namespace bs;
 namespace {
 
 #include "bs_mpc_core.cuh"
+#include "bs_greedy_warp.cuh"
 
-constexpr int kPrefillThreads = 128;
 constexpr int kReportThreads = 256;
 constexpr long long kEventGuard = 4000000000ll;
 
@@ -733,21 +733,42 @@ struct PrefillSim {
   }
 };
 
-__global__ void __launch_bounds__(kPrefillThreads) prefill_kernel(DReplay R, const int* pre_ids, int n_pre) {
-  __shared__ GreedyShared S;
+// One warp per prefill instance: lane 0 runs the event loop, the whole warp
+// runs every controller consultation (greedy_warp, bs_greedy_warp.cuh).
+// Per-warp dynamic shared memory: the greedy state and snapshot, the
+// per-frequency model caches and the compact (k, f) tables.
+struct PreWarp {
+  WGreedyShared G;
+  DProblem pr;
+  DMpcOut out;
+};
+
+constexpr int kPrefillWarps = 4;
+
+__host__ __device__ inline size_t pre_warp_bytes(int max_ns, int max_h, int max_nc) {
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  return a16(sizeof(PreWarp)) + a16(pre_cache_bytes(max_ns)) + a16(8 * wtable_doubles(max_h, max_nc));
+}
+
+__global__ void __launch_bounds__(kPrefillWarps * 32) prefill_kernel(DReplay R, const int* pre_ids, int n_pre,
+                                                                    int max_ns, int max_h, int max_nc) {
   extern __shared__ __align__(16) unsigned char pre_dsm[];
-  __shared__ DProblem s_pr;
-  __shared__ DMpcOut s_out;
-  __shared__ int s_cmd;
-  if (blockIdx.x >= n_pre) return;
-  const int gi = pre_ids[blockIdx.x];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int wid = blockIdx.x * kPrefillWarps + wib;
+  if (wid >= n_pre) return;  // whole warps only
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  unsigned char* base = pre_dsm + static_cast<size_t>(wib) * pre_warp_bytes(max_ns, max_h, max_nc);
+  PreWarp& S = *reinterpret_cast<PreWarp*>(base);
+  const int gi = pre_ids[wid];
   const DInst I = R.inst[gi];
   const DRCfg* C = &R.cfgs[R.scen[I.scen].cfg];
-  // slots [0, nc): the MPC candidates (indexed like DTables' f); slot nc: base
+  // cache slots [0, nc): the MPC candidates (indexed like the tables' f); slot nc: base
   const int nc = C->controlled ? C->mpc.nc : 0;
   const int ns = nc + 1;
-  const PreCache G = pre_cache_at(pre_dsm, ns);
-  for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+  const PreCache G = pre_cache_at(base + a16(sizeof(PreWarp)), ns);
+  double* tab = reinterpret_cast<double*>(base + a16(sizeof(PreWarp)) + a16(pre_cache_bytes(max_ns)));
+  if (lane == 0 && C->controlled) wtables_bind(S.G.T, tab, C->mpc.horizon, C->mpc.nc);
+  for (int t = lane; t < ns; t += 32) {
     const double f = t < nc ? C->mpc.cand[t] : I.base_freq;
     G.f[t] = f;
     int err = 0;
@@ -755,29 +776,28 @@ __global__ void __launch_bounds__(kPrefillThreads) prefill_kernel(DReplay R, con
     G.idle_err[t] = idle_w(R.sim.idle, I.tp, f, &p, &err) ? 0 : err;
     G.idle[t] = p;
   }
-  for (int t = threadIdx.x; t < 4 * ns; t += blockDim.x) {
+  for (int t = lane; t < 4 * ns; t += 32) {
     const int g = t / ns, k = t - g * ns;
     const double f = k < nc ? C->mpc.cand[k] : I.base_freq;
     const FastGrid fg = fast_grid(g < 2 ? R.sim.grid[g == 0 ? 0 : 2] : R.ctl.grid[g == 2 ? 0 : 2], I.tp, f);
     (g == 0 ? G.lat : g == 1 ? G.pw : g == 2 ? G.clat : G.cpw)[k] = fg;
   }
-  __syncthreads();
+  __syncwarp();
   PrefillSim sim;
-  if (threadIdx.x == 0) sim.init(&R, &I, C, &G);  // G: views, valid for the block's lifetime
+  if (lane == 0) sim.init(&R, &I, C, &G);
   for (;;) {
-    if (threadIdx.x == 0) s_cmd = sim.advance(&s_out, &s_pr);
-    __syncthreads();
-    if (s_cmd == 0) break;
-    greedy_block(R.ctl, s_pr, C->mpc, R.W + s_pr.wait_off, nullptr, S, &s_out, nullptr, G.clat, G.cpw);
-    __syncthreads();
+    int cmd = 0;
+    if (lane == 0) cmd = sim.advance(&S.out, &S.pr);
+    cmd = __shfl_sync(0xffffffffu, cmd, 0);
+    if (cmd == 0) break;
+    greedy_warp(R.ctl, S.pr, C->mpc, R.W + S.pr.wait_off, nullptr, S.G, &S.out, nullptr, G.clat, G.cpw);
   }
-  if (threadIdx.x == 0) {
-    DInstState* s = &R.st[gi];
-    save_state(s, sim.w, sim.now, sim.fb);
-    s->n_done = sim.n_done;
+  if (lane == 0) {
+    DInstState* st = &R.st[gi];
+    save_state(st, sim.w, sim.now, sim.fb);
+    st->n_done = sim.n_done;
   }
 }
-
 
 // --- phase 2 routing ----------------------------------------------------------------
 
@@ -1886,13 +1906,19 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
     for (auto& e : ev) BS_CUDA_TRY(ctx, cudaEventCreate(&e));
     BS_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
     if (!pre_ids.empty()) {
-      int max_ns = 1;
-      for (const DRCfg& c : hcfg) max_ns = std::max(max_ns, (c.controlled ? c.mpc.nc : 0) + 1);
-      const size_t psmem = pre_cache_bytes(max_ns);
+      int max_ns = 1, max_h = 1, max_nc = 1;
+      for (const DRCfg& c : hcfg) {
+        if (!c.controlled) continue;
+        max_ns = std::max(max_ns, c.mpc.nc + 1);
+        max_h = std::max(max_h, c.mpc.horizon);
+        max_nc = std::max(max_nc, c.mpc.nc);
+      }
+      const size_t psmem = kPrefillWarps * pre_warp_bytes(max_ns, max_h, max_nc);
       BS_CUDA_TRY(ctx, cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(psmem)));
-      prefill_kernel<<<static_cast<int>(pre_ids.size()), kPrefillThreads, psmem, ctx->stream>>>(
-          R, dpre, static_cast<int>(pre_ids.size()));
+      const int np_ = static_cast<int>(pre_ids.size());
+      prefill_kernel<<<(np_ + kPrefillWarps - 1) / kPrefillWarps, kPrefillWarps * 32, psmem, ctx->stream>>>(
+          R, dpre, np_, max_ns, max_h, max_nc);
       BS_LAUNCH_CHECK(ctx);
     }
     BS_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
