@@ -741,16 +741,20 @@ struct PreWarp {
   WGreedyShared G;
   DProblem pr;
   DMpcOut out;
+  PrefillSim sim;  // lane 0's event-loop state, kept out of the register file
 };
 
 constexpr int kPrefillWarps = 4;
+#ifndef BS_PREFILL_MINB
+#define BS_PREFILL_MINB 4  // resident CTAs per SM the prefill kernel is register-budgeted for
+#endif
 
 __host__ __device__ inline size_t pre_warp_bytes(int max_ns, int max_h, int max_nc) {
   auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
   return a16(sizeof(PreWarp)) + a16(pre_cache_bytes(max_ns)) + a16(8 * wtable_doubles(max_h, max_nc));
 }
 
-__global__ void __launch_bounds__(kPrefillWarps * 32) prefill_kernel(DReplay R, const int* pre_ids, int n_pre,
+__global__ void __launch_bounds__(kPrefillWarps * 32, BS_PREFILL_MINB) prefill_kernel(DReplay R, const int* pre_ids, int n_pre,
                                                                     int max_ns, int max_h, int max_nc) {
   extern __shared__ __align__(16) unsigned char pre_dsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -783,7 +787,7 @@ __global__ void __launch_bounds__(kPrefillWarps * 32) prefill_kernel(DReplay R, 
     (g == 0 ? G.lat : g == 1 ? G.pw : g == 2 ? G.clat : G.cpw)[k] = fg;
   }
   __syncwarp();
-  PrefillSim sim;
+  PrefillSim& sim = S.sim;
   if (lane == 0) sim.init(&R, &I, C, &G);
   for (;;) {
     int cmd = 0;
@@ -887,6 +891,10 @@ __global__ void route_kernel(DReplay R, int n_scen) {
 
 // --- decode instances -----------------------------------------------------------------
 
+#ifndef BS_DECODE_MINB
+#define BS_DECODE_MINB 4
+#endif
+
 // select_decode_freq_ex (dvfs.hpp:274-293) as a warp ladder walk (lane j
 // evaluates rung j of each 32-rung chunk; a ballot finds where the
 // reference's ascending walk stops).  Warp-uniform; false on ModelError.
@@ -940,7 +948,7 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 // over lanes for the per-iteration emissions (every resident emits one token
 // at every iteration end, simulator.hpp:544-557), whose per-request
 // reductions (first/last token, worst gap) are kept in the resident entry.
-__global__ void __launch_bounds__(128) decode_kernel(DReplay R, const int* dec_ids, int n_dec, int max_slots) {
+__global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, const int* dec_ids, int n_dec, int max_slots) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
