@@ -2,9 +2,10 @@
 // decision by ONE warp (included after bs_mpc_core.cuh inside a translation
 // unit's anonymous namespace).
 //
-// Same decision, counters and errors as greedy_block, organised for many
-// concurrent decisions per SM (the cluster replay runs one prefill instance
-// per warp):
+// Same decision, level statistics, eval counts and ModelError order as the
+// reference, organised for many concurrent decisions per SM (bs_mpc_greedy
+// runs one decision per warp, the cluster replay one prefill instance per
+// warp):
 //   * compact per-warp tables in shared memory, row stride = |cand|;
 //   * positions of a level by a ballot over batches;
 //   * a level's mutations by an exact prefix-sharing depth-first walk:

@@ -35,6 +35,7 @@ constexpr double kFilterMinBest = 0x1p-100;
 constexpr double kFilterMinDen = 0x1p-900;
 
 #include "bs_mpc_core.cuh"
+#include "bs_greedy_warp.cuh"
 
 #include "bs_exhaustive.cuh"
 
@@ -84,15 +85,36 @@ __global__ void finalize_kernel(const DTables* __restrict__ tables, const DMpcCf
 // ---------------------------------------------------------------------------
 // greedy_freq_select (dvfs.hpp:185-259): one CTA per decision.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
-                                                                const DWaiting* W, const DRunning* R, DMpcOut* out,
-                                                                DLevel* levels, int n) {
-  __shared__ GreedyShared S;
-  const int d = blockIdx.x;
+// One warp per decision (greedy_warp, bs_greedy_warp.cuh): per-warp
+// dynamic shared memory holds the greedy state, the result and the compact
+// (k, f) tables.
+constexpr int kGreedyWarps = 4;
+
+__host__ __device__ inline size_t greedy_warp_bytes(int max_h, int max_nc) {
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  return a16(sizeof(WGreedyShared)) + a16(sizeof(DMpcOut)) + a16(8 * wtable_doubles(max_h, max_nc));
+}
+
+__global__ void __launch_bounds__(kGreedyWarps * 32) greedy_kernel(DModels m, const DMpcCfg* cfgs,
+                                                                  const DProblem* probs, const DWaiting* W,
+                                                                  const DRunning* R, DMpcOut* out, DLevel* levels,
+                                                                  int n, int max_h, int max_nc) {
+  extern __shared__ __align__(16) unsigned char gdsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int d = blockIdx.x * kGreedyWarps + wib;
   if (d >= n) return;
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  unsigned char* base = gdsm + static_cast<size_t>(wib) * greedy_warp_bytes(max_h, max_nc);
+  WGreedyShared& S = *reinterpret_cast<WGreedyShared*>(base);
+  DMpcOut* o = reinterpret_cast<DMpcOut*>(base + a16(sizeof(WGreedyShared)));
+  double* tab = reinterpret_cast<double*>(base + a16(sizeof(WGreedyShared)) + a16(sizeof(DMpcOut)));
   const DProblem pr = probs[d];
-  greedy_block(m, pr, cfgs[pr.cfg], W + pr.wait_off, R + pr.run_off, S, &out[d],
-               levels + static_cast<size_t>(d) * BS_MAX_LEVELS);
+  const DMpcCfg& c = cfgs[pr.cfg];
+  if (lane == 0) wtables_bind(S.T, tab, c.horizon, c.nc);
+  __syncwarp();
+  greedy_warp(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o, levels + static_cast<size_t>(d) * BS_MAX_LEVELS,
+              nullptr, nullptr);
+  if (lane == 0) out[d] = *o;
 }
 
 // ---------------------------------------------------------------------------
@@ -334,8 +356,12 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   }
   BS_REC(0);
   if (run->mode == kGreedy) {
-    greedy_kernel<<<n, kGreedyThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
-                                                         run->dOut, run->dLv, n);
+    const size_t smem = kGreedyWarps * greedy_warp_bytes(pk.max_horizon, pk.max_nc);
+    BS_CUDA_TRY(ctx, cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+    greedy_kernel<<<(n + kGreedyWarps - 1) / kGreedyWarps, kGreedyWarps * 32, smem, ctx->stream>>>(
+        models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running, run->dOut, run->dLv, n, pk.max_horizon,
+        pk.max_nc);
     BS_LAUNCH_CHECK(ctx);
     BS_REC(1);
     return BS_OK;

@@ -1,11 +1,9 @@
 // bs_mpc_core.cuh — prefill-MPC building blocks shared by the MPC kernels
 // (bs_mpc.cu) and the cluster replay (bs_replay.cu): project_batches on the
-// device, the per-decision (k, f) tables, the assignment evaluator and the
-// block-cooperative greedy search.  Included inside each translation unit's
+// device, the per-decision (k, f) tables of the exhaustive search and the
+// assignment evaluator.  The greedy search is bs_greedy_warp.cuh.  Included inside each translation unit's
 // anonymous namespace.  Reference: proj/include/pdsim/dvfs.hpp.
 #pragma once
-
-constexpr int kGreedyThreads = 256;
 
 __host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) {
   unsigned long long r = 1;
@@ -246,185 +244,4 @@ __device__ double tw_objective(const DTables& T, const unsigned char* idx) {
     den = __dadd_rn(den, T.A[k][idx[k]]);
   }
   return den > 0.0 ? __ddiv_rn(num, den) : 0.0;
-}
-
-// Shared state of one block-cooperative greedy decision.
-struct GreedyShared {
-  DTables T;
-  int status;
-  int np;
-  int init_feas;
-  int accepted;
-  double obj;
-  unsigned long long feas;
-  unsigned long long err;  // min over (code << 2 | type) of erroring mutations
-  unsigned long long wbo[kGreedyThreads / 32], wbc[kGreedyThreads / 32];
-  int pos[kMaxK];
-  unsigned char cur[kMaxK];
-};
-
-// greedy_freq_select (dvfs.hpp:185-259) for one decision by the whole CTA
-// (blockDim.x <= kGreedyThreads, a multiple of 32); every thread must call
-// it.  Results in *o (and per-level stats in lv when non-null); o may live
-// in shared or global memory.  Returns with the block synchronised.
-__device__ void greedy_block(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
-                             const DRunning* R, GreedyShared& S, DMpcOut* o, DLevel* lv,
-                             const FastGrid* fl = nullptr, const FastGrid* fp = nullptr) {
-  build_tables(m, pr, c, W, R, &S.T, &S.status, fl, fp);
-  const int K = S.T.K, nc = c.nc;
-  if (threadIdx.x == 0) {
-    memset(o, 0, sizeof *o);
-    o->status = S.status;
-    o->K = K;
-  }
-  if (S.status != BS_OK) return;
-  if (K == 0) {  // dvfs.hpp:194-197
-    if (threadIdx.x == 0) o->feasible = 1;
-    return;
-  }
-  // all-max initialization (dvfs.hpp:201-205)
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < K; ++k) S.cur[k] = static_cast<unsigned char>(nc - 1);
-    double obj = 0.0;
-    int err;
-    const int feas = eval_assignment(S.T, pr, c, S.cur, &obj, &err);
-    if (!feas && !err) {
-      // infeasible: objective still computed (dvfs.hpp:204), may raise
-      for (int k = 0; k < K && !err; ++k) {
-        if ((S.T.bad_lat[k] >> (nc - 1)) & 1u) err = 1;
-        else if ((S.T.bad_pow[k] >> (nc - 1)) & 1u) err = 2;
-      }
-      obj = tw_objective(S.T, S.cur);
-    }
-    if (err) o->status = BS_MODEL_ERROR;
-    S.init_feas = feas;
-    S.obj = obj;
-    o->feasible = feas;
-    o->eval_count = 1;
-    o->objective = obj;
-  }
-  __syncthreads();
-  if (o->status != BS_OK) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (S.init_feas && nc > 1) {
-    const int last_level = nc >= 3 ? nc - 2 : 1;
-    // avail (descending) position j <-> ascending index nc - 1 - j
-    for (int l = 1; l <= last_level; ++l) {
-      const int target = nc - l;  // avail[l-1]
-      const int r1 = nc - 1 - l;  // avail[l]
-      const int r2 = l + 1 < nc ? nc - 2 - l : -1;
-      const unsigned long long base = r2 >= 0 ? 3ull : 2ull;
-      if (threadIdx.x == 0) {
-        int np = 0;
-        for (int k = 0; k < K; ++k)
-          if (S.cur[k] == target) S.pos[np++] = k;
-        S.np = np;
-        S.feas = 0;
-        S.err = ~0ull;
-      }
-      __syncthreads();
-      const int np = S.np;
-      if (np == 0) break;  // dvfs.hpp:222
-      const unsigned long long combos = ipow(base, np);
-      unsigned char mut[kMaxK];
-      for (int k = 0; k < K; ++k) mut[k] = S.cur[k];
-      unsigned long long bo = ~0ull, bc = ~0ull, feas = 0, errkey = ~0ull;
-      for (unsigned long long code = 1 + threadIdx.x; code < combos; code += blockDim.x) {
-        unsigned long long cc = code, lex = 0;
-        for (int i = 0; i < np; ++i) {  // digit i -> S.pos[i], least significant first (dvfs.hpp:233-237)
-          const unsigned long long digit = cc % base;
-          cc /= base;
-          mut[S.pos[i]] = static_cast<unsigned char>(digit == 0 ? target : (digit == 1 ? r1 : r2));
-        }
-        // lexicographic key of the frequency vector: positions in batch
-        // order, smaller frequency (larger digit) first
-        for (int i = 0; i < np; ++i) {
-          const unsigned char v = mut[S.pos[i]];
-          const unsigned long long digit = v == target ? 0 : (v == r1 ? 1 : 2);
-          lex = lex * base + (base - 1 - digit);
-        }
-        double obj = 0.0;
-        int err;
-        const int ok = eval_assignment(S.T, pr, c, mut, &obj, &err);
-        if (err) {
-          const unsigned long long ek = (code << 2) | static_cast<unsigned long long>(err);
-          errkey = ek < errkey ? ek : errkey;
-          continue;
-        }
-        if (!ok) continue;
-        ++feas;
-        const unsigned long long ob = static_cast<unsigned long long>(__double_as_longlong(obj));
-        if (key_less(ob, lex, bo, bc)) {
-          bo = ob;
-          bc = lex;
-        }
-      }
-      // block reduction of (obj, lex), feasible count, first error
-#pragma unroll
-      for (int of = 16; of > 0; of >>= 1) {
-        const unsigned long long oo = __shfl_xor_sync(0xffffffffu, bo, of);
-        const unsigned long long oc = __shfl_xor_sync(0xffffffffu, bc, of);
-        if (key_less(oo, oc, bo, bc)) {
-          bo = oo;
-          bc = oc;
-        }
-        feas += __shfl_xor_sync(0xffffffffu, feas, of);
-        const unsigned long long oe = __shfl_xor_sync(0xffffffffu, errkey, of);
-        errkey = oe < errkey ? oe : errkey;
-      }
-      if (lane == 0) {
-        S.wbo[warp] = bo;
-        S.wbc[warp] = bc;
-        atomicAdd(&S.feas, feas);
-        atomicMin(&S.err, errkey);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-          if (key_less(S.wbo[w], S.wbc[w], bo, bc)) {
-            bo = S.wbo[w];
-            bc = S.wbc[w];
-          }
-        // every mutation of the level is evaluated before acceptance
-        o->eval_count += static_cast<long long>(combos - 1);
-        DLevel L;
-        L.k_prime = np;
-        L.replaced_mhz = c.cand[target];
-        L.mutations = static_cast<long long>(combos - 1);
-        L.feasible_mutations = static_cast<long long>(S.feas);
-        L.accepted = 0;
-        if (S.err != ~0ull) {
-          o->status = BS_MODEL_ERROR;
-          o->n_levels = -static_cast<int>(S.err & 3ull);  // error type for the message
-        } else {
-          // improved iff best_p < cur or (== and lex_less(best, cur)); every
-          // mutation is lexicographically below the current assignment
-          const double bp = __longlong_as_double(static_cast<long long>(bo));
-          if (bo != ~0ull && bp <= S.obj) {
-            // decode the lex key back into digits
-            unsigned long long lx = bc;
-            for (int i = np - 1; i >= 0; --i) {
-              const unsigned long long digit = base - 1 - (lx % base);
-              lx /= base;
-              S.cur[S.pos[i]] = static_cast<unsigned char>(digit == 0 ? target : (digit == 1 ? r1 : r2));
-            }
-            S.obj = bp;
-            o->objective = bp;
-            L.accepted = 1;
-          }
-          if (lv) lv[o->n_levels] = L;
-          o->n_levels += 1;
-        }
-        S.accepted = L.accepted;  // broadcast acceptance (not S.feas: thread 0 resets that at the
-                                  // next level while slower warps may still be testing this flag)
-      }
-      __syncthreads();
-      if (o->status != BS_OK || S.accepted == 0) break;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && o->status == BS_OK) {
-    for (int k = 0; k < K; ++k) o->idx[k] = S.cur[k];
-  }
-  __syncthreads();
 }

@@ -7,12 +7,14 @@
 //                   a cheap sequential scan that fixes every prefill
 //                   instance's request list, so all device buffers are sized
 //                   exactly), packing into one H2D copy.
-//   prefill_kernel  one CTA per prefill instance.  Thread 0 runs the event
+//   prefill_kernel  one warp per prefill instance.  Lane 0 runs the event
 //                   loop of simulate_prefill_instance (simulator.hpp:
 //                   278-409); at every controller consultation (batch
-//                   boundary, arrival while running) the whole CTA runs the
-//                   greedy MPC (greedy_block, bs_mpc_core.cuh) on the live
-//                   queue, read in place from HBM.
+//                   boundary, arrival while running) the whole warp runs the
+//                   greedy MPC (greedy_warp, bs_greedy_warp.cuh) on the live
+//                   queue, read in place from HBM.  Every prediction goes
+//                   through per-frequency reduced-axis grids (FastGrid) cached
+//                   in shared memory.
 //   route_kernel    one thread per scenario: completions merged by
 //                   (done, id) across prefill instances and routed to decode
 //                   instances (deficit with load 1, simulator.hpp:840-853).
