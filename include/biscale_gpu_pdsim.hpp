@@ -421,10 +421,21 @@ inline pdsim::PlacementPlan solve_placement(const pdsim::PlacementProblem& p) {
 
 // solve_max_throughput (placement.hpp:421-499).
 inline pdsim::PlacementPlan solve_max_throughput(const pdsim::PlacementProblem& p, double max_freq_mhz) {
-  return detail::solve_with(p, [&](const bs_table_entry* t, int n, int64_t* counts, double* obj, int32_t* used) {
-    return bs_placement_max_throughput(nullptr, t, n, p.total_gpus, p.target_rps, p.alpha, max_freq_mhz, counts,
-                                       obj, used);
-  });
+  pdsim::PlacementPlan plan =
+      detail::solve_with(p, [&](const bs_table_entry* t, int n, int64_t* counts, double* obj, int32_t* used) {
+        return bs_placement_max_throughput(nullptr, t, n, p.total_gpus, p.target_rps, p.alpha, max_freq_mhz, counts,
+                                           obj, used);
+      });
+  // the plan carries the restricted table (placement.hpp:423-430, 486)
+  for (auto& e : plan.table) {
+    if (e.config.base_freq_mhz != max_freq_mhz) {
+      e.r_c = 0.0;
+      e.e_c.reset();
+      e.error = "below maximum frequency";
+    }
+  }
+  plan.instances = pdsim::derive_routing_weights(plan.counts, plan.table);
+  return plan;
 }
 
 // TwoTierFactory (dvfs.hpp:370-390): drop-in ControllerFactory for

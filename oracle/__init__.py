@@ -89,6 +89,21 @@ def load_oracle() -> C.CDLL:
     return _oracle
 
 
+class ref_runner_config(C.Structure):
+    """RunnerConfig as a POD (ref_driver.h)."""
+    _fields_ = [("slo", A.bs_slo), ("total_gpus", C.c_int32), ("n_tp", C.c_int32), ("tp_options", _P(C.c_int32)),
+                ("ladder", _dp), ("n_ladder", C.c_int32), ("mpc_k", C.c_int32), ("scheduler", A.bs_scheduler_policy),
+                ("alpha", C.c_double), ("peak_subwindow_s", C.c_double), ("search", A.bs_goodput_search),
+                ("plan_policy", A.bs_scheduler_policy), ("rampup_s", C.c_double),
+                ("switch_latency_ms", C.c_double), ("mpc_n", C.c_int32), ("_pad", C.c_int32),
+                ("mpc_margin", C.c_double), ("kv_threshold", C.c_double), ("decode_margin", C.c_double)]
+
+
+class ref_window_run(C.Structure):
+    _fields_ = [("window", C.c_int32), ("policy", C.c_int32), ("gpus_used", C.c_int32), ("slo_pass", C.c_int32),
+                ("objective_w", C.c_double), ("target_rps", C.c_double), ("report", A.bs_replay_summary)]
+
+
 def load_ref() -> C.CDLL:
     global _ref
     if _ref is None:
@@ -114,6 +129,9 @@ def load_ref() -> C.CDLL:
                                           _P(C.c_int64), _dp, _P(C.c_int32)]),
             "solve_max_throughput": (C.c_int, [_P(A.bs_table_entry), C.c_int, C.c_int, C.c_double, C.c_double,
                                                C.c_double, _P(C.c_int64), _dp, _P(C.c_int32)]),
+            "run_experiment": (C.c_int, [_P(A.bs_model_set), _P(A.bs_trace), C.c_double, _P(C.c_int32), C.c_int,
+                                         _P(ref_runner_config), _P(ref_window_run), C.c_int, _P(C.c_int),
+                                         _P(C.c_int32)]),
             "replay": (C.c_int, [_P(A.bs_model_set), _P(A.bs_model_set), _P(A.bs_replay_config), _P(A.bs_scenario),
                                  C.c_int, _P(A.bs_replay_summary), _P(A.bs_replay_request), _P(A.bs_replay_logs),
                                  C.c_int]),

@@ -771,3 +771,72 @@ extern "C" int ref_replay(const bs_model_set* sim_models, const bs_model_set* ct
     for (auto& th : pool) th.join();
   });
 }
+
+// --- run_experiment (runner.hpp:155-172) ------------------------------------------
+
+extern "C" int ref_run_experiment(const bs_model_set* models, const bs_trace* trace, double window_ms,
+                                  const int32_t* policies, int n_policies, const ref_runner_config* c,
+                                  ref_window_run* out, int cap, int* n_out, int32_t* two_tier_slo_pass) {
+  return guarded([&] {
+    const ModelSet m = to_models(*models);
+    RunnerConfig cfg;
+    cfg.slo = to_slo(c->slo);
+    cfg.total_gpus = c->total_gpus;
+    cfg.tp_options.assign(c->tp_options, c->tp_options + c->n_tp);
+    cfg.ladder.freqs_mhz.assign(c->ladder, c->ladder + c->n_ladder);
+    cfg.scheduler = to_policy(c->scheduler);
+    cfg.plan.alpha = c->alpha;
+    cfg.plan.peak_subwindow_s = c->peak_subwindow_s;
+    cfg.plan.search = to_search(c->search);
+    cfg.plan.policy = to_policy(c->plan_policy);
+    cfg.rampup_s = c->rampup_s;
+    cfg.switch_latency_ms = c->switch_latency_ms;
+    cfg.mpc_horizon_k = c->mpc_k;
+    cfg.mpc_ladder_n = c->mpc_n;
+    cfg.mpc_margin = c->mpc_margin;
+    cfg.kv_threshold = c->kv_threshold;
+    cfg.decode_margin = c->decode_margin;
+    std::vector<Policy> pols;
+    for (int i = 0; i < n_policies; ++i) pols.push_back(static_cast<Policy>(policies[i]));
+    ExperimentResult r = run_experiment(to_trace(*trace), window_ms, pols, cfg, m);
+    *n_out = static_cast<int>(r.runs.size());
+    *two_tier_slo_pass = r.two_tier_slo_pass ? 1 : 0;
+    for (int i = 0; i < *n_out && i < cap; ++i) {
+      const WindowRun& w = r.runs[static_cast<std::size_t>(i)];
+      ref_window_run& o = out[i];
+      std::memset(&o, 0, sizeof o);
+      o.window = w.window_index;
+      o.policy = static_cast<int32_t>(w.policy);
+      o.gpus_used = w.plan.gpus_used;
+      o.slo_pass = w.slo_pass ? 1 : 0;
+      o.objective_w = w.plan.objective_w;
+      o.target_rps = w.plan.target_rps;
+      bs_replay_summary& s = o.report;
+      s.horizon_ms = w.sim.horizon_ms;
+      s.completed_requests = w.sim.completed_requests;
+      s.generated_tokens = w.sim.generated_tokens;
+      s.n_batches = static_cast<int64_t>(w.sim.batches.size());
+      s.n_idles = static_cast<int64_t>(w.sim.idles.size());
+      s.n_decisions = static_cast<int64_t>(w.sim.decisions.records.size());
+      for (const auto& d : w.sim.decisions.records) s.decisions_by_trigger[static_cast<int>(d.trigger)] += 1;
+      const MetricsReport& rep = w.report;
+      s.has_p99_ttft = rep.p99_ttft_ms.has_value();
+      s.p99_ttft_ms = rep.p99_ttft_ms.value_or(NAN);
+      s.has_p99_tpot = rep.p99_mean_tpot_ms.has_value();
+      s.p99_mean_tpot_ms = rep.p99_mean_tpot_ms.value_or(NAN);
+      s.has_e_first = rep.energy_per_first_token_j.has_value();
+      s.energy_per_first_token_j = rep.energy_per_first_token_j.value_or(NAN);
+      s.has_e_output = rep.energy_per_output_token_j.has_value();
+      s.energy_per_output_token_j = rep.energy_per_output_token_j.value_or(NAN);
+      s.avg_power_prefill_w = rep.avg_power_prefill_w;
+      s.avg_power_decode_w = rep.avg_power_decode_w;
+      s.prefill_energy_j = rep.prefill_energy_j;
+      s.decode_energy_j = rep.decode_energy_j;
+      s.span_ms = rep.span_ms;
+      s.report_completed = rep.completed_requests;
+      s.report_generated = rep.generated_tokens;
+      s.ttft_violations = rep.ttft_violations;
+      s.tpot_violations = rep.tpot_violations;
+    }
+  });
+}

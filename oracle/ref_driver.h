@@ -8,6 +8,39 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+/* RunnerConfig (runner.hpp:39-86) as a POD, for ref_run_experiment. */
+typedef struct ref_runner_config {
+  bs_slo slo;
+  int32_t total_gpus;
+  int32_t n_tp;
+  const int32_t* tp_options;
+  const double* ladder;
+  int32_t n_ladder;
+  int32_t mpc_k;
+  bs_scheduler_policy scheduler;
+  double alpha;
+  double peak_subwindow_s;
+  bs_goodput_search search;
+  bs_scheduler_policy plan_policy;
+  double rampup_s;
+  double switch_latency_ms;
+  int32_t mpc_n;
+  int32_t _pad;
+  double mpc_margin;
+  double kv_threshold;
+  double decode_margin;
+} ref_runner_config;
+
+typedef struct ref_window_run {
+  int32_t window;
+  int32_t policy;
+  int32_t gpus_used;
+  int32_t slo_pass;
+  double objective_w;
+  double target_rps;
+  bs_replay_summary report; /* SimResult counters + MetricsReport */
+} ref_window_run;
+
 const char* ref_last_error(void);
 int ref_interpolate(const bs_grid* grid, const double* coords, int n, double* out, uint32_t* clamp_events);
 int ref_predict(const bs_model_set* models, int which, const bs_features* feats, const int32_t* tp,
@@ -46,6 +79,9 @@ int ref_simulate(const bs_model_set* models, const bs_trace* traces, int n, cons
                  const bs_scheduler_policy* policy, const bs_slo* slo, bs_sim_summary* out);
 int ref_solve_max_throughput(const bs_table_entry* table, int n, int total_gpus, double target_rps, double alpha,
                              double max_freq_mhz, int64_t* counts, double* objective_w, int32_t* gpus_used);
+int ref_run_experiment(const bs_model_set* models, const bs_trace* trace, double window_ms, const int32_t* policies,
+                       int n_policies, const ref_runner_config* cfg, ref_window_run* out, int cap, int* n_out,
+                       int32_t* two_tier_slo_pass);
 int ref_replay(const bs_model_set* sim_models, const bs_model_set* ctl_models, const bs_replay_config* cfgs,
                const bs_scenario* sc, int n, bs_replay_summary* out, bs_replay_request* requests,
                bs_replay_logs* logs, int n_threads);

@@ -1460,6 +1460,8 @@ class MetricsReport:
     generated_tokens: int = 0
     ttft_violations: int = 0
     tpot_violations: int = 0
+    window_id: str = ""
+    system: str = ""
 
 
 @dataclass
@@ -1606,3 +1608,141 @@ def simulate_cluster_report(trace: Trace, cluster: ClusterSpec, policy: Schedule
     window report (runner.hpp:131-133)."""
     return replay([ReplayScenario(trace, cluster, policy, controllers, opts or SimOptions(), slo or SLOSpec(),
                                   rampup_s)], models, device, requests=True)[0]
+
+
+# ---------------------------------------------------------------------------
+# runner.hpp: policies, window plans, run_experiment
+# ---------------------------------------------------------------------------
+
+
+class Policy(enum.IntEnum):
+    maxfreq_distserve = 0
+    place_only = 1
+    two_tier = 2
+
+
+POLICY_NAMES = {Policy.maxfreq_distserve: "maxfreq-distserve", Policy.place_only: "place-only",
+                Policy.two_tier: "two-tier"}
+
+
+@dataclass
+class RunnerConfig:
+    """RunnerConfig (runner.hpp:39-86)."""
+
+    slo: SLOSpec = field(default_factory=SLOSpec)
+    total_gpus: int = 8
+    tp_options: list = field(default_factory=lambda: [1])
+    ladder: FrequencyLadder = field(default_factory=FrequencyLadder)
+    scheduler: SchedulerPolicy = field(default_factory=SchedulerPolicy)
+    plan: PlanOptions = field(default_factory=PlanOptions)
+    rampup_s: float = 30.0
+    switch_latency_ms: float = 30.0
+    mpc_horizon_k: int = 8
+    mpc_ladder_n: int = 7
+    mpc_margin: float = 0.05
+    kv_threshold: float = 0.9
+    decode_margin: float = 0.05
+
+    def mpc_config(self) -> MpcConfig:
+        return MpcConfig(self.mpc_horizon_k, self.mpc_ladder_n, self.ladder, self.slo, self.switch_latency_ms,
+                         self.mpc_margin)
+
+    def decode_config(self) -> DecodePolicyConfig:
+        return DecodePolicyConfig(self.slo.tpot_ms, self.kv_threshold, self.ladder, self.decode_margin)
+
+    def validate(self) -> None:
+        self.slo.validate()
+        self.ladder.validate()
+        self.scheduler.validate()
+        if self.total_gpus <= 0:
+            raise ParameterError("total_gpus must be positive")
+        if not self.tp_options:
+            raise ParameterError("tp_options must not be empty")
+        if any(tp <= 0 for tp in self.tp_options):
+            raise ParameterError("tp options must be positive")
+        if self.rampup_s < 0.0:
+            raise ParameterError("rampup_s must be >= 0")
+        self.mpc_config().validate()
+        self.decode_config().validate()
+
+
+@dataclass
+class WindowPlans:
+    target_rps: float = 0.0
+    table: list = field(default_factory=list)
+    ilp: PlacementPlan = field(default_factory=PlacementPlan)
+    maxfreq: PlacementPlan = field(default_factory=PlacementPlan)
+
+
+@dataclass
+class WindowRun:
+    window_index: int = 0
+    policy: Policy = Policy.maxfreq_distserve
+    plan: PlacementPlan = field(default_factory=PlacementPlan)
+    result: ReplayResult = field(default_factory=ReplayResult)
+    report: MetricsReport = field(default_factory=MetricsReport)
+    slo_pass: bool = False
+
+
+@dataclass
+class ExperimentResult:
+    runs: list = field(default_factory=list)
+    reports: list = field(default_factory=list)
+    two_tier_slo_pass: bool = True
+
+
+def plan_window_policies(history: Trace, cfg: RunnerConfig, models: ModelSet,
+                         device: Device | None = None) -> WindowPlans:
+    """plan_window_policies (runner.hpp:98-110): one GPU config table shared
+    by the ILP plan and the max-frequency baseline."""
+    cfg.validate()
+    wp = plan_window(history, cfg.total_gpus, cfg.slo, models, cfg.ladder, cfg.tp_options, cfg.plan, device)
+    out = WindowPlans(wp.predicted_peak_rps, wp.table, wp.plan)
+    out.maxfreq = solve_max_throughput(PlacementProblem(out.table, cfg.total_gpus, out.target_rps, cfg.plan.alpha),
+                                       cfg.ladder.max_mhz(), device)
+    return out
+
+
+def _scenario_for(window: Trace, plan: PlacementPlan, policy: Policy, cfg: RunnerConfig,
+                  models: ModelSet) -> ReplayScenario:
+    """run_policy (runner.hpp:112-122) as a replay scenario."""
+    fac = None
+    if policy == Policy.two_tier:
+        fac = TwoTierFactory(cfg.mpc_config(), cfg.decode_config(), models, cfg.scheduler)
+    return ReplayScenario(window, ClusterSpec(list(plan.instances)), cfg.scheduler, fac,
+                          SimOptions(cfg.switch_latency_ms), cfg.slo, cfg.rampup_s)
+
+
+def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, models: ModelSet,
+                   device: Device | None = None) -> ExperimentResult:
+    """run_experiment (runner.hpp:155-172): window w is planned from window
+    w-1 (the first from itself) with the GPU config table + ILP; then every
+    (window, policy) replay runs in ONE bs_replay call (windows are
+    independent once planned).  Reports, SLO verdicts and their order follow
+    the reference."""
+    dev = device or default_device()
+    cfg.validate()
+    policies = list(policies)
+    if not policies:
+        raise ParameterError("no policies selected")
+    windows = split_windows(trace, window_ms)
+    plans = [plan_window_policies(windows[0] if w == 0 else windows[w - 1], cfg, models, dev)
+             for w in range(len(windows))]
+    scs, keys = [], []
+    for w, win in enumerate(windows):
+        for pol in policies:
+            plan = plans[w].maxfreq if pol == Policy.maxfreq_distserve else plans[w].ilp
+            scs.append(_scenario_for(win, plan, pol, cfg, models))
+            keys.append((w, pol, plan))
+    results = replay(scs, models, dev)
+    out = ExperimentResult()
+    for (w, pol, plan), res in zip(keys, results):
+        rep = res.report
+        rep.window_id, rep.system = f"w{w}", POLICY_NAMES[pol]
+        ok = (rep.p99_ttft_ms is None or rep.p99_ttft_ms <= cfg.slo.ttft_ms) and \
+             (rep.p99_mean_tpot_ms is None or rep.p99_mean_tpot_ms <= cfg.slo.tpot_ms)
+        if pol == Policy.two_tier and not ok:
+            out.two_tier_slo_pass = False
+        out.reports.append(rep)
+        out.runs.append(WindowRun(w, pol, plan, res, rep, ok))
+    return out
