@@ -22,9 +22,11 @@ Extra keys, one object per other BASELINE.json configuration (each with its
 own device timing, the reference on the host cores and a parity check):
   c3_placement   configs[2]: config table + ILP, placement configs/s
   c4_replay      configs[3]-shaped what-if replay sweep, scenarios/s
+  c4_experiment  configs[3]'s window loop: run_experiment over a bursty hour
+                 (plan per window + 3 policies replayed), window runs/s
   c5_greedy      configs[4] greedy MPC (H8 x 24 levels), decisions/s
   c5_exhaustive  configs[4] exhaustive MPC (24^8 per decision), decisions/s
-(`--only c3|c4|c5g|c5x` runs one alone; `--no-extras` skips them.)
+(`--only c3|c4|c4x|c5g|c5x` runs one alone; `--no-extras` skips them.)
 
 Multi-GPU (torchrun): weak scaling, every rank evaluates its own corpus
 (independent decisions), no data-path collective; max-over-ranks time.  The
@@ -66,7 +68,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU baseline sample duration")
     ap.add_argument("--no-extras", action="store_true", help="skip the C3/C4/C5 sub-benchmarks")
-    ap.add_argument("--only", choices=["c3", "c4", "c5g", "c5x"], default=None,
+    ap.add_argument("--only", choices=["c3", "c4", "c4x", "c5g", "c5x"], default=None,
                     help="run one sub-benchmark alone and print its JSON object")
     ap.add_argument("--c4-scenarios", type=int, default=1024)
     ap.add_argument("--c5x-decisions", type=int, default=256)
@@ -442,9 +444,79 @@ def bench_c5(dev, mode: str, rank: int, world: int, local: int, n_dec: int, with
     return out
 
 
+def bench_c4_experiment(dev, with_cpu: bool) -> dict:
+    """configs[3]'s per-window loop: run_experiment (runner.hpp:155-172) over a
+    bursty 1-hour trace in 5-minute windows -- every window planned from the
+    previous one (config table + ILP + max-throughput baseline for a 16-GPU
+    cluster) and replayed under the three policies with per-iteration
+    decisions; reference run_experiment beside it."""
+    import ctypes as C
+
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import workloads as Wk
+
+    lad = Wk.ladder(16)
+    models = Wk.llama_models(lad)
+    trace = P.gen_gamma_trace(12.0, 0.5, 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)),
+                              7)
+    cfg = P.RunnerConfig(slo=P.SLOSpec(600.0, 100.0), total_gpus=16, tp_options=[1, 2, 4, 8], ladder=lad,
+                         scheduler=P.SchedulerPolicy(max_batch_tokens=2048), rampup_s=30.0)
+    cfg.plan.policy = P.SchedulerPolicy(max_batch_tokens=2048)
+    pols = [P.Policy.maxfreq_distserve, P.Policy.place_only, P.Policy.two_tier]
+    P.run_experiment(trace, 300e3, pols, cfg, models, dev)  # warm-up
+    t0 = time.perf_counter()
+    res = P.run_experiment(trace, 300e3, pols, cfg, models, dev)
+    t_gpu = time.perf_counter() - t0
+    runs = len(res.runs)
+    out = {"workload": "run_experiment: 1-hour gamma(0.5) trace at 12 rps, 12 five-minute windows x 3 policies "
+                       "(maxfreq-distserve, place-only, two-tier), 16 GPUs, TP{1,2,4,8} x 16 rungs",
+           "value": runs / t_gpu, "unit": "window runs/s", "seconds": t_gpu,
+           "decisions": sum(r.result.n_decisions for r in res.runs), "phase_s": res.seconds,
+           "two_tier_slo_pass": res.two_tier_slo_pass,
+           "timing": "end to end through pdsim.run_experiment (host trace in, reports out)"}
+    if with_cpu:
+        import oracle
+
+        ref = oracle.load_ref()
+        keep: list = []
+        c = oracle.ref_runner_config()
+        c.slo = P.c_slo(cfg.slo)
+        c.total_gpus = cfg.total_gpus
+        tps = (C.c_int32 * 4)(*cfg.tp_options)
+        ld = (C.c_double * len(lad.freqs_mhz))(*lad.freqs_mhz)
+        keep += [tps, ld]
+        c.n_tp, c.tp_options, c.ladder, c.n_ladder = 4, tps, ld, len(lad.freqs_mhz)
+        c.scheduler = P.c_policy(cfg.scheduler)
+        c.alpha, c.peak_subwindow_s = cfg.plan.alpha, cfg.plan.peak_subwindow_s
+        c.search, c.plan_policy = P.c_search(cfg.plan.search), P.c_policy(cfg.plan.policy)
+        c.rampup_s, c.switch_latency_ms = cfg.rampup_s, cfg.switch_latency_ms
+        c.mpc_k, c.mpc_n, c.mpc_margin = cfg.mpc_horizon_k, cfg.mpc_ladder_n, cfg.mpc_margin
+        c.kv_threshold, c.decode_margin = cfg.kv_threshold, cfg.decode_margin
+        cap = 64
+        o = (oracle.ref_window_run * cap)()
+        n_out, tt = C.c_int(), C.c_int32()
+        cm, ct = P.c_model_set(models, keep), P.c_trace(trace, keep)
+        pa = (C.c_int32 * 3)(*[int(p) for p in pols])
+        t0 = time.perf_counter()
+        rc = ref.ref_run_experiment(C.byref(cm), C.byref(ct), 300e3, pa, 3, C.byref(c), o, cap, C.byref(n_out),
+                                    C.byref(tt))
+        t_cpu = time.perf_counter() - t0
+        same = rc == 0 and n_out.value == runs and all(
+            (o[i].gpus_used, o[i].objective_w, o[i].report.n_decisions, o[i].report.prefill_energy_j,
+             o[i].report.decode_energy_j, o[i].report.ttft_violations) ==
+            (r.plan.gpus_used, r.plan.objective_w, r.result.n_decisions, r.report.prefill_energy_j,
+             r.report.decode_energy_j, r.report.ttft_violations) for i, r in enumerate(res.runs))
+        out["cpu_baseline"] = {"value": runs / t_cpu, "unit": "window runs/s", "cores": cpu_threads(),
+                               "kind": "reference", "seconds": t_cpu,
+                               "sample": "the whole experiment: pdsim::run_experiment (build_config_table on "
+                                         "std::async threads; simulations single-threaded, as the reference runs)"}
+        out["identical_to_reference"] = bool(same)
+    return out
+
+
 def run_extras(args, dev, rank, world, local) -> dict:
     with_cpu = world == 1 and not args.no_cpu_baseline
-    todo = [args.only] if args.only else ["c3", "c4", "c5g", "c5x"]
+    todo = [args.only] if args.only else ["c3", "c4", "c4x", "c5g", "c5x"]
     out = {}
     for k in todo:
         if k == "c3":
@@ -452,6 +524,9 @@ def run_extras(args, dev, rank, world, local) -> dict:
                 out["c3_placement"] = bench_c3(dev, with_cpu)
         elif k == "c4":
             out["c4_replay"] = bench_c4(dev, rank, world, local, args.c4_scenarios, with_cpu)
+        elif k == "c4x":
+            if world == 1:
+                out["c4_experiment"] = bench_c4_experiment(dev, with_cpu)
         elif k == "c5g":
             out["c5_greedy"] = bench_c5(dev, "greedy", rank, world, local, 4096, with_cpu)
         else:

@@ -37,6 +37,7 @@ struct WTables {
 
 struct WGreedyShared {
   WTables T;
+  FastBrk blat[kMaxK], bpow[kMaxK];  // per-batch brackets shared by every candidate's reduced grid
   int np;
   int accepted;
   double obj;
@@ -198,9 +199,11 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
 // fl / fp: the controller's latency / power grids reduced per candidate
 // (FastGrid), or null for the generic interpolator.  lv (optional): level
 // stats.  Results in *o (lane 0 writes; the warp is synchronised on return).
+//   share: every fl[f] (and every fp[f]) has the brackets of fl[0] (fp[0])
+//   (fast_same_brackets), so each batch is bracketed once for all candidates.
 __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
                             const DRunning* R, WGreedyShared& S, DMpcOut* o, DLevel* lv, const FastGrid* fl,
-                            const FastGrid* fp) {
+                            const FastGrid* fp, bool share = false) {
   const int lane = threadIdx.x & 31;
   WTables& T = S.T;
   if (lane == 0) {
@@ -223,10 +226,21 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
     return;
   }
   unsigned anybad = 0;
+  const bool shared_brk = fl && share;
+  if (shared_brk) {
+    if (lane < K) {
+      fast_brackets(fl[0], T.n_req[lane], T.sum_len[lane], S.blat[lane]);
+      fast_brackets(fp[0], T.n_req[lane], T.sum_len[lane], S.bpow[lane]);
+    }
+    __syncwarp();
+  }
   for (int e = lane; e < K * nc; e += 32) {
     const int k = e / nc, f = e - k * nc;
     double L, P;
-    if (fl) {
+    if (shared_brk) {
+      L = fast_corners(fl[f], S.blat[k]);
+      P = fast_corners(fp[f], S.bpow[k]);
+    } else if (fl) {
       L = fast_interp(fl[f], T.n_req[k], T.sum_len[k]);
       P = fast_interp(fp[f], T.n_req[k], T.sum_len[k]);
     } else {

@@ -789,6 +789,9 @@ __global__ void __launch_bounds__(kPrefillWarps * 32, BS_PREFILL_MINB) prefill_k
     (g == 0 ? G.lat : g == 1 ? G.pw : g == 2 ? G.clat : G.cpw)[k] = fg;
   }
   __syncwarp();
+  bool share = true;  // every candidate's controller grids bracket like candidate 0's
+  for (int f = 1; f < nc; ++f)
+    share = share && fast_same_brackets(G.clat[0], G.clat[f]) && fast_same_brackets(G.cpw[0], G.cpw[f]);
   PrefillSim& sim = S.sim;
   if (lane == 0) sim.init(&R, &I, C, &G);
   for (;;) {
@@ -796,7 +799,7 @@ __global__ void __launch_bounds__(kPrefillWarps * 32, BS_PREFILL_MINB) prefill_k
     if (lane == 0) cmd = sim.advance(&S.out, &S.pr);
     cmd = __shfl_sync(0xffffffffu, cmd, 0);
     if (cmd == 0) break;
-    greedy_warp(R.ctl, S.pr, C->mpc, R.W + S.pr.wait_off, nullptr, S.G, &S.out, nullptr, G.clat, G.cpw);
+    greedy_warp(R.ctl, S.pr, C->mpc, R.W + S.pr.wait_off, nullptr, S.G, &S.out, nullptr, G.clat, G.cpw, share);
   }
   if (lane == 0) {
     DInstState* st = &R.st[gi];

@@ -178,29 +178,47 @@ __device__ __forceinline__ void bracket_count(const double* __restrict__ k, int 
   *frac = __ddiv_rn(__dsub_rn(x, klo), __dsub_rn(khi, klo));
 }
 
-__device__ __forceinline__ double fast_interp(const FastGrid& g, long long n_req, long long sum_len) {
+// The (lo, frac) of every active axis of a FastGrid at one query.
+struct FastBrk {
   int lo[kMaxRank];
   double frac[kMaxRank];
+};
+
+__device__ __forceinline__ void fast_brackets(const FastGrid& g, long long n_req, long long sum_len, FastBrk& b) {
 #pragma unroll
   for (int a = 0; a < kMaxRank; ++a) {
     if (a >= g.na) break;
     if (g.fixed[a]) {
-      lo[a] = g.lo[a];
-      frac[a] = g.frac[a];
+      b.lo[a] = g.lo[a];
+      b.frac[a] = g.frac[a];
     } else {  // active varying axes have >= 2 knots (single-knot axes are dropped)
       bracket_count(g.knots[a], g.n[a], static_cast<double>(g.role[a] == BS_AXIS_SUM_LEN ? sum_len : n_req),
-                    &lo[a], &frac[a]);
+                    &b.lo[a], &b.frac[a]);
     }
   }
+}
+
+// The corner sum of NdGrid::interpolate over the active axes.
+__device__ __forceinline__ double fast_corners(const FastGrid& g, const FastBrk& b) {
   double acc = 0.0;
   if (g.na == 2) {  // the common case: (sum_len, n_requests) with tp and freq on knots
-    const double w0[2] = {__dsub_rn(1.0, frac[0]), frac[0]};
-    const double w1[2] = {__dsub_rn(1.0, frac[1]), frac[1]};
+    const double w0[2] = {__dsub_rn(1.0, b.frac[0]), b.frac[0]};
+    const double w1[2] = {__dsub_rn(1.0, b.frac[1]), b.frac[1]};
 #pragma unroll
     for (int mask = 0; mask < 4; ++mask) {
       const int h0 = mask & 1, h1 = mask >> 1;
       const double weight = __dmul_rn(__dmul_rn(1.0, w0[h0]), w1[h1]);
-      const long long flat = g.base + (lo[0] + h0) * g.stride[0] + (lo[1] + h1) * g.stride[1];
+      const long long flat = g.base + (b.lo[0] + h0) * g.stride[0] + (b.lo[1] + h1) * g.stride[1];
+      if (weight != 0.0) acc = __dadd_rn(acc, __dmul_rn(weight, __ldg(g.values + flat)));
+    }
+    return acc;
+  }
+  if (g.na == 1) {  // e.g. prefill power over sum_len
+    const double w0[2] = {__dsub_rn(1.0, b.frac[0]), b.frac[0]};
+#pragma unroll
+    for (int h0 = 0; h0 < 2; ++h0) {
+      const double weight = __dmul_rn(1.0, w0[h0]);
+      const long long flat = g.base + (b.lo[0] + h0) * g.stride[0];
       if (weight != 0.0) acc = __dadd_rn(acc, __dmul_rn(weight, __ldg(g.values + flat)));
     }
     return acc;
@@ -213,12 +231,32 @@ __device__ __forceinline__ double fast_interp(const FastGrid& g, long long n_req
     for (int a = 0; a < kMaxRank; ++a) {
       if (a >= g.na) break;
       const int high = (mask >> a) & 1;
-      weight = __dmul_rn(weight, high ? frac[a] : __dsub_rn(1.0, frac[a]));
-      flat += (lo[a] + high) * g.stride[a];
+      weight = __dmul_rn(weight, high ? b.frac[a] : __dsub_rn(1.0, b.frac[a]));
+      flat += (b.lo[a] + high) * g.stride[a];
     }
     if (weight != 0.0) acc = __dadd_rn(acc, __dmul_rn(weight, __ldg(g.values + flat)));
   }
   return acc;
+}
+
+__device__ __forceinline__ double fast_interp(const FastGrid& g, long long n_req, long long sum_len) {
+  FastBrk b;
+  fast_brackets(g, n_req, sum_len, b);
+  return fast_corners(g, b);
+}
+
+// Two reductions of the same grid whose active axes, knots and fixed-axis
+// brackets coincide (only the dropped axes' offsets differ, e.g. the same tp
+// at two on-knot frequencies): brackets of one serve the other.
+__device__ __forceinline__ bool fast_same_brackets(const FastGrid& a, const FastGrid& b) {
+  if (a.na != b.na || a.bad != b.bad || a.values != b.values) return false;
+  for (int i = 0; i < a.na; ++i) {
+    if (a.role[i] != b.role[i] || a.n[i] != b.n[i] || a.knots[i] != b.knots[i] || a.stride[i] != b.stride[i] ||
+        a.fixed[i] != b.fixed[i])
+      return false;
+    if (a.fixed[i] && (a.lo[i] != b.lo[i] || a.frac[i] != b.frac[i])) return false;
+  }
+  return true;
 }
 
 // predict_latency / predict_power at the instance's (tp, freq); false on

@@ -1689,6 +1689,7 @@ class ExperimentResult:
     runs: list = field(default_factory=list)
     reports: list = field(default_factory=list)
     two_tier_slo_pass: bool = True
+    seconds: dict = field(default_factory=dict)  # wall time of the planning and replay phases
 
 
 def plan_window_policies(history: Trace, cfg: RunnerConfig, models: ModelSet,
@@ -1713,8 +1714,20 @@ def _scenario_for(window: Trace, plan: PlacementPlan, policy: Policy, cfg: Runne
                           SimOptions(cfg.switch_latency_ms), cfg.slo, cfg.rampup_s)
 
 
+_ctx_pools: dict = {}
+
+
+def _context_pool(device: int, n: int) -> list:
+    """n library contexts on one GPU (each its own stream), reused across calls."""
+    with _default_lock:
+        pool = _ctx_pools.setdefault(device, [])
+        while len(pool) < n:
+            pool.append(Device(device))
+        return pool[:n]
+
+
 def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, models: ModelSet,
-                   device: Device | None = None) -> ExperimentResult:
+                   device: Device | None = None, plan_workers: int = 16) -> ExperimentResult:
     """run_experiment (runner.hpp:155-172): window w is planned from window
     w-1 (the first from itself) with the GPU config table + ILP; then every
     (window, policy) replay runs in ONE bs_replay call (windows are
@@ -1726,16 +1739,34 @@ def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, 
     if not policies:
         raise ParameterError("no policies selected")
     windows = split_windows(trace, window_ms)
-    plans = [plan_window_policies(windows[0] if w == 0 else windows[w - 1], cfg, models, dev)
-             for w in range(len(windows))]
+    # windows are planned independently (window w from window w - 1): one
+    # context (own CUDA stream) per worker thread, so the config tables'
+    # kernels overlap on the GPU and the critical path is the longest table,
+    # not their sum (the reference parallelises inside build_config_table)
+    import time as _time
+
+    t0 = _time.perf_counter()
+    histories = [windows[0] if w == 0 else windows[w - 1] for w in range(len(windows))]
+    workers = min(len(windows), plan_workers)
+    if workers <= 1:
+        plans = [plan_window_policies(h, cfg, models, dev) for h in histories]
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        pool = _context_pool(dev.device, workers)
+        with ThreadPoolExecutor(workers) as ex:
+            plans = list(ex.map(lambda a: plan_window_policies(a[1], cfg, models, pool[a[0] % workers]),
+                                enumerate(histories)))
     scs, keys = [], []
     for w, win in enumerate(windows):
         for pol in policies:
             plan = plans[w].maxfreq if pol == Policy.maxfreq_distserve else plans[w].ilp
             scs.append(_scenario_for(win, plan, pol, cfg, models))
             keys.append((w, pol, plan))
+    t1 = _time.perf_counter()
     results = replay(scs, models, dev)
     out = ExperimentResult()
+    out.seconds = {"plan": t1 - t0, "replay": _time.perf_counter() - t1}
     for (w, pol, plan), res in zip(keys, results):
         rep = res.report
         rep.window_id, rep.system = f"w{w}", POLICY_NAMES[pol]
