@@ -23,6 +23,11 @@
 //                                         in plan_window (placement.hpp:576)
 //   pdsim_gpu::solve_placement /        replace solve_placement (357-416) and
 //   solve_max_throughput                  solve_max_throughput (421-499)
+//   pdsim_gpu::plan_window /            plan_window (placement.hpp:558-582),
+//   plan_window_policies                  plan_window_policies (runner.hpp:98-110)
+//   pdsim_gpu::run_experiment           run_experiment (runner.hpp:155-172):
+//                                         GPU plans + every (window, policy)
+//                                         replay in one bs_replay call
 //
 // Status codes are rethrown as the reference's exception types with the
 // library's message.  predicted_latency_ms is evaluated with the reference's
@@ -40,7 +45,9 @@
 #include "biscale_gpu.h"
 #include "pdsim/dvfs.hpp"
 #include "pdsim/errors.hpp"
+#include "pdsim/metrics.hpp"
 #include "pdsim/placement.hpp"
+#include "pdsim/runner.hpp"
 
 namespace pdsim_gpu {
 
@@ -463,5 +470,175 @@ class GpuTwoTierFactory : public pdsim::ControllerFactory {
   const DeviceModels* dm_;
   pdsim::SchedulerPolicy policy_;
 };
+
+
+// --- cluster replay and the window loop -------------------------------------------
+
+// One run_policy (runner.hpp:112-122) + its window report (runner.hpp:131-133),
+// as the device replays it.  `sim` carries SimResult's counters and horizon;
+// its record vectors stay empty (the device reduces requests to what the
+// metrics read -- use bs_replay's logs for full records).
+struct ReplayRun {
+  pdsim::SimResult sim;
+  pdsim::MetricsReport report;
+  int status = BS_OK;
+};
+
+namespace detail {
+
+inline bs_replay_config replay_config(const pdsim::RunnerConfig& cfg, bool controlled, std::vector<double>& keep) {
+  bs_replay_config c{};
+  keep = cfg.ladder.freqs_mhz;
+  if (controlled) {
+    c.mpc = to_mpc(cfg.mpc_config());
+    c.mpc.ladder_mhz = keep.data();
+    const pdsim::DecodePolicyConfig d = cfg.decode_config();
+    c.decode.tbt_slo_ms = d.tbt_slo_ms;
+    c.decode.kv_threshold = d.kv_threshold;
+    c.decode.margin = d.margin;
+    c.decode.n_ladder = static_cast<int32_t>(keep.size());
+    c.decode.ladder_mhz = keep.data();
+    c.controlled = 1;
+  }
+  c.policy = to_policy(cfg.scheduler);
+  c.slo = bs_slo{cfg.slo.ttft_ms, cfg.slo.tpot_ms, cfg.slo.percentile};
+  c.switch_latency_ms = cfg.switch_latency_ms;
+  c.horizon_ms = -1.0;
+  c.rampup_s = cfg.rampup_s;
+  return c;
+}
+
+inline void fill_run(const bs_replay_summary& o, ReplayRun& r) {
+  r.status = o.status;
+  r.sim.horizon_ms = o.horizon_ms;
+  r.sim.completed_requests = o.completed_requests;
+  r.sim.generated_tokens = o.generated_tokens;
+  pdsim::MetricsReport& m = r.report;
+  if (o.has_p99_ttft) m.p99_ttft_ms = o.p99_ttft_ms;
+  if (o.has_p99_tpot) m.p99_mean_tpot_ms = o.p99_mean_tpot_ms;
+  if (o.has_e_first) m.energy_per_first_token_j = o.energy_per_first_token_j;
+  if (o.has_e_output) m.energy_per_output_token_j = o.energy_per_output_token_j;
+  m.avg_power_prefill_w = o.avg_power_prefill_w;
+  m.avg_power_decode_w = o.avg_power_decode_w;
+  m.prefill_energy_j = o.prefill_energy_j;
+  m.decode_energy_j = o.decode_energy_j;
+  m.span_ms = o.span_ms;
+  m.completed_requests = o.report_completed;
+  m.generated_tokens = o.report_generated;
+  m.ttft_violations = o.ttft_violations;
+  m.tpot_violations = o.tpot_violations;
+}
+
+}  // namespace detail
+
+// plan_window (placement.hpp:558-582) with the GPU config table and ILP.
+inline pdsim::WindowPlanResult plan_window(const DeviceModels& dm, const pdsim::Trace& history, int total_gpus,
+                                           const pdsim::SLOSpec& slo, const pdsim::FrequencyLadder& ladder,
+                                           const std::vector<int>& tp_options, const pdsim::PlanOptions& opts = {}) {
+  history.validate();
+  if (history.requests.empty()) throw pdsim::ParameterError("plan_window: empty history");
+  pdsim::Trace predicted = pdsim::predict_next_window(history);
+  pdsim::WindowPlanResult res;
+  res.predicted_peak_rps = pdsim::peak_rps(predicted, opts.peak_subwindow_s);
+  const pdsim::Trace& probe = opts.probe_trace ? *opts.probe_trace : predicted;
+  const std::vector<pdsim::InstanceConfig> candidates = pdsim::enumerate_candidates(ladder, tp_options);
+  res.table = pdsim_gpu::build_config_table(dm, candidates, probe, slo, opts.policy, opts.search);
+  pdsim::PlacementProblem problem{res.table, total_gpus, res.predicted_peak_rps, opts.alpha};
+  res.plan = pdsim_gpu::solve_placement(problem);
+  return res;
+}
+
+// plan_window_policies (runner.hpp:98-110) on the GPU.
+inline pdsim::WindowPlans plan_window_policies(const DeviceModels& dm, const pdsim::Trace& history,
+                                               const pdsim::RunnerConfig& cfg) {
+  cfg.validate();
+  pdsim::WindowPlanResult wp = pdsim_gpu::plan_window(dm, history, cfg.total_gpus, cfg.slo, cfg.ladder, cfg.tp_options, cfg.plan);
+  pdsim::WindowPlans out;
+  out.target_rps = wp.predicted_peak_rps;
+  out.table = wp.table;
+  out.ilp = wp.plan;
+  pdsim::PlacementProblem p{out.table, cfg.total_gpus, out.target_rps, cfg.plan.alpha};
+  out.maxfreq = pdsim_gpu::solve_max_throughput(p, cfg.ladder.max_mhz());
+  return out;
+}
+
+// run_policy + the window report for a batch of (window, plan, policy)
+// triples in ONE device call (bs_replay).  Throws like the reference on the
+// first failing run.
+inline std::vector<ReplayRun> replay_policies(const DeviceModels& dm, const std::vector<const pdsim::Trace*>& windows,
+                                              const std::vector<const pdsim::PlacementPlan*>& plans,
+                                              const std::vector<pdsim::Policy>& policies,
+                                              const pdsim::RunnerConfig& cfg) {
+  const std::size_t n = windows.size();
+  std::vector<double> lad_ctl, lad_fix;
+  const bs_replay_config cfgs[2] = {detail::replay_config(cfg, false, lad_fix),
+                                    detail::replay_config(cfg, true, lad_ctl)};
+  std::vector<detail::TraceView> tvs;
+  tvs.reserve(n);
+  std::vector<std::vector<bs_cluster_instance>> inst(n);
+  std::vector<bs_scenario> sc(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    tvs.emplace_back(*windows[i]);
+    for (const auto& ci : plans[i]->instances)
+      inst[i].push_back(bs_cluster_instance{
+          bs_instance_config{ci.config.phase == pdsim::Phase::prefill ? BS_PHASE_PREFILL : BS_PHASE_DECODE,
+                             ci.config.tp, ci.config.base_freq_mhz},
+          ci.weight});
+    sc[i].trace = tvs[i].t;
+    sc[i].instances = inst[i].data();
+    sc[i].n_instances = static_cast<int32_t>(inst[i].size());
+    sc[i].config = policies[i] == pdsim::Policy::two_tier ? 1 : 0;
+  }
+  std::vector<bs_replay_summary> out(n);
+  dm.device().check(bs_replay(dm.device().get(), dm.get(), dm.get(), cfgs, 2, sc.data(), static_cast<int>(n),
+                              out.data(), nullptr, nullptr));
+  std::vector<ReplayRun> runs(n);
+  for (std::size_t i = 0; i < n; ++i) detail::fill_run(out[i], runs[i]);
+  return runs;
+}
+
+// run_experiment (runner.hpp:155-172): window w planned from window w-1 on
+// the GPU, then every (window, policy) replayed in one device call.  Result
+// as the reference's, except that runs[i].sim holds SimResult's counters
+// only (see ReplayRun).
+inline pdsim::ExperimentResult run_experiment(const DeviceModels& dm, const pdsim::Trace& trace, double window_ms,
+                                              const std::vector<pdsim::Policy>& policies,
+                                              const pdsim::RunnerConfig& cfg) {
+  cfg.validate();
+  if (policies.empty()) throw pdsim::ParameterError("no policies selected");
+  std::vector<pdsim::Trace> windows = pdsim::split_windows(trace, window_ms);
+  std::vector<pdsim::WindowPlans> plans;
+  plans.reserve(windows.size());
+  for (std::size_t w = 0; w < windows.size(); ++w)
+    plans.push_back(pdsim_gpu::plan_window_policies(dm, w == 0 ? windows[0] : windows[w - 1], cfg));
+  std::vector<const pdsim::Trace*> wins;
+  std::vector<const pdsim::PlacementPlan*> pls;
+  std::vector<pdsim::Policy> pols;
+  for (std::size_t w = 0; w < windows.size(); ++w)
+    for (pdsim::Policy pol : policies) {
+      wins.push_back(&windows[w]);
+      pls.push_back(pol == pdsim::Policy::maxfreq_distserve ? &plans[w].maxfreq : &plans[w].ilp);
+      pols.push_back(pol);
+    }
+  std::vector<ReplayRun> runs = pdsim_gpu::replay_policies(dm, wins, pls, pols, cfg);
+  pdsim::ExperimentResult out;
+  for (std::size_t i = 0; i < runs.size(); ++i) {
+    const std::size_t w = i / policies.size();
+    pdsim::WindowRun run;
+    run.window_index = static_cast<int>(w);
+    run.policy = pols[i];
+    run.plan = *pls[i];
+    run.sim = std::move(runs[i].sim);
+    run.report = runs[i].report;
+    run.report.window_id = "w" + std::to_string(w);
+    run.report.system = pdsim::policy_name(pols[i]);
+    run.slo_pass = (!run.report.p99_ttft_ms || *run.report.p99_ttft_ms <= cfg.slo.ttft_ms) &&
+                   (!run.report.p99_mean_tpot_ms || *run.report.p99_mean_tpot_ms <= cfg.slo.tpot_ms);
+    if (run.policy == pdsim::Policy::two_tier && !run.slo_pass) out.two_tier_slo_pass = false;
+    out.reports.push_back(run.report);
+    out.runs.push_back(std::move(run));
+  }
+  return out;
+}
 
 }  // namespace pdsim_gpu

@@ -46,3 +46,20 @@ def test_reference_planner_with_gpu_config_table(args):
     assert line["table_mismatch"] == 0, line
     assert line["match"], line
     assert res.returncode == 0
+
+
+@pytest.mark.parametrize("args", [
+    ["--seed", "7", "--minutes", "6", "--window-s", "120", "--rps", "8"],
+    ["--seed", "12", "--minutes", "4", "--window-s", "60", "--rps", "14", "--shape", "0.5", "--gpus", "16"],
+])
+def test_reference_experiment_vs_gpu_experiment(args):
+    """run_experiment (runner.hpp:155-172) vs pdsim_gpu::run_experiment (GPU
+    plans + batched replay) through the C++ shim: plans, SimResult counters,
+    MetricsReports and SLO verdicts run by run."""
+    if not oracle.EXPERIMENT_BIN.exists():
+        pytest.skip("experiment_parity not built (needs /root/reference at build time)")
+    res = subprocess.run([str(oracle.EXPERIMENT_BIN), *args], capture_output=True, text=True, timeout=900)
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["runs"] > 0 and line["mismatch"] == 0, line
+    assert line["match"], line
+    assert res.returncode == 0
