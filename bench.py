@@ -71,7 +71,7 @@ def parse():
     ap.add_argument("--only", choices=["c3", "c4", "c4x", "c5g", "c5x"], default=None,
                     help="run one sub-benchmark alone and print its JSON object")
     ap.add_argument("--c4-scenarios", type=int, default=1024)
-    ap.add_argument("--c5x-decisions", type=int, default=256)
+    ap.add_argument("--c5x-decisions", type=int, default=4096)
     return ap.parse_args()
 
 

@@ -25,7 +25,9 @@ struct ExCtl {
   unsigned long long overflow;  // appends dropped for lack of capacity (must stay 0)
 };
 
-// Bottom levels swept per final node.
+// Bottom levels swept per final node: 2, or 3 for trees wider than 2^24
+// prefixes at depth K - 2 (measured at C5, 24^8: the deeper final list of
+// I = 2 costs more traffic and frontier work than the longer sweep saves).
 __host__ __device__ inline int sweep_levels(int K, int nc) {
   if (K <= 2) return K;
   double np = 1.0;
@@ -177,6 +179,9 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
 __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl, Frontier in,
                                                   Frontier out, FinalList fin, int nc_max, unsigned long long cap_out,
                                                   unsigned long long cap_final) {
+  // an overflowed level still counts every append (the exact need of the
+  // retry); the levels below it are not expanded
+  if (ctl->overflow) return;
   const unsigned long long n_in = ctl->level_count[k];
   const unsigned long long total = n_in * static_cast<unsigned long long>(nc_max);
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
@@ -474,8 +479,10 @@ __device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsig
 
 // One thread per final node: the I bottom levels of its subtree.
 __global__ void __launch_bounds__(256, BS_SWEEP_MINB) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
-                                                    FinalList fin, Key128* best, unsigned long long* feas) {
-  const unsigned long long n_fin = ctl->final_count;
+                                                    FinalList fin, Key128* best, unsigned long long* feas,
+                                                    unsigned long long cap_final) {
+  if (ctl->overflow) return;  // the run is repeated with larger lists (one_shot): skip the sweep
+  const unsigned long long n_fin = ctl->final_count < cap_final ? ctl->final_count : cap_final;
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
   for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < n_fin;
        base += stride) {

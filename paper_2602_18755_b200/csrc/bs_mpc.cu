@@ -210,6 +210,7 @@ int report_status(bs_ctx_t ctx, const bs_mpc_result* out, int n) {
 }
 
 enum Mode { kExhaustive = 0, kGreedy = 1 };
+constexpr int kOverflowStatus = BS_CUDA_ERROR + 1;  // internal: frontier capacity exceeded
 constexpr int kNumEvents = 6;  // exhaustive phases: prepare, seed, bfs, sweep, finalize
 
 // One batch of MPC decisions resident in HBM: packed problems, scratch, and
@@ -235,6 +236,7 @@ struct MpcRun {
   DMpcOut* dOut = nullptr;
   DLevel* dLv = nullptr;
   int bfs_grid = 0, sweep_grid = 0;
+  ExCtl ctl_host{};  // counters of an overflowed run (exact totals of the levels before the first overflow)
   cudaEvent_t ev[kNumEvents] = {};
   bool have_events = false;
 };
@@ -282,12 +284,19 @@ void bind_exhaustive(MpcRun* r, char* base, const ExLayout& L) {
   r->dOut = reinterpret_cast<DMpcOut*>(base + L.out);
 }
 
-constexpr size_t kMaxExhaustiveScratch = 24ull << 30;
+constexpr size_t kMaxExhaustiveScratch = 48ull << 30;
 
 // Packs the problems (one H2D copy), validates configurations and sizes the
 // exhaustive frontiers from the horizons (K <= horizon_K).
+// Frontier capacities: the worst case (every prefix feasible), clamped to a
+// scratch budget; a run whose appends overflow is re-run with capacities
+// from the observed counts, or split (one_shot).
+constexpr unsigned long long kFinalCapMax = 2000000000ull;  // 12 B each: 24 GB
+constexpr unsigned long long kLevelCapMax = 250000000ull;   // 40 B each, two ping-pong lists: 20 GB
+
 int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
-             const bs_mpc_problem* problems, int n, int mode, MpcRun* run) {
+             const bs_mpc_problem* problems, int n, int mode, MpcRun* run, unsigned long long cap_level_hint = 0,
+             unsigned long long cap_final_hint = 0) {
   run->mode = mode;
   run->n = n;
   if (n > (1 << 24)) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: at most 2^24 problems per call");
@@ -323,6 +332,10 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
     run->cap_level += ipow(static_cast<unsigned long long>(c.nc), FD > 0 ? FD - 1 : 0);
   }
   if (mode == kExhaustive) {
+    if (cap_level_hint) run->cap_level = std::min(run->cap_level, cap_level_hint);
+    if (cap_final_hint) run->cap_final = std::min(run->cap_final, cap_final_hint);
+    run->cap_level = std::min(run->cap_level, kLevelCapMax);
+    run->cap_final = std::min(run->cap_final, kFinalCapMax);
     run->cap_level = std::max<unsigned long long>(run->cap_level, static_cast<unsigned long long>(n));
     run->cap_final = std::max<unsigned long long>(run->cap_final, static_cast<unsigned long long>(n));
     const ExLayout L = ex_layout(*run, 0);
@@ -386,7 +399,8 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
     BS_LAUNCH_CHECK(ctx);
   }
   BS_REC(3);
-  sweep_kernel<<<run->sweep_grid, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest, run->dFeas);
+  sweep_kernel<<<run->sweep_grid, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest, run->dFeas,
+                                                         run->cap_final);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(4);
   finalize_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, pk.cfgs, pk.problems, run->dBest, run->dFeas,
@@ -417,9 +431,11 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
     ctx->last_d2h += 8;
   }
   BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  if (*hOverflow)
-    return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: %llu frontier appends overflowed (capacity bug)",
-                     *hOverflow);
+  if (*hOverflow) {
+    BS_CUDA_TRY(ctx, cudaMemcpy(&run->ctl_host, run->dCtl, sizeof(ExCtl), cudaMemcpyDeviceToHost));
+    return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
+                     "batch; split it into smaller calls", *hOverflow);
+  }
   for (int i = 0; i < n; ++i)
     expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
                   run->target[i], &out[i], run->mode == kExhaustive);
@@ -429,25 +445,59 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
 int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
              int n_cfgs, const bs_mpc_problem* problems, int n, bs_mpc_result* out, int mode) {
   if (!ctx || !models) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: null context or models");
-  MpcRun run;
-  int rc = run_pack(ctx, cfgs, policies, n_cfgs, problems, n, mode, &run);
-  if (rc) return rc;
-  ctx->last_h2d = run.pk.h2d_bytes;
-  ctx->last_d2h = 0;
-  if (n == 0) return BS_OK;
-  if (mode == kExhaustive) {
-    const ExLayout L = ex_layout(run, 0);
-    char* base = static_cast<char*>(ctx->dev_buf(kSlotWork, L.total));
-    if (!base) return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: device allocation of %zu bytes failed", L.total);
-    bind_exhaustive(&run, base, L);
-  } else {
-    run.dOut = static_cast<DMpcOut*>(ctx->dev_buf(kSlotOut, out_bytes(n)));
-    run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n)));
-    if (!run.dOut || !run.dLv) return set_error(ctx, BS_CUDA_ERROR, "mpc greedy: allocation failed");
+  unsigned long long cap_level = 0, cap_final = 0;  // 0: worst case (clamped)
+  for (int attempt = 0;; ++attempt) {
+    MpcRun run;
+    int rc = run_pack(ctx, cfgs, policies, n_cfgs, problems, n, mode, &run, cap_level, cap_final);
+    if (rc) return rc;
+    ctx->last_h2d = run.pk.h2d_bytes;
+    ctx->last_d2h = 0;
+    if (n == 0) return BS_OK;
+    if (mode == kExhaustive) {
+      const ExLayout L = ex_layout(run, 0);
+      char* base = static_cast<char*>(ctx->dev_buf(kSlotWork, L.total));
+      if (!base) return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: device allocation of %zu bytes failed", L.total);
+      bind_exhaustive(&run, base, L);
+    } else {
+      run.dOut = static_cast<DMpcOut*>(ctx->dev_buf(kSlotOut, out_bytes(n)));
+      run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n)));
+      if (!run.dOut || !run.dLv) return set_error(ctx, BS_CUDA_ERROR, "mpc greedy: allocation failed");
+    }
+    rc = run_enqueue(ctx, models, &run, false);
+    if (rc) return rc;
+    rc = run_results(ctx, &run, out);
+    if (rc != kOverflowStatus) return rc;
+    // Overflow: counts up to the first overflowing level are exact totals;
+    // retry with room for them, or split the batch when they exceed the budget.
+    unsigned long long need_level = 0;
+    for (int k = 0; k <= kMaxK; ++k) need_level = std::max(need_level, run.ctl_host.level_count[k]);
+    const unsigned long long need_final = run.ctl_host.final_count;
+    const unsigned long long grow_level = need_level + need_level / 4 + 1024;
+    const unsigned long long grow_final = need_final + need_final / 4 + 1024;
+    const bool fits = grow_level <= kLevelCapMax && grow_final <= kFinalCapMax;
+    if (fits && attempt < kMaxK + 2 && (grow_level > run.cap_level || grow_final > run.cap_final)) {
+      cap_level = std::max(grow_level, run.cap_level);
+      cap_final = std::max(grow_final, run.cap_final);
+      continue;
+    }
+    if (n == 1) return set_error(ctx, BS_PARAMETER_ERROR, "mpc exhaustive: one decision exceeds the frontier budget");
+    // split into pieces sized from the observed (lower-bound) need
+    const double over = std::max(static_cast<double>(grow_level) / kLevelCapMax,
+                                 static_cast<double>(grow_final) / kFinalCapMax);
+    const int pieces = std::min(n, std::max(2, static_cast<int>(std::ceil(over * 1.25))));
+    uint64_t h2d = ctx->last_h2d, d2h = ctx->last_d2h;
+    for (int p = 0; p < pieces; ++p) {
+      const int a = static_cast<int>(static_cast<long long>(n) * p / pieces);
+      const int b = static_cast<int>(static_cast<long long>(n) * (p + 1) / pieces);
+      rc = one_shot(ctx, models, cfgs, policies, n_cfgs, problems + a, b - a, out + a, mode);
+      if (rc) return rc;
+      h2d += ctx->last_h2d;
+      d2h += ctx->last_d2h;
+    }
+    ctx->last_h2d = h2d;
+    ctx->last_d2h = d2h;
+    return BS_OK;
   }
-  rc = run_enqueue(ctx, models, &run, false);
-  if (rc) return rc;
-  return run_results(ctx, &run, out);
 }
 
 }  // namespace
@@ -493,46 +543,7 @@ int bs_project_batches(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_schedul
 int bs_mpc_exhaustive(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
                       const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
                       bs_mpc_result* out) {
-  if (!ctx || !models) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: null context or models");
-  if (n_cfgs < 1 || !cfgs || !policies || n <= 0)
-    return one_shot(ctx, models, cfgs, policies, n_cfgs, problems, n, out, kExhaustive);
-  // Frontier scratch is sized for the worst case (every prefix feasible), so
-  // wide trees (e.g. 24^8) are run in consecutive chunks of decisions whose
-  // worst case fits the scratch budget; results are independent per decision.
-  std::vector<double> per_cfg(n_cfgs, 0.0);
-  for (int c = 0; c < n_cfgs; ++c) {
-    DMpcCfg hc;
-    if (pack_mpc_cfg(ctx, cfgs[c], policies[c], &hc) != BS_OK) {
-      per_cfg[c] = 0.0;  // reported by the chunk that contains it
-      continue;
-    }
-    const int FD = hc.horizon - sweep_levels(hc.horizon, hc.nc);
-    per_cfg[c] = 12.0 * static_cast<double>(ipow(hc.nc, FD)) +
-                 80.0 * static_cast<double>(ipow(hc.nc, FD > 0 ? FD - 1 : 0)) + sizeof(DTables) + 256.0;
-  }
-  ctx->err.clear();
-  const double budget = 0.66 * static_cast<double>(kMaxExhaustiveScratch);
-  uint64_t h2d = 0, d2h = 0;
-  int a = 0;
-  while (a < n) {
-    double need = 0.0;
-    int b = a;
-    while (b < n) {
-      const int ci = problems[b].cfg_index;
-      const double w = (ci >= 0 && ci < n_cfgs) ? per_cfg[ci] : 0.0;
-      if (b > a && need + w > budget) break;
-      need += w;
-      ++b;
-    }
-    const int rc = one_shot(ctx, models, cfgs, policies, n_cfgs, problems + a, b - a, out + a, kExhaustive);
-    h2d += ctx->last_h2d;
-    d2h += ctx->last_d2h;
-    if (rc != BS_OK) return rc;
-    a = b;
-  }
-  ctx->last_h2d = h2d;
-  ctx->last_d2h = d2h;
-  return BS_OK;
+  return one_shot(ctx, models, cfgs, policies, n_cfgs, problems, n, out, kExhaustive);
 }
 
 int bs_mpc_greedy(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
@@ -595,7 +606,10 @@ int bs_mpc_plan_run(bs_ctx_t ctx, bs_mpc_plan_t plan, int record_kernel_times) {
 
 int bs_mpc_plan_results(bs_ctx_t ctx, bs_mpc_plan_t plan, bs_mpc_result* out) {
   if (!ctx || !plan) return set_error(ctx, BS_PARAMETER_ERROR, "bs_mpc_plan_results: null argument");
-  return run_results(ctx, &plan->run, out);
+  const int rc = run_results(ctx, &plan->run, out);
+  // a resident plan's frontiers are fixed at creation: report an overflow as
+  // a parameter problem of the batch (one-shot calls re-run or split instead)
+  return rc == kOverflowStatus ? set_error(ctx, BS_PARAMETER_ERROR, "%s", ctx->err.c_str()) : rc;
 }
 
 int bs_mpc_plan_kernel_ms(bs_ctx_t ctx, bs_mpc_plan_t plan, float* ms, int n_ms) {
