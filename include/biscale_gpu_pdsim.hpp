@@ -36,9 +36,11 @@
 // but a host call avoids a launch on the simulator's critical path).
 #pragma once
 
+#include <algorithm>
 #include <cstdio>
 #include <memory>
 #include <optional>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -475,9 +477,8 @@ class GpuTwoTierFactory : public pdsim::ControllerFactory {
 // --- cluster replay and the window loop -------------------------------------------
 
 // One run_policy (runner.hpp:112-122) + its window report (runner.hpp:131-133),
-// as the device replays it.  `sim` carries SimResult's counters and horizon;
-// its record vectors stay empty (the device reduces requests to what the
-// metrics read -- use bs_replay's logs for full records).
+// as the device replays it.  `sim` carries SimResult's counters and horizon,
+// and its records when requested.
 struct ReplayRun {
   pdsim::SimResult sim;
   pdsim::MetricsReport report;
@@ -565,10 +566,14 @@ inline pdsim::WindowPlans plan_window_policies(const DeviceModels& dm, const pds
 // run_policy + the window report for a batch of (window, plan, policy)
 // triples in ONE device call (bs_replay).  Throws like the reference on the
 // first failing run.
+// records: also fill each SimResult's requests, batches, idles and
+// decisions (the reference's CSV writers then produce the same files; a
+// request's token_times_ms holds only its first and last emission, which is
+// what save_request_csv and the metrics read).
 inline std::vector<ReplayRun> replay_policies(const DeviceModels& dm, const std::vector<const pdsim::Trace*>& windows,
                                               const std::vector<const pdsim::PlacementPlan*>& plans,
                                               const std::vector<pdsim::Policy>& policies,
-                                              const pdsim::RunnerConfig& cfg) {
+                                              const pdsim::RunnerConfig& cfg, bool records = false) {
   const std::size_t n = windows.size();
   std::vector<double> lad_ctl, lad_fix;
   const bs_replay_config cfgs[2] = {detail::replay_config(cfg, false, lad_fix),
@@ -590,20 +595,95 @@ inline std::vector<ReplayRun> replay_policies(const DeviceModels& dm, const std:
     sc[i].config = policies[i] == pdsim::Policy::two_tier ? 1 : 0;
   }
   std::vector<bs_replay_summary> out(n);
+  std::vector<bs_replay_request> reqs;
+  std::vector<std::vector<bs_batch_record>> bat(records ? n : 0);
+  std::vector<std::vector<bs_idle_record>> idl(records ? n : 0);
+  std::vector<std::vector<bs_decision_record>> dec(records ? n : 0);
+  std::vector<bs_replay_logs> logs(records ? n : 0);
+  if (records) {
+    std::size_t total = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+      int64_t cap = 1024;
+      for (const auto& r : windows[i]->requests) cap += r.output_len + 4;
+      total += windows[i]->requests.size();
+      bat[i].resize(static_cast<std::size_t>(cap));
+      idl[i].resize(static_cast<std::size_t>(cap));
+      dec[i].resize(static_cast<std::size_t>(cap));
+      logs[i] = bs_replay_logs{bat[i].data(), cap, 0, idl[i].data(), cap, 0, dec[i].data(), cap, 0};
+    }
+    reqs.resize(std::max<std::size_t>(total, 1));
+  }
   dm.device().check(bs_replay(dm.device().get(), dm.get(), dm.get(), cfgs, 2, sc.data(), static_cast<int>(n),
-                              out.data(), nullptr, nullptr));
+                              out.data(), records ? reqs.data() : nullptr, records ? logs.data() : nullptr));
   std::vector<ReplayRun> runs(n);
-  for (std::size_t i = 0; i < n; ++i) detail::fill_run(out[i], runs[i]);
+  std::size_t q = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    detail::fill_run(out[i], runs[i]);
+    if (!records) continue;
+    if (logs[i].n_batches > logs[i].batch_cap || logs[i].n_idles > logs[i].idle_cap ||
+        logs[i].n_decisions > logs[i].decision_cap)
+      throw std::runtime_error("biscale_gpu: replay log capacity exceeded");
+    pdsim::SimResult& sim = runs[i].sim;
+    for (const auto& ci : plans[i]->instances) sim.instances.push_back(ci.config);
+    const auto& rq = windows[i]->requests;
+    for (std::size_t k = 0; k < rq.size(); ++k, ++q) {
+      const bs_replay_request& r = reqs[q];
+      pdsim::RequestRecord rec;
+      rec.id = rq[k].id;
+      rec.arrival_ms = rq[k].arrival_ms;
+      rec.input_len = rq[k].input_len;
+      rec.output_len = rq[k].output_len;
+      rec.prefill_instance = r.prefill_instance;
+      rec.decode_instance = r.decode_instance;
+      if (r.prefill_done_ms == r.prefill_done_ms) rec.prefill_done_ms = r.prefill_done_ms;
+      if (r.decode_instance >= 0) rec.decode_join_ms = r.prefill_done_ms;
+      if (r.decode_first_start_ms == r.decode_first_start_ms) rec.decode_first_start_ms = r.decode_first_start_ms;
+      if (r.n_tokens >= 1) rec.token_times_ms.push_back(r.first_token_ms);
+      if (r.n_tokens >= 2) rec.token_times_ms.push_back(r.last_token_ms);
+      rec.completed = r.completed != 0;
+      sim.requests.push_back(std::move(rec));
+    }
+    std::stable_sort(sim.requests.begin(), sim.requests.end(),
+                     [](const pdsim::RequestRecord& a, const pdsim::RequestRecord& b) { return a.id < b.id; });
+    auto phase_of = [](int32_t p) { return p == BS_PHASE_PREFILL ? pdsim::Phase::prefill : pdsim::Phase::decode; };
+    for (int64_t k = 0; k < logs[i].n_batches; ++k) {
+      const bs_batch_record& b = bat[i][static_cast<std::size_t>(k)];
+      pdsim::BatchRecord r;
+      r.instance = b.instance;
+      r.phase = phase_of(b.phase);
+      r.batch_seq = b.batch_seq;
+      r.start_ms = b.start_ms;
+      r.end_ms = b.end_ms;
+      r.features.n_requests = b.n_requests;
+      r.features.sum_len = b.sum_len;
+      r.freq_mhz = b.freq_mhz;
+      r.power_w = b.power_w;
+      r.energy_j = b.energy_j;
+      sim.batches.push_back(std::move(r));
+    }
+    for (int64_t k = 0; k < logs[i].n_idles; ++k) {
+      const bs_idle_record& b = idl[i][static_cast<std::size_t>(k)];
+      sim.idles.push_back(pdsim::IdleRecord{b.instance, phase_of(b.phase), b.start_ms, b.end_ms, b.freq_mhz,
+                                            b.power_w, b.energy_j});
+    }
+    for (int64_t k = 0; k < logs[i].n_decisions; ++k) {
+      const bs_decision_record& d = dec[i][static_cast<std::size_t>(k)];
+      sim.decisions.records.push_back(pdsim::DecisionRecord{d.time_ms, d.instance,
+                                                            static_cast<pdsim::Trigger>(d.trigger),
+                                                            d.chosen_freq_mhz, d.feasible != 0, d.eval_count});
+    }
+  }
   return runs;
 }
 
 // run_experiment (runner.hpp:155-172): window w planned from window w-1 on
 // the GPU, then every (window, policy) replayed in one device call.  Result
-// as the reference's, except that runs[i].sim holds SimResult's counters
-// only (see ReplayRun).
+// as the reference's; runs[i].sim holds SimResult's counters, plus the
+// records when `records` (see replay_policies), so the CLI's writers
+// (cli.hpp:371-378) produce the reference's files.
 inline pdsim::ExperimentResult run_experiment(const DeviceModels& dm, const pdsim::Trace& trace, double window_ms,
                                               const std::vector<pdsim::Policy>& policies,
-                                              const pdsim::RunnerConfig& cfg) {
+                                              const pdsim::RunnerConfig& cfg, bool records = false) {
   cfg.validate();
   if (policies.empty()) throw pdsim::ParameterError("no policies selected");
   std::vector<pdsim::Trace> windows = pdsim::split_windows(trace, window_ms);
@@ -620,7 +700,7 @@ inline pdsim::ExperimentResult run_experiment(const DeviceModels& dm, const pdsi
       pls.push_back(pol == pdsim::Policy::maxfreq_distserve ? &plans[w].maxfreq : &plans[w].ilp);
       pols.push_back(pol);
     }
-  std::vector<ReplayRun> runs = pdsim_gpu::replay_policies(dm, wins, pls, pols, cfg);
+  std::vector<ReplayRun> runs = pdsim_gpu::replay_policies(dm, wins, pls, pols, cfg, records);
   pdsim::ExperimentResult out;
   for (std::size_t i = 0; i < runs.size(); ++i) {
     const std::size_t w = i / policies.size();

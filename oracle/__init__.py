@@ -21,6 +21,7 @@ REF_SO = HERE / "_ref" / "libpdsim_ref.so"
 REPLAY_BIN = HERE / "_ref" / "replay_parity"
 PLACEMENT_BIN = HERE / "_ref" / "placement_parity"
 EXPERIMENT_BIN = HERE / "_ref" / "experiment_parity"
+CSV_BIN = HERE / "_ref" / "csv_parity"
 REFERENCE_ROOT = Path("/root/reference")
 
 _P = C.POINTER

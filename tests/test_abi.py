@@ -89,4 +89,5 @@ def test_pdsim_shim_compiles_against_reference():
         pytest.skip("/root/reference absent")
     res = subprocess.run(["make", "-C", str(oracle.HERE), "replay"], capture_output=True, text=True)
     assert res.returncode == 0, res.stdout + res.stderr
-    assert oracle.REPLAY_BIN.exists() and oracle.PLACEMENT_BIN.exists() and oracle.EXPERIMENT_BIN.exists()
+    assert oracle.REPLAY_BIN.exists() and oracle.PLACEMENT_BIN.exists() and oracle.EXPERIMENT_BIN.exists() and \
+        oracle.CSV_BIN.exists()

@@ -63,3 +63,21 @@ def test_reference_experiment_vs_gpu_experiment(args):
     assert line["runs"] > 0 and line["mismatch"] == 0, line
     assert line["match"], line
     assert res.returncode == 0
+
+
+@pytest.mark.parametrize("args", [
+    ["--seed", "7", "--minutes", "4", "--window-s", "120", "--rps", "8"],
+    ["--seed", "21", "--minutes", "3", "--window-s", "60", "--rps", "12"],
+])
+def test_cli_output_files_identical(args, tmp_path):
+    """The CLI run's files (plan JSON, requests / batches / decisions CSVs,
+    report.csv; cli.hpp:371-378) written by the reference's own writers from
+    the reference's run_experiment and from pdsim_gpu::run_experiment with
+    records: byte-identical."""
+    if not oracle.CSV_BIN.exists():
+        pytest.skip("csv_parity not built (needs /root/reference at build time)")
+    res = subprocess.run([str(oracle.CSV_BIN), *args, str(tmp_path)], capture_output=True, text=True, timeout=900)
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["files"] > 10 and line["bytes"] > 10000, line
+    assert line["differ"] == 0 and line["match"], line
+    assert res.returncode == 0
