@@ -217,3 +217,28 @@ def test_replay_miscalibrated_controller_fires_safety(gpu_device, ref_lib):
         scs.append(s)
     got = check_same(gpu_device, ref_lib, scs, truth)
     assert sum(g.decisions_by_trigger[2] for g in got) > 0
+
+
+def test_replay_edge_traces(gpu_device, ref_lib):
+    """Empty trace, single request, one-token outputs (no TPOT), a burst of
+    simultaneous arrivals, and a ramp-up longer than the trace (empty view)."""
+    lad = W.ladder(8)
+    models = W.llama_models(lad)
+    scs = []
+    _, base = scenario(5.0, 20, 31)
+    variants = [
+        [],
+        [P.Request(0, 100.0, 700, 50)],
+        [P.Request(i, 10.0 * i, 300 + 10 * i, 1) for i in range(40)],
+        [P.Request(i, 500.0, 200 + i, 20 + i) for i in range(64)],
+    ]
+    for k, reqs in enumerate(variants):
+        _, s = scenario(5.0, 20, 40 + k)
+        s.trace = P.Trace(reqs, 20e3)
+        s.controllers.models = models
+        scs.append(s)
+    _, late = scenario(5.0, 20, 50, rampup=60.0)
+    late.controllers.models = models
+    scs.append(late)
+    got = check_same(gpu_device, ref_lib, scs, models)
+    assert all(g.status == 0 for g in got)
