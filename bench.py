@@ -638,17 +638,31 @@ def main():
     same = all(res[i].best_code == out[i].best_code and res[i].objective_w == out[i].objective_w
                for i in range(D))
     lib.bs_mpc_plan_destroy(dev.handle, plan)
+    gathered = None
+    if world > 1:  # the final gather of per-decision results over NCCL (outside the timed region)
+        import struct
+
+        from paper_2602_18755_b200 import sharding as S
+
+        rows = torch.tensor([[struct.unpack("<q", struct.pack("<d", out[i].objective_w))[0],
+                              int(out[i].best_code) & 0x7FFFFFFFFFFFFFFF, int(out[i].feasible_count)]
+                             for i in range(D)], dtype=torch.int64, device=f"cuda:{local}")
+        table = S.gather_rows(rows, world * D)
+        gathered = {"rows": int(table.shape[0]), "bytes": int(table.numel() * 8),
+                    "rank0_rows_match": bool(torch.equal(table[:D], rows)) if rank == 0 else None}
 
     # --- roofline ----------------------------------------------------------------
     peak, peak_ms = C.c_double(), C.c_double()
     dev.check(lib.bs_fp64_peak(dev.handle, C.byref(peak), C.byref(peak_ms)))
     leaf_avg_ms = statistics.mean(leaf_ms)
     achieved = W_OPS * D * TRAJ_PER_DECISION / (leaf_avg_ms * 1e-3)
-    traffic = None
+    traffic, executed = None, None
     tpath = ROOT / "profiles" / "leaf_traffic.json"
     if tpath.exists():
         try:
-            traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch")
+            prof = json.loads(tpath.read_text())
+            traffic = prof.get("dram_bytes_per_launch")
+            executed = prof.get("executed")
         except Exception:
             traffic = None
 
@@ -684,11 +698,12 @@ def main():
                     "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
                     "matches_resident": bool(same)},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / peak.value, "traffic": traffic,
+                         "frac": achieved / peak.value, "traffic": traffic, "executed": executed,
                          "note": "W = 5H+2 = 32 FP64 ops per trajectory (SURVEY §8d) over the sweep kernel's event "
                                  "time; prefix sharing and infeasible-subtree pruning execute fewer ops, so frac may "
                                  "exceed 1; peak = measured non-FMA DADD issue rate (bs_fp64_peak)"},
             "gpu_launches": int(launches),
+            "gather": gathered,
             "clocks": clk,
             "cpu_baseline": cpu,
         }
