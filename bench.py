@@ -253,9 +253,21 @@ def bench_c3(dev, with_cpu: bool, repeats: int = 3) -> dict:
     t_ilp = time.perf_counter() - t0
     t_table = statistics.median(times)
     k_max = int(base.mean_rps() // search.tolerance_rps)
-    out = {"workload": "C3: 1-hour gamma(0.5) window at 12 rps, 128 candidates (2 phases x TP{1,2,4,8} x 16 "
-                       "rungs), max_batch_tokens 2048, G = 16", "requests": len(base.requests),
-           "value": len(cands) / t_table, "unit": "placement configs/s", "table_s": t_table,
+    # the stream of bursty 1-hour windows (configs[2]: "over bursty 1-hour trace windows"): four
+    # consecutive windows, their tables built concurrently on one GPU
+    day = P.gen_gamma_trace(12.0, 0.5, 4 * 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)),
+                            7)
+    wins = P.split_windows(day, 3600e3)
+    P.build_config_tables(wins, cands, slo, models, pol, search, dev)  # warm-up (one probe grid for all windows)
+    t0 = time.perf_counter()
+    P.build_config_tables(wins, cands, slo, models, pol, search, dev)
+    t_stream = time.perf_counter() - t0
+    out = {"workload": "C3: bursty 1-hour gamma(0.5) windows at 12 rps, 128 candidates per window (2 phases x "
+                       "TP{1,2,4,8} x 16 rungs), max_batch_tokens 2048, G = 16", "requests": len(base.requests),
+           "value": len(wins) * len(cands) / t_stream, "unit": "placement configs/s",
+           "value_note": f"{len(wins)} consecutive windows, all tables in one probe grid ({t_stream:.2f} s); one table "
+                         "alone is bound by its longest probe (table_s)",
+           "single_table_configs_per_s": len(cands) / t_table, "table_s": t_table,
            "probes_per_s": k_max * len(cands) / t_table, "ilp_s": t_ilp, "gpus_used": plan.gpus_used,
            "objective_w": plan.objective_w, "phase_ms": {"mask": st[0], "probe": st[1], "energy": st[2]},
            "events_simulated": st[4], "e2e_note": "value is end to end through pdsim.build_config_table "

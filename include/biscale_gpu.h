@@ -30,9 +30,14 @@
  *                           DecodePolicyController::decide (dvfs.hpp:347-350)
  *   bs_goodput_table        build_config_table (placement.hpp:240-260) over
  *                           evaluate_candidate / max_goodput
- *                           (placement.hpp:154-238)
+ *                           (placement.hpp:154-238); bs_goodput_tables for
+ *                           several probe traces in one grid (plan_window of
+ *                           every window of run_experiment, runner.hpp:155-172)
  *   bs_placement_solve      solve_placement (placement.hpp:357-416)
  *   bs_placement_max_throughput  solve_max_throughput (placement.hpp:421-499)
+ *   bs_replay               simulate_cluster (simulator.hpp:758-893) with the
+ *                           TwoTierFactory controllers (dvfs.hpp:370-390),
+ *                           trim_steady_state + make_report (metrics.hpp:71-156)
  *
  * Threading: a context is not thread-safe (one per host thread, each with its
  * own CUDA stream).  Uploaded models are immutable; kernels are re-entrant.
@@ -438,6 +443,14 @@ int bs_downsample_keep(bs_ctx_t ctx, const bs_trace* trace, const bs_goodput_sea
 int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, const bs_slo* slo,
                      const bs_scheduler_policy* policy, const bs_goodput_search* search,
                      const bs_instance_config* cands, int n_cand, bs_table_entry* out);
+
+/* build_config_table for n_tables probe traces (e.g. consecutive windows)
+ * in ONE probe grid, long probes of every table first: out is
+ * n_tables x n_cand (table-major).  A stream of tables is then bound by the
+ * device's throughput, not by each table's longest probe in turn. */
+int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, int n_tables, const bs_slo* slo,
+                      const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                      const bs_instance_config* cands, int n_cand, bs_table_entry* out);
 
 /* simulate_instance (simulator.hpp:667-739) at the instance's fixed
  * frequency (no controller) + sim_meets_slo (placement.hpp:119-131) +

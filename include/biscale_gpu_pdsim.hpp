@@ -420,6 +420,40 @@ inline std::vector<pdsim::ConfigTableEntry> build_config_table(const DeviceModel
   return table;
 }
 
+// build_config_table for several probe traces in one device call
+// (bs_goodput_tables): tables[t] belongs to bases[t].
+inline std::vector<std::vector<pdsim::ConfigTableEntry>> build_config_tables(
+    const DeviceModels& dm, const std::vector<pdsim::InstanceConfig>& candidates,
+    const std::vector<const pdsim::Trace*>& bases, const pdsim::SLOSpec& slo, const pdsim::SchedulerPolicy& policy,
+    const pdsim::GoodputSearch& search) {
+  if (candidates.empty()) throw pdsim::ParameterError("config table: no candidates");
+  std::vector<detail::TraceView> tvs;
+  tvs.reserve(bases.size());
+  std::vector<bs_trace> trs;
+  for (const pdsim::Trace* b : bases) {
+    tvs.emplace_back(*b);
+    trs.push_back(tvs.back().t);
+  }
+  const bs_slo s{slo.ttft_ms, slo.tpot_ms, slo.percentile};
+  const bs_scheduler_policy pol = detail::to_policy(policy);
+  bs_goodput_search g{};
+  g.tolerance_rps = search.tolerance_rps;
+  g.probe_count = search.probe_count;
+  g.seed = search.seed;
+  std::vector<bs_instance_config> cands;
+  for (const auto& c : candidates)
+    cands.push_back(bs_instance_config{c.phase == pdsim::Phase::prefill ? BS_PHASE_PREFILL : BS_PHASE_DECODE, c.tp,
+                                       c.base_freq_mhz});
+  const std::size_t n = cands.size();
+  std::vector<bs_table_entry> out(n * bases.size());
+  dm.device().check(bs_goodput_tables(dm.device().get(), dm.get(), trs.data(), static_cast<int>(trs.size()), &s,
+                                      &pol, &g, cands.data(), static_cast<int>(n), out.data()));
+  std::vector<std::vector<pdsim::ConfigTableEntry>> tables(bases.size());
+  for (std::size_t t = 0; t < bases.size(); ++t)
+    for (std::size_t c = 0; c < n; ++c) tables[t].push_back(detail::from_entry(out[t * n + c]));
+  return tables;
+}
+
 // solve_placement (placement.hpp:357-416), same fold order and tie-breaks;
 // InfeasibleError with the reference's constraint and message.
 inline pdsim::PlacementPlan solve_placement(const pdsim::PlacementProblem& p) {
@@ -687,10 +721,29 @@ inline pdsim::ExperimentResult run_experiment(const DeviceModels& dm, const pdsi
   cfg.validate();
   if (policies.empty()) throw pdsim::ParameterError("no policies selected");
   std::vector<pdsim::Trace> windows = pdsim::split_windows(trace, window_ms);
-  std::vector<pdsim::WindowPlans> plans;
-  plans.reserve(windows.size());
-  for (std::size_t w = 0; w < windows.size(); ++w)
-    plans.push_back(pdsim_gpu::plan_window_policies(dm, w == 0 ? windows[0] : windows[w - 1], cfg));
+  // plan_window (placement.hpp:558-582) for every window, all the config
+  // tables in one device call (bs_goodput_tables)
+  std::vector<pdsim::Trace> predicted;
+  for (std::size_t w = 0; w < windows.size(); ++w) {
+    const pdsim::Trace& history = w == 0 ? windows[0] : windows[w - 1];
+    history.validate();
+    if (history.requests.empty()) throw pdsim::ParameterError("plan_window: empty history");
+    predicted.push_back(pdsim::predict_next_window(history));
+  }
+  std::vector<const pdsim::Trace*> probes;
+  for (const auto& p : predicted) probes.push_back(cfg.plan.probe_trace ? &*cfg.plan.probe_trace : &p);
+  const std::vector<pdsim::InstanceConfig> candidates = pdsim::enumerate_candidates(cfg.ladder, cfg.tp_options);
+  std::vector<std::vector<pdsim::ConfigTableEntry>> tables =
+      pdsim_gpu::build_config_tables(dm, candidates, probes, cfg.slo, cfg.plan.policy, cfg.plan.search);
+  std::vector<pdsim::WindowPlans> plans(windows.size());
+  for (std::size_t w = 0; w < windows.size(); ++w) {
+    pdsim::WindowPlans& wp = plans[w];
+    wp.target_rps = pdsim::peak_rps(predicted[w], cfg.plan.peak_subwindow_s);
+    wp.table = std::move(tables[w]);
+    pdsim::PlacementProblem p{wp.table, cfg.total_gpus, wp.target_rps, cfg.plan.alpha};
+    wp.ilp = pdsim_gpu::solve_placement(p);
+    wp.maxfreq = pdsim_gpu::solve_max_throughput(p, cfg.ladder.max_mhz());
+  }
   std::vector<const pdsim::Trace*> wins;
   std::vector<const pdsim::PlacementPlan*> pls;
   std::vector<pdsim::Policy> pols;

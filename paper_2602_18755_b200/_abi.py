@@ -369,6 +369,9 @@ PROTOTYPES = [
     ("bs_goodput_table", C.c_int, [ctx_t, models_t, C.POINTER(bs_trace), C.POINTER(bs_slo),
                                    C.POINTER(bs_scheduler_policy), C.POINTER(bs_goodput_search),
                                    C.POINTER(bs_instance_config), C.c_int, C.POINTER(bs_table_entry)]),
+    ("bs_goodput_tables", C.c_int, [ctx_t, models_t, C.POINTER(bs_trace), C.c_int, C.POINTER(bs_slo),
+                                    C.POINTER(bs_scheduler_policy), C.POINTER(bs_goodput_search),
+                                    C.POINTER(bs_instance_config), C.c_int, C.POINTER(bs_table_entry)]),
     ("bs_simulate_instance", C.c_int, [ctx_t, models_t, C.POINTER(bs_trace), C.c_int, C.POINTER(bs_instance_config),
                                        C.POINTER(bs_scheduler_policy), C.POINTER(bs_slo), C.POINTER(bs_sim_summary)]),
     ("bs_placement_solve", C.c_int, [ctx_t, C.POINTER(bs_table_entry), C.c_int, C.c_int, C.c_double, C.c_double,

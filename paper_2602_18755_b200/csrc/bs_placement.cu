@@ -24,6 +24,7 @@
 //                  tie-breaks.
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -53,12 +54,21 @@ struct MaskParams {
 // One warp per stream s = (k - 1) * reps + j.  The mt19937_64 twist in three
 // dependency phases (indices [0,156), [156,311), 311) so the warp computes it
 // in parallel; outputs are consumed in order, one per request.
-__global__ void __launch_bounds__(kMaskWarps * 32) mask_kernel(MaskParams mp, int* kept, long long* kept_count) {
+// Several tables at once: stream S of the launch belongs to the table t with
+// stream_off[t] <= S < stream_off[t + 1]; its kept list starts at
+// kept_off[t] + (S - stream_off[t]) * n_t.
+__global__ void __launch_bounds__(kMaskWarps * 32) mask_kernel(const MaskParams* mps, int n_tables,
+                                                               const long long* stream_off, const long long* kept_off,
+                                                               int* kept, long long* kept_count) {
   __shared__ unsigned long long st[kMaskWarps][kMtN];
   __shared__ unsigned long long tmp[kMaskWarps][kMtN];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int s = blockIdx.x * kMaskWarps + w;
-  if (s >= mp.k_max * mp.reps) return;
+  const long long S = static_cast<long long>(blockIdx.x) * kMaskWarps + w;
+  if (S >= stream_off[n_tables]) return;
+  int tb = 0;
+  while (stream_off[tb + 1] <= S) ++tb;
+  const MaskParams mp = mps[tb];
+  const long long s = S - stream_off[tb];
   const long long k = s / mp.reps + 1;
   const int j = s % mp.reps;
   // keep = min(1, k * tol / base_rate)  (placement.hpp:146-147)
@@ -72,7 +82,7 @@ __global__ void __launch_bounds__(kMaskWarps * 32) mask_kernel(MaskParams mp, in
     for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
   }
   __syncwarp();
-  int* out = kept + static_cast<size_t>(s) * mp.n;
+  int* out = kept + kept_off[tb] + static_cast<size_t>(s) * mp.n;
   long long count = 0;
   for (long long base = 0; base < mp.n; base += kMtN) {
     // twist
@@ -107,7 +117,7 @@ __global__ void __launch_bounds__(kMaskWarps * 32) mask_kernel(MaskParams mp, in
     }
     __syncwarp();
   }
-  if (lane == 0) kept_count[s] = count;
+  if (lane == 0) kept_count[S] = count;
 }
 
 // --- probes ---------------------------------------------------------------------
@@ -186,17 +196,35 @@ __device__ __forceinline__ WarpScratch carve_scratch(unsigned char* smem, int wa
 // (bs_sim.cuh), which evaluates up to 32 iterations' predictions at once.
 // Packing 32 probes into one warp instead would serialise their divergent
 // paths.
-__global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_cand, int n_streams, long long n_base,
-                             const int* kept, const long long* kept_count, PolicyDev pol, Resident* heaps,
-                             int heap_cap, int heap_in_smem, const int* order, ProbeOut* out) {
+// One probe of a multi-table launch: table, candidate, stream of the table.
+struct ProbeId {
+  int t;
+  int c;
+  long long s;
+};
+
+// Per-table views of the concatenated inputs.
+struct TableDev {
+  long long req_off;     // first request in the concatenated trace arrays
+  long long n;           // requests of the table's base trace
+  long long stream_off;  // first (k, replicate) stream in kept_count
+  long long kept_off;    // first kept index slot
+  long long probe_off;   // first probe output: + c * n_streams + s
+  long long n_streams;
+  double duration_ms;
+};
+
+__global__ void probe_kernel(DModels m, TraceDev tr, const TableDev* tabs, const DCand* cands, const int* kept,
+                             const long long* kept_count, PolicyDev pol, Resident* heaps, int heap_cap,
+                             int heap_in_smem, const ProbeId* order, long long n_probes, ProbeOut* out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long slot = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (slot >= static_cast<long long>(n_cand) * n_streams) return;
-  const long long gid = order[slot];  // launch order: likely-long probes first
-  const int c = static_cast<int>(gid / n_streams);
-  const int s = static_cast<int>(gid % n_streams);
-  const DCand cd = cands[c];
+  if (slot >= n_probes) return;
+  const ProbeId id = order[slot];  // launch order: likely-long probes first, across every table
+  const TableDev tb = tabs[id.t];
+  const long long gid = tb.probe_off + static_cast<long long>(id.c) * tb.n_streams + id.s;
+  const DCand cd = cands[id.c];
   ProbeOut o;
   o.status = BS_OK;
   o.model_err = 0;
@@ -206,19 +234,19 @@ __global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_c
   o.completed = 0;
   o.busy_j = 0.0;
   o.idle_j = 0.0;
-  const long long nk = kept_count[s];
+  const long long nk = kept_count[tb.stream_off + id.s];
   if (nk == 0) {  // placement.hpp:169: an empty probe passes
     o.empty = 1;
     if (lane == 0) out[gid] = o;
     return;
   }
   SimTrace st;
-  st.arrival = tr.arrival;
-  st.input = tr.input;
-  st.output = tr.output;
-  st.kept = kept + static_cast<size_t>(s) * n_base;
+  st.arrival = tr.arrival + tb.req_off;
+  st.input = tr.input + tb.req_off;
+  st.output = tr.output + tb.req_off;
+  st.kept = kept + tb.kept_off + static_cast<size_t>(id.s) * tb.n;
   st.n = nk;
-  st.duration_ms = tr.duration_ms;
+  st.duration_ms = tb.duration_ms;
   const SimParams p = make_params(cd, pol, cd.safe);
   SimOut r;
   if (cd.phase == BS_PHASE_PREFILL) {
@@ -226,7 +254,7 @@ __global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_c
     r = simulate_prefill(m, st, p);
   } else {
     const WarpScratch ws =
-        carve_scratch(smem, warp, heap_cap, heap_in_smem != 0, heaps + static_cast<size_t>(gid) * heap_cap);
+        carve_scratch(smem, warp, heap_cap, heap_in_smem != 0, heaps + static_cast<size_t>(slot) * heap_cap);
     r = simulate_decode_warp(m, st, p, ws, heap_cap, lane);
     if (lane != 0) return;
   }
@@ -238,59 +266,6 @@ __global__ void probe_kernel(DModels m, TraceDev tr, const DCand* cands, int n_c
   o.busy_j = r.busy_j;
   o.idle_j = r.idle_j;
   out[gid] = o;
-}
-
-struct EnergyOut {
-  int status;
-  int model_err;
-  long long completed;
-  double busy_j;
-  double idle_j;
-};
-
-__global__ void energy_kernel(DModels m, TraceDev tr, const DCand* cands, const int* cand_stream, int n_cand,
-                              long long n_base, const int* kept, const long long* kept_count, PolicyDev pol,
-                              Resident* heaps, int heap_cap, int heap_in_smem, EnergyOut* out) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // one warp per candidate
-  if (c >= n_cand) return;
-  const int s = cand_stream[c];
-  EnergyOut o;
-  o.status = BS_OK;
-  o.model_err = 0;
-  o.completed = 0;
-  o.busy_j = 0.0;
-  o.idle_j = 0.0;
-  if (s < 0) {
-    if (lane == 0) out[c] = o;
-    return;
-  }
-  SimTrace st;
-  st.arrival = tr.arrival;
-  st.input = tr.input;
-  st.output = tr.output;
-  st.kept = kept + static_cast<size_t>(s) * n_base;
-  st.n = kept_count[s];
-  st.duration_ms = tr.duration_ms;
-  const DCand cd = cands[c];
-  const SimParams p = make_params(cd, pol, 0);
-  SimOut r;
-  if (cd.phase == BS_PHASE_PREFILL) {
-    if (lane != 0) return;
-    r = simulate_prefill(m, st, p);
-  } else {
-    const WarpScratch ws =
-        carve_scratch(smem, warp, heap_cap, heap_in_smem != 0, heaps + static_cast<size_t>(c) * heap_cap);
-    r = simulate_decode_warp(m, st, p, ws, heap_cap, lane);
-    if (lane != 0) return;
-  }
-  o.status = r.status;
-  o.model_err = r.model_err;
-  o.completed = r.completed;
-  o.busy_j = r.busy_j;
-  o.idle_j = r.idle_j;
-  out[c] = o;
 }
 
 // Whole-trace simulations (bs_simulate_instance): thread i runs trace i.
@@ -520,11 +495,22 @@ int bs_downsample_keep(bs_ctx_t ctx, const bs_trace* trace, const bs_goodput_sea
   mp.base_rate = base_rate;
   mp.seed = search->seed;
   const long long streams = static_cast<long long>(mp.k_max) * mp.reps;
-  int* dk = static_cast<int*>(ctx->dev_buf(kSlotMisc, 4ull * streams * mp.n + 8ull * streams + 256));
-  if (!dk) return set_error(ctx, BS_CUDA_ERROR, "downsample: allocation failed");
-  long long* dc = reinterpret_cast<long long*>(reinterpret_cast<char*>(dk) + ((4ull * streams * mp.n + 255) / 256) * 256);
+  const size_t o_c = ((4ull * streams * mp.n + 255) / 256) * 256, o_p = o_c + ((8ull * streams + 255) / 256) * 256;
+  char* base = static_cast<char*>(ctx->dev_buf(kSlotMisc, o_p + 512));
+  if (!base) return set_error(ctx, BS_CUDA_ERROR, "downsample: allocation failed");
+  int* dk = reinterpret_cast<int*>(base);
+  long long* dc = reinterpret_cast<long long*>(base + o_c);
+  struct {
+    MaskParams mp;
+    long long so[2];
+    long long ko[1];
+  } hp{mp, {0, streams}, {0}};
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(base + o_p, &hp, sizeof hp, cudaMemcpyHostToDevice, ctx->stream));
+  const MaskParams* dmp = reinterpret_cast<const MaskParams*>(base + o_p);
+  const long long* dso = reinterpret_cast<const long long*>(base + o_p + offsetof(decltype(hp), so));
+  const long long* dko = reinterpret_cast<const long long*>(base + o_p + offsetof(decltype(hp), ko));
   mask_kernel<<<static_cast<unsigned>((streams + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, ctx->stream>>>(
-      mp, dk, dc);
+      dmp, 1, dso, dko, dk, dc);
   BS_LAUNCH_CHECK(ctx);
   const long long s = (k - 1) * mp.reps + replicate;
   long long cnt = 0;
@@ -535,14 +521,9 @@ int bs_downsample_keep(bs_ctx_t ctx, const bs_trace* trace, const bs_goodput_sea
   return BS_OK;
 }
 
-int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, const bs_slo* slo,
-                     const bs_scheduler_policy* policy, const bs_goodput_search* search,
-                     const bs_instance_config* cands, int n_cand, bs_table_entry* out) {
-  if (!ctx || !models || !base || !slo || !policy || !search || (!cands && n_cand > 0))
-    return set_error(ctx, BS_PARAMETER_ERROR, "bs_goodput_table: null argument");
+static int validate_table_args(bs_ctx_t ctx, const bs_slo* slo, const bs_scheduler_policy* policy,
+                               const bs_goodput_search* search, const bs_instance_config* cands, int n_cand) {
   if (n_cand < 1) return set_error(ctx, BS_PARAMETER_ERROR, "config table: no candidates");
-  int rc = validate_trace(ctx, *base);
-  if (rc) return rc;
   if (slo->ttft_ms <= 0.0 || slo->tpot_ms <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "slo: bounds must be > 0");
   if (slo->percentile <= 0.0 || slo->percentile > 1.0)
     return set_error(ctx, BS_PARAMETER_ERROR, "slo: percentile must be in (0,1]");
@@ -557,20 +538,60 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
     return set_error(ctx, BS_PARAMETER_ERROR, "scheduler: max_batch_requests must be >= 1");
   if (policy->kv_capacity_tokens < 1)
     return set_error(ctx, BS_PARAMETER_ERROR, "scheduler: kv_capacity_tokens must be >= 1");
+  return BS_OK;
+}
 
-  const long long n = base->n;
-  // Trace::mean_rps (workload.hpp:32-35) and k_max (placement.hpp:161-162)
-  const double base_rate = base->duration_ms <= 0.0 ? 0.0 : static_cast<double>(n) / (base->duration_ms / 1000.0);
-  const long long k_max = static_cast<long long>(std::floor(base_rate / search->tolerance_rps));
-  const int reps = search->probe_count;
-  for (int c = 0; c < n_cand; ++c) {
-    std::memset(&out[c], 0, sizeof(bs_table_entry));
-    out[c].config = cands[c];
-    out[c].g_c = cands[c].tp;
+int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, const bs_slo* slo,
+                     const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                     const bs_instance_config* cands, int n_cand, bs_table_entry* out) {
+  return bs_goodput_tables(ctx, models, base, 1, slo, policy, search, cands, n_cand, out);
+}
+
+int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, int n_tables, const bs_slo* slo,
+                      const bs_scheduler_policy* policy, const bs_goodput_search* search,
+                      const bs_instance_config* cands, int n_cand, bs_table_entry* out) {
+  if (!ctx || !models || !bases || !slo || !policy || !search || (!cands && n_cand > 0) || n_tables < 0 ||
+      (n_tables > 0 && !out))
+    return set_error(ctx, BS_PARAMETER_ERROR, "bs_goodput_table: null argument");
+  if (n_tables == 0) return BS_OK;
+  int rc = validate_table_args(ctx, slo, policy, search, cands, n_cand);
+  if (rc) return rc;
+  for (int t = 0; t < n_tables; ++t) {
+    rc = validate_trace(ctx, bases[t]);
+    if (rc) return rc;
   }
+  const int reps = search->probe_count;
   ctx->last_h2d = 0;
   ctx->last_d2h = 0;
-  if (k_max < 1 || n == 0) return BS_OK;  // r_c = 0 everywhere
+
+  // per table: Trace::mean_rps (workload.hpp:32-35) and k_max (placement.hpp:161-162)
+  std::vector<long long> k_max(n_tables), n_of(n_tables);
+  std::vector<double> rate(n_tables);
+  std::vector<TableDev> tabs(n_tables);
+  std::vector<MaskParams> mps(n_tables);
+  long long req_total = 0, stream_total = 0, kept_total = 0, probe_total = 0;
+  for (int t = 0; t < n_tables; ++t) {
+    const bs_trace& b = bases[t];
+    n_of[t] = b.n;
+    rate[t] = b.duration_ms <= 0.0 ? 0.0 : static_cast<double>(b.n) / (b.duration_ms / 1000.0);
+    k_max[t] = static_cast<long long>(std::floor(rate[t] / search->tolerance_rps));
+    for (int c = 0; c < n_cand; ++c) {
+      bs_table_entry& e = out[static_cast<size_t>(t) * n_cand + c];
+      std::memset(&e, 0, sizeof(bs_table_entry));
+      e.config = cands[c];
+      e.g_c = cands[c].tp;
+    }
+    const bool active = k_max[t] >= 1 && b.n > 0;  // otherwise r_c = 0 everywhere
+    const long long streams = active ? k_max[t] * reps : 0;
+    tabs[t] = TableDev{req_total, b.n, stream_total, kept_total, probe_total, streams, b.duration_ms};
+    mps[t] = MaskParams{b.n, static_cast<int>(active ? k_max[t] : 0), reps, search->tolerance_rps, rate[t],
+                        search->seed};
+    req_total += b.n;
+    stream_total += streams;
+    kept_total += streams * b.n;
+    probe_total += streams * n_cand;
+  }
+  if (probe_total == 0) return BS_OK;
 
   // per-candidate safety (no ModelError reachable): grids positive, axes
   // known, idle entry for tp present with at least one point
@@ -598,119 +619,110 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
     }
   }
   // decode scratch: at most min(max_batch_requests, n, kv / min_need) residents
-  long long min_need = INT64_MAX;
-  for (long long i = 0; i < n; ++i)
-    min_need = std::min<long long>(min_need, base->requests[i].input_len + base->requests[i].output_len);
-  long long heap_cap = std::min<long long>(policy->max_batch_requests, n);
-  heap_cap = std::min<long long>(heap_cap, std::max<long long>(1, policy->kv_capacity_tokens / std::max(1LL, min_need)));
+  long long heap_cap = 1;
+  for (int t = 0; t < n_tables; ++t) {
+    if (tabs[t].n_streams == 0) continue;
+    long long min_need = INT64_MAX;
+    for (long long i = 0; i < bases[t].n; ++i)
+      min_need = std::min<long long>(min_need, bases[t].requests[i].input_len + bases[t].requests[i].output_len);
+    long long hcap = std::min<long long>(policy->max_batch_requests, bases[t].n);
+    hcap = std::min<long long>(hcap, std::max<long long>(1, policy->kv_capacity_tokens / std::max(1LL, min_need)));
+    heap_cap = std::max(heap_cap, hcap);
+  }
   bool any_decode = false;
   for (int c = 0; c < n_cand; ++c) any_decode |= cands[c].phase == BS_PHASE_DECODE;
 
-  const long long n_streams = k_max * reps;
-  const long long n_probes = n_streams * n_cand;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  const size_t o_arr = 0, o_in = up(8ull * n), o_out = o_in + up(8ull * n), o_cand = o_out + up(8ull * n);
-  const size_t o_order = o_cand + up(sizeof(DCand) * n_cand) + up(4ull * n_cand);
-  const size_t in_bytes = o_order + up(4ull * n_cand * n_streams);
-  const size_t o_kept = in_bytes, o_kc = o_kept + up(4ull * n_streams * n), o_probe = o_kc + up(8ull * n_streams);
-  const size_t o_heap = o_probe + up(sizeof(ProbeOut) * n_probes);
-  const size_t heap_rows = any_decode ? static_cast<size_t>(std::max<long long>(n_probes, n_cand)) : 0;
-  const size_t o_en = o_heap + up(sizeof(Resident) * heap_rows * heap_cap);
-  const size_t total = o_en + up(sizeof(EnergyOut) * n_cand);
+  const size_t o_arr = 0, o_in = up(8ull * req_total), o_out = o_in + up(8ull * req_total);
+  const size_t o_cand = o_out + up(8ull * req_total);
+  const size_t o_tabs = o_cand + up(sizeof(DCand) * n_cand);
+  const size_t o_mps = o_tabs + up(sizeof(TableDev) * n_tables);
+  const size_t o_soff = o_mps + up(sizeof(MaskParams) * n_tables);
+  const size_t o_koff = o_soff + up(8ull * (n_tables + 1));
+  const size_t o_order = o_koff + up(8ull * n_tables);
+  const size_t in_bytes = o_order + up(sizeof(ProbeId) * probe_total);
+  const size_t o_kept = in_bytes, o_kc = o_kept + up(4ull * kept_total), o_probe = o_kc + up(8ull * stream_total);
+  const size_t o_heap = o_probe + up(sizeof(ProbeOut) * probe_total);
+  const size_t heap_rows = any_decode ? static_cast<size_t>(probe_total) : 0;
+  const size_t total = o_heap + up(sizeof(Resident) * heap_rows * heap_cap);
   char* d = static_cast<char*>(ctx->dev_buf(kSlotWork, total));
-  char* h = static_cast<char*>(ctx->host_buf(kSlotWork, in_bytes + sizeof(ProbeOut) * n_probes + sizeof(EnergyOut) * n_cand + 256));
+  char* h = static_cast<char*>(ctx->host_buf(kSlotWork, in_bytes + sizeof(ProbeOut) * probe_total + 256));
   if (!d || !h) return set_error(ctx, BS_CUDA_ERROR, "config table: allocation of %zu bytes failed", total);
   double* ha = reinterpret_cast<double*>(h + o_arr);
   long long* hi = reinterpret_cast<long long*>(h + o_in);
   long long* ho = reinterpret_cast<long long*>(h + o_out);
-  for (long long i = 0; i < n; ++i) {
-    ha[i] = base->requests[i].arrival_ms;
-    hi[i] = base->requests[i].input_len;
-    ho[i] = base->requests[i].output_len;
-  }
+  for (int t = 0; t < n_tables; ++t)
+    for (long long i = 0; i < bases[t].n; ++i) {
+      ha[tabs[t].req_off + i] = bases[t].requests[i].arrival_ms;
+      hi[tabs[t].req_off + i] = bases[t].requests[i].input_len;
+      ho[tabs[t].req_off + i] = bases[t].requests[i].output_len;
+    }
   std::memcpy(h + o_cand, hc.data(), sizeof(DCand) * n_cand);
-  {  // decode probes at high rate steps run longest (feasible ones never stop early): launch them first
-    int* ho_ = reinterpret_cast<int*>(h + o_order);
+  std::memcpy(h + o_tabs, tabs.data(), sizeof(TableDev) * n_tables);
+  std::memcpy(h + o_mps, mps.data(), sizeof(MaskParams) * n_tables);
+  {
+    long long* so = reinterpret_cast<long long*>(h + o_soff);
+    long long* ko = reinterpret_cast<long long*>(h + o_koff);
+    for (int t = 0; t < n_tables; ++t) {
+      so[t] = tabs[t].stream_off;
+      ko[t] = tabs[t].kept_off;
+    }
+    so[n_tables] = stream_total;
+  }
+  {  // launch order, across tables: decode probes at high rate steps run longest (feasible ones never
+     // stop early), then by rate step; long ones first
+    ProbeId* po = reinterpret_cast<ProbeId*>(h + o_order);
     long long w = 0;
+    long long kmax_all = 0;
+    for (int t = 0; t < n_tables; ++t) kmax_all = std::max(kmax_all, tabs[t].n_streams / std::max(1, reps));
     for (int pass = 0; pass < 2; ++pass)
-      for (long long k = k_max; k >= 1; --k)
-        for (int c = 0; c < n_cand; ++c) {
-          if ((cands[c].phase == BS_PHASE_DECODE) != (pass == 0)) continue;
-          for (int j = 0; j < reps; ++j) ho_[w++] = static_cast<int>(static_cast<long long>(c) * n_streams + (k - 1) * reps + j);
+      for (long long k = kmax_all; k >= 1; --k)
+        for (int t = 0; t < n_tables; ++t) {
+          if (k > tabs[t].n_streams / std::max(1, reps)) continue;
+          for (int c = 0; c < n_cand; ++c) {
+            if ((cands[c].phase == BS_PHASE_DECODE) != (pass == 0)) continue;
+            for (int j = 0; j < reps; ++j) po[w++] = ProbeId{t, c, (k - 1) * reps + j};
+          }
         }
   }
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->last_h2d = in_bytes;
   TraceDev tr{reinterpret_cast<const double*>(d + o_arr), reinterpret_cast<const long long*>(d + o_in),
-              reinterpret_cast<const long long*>(d + o_out), base->duration_ms};
-  MaskParams mp{n, static_cast<int>(k_max), reps, search->tolerance_rps, base_rate, search->seed};
+              reinterpret_cast<const long long*>(d + o_out), 0.0};
   int* dkept = reinterpret_cast<int*>(d + o_kept);
   long long* dkc = reinterpret_cast<long long*>(d + o_kc);
-  cudaEvent_t ev[4];
+  cudaEvent_t ev[3];
   for (auto& e : ev) BS_CUDA_TRY(ctx, cudaEventCreate(&e));
   BS_CUDA_TRY(ctx, cudaEventRecord(ev[0], ctx->stream));
-  mask_kernel<<<static_cast<unsigned>((n_streams + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0, ctx->stream>>>(
-      mp, dkept, dkc);
+  mask_kernel<<<static_cast<unsigned>((stream_total + kMaskWarps - 1) / kMaskWarps), kMaskWarps * 32, 0,
+                ctx->stream>>>(reinterpret_cast<const MaskParams*>(d + o_mps), n_tables,
+                               reinterpret_cast<const long long*>(d + o_soff),
+                               reinterpret_cast<const long long*>(d + o_koff), dkept, dkc);
   BS_LAUNCH_CHECK(ctx);
   BS_CUDA_TRY(ctx, cudaEventRecord(ev[1], ctx->stream));
   PolicyDev pol{policy->max_batch_tokens, policy->max_batch_requests, policy->kv_capacity_tokens, policy->chunking,
                 slo->ttft_ms, slo->tpot_ms};
   ProbeOut* dprobe = reinterpret_cast<ProbeOut*>(d + o_probe);
   Resident* dheap = reinterpret_cast<Resident*>(d + o_heap);
-  const DCand* dc = reinterpret_cast<const DCand*>(d + o_cand);
-  const int* dorder = reinterpret_cast<const int*>(d + o_order);
   const bool heap_smem = heap_cap <= 1024;
   const size_t smem4 = 4 * warp_scratch_bytes(static_cast<int>(heap_cap), heap_smem);
   BS_CUDA_TRY(ctx, set_smem_limit(reinterpret_cast<const void*>(probe_kernel), smem4));
-  probe_kernel<<<static_cast<unsigned>((n_probes * 32 + 127) / 128), 128, smem4, ctx->stream>>>(
-      models->dm, tr, dc, n_cand, static_cast<int>(n_streams), n, dkept, dkc, pol, dheap, static_cast<int>(heap_cap),
-      heap_smem ? 1 : 0, dorder, dprobe);
+  probe_kernel<<<static_cast<unsigned>((probe_total * 32 + 127) / 128), 128, smem4, ctx->stream>>>(
+      models->dm, tr, reinterpret_cast<const TableDev*>(d + o_tabs), reinterpret_cast<const DCand*>(d + o_cand),
+      dkept, dkc, pol, dheap, static_cast<int>(heap_cap), heap_smem ? 1 : 0,
+      reinterpret_cast<const ProbeId*>(d + o_order), probe_total, dprobe);
   BS_LAUNCH_CHECK(ctx);
   BS_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
   ProbeOut* hp = reinterpret_cast<ProbeOut*>(h + in_bytes);
-  BS_CUDA_TRY(ctx, cudaMemcpyAsync(hp, dprobe, sizeof(ProbeOut) * n_probes, cudaMemcpyDeviceToHost, ctx->stream));
+  BS_CUDA_TRY(ctx, cudaMemcpyAsync(hp, dprobe, sizeof(ProbeOut) * probe_total, cudaMemcpyDeviceToHost, ctx->stream));
   BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  ctx->last_d2h = sizeof(ProbeOut) * n_probes;
-
-  // replay each candidate's search; feasible(k) = every replicate passes
-  // (empty probes pass, SimulationError fails, ModelError propagates)
-  std::vector<int> cand_stream(n_cand, -1);
-  std::vector<SearchResult> sr(n_cand);
-  for (int c = 0; c < n_cand; ++c) {
-    auto outcome = [&](long long k) -> int {
-      for (int j = 0; j < reps; ++j) {
-        const ProbeOut& p = hp[static_cast<size_t>(c) * n_streams + (k - 1) * reps + j];
-        if (p.empty) continue;
-        if (p.status == BS_MODEL_ERROR) return -p.model_err;
-        if (p.status == BS_PARAMETER_ERROR) return -100;
-        if (p.status != BS_OK || !p.meets) return 0;
-      }
-      return 1;
-    };
-    sr[c] = replay_search(k_max, outcome);
-    if (sr[c].model_err == 100) return set_error(ctx, BS_CUDA_ERROR, "config table: device resident scratch too small");
-    if (sr[c].model_err) {
-      out[c].error_code = BS_MODEL_ERROR;
-      std::snprintf(out[c].error, sizeof out[c].error, "%s", model_err_msg(sr[c].model_err));
-      if (sr[c].model_err == 3)
-        std::snprintf(out[c].error, sizeof out[c].error, "idle model: tp %d not present", cands[c].tp);
-      continue;
-    }
-    out[c].k_star = sr[c].k_star;
-    out[c].r_c = static_cast<double>(sr[c].k_star) * search->tolerance_rps;  // placement.hpp:182, 197
-    out[c].saturated = sr[c].saturated ? 1 : 0;
-    if (out[c].r_c > 0.0) cand_stream[c] = static_cast<int>((sr[c].k_star - 1) * reps + 0);
-  }
-  // E_c at (k*, replicate 0) (placement.hpp:227-231): that probe passed, so
-  // it never stopped early and its run is exactly simulate_instance on the
-  // same probe trace -- reuse its energy accounting.  An empty probe trace
-  // only records the idle span [0, duration] (simulator.hpp:731-733).
+  ctx->last_d2h = sizeof(ProbeOut) * probe_total;
   {
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
     long long mx = 0, sum = 0;
-    for (long long i = 0; i < n_probes; ++i) {
+    for (long long i = 0; i < probe_total; ++i) {
       mx = std::max(mx, hp[i].events);
       sum += hp[i].events;
     }
@@ -722,33 +734,67 @@ int bs_goodput_table(bs_ctx_t ctx, bs_models_t models, const bs_trace* base, con
     ctx->n_stats = 5;
     for (auto& e : ev) cudaEventDestroy(e);
   }
-  for (int c = 0; c < n_cand; ++c) {
-    if (cand_stream[c] < 0) continue;
-    const ProbeOut& e = hp[static_cast<size_t>(c) * n_streams + cand_stream[c]];
-    if (e.empty) {
-      if (!idle_tp_ok[c]) {
-        out[c].error_code = BS_MODEL_ERROR;
-        out[c].r_c = 0.0;
-        out[c].k_star = 0;
-        out[c].saturated = 0;
-        std::snprintf(out[c].error, sizeof out[c].error, "idle model: tp %d not present", cands[c].tp);
-      } else {
-        out[c].error_code = -1;
-        std::snprintf(out[c].error, sizeof out[c].error, "no completed request at R_c");
+
+  for (int t = 0; t < n_tables; ++t) {
+    const TableDev& tb = tabs[t];
+    if (tb.n_streams == 0) continue;
+    const ProbeOut* hpt = hp + tb.probe_off;
+    bs_table_entry* ot = out + static_cast<size_t>(t) * n_cand;
+    // replay each candidate's search; feasible(k) = every replicate passes
+    // (empty probes pass, SimulationError fails, ModelError propagates)
+    for (int c = 0; c < n_cand; ++c) {
+      auto outcome = [&](long long k) -> int {
+        for (int j = 0; j < reps; ++j) {
+          const ProbeOut& p = hpt[static_cast<size_t>(c) * tb.n_streams + (k - 1) * reps + j];
+          if (p.empty) continue;
+          if (p.status == BS_MODEL_ERROR) return -p.model_err;
+          if (p.status == BS_PARAMETER_ERROR) return -100;
+          if (p.status != BS_OK || !p.meets) return 0;
+        }
+        return 1;
+      };
+      const SearchResult sr = replay_search(k_max[t], outcome);
+      if (sr.model_err == 100) return set_error(ctx, BS_CUDA_ERROR, "config table: device resident scratch too small");
+      if (sr.model_err) {
+        ot[c].error_code = BS_MODEL_ERROR;
+        std::snprintf(ot[c].error, sizeof ot[c].error, "%s", model_err_msg(sr.model_err));
+        if (sr.model_err == 3)
+          std::snprintf(ot[c].error, sizeof ot[c].error, "idle model: tp %d not present", cands[c].tp);
+        continue;
       }
-      continue;
+      ot[c].k_star = sr.k_star;
+      ot[c].r_c = static_cast<double>(sr.k_star) * search->tolerance_rps;  // placement.hpp:182, 197
+      ot[c].saturated = sr.saturated ? 1 : 0;
+      if (ot[c].r_c <= 0.0) continue;
+      // E_c at (k*, replicate 0) (placement.hpp:227-231): that probe passed, so it never stopped early
+      // and its run is exactly simulate_instance on the same probe trace -- reuse its energy accounting.
+      // An empty probe trace only records the idle span [0, duration] (simulator.hpp:731-733).
+      const ProbeOut& e = hpt[static_cast<size_t>(c) * tb.n_streams + (sr.k_star - 1) * reps];
+      if (e.empty) {
+        if (!idle_tp_ok[c]) {
+          ot[c].error_code = BS_MODEL_ERROR;
+          ot[c].r_c = 0.0;
+          ot[c].k_star = 0;
+          ot[c].saturated = 0;
+          std::snprintf(ot[c].error, sizeof ot[c].error, "idle model: tp %d not present", cands[c].tp);
+        } else {
+          ot[c].error_code = -1;
+          std::snprintf(ot[c].error, sizeof ot[c].error, "no completed request at R_c");
+        }
+        continue;
+      }
+      if (e.status != BS_OK || !e.meets) return set_error(ctx, BS_CUDA_ERROR, "config table: inconsistent probe at k*");
+      // energy_per_request (placement.hpp:205-213)
+      if (e.completed < 1) {
+        ot[c].error_code = -1;
+        std::snprintf(ot[c].error, sizeof ot[c].error, "no completed request at R_c");
+        continue;
+      }
+      double en = e.busy_j;
+      if (cands[c].phase == BS_PHASE_PREFILL) en = en + e.idle_j;
+      ot[c].e_c = en / static_cast<double>(e.completed);
+      ot[c].has_e_c = 1;
     }
-    if (e.status != BS_OK || !e.meets) return set_error(ctx, BS_CUDA_ERROR, "config table: inconsistent probe at k*");
-    // energy_per_request (placement.hpp:205-213)
-    if (e.completed < 1) {
-      out[c].error_code = -1;
-      std::snprintf(out[c].error, sizeof out[c].error, "no completed request at R_c");
-      continue;
-    }
-    double en = e.busy_j;
-    if (cands[c].phase == BS_PHASE_PREFILL) en = en + e.idle_j;
-    out[c].e_c = en / static_cast<double>(e.completed);
-    out[c].has_e_c = 1;
   }
   return BS_OK;
 }

@@ -1726,11 +1726,37 @@ def _context_pool(device: int, n: int) -> list:
         return pool[:n]
 
 
+def build_config_tables(bases, candidates, slo: SLOSpec, models: ModelSet, policy: SchedulerPolicy,
+                        search: GoodputSearch, device: Device | None = None) -> list:
+    """build_config_table for several probe traces (e.g. consecutive windows)
+    in one device call (bs_goodput_tables): every table's probes share one
+    grid, long probes first, so a stream of tables is bound by the device's
+    throughput rather than by each table's longest probe in turn."""
+    bases = list(bases)
+    if not candidates:
+        raise ParameterError("config table: no candidates")
+    if not bases:
+        return []
+    dev = device or default_device()
+    keep: list = []
+    trs = (_abi.bs_trace * len(bases))()
+    for i, b in enumerate(bases):
+        trs[i] = c_trace(b, keep)
+    cs, cp, cg = c_slo(slo), c_policy(policy), c_search(search)
+    cands = c_candidates(candidates)
+    n = len(candidates)
+    out = (_abi.bs_table_entry * (n * len(bases)))()
+    dev.check(dev._lib.bs_goodput_tables(dev.handle, dev.models(models), trs, len(bases), C.byref(cs), C.byref(cp),
+                                         C.byref(cg), cands, n, out))
+    return [[entry_from_c(out[t * n + i]) for i in range(n)] for t in range(len(bases))]
+
+
 def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, models: ModelSet,
-                   device: Device | None = None, plan_workers: int = 16) -> ExperimentResult:
+                   device: Device | None = None) -> ExperimentResult:
     """run_experiment (runner.hpp:155-172): window w is planned from window
-    w-1 (the first from itself) with the GPU config table + ILP; then every
-    (window, policy) replay runs in ONE bs_replay call (windows are
+    w-1 (the first from itself): every window's config table in ONE
+    bs_goodput_tables call, then the ILP and the max-throughput baseline;
+    then every (window, policy) replay in ONE bs_replay call (windows are
     independent once planned).  Reports, SLO verdicts and their order follow
     the reference."""
     dev = device or default_device()
@@ -1747,16 +1773,24 @@ def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, 
 
     t0 = _time.perf_counter()
     histories = [windows[0] if w == 0 else windows[w - 1] for w in range(len(windows))]
-    workers = min(len(windows), plan_workers)
-    if workers <= 1:
-        plans = [plan_window_policies(h, cfg, models, dev) for h in histories]
-    else:
-        from concurrent.futures import ThreadPoolExecutor
-
-        pool = _context_pool(dev.device, workers)
-        with ThreadPoolExecutor(workers) as ex:
-            plans = list(ex.map(lambda a: plan_window_policies(a[1], cfg, models, pool[a[0] % workers]),
-                                enumerate(histories)))
+    # plan_window (placement.hpp:558-582) for every window, with all the
+    # windows' config tables in ONE device call
+    for h in histories:
+        h.validate()
+        if not h.requests:
+            raise ParameterError("plan_window: empty history")
+    opts = cfg.plan
+    predicted = [predict_next_window(h) for h in histories]
+    probes = [opts.probe_trace if opts.probe_trace is not None else p for p in predicted]
+    candidates = enumerate_candidates(cfg.ladder, cfg.tp_options)
+    tables = build_config_tables(probes, candidates, cfg.slo, models, opts.policy, opts.search, dev)
+    plans = []
+    for p, table in zip(predicted, tables):
+        target = peak_rps(p, opts.peak_subwindow_s)
+        ilp = solve_placement(PlacementProblem(table, cfg.total_gpus, target, opts.alpha), dev)
+        mx = solve_max_throughput(PlacementProblem(table, cfg.total_gpus, target, opts.alpha), cfg.ladder.max_mhz(),
+                                  dev)
+        plans.append(WindowPlans(target, table, ilp, mx))
     scs, keys = [], []
     for w, win in enumerate(windows):
         for pol in policies:

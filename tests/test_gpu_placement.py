@@ -231,3 +231,25 @@ def test_config_table_llama_matches_reference(gpu_device, ref_lib, seed):
     assert sum(e.usable() for e in got) > 8
     plan = P.solve_placement(P.PlacementProblem(got, 16, P.peak_rps(base, 10.0), 0.05))
     assert plan.gpus_used <= 16
+
+
+def test_batched_tables_match_reference(gpu_device, ref_lib):
+    """bs_goodput_tables: several windows' tables in one probe grid (with an
+    empty window and a window too thin for any rate step) equal the
+    reference's build_config_table of each window, entry for entry."""
+    lad = W.ladder(8)
+    m = W.llama_models(lad)
+    day = P.gen_gamma_trace(10.0, 0.5, 3 * 60_000.0, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)),
+                            19)
+    wins = P.split_windows(day, 60_000.0)
+    wins.append(P.Trace([], 60_000.0))
+    wins.append(P.Trace([P.Request(0, 10.0, 300, 20)], 60_000.0))
+    cands = P.enumerate_candidates(lad, [1, 2, 4])
+    pol = P.SchedulerPolicy(max_batch_tokens=2048)
+    slo = P.SLOSpec(600.0, 100.0)
+    for search in (P.GoodputSearch(), P.GoodputSearch(probe_count=2, tolerance_rps=0.5)):
+        tables = P.build_config_tables(wins, cands, slo, m, pol, search, gpu_device)
+        assert len(tables) == len(wins)
+        for w, table in zip(wins, tables):
+            want = _ref_table(ref_lib, m, w, slo, pol, search, cands)
+            assert [_cmp(e) for e in table] == [_cmp(e) for e in want]
