@@ -214,7 +214,11 @@ struct TableDev {
   double duration_ms;
 };
 
-__global__ void probe_kernel(DModels m, TraceDev tr, const TableDev* tabs, const DCand* cands, const int* kept,
+#ifndef BS_PROBE_MINB
+#define BS_PROBE_MINB 3  // resident CTAs per SM the probe kernel is register-budgeted for (throughput of a stream of tables over the latency of one)
+#endif
+
+__global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, TraceDev tr, const TableDev* tabs, const DCand* cands, const int* kept,
                              const long long* kept_count, PolicyDev pol, Resident* heaps, int heap_cap,
                              int heap_in_smem, const ProbeId* order, long long n_probes, ProbeOut* out) {
   extern __shared__ __align__(16) unsigned char smem[];
