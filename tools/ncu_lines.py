@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-usage: python tools_ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [LIB.so] [TOP]
+usage: python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [LIB.so] [TOP]
 
 ncu's source page gives per-SASS-instruction samples with runtime
 addresses; nvdisasm -g on the library's cubin gives per-instruction source
