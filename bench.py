@@ -225,7 +225,7 @@ def _barrier(world: int):
         dist.barrier()
 
 
-def bench_c3(dev, with_cpu: bool, repeats: int = 3) -> dict:
+def bench_c3(dev, with_cpu: bool, repeats: int = 3, rank: int = 0, world: int = 1, local: int = 0) -> dict:
     """configs[2]: coarse-tier placement for a 16-GPU cluster over a bursty
     1-hour window: the config table (goodput search + E_c of every
     candidate, build_config_table placement.hpp:240-260) + the ILP."""
@@ -258,10 +258,22 @@ def bench_c3(dev, with_cpu: bool, repeats: int = 3) -> dict:
     day = P.gen_gamma_trace(12.0, 0.5, 4 * 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)),
                             7)
     wins = P.split_windows(day, 3600e3)
-    P.build_config_tables(wins, cands, slo, models, pol, search, dev)  # warm-up (one probe grid for all windows)
-    t0 = time.perf_counter()
-    P.build_config_tables(wins, cands, slo, models, pol, search, dev)
-    t_stream = time.perf_counter() - t0
+    if world > 1:  # windows sharded across ranks, tables all-gathered
+        from paper_2602_18755_b200 import sharding as S
+
+        lo, hi = S.shard_bounds(len(wins), rank, world)
+        P.build_config_tables(wins[lo:hi], cands, slo, models, pol, search, dev)  # warm-up
+        _barrier(world)
+        t0 = time.perf_counter()
+        mine = P.build_config_tables(wins[lo:hi], cands, slo, models, pol, search, dev)
+        t_stream = _dist_max(time.perf_counter() - t0, world, local)
+        gathered = S.gather_tables(mine, len(wins), device=f"cuda:{local}")
+        assert len(gathered) == len(wins)
+    else:
+        P.build_config_tables(wins, cands, slo, models, pol, search, dev)  # warm-up (one probe grid for all windows)
+        t0 = time.perf_counter()
+        P.build_config_tables(wins, cands, slo, models, pol, search, dev)
+        t_stream = time.perf_counter() - t0
     out = {"workload": "C3: bursty 1-hour gamma(0.5) windows at 12 rps, 128 candidates per window (2 phases x "
                        "TP{1,2,4,8} x 16 rungs), max_batch_tokens 2048, G = 16", "requests": len(base.requests),
            "value": len(wins) * len(cands) / t_stream, "unit": "placement configs/s",
@@ -532,8 +544,7 @@ def run_extras(args, dev, rank, world, local) -> dict:
     out = {}
     for k in todo:
         if k == "c3":
-            if world == 1:
-                out["c3_placement"] = bench_c3(dev, with_cpu)
+            out["c3_placement"] = bench_c3(dev, with_cpu, rank=rank, world=world, local=local)
         elif k == "c4":
             out["c4_replay"] = bench_c4(dev, rank, world, local, args.c4_scenarios, with_cpu)
         elif k == "c4x":

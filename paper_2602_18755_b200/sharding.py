@@ -14,6 +14,9 @@ is at the end:
   over the code among the ranks holding that objective (others contribute
   INT64_MAX).  This is the exhaustive-MPC tie rule (dvfs.hpp:243: smallest
   objective, then lexicographically smallest assignment = smallest code).
+* ``gather_tables``: config tables built for a rank's shard of windows
+  (C3 / run_experiment planning), all-gathered as fixed-size rows (SURVEY.md
+  §8e: "ncclAllGather of table slices").
 * ``max_over_ranks``: the timing rule of bench.py (max of per-rank device
   times).
 
@@ -102,3 +105,50 @@ def max_over_ranks(value: float, group=None, device: str | torch.device = "cpu")
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+_ENTRY_FIELDS = 8  # phase, tp, freq bits, r_c bits, e_c bits (or -1), g_c, flags, k*
+_ERRORS = ["", "latency model returned non-positive value", "power model returned non-positive value",
+           "idle model: tp {tp} not present", "no completed request at R_c", "grid: unknown axis",
+           "idle model: empty frequency set"]
+
+
+def _bits(x: float) -> int:
+    return struct.unpack("<q", struct.pack("<d", float(x)))[0]
+
+
+def _pack_entry(e) -> list:
+    """flags: bit 0 saturated, bits 1.. the entry's error text (an index into
+    the messages build_config_table can produce)."""
+    kind = 0
+    if e.error:
+        kind = next((i for i, m in enumerate(_ERRORS) if i and m.format(tp=e.config.tp) == e.error), -1)
+        if kind < 0:
+            raise ValueError(f"gather_tables: unexpected entry error {e.error!r}")
+    return [int(e.config.phase), int(e.config.tp), _bits(e.config.base_freq_mhz), _bits(e.r_c),
+            _bits(e.e_c) if e.e_c is not None else -1, int(e.g_c), (1 if e.saturated else 0) | (kind << 1),
+            int(e.k_star)]
+
+
+def _unpack_entry(row):
+    from . import pdsim as P
+
+    f = lambda q: struct.unpack("<d", struct.pack("<q", int(q)))[0]  # noqa: E731
+    phase, tp, fb, rb, eb, g, flags, ks = (int(x) for x in row)
+    return P.ConfigTableEntry(P.InstanceConfig(P.Phase(phase), tp, f(fb)), f(rb), None if eb == -1 else f(eb), g,
+                              bool(flags & 1), _ERRORS[flags >> 1].format(tp=tp), ks)
+
+
+def gather_tables(local_tables: list, n_tables: int, group=None, device: str | torch.device = "cpu") -> list:
+    """All-gather config tables built for this rank's shard
+    (shard_bounds(n_tables, rank, world)) of n_tables windows; every table
+    has the same candidate list.  Returns all n_tables tables in window
+    order on every rank (every field, error text included, round-trips)."""
+    n_cand = len(local_tables[0]) if local_tables else 0
+    n_cand = int(max_over_ranks(float(n_cand), group, device))
+    flat = [_pack_entry(e) for t in local_tables for e in t]
+    rows = torch.tensor(flat, dtype=torch.int64, device=device).reshape(len(local_tables), n_cand * _ENTRY_FIELDS) \
+        if flat else torch.zeros((0, n_cand * _ENTRY_FIELDS), dtype=torch.int64, device=device)
+    allrows = gather_rows(rows, n_tables, group)
+    return [[_unpack_entry(allrows[i, c * _ENTRY_FIELDS:(c + 1) * _ENTRY_FIELDS].tolist()) for c in range(n_cand)]
+            for i in range(n_tables)]

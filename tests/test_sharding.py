@@ -135,3 +135,72 @@ def test_world2_gloo_gather_and_sliced_argmin(oracle_lib):
         assert outs[0][2] == (whole.objective_w, whole.best_code)
     else:
         assert outs[0][2] == (None, None)
+
+
+def _table_worker(rank: int, world: int, port: int, outq):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2602_18755_b200 import _abi as A
+        from paper_2602_18755_b200 import pdsim as P
+        from paper_2602_18755_b200 import workloads as W
+
+        ref = oracle.load_ref()
+        lad = W.ladder(5)
+        m = W.llama_models(lad)
+        day = P.gen_gamma_trace(6.0, 0.5, 5 * 20_000.0,
+                                P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), 4)
+        wins = P.split_windows(day, 20_000.0)
+        cands = P.enumerate_candidates(lad, [2, 4])
+        lo, hi = S.shard_bounds(len(wins), rank, world)
+        keep: list = []
+        cm = P.c_model_set(m, keep)
+        local = []
+        for w in wins[lo:hi]:  # the CPU reference stands in for each rank's device here
+            out = (A.bs_table_entry * len(cands))()
+            assert ref.ref_config_table(C.byref(cm), C.byref(P.c_trace(w, keep)), C.byref(P.c_slo(P.SLOSpec())),
+                                        C.byref(P.c_policy(P.SchedulerPolicy(max_batch_tokens=1024))),
+                                        C.byref(P.c_search(P.GoodputSearch())), P.c_candidates(cands), len(cands),
+                                        out) == 0
+            local.append([P.entry_from_c(out[i]) for i in range(len(cands))])
+        tables = S.gather_tables(local, len(wins))
+        outq.put((rank, [[(e.config.tp, e.r_c, e.e_c, e.saturated, e.error) for e in t] for t in tables]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gloo_gather_tables(ref_lib):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_table_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert outs[0][1] == outs[1][1] and len(outs[0][1]) == 5
+    # single process: the same five tables
+    from paper_2602_18755_b200 import _abi as A
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import workloads as W
+
+    lad = W.ladder(5)
+    m = W.llama_models(lad)
+    day = P.gen_gamma_trace(6.0, 0.5, 5 * 20_000.0, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), 4)
+    cands = P.enumerate_candidates(lad, [2, 4])
+    keep: list = []
+    cm = P.c_model_set(m, keep)
+    want = []
+    for w in P.split_windows(day, 20_000.0):
+        out = (A.bs_table_entry * len(cands))()
+        assert ref_lib.ref_config_table(C.byref(cm), C.byref(P.c_trace(w, keep)), C.byref(P.c_slo(P.SLOSpec())),
+                                        C.byref(P.c_policy(P.SchedulerPolicy(max_batch_tokens=1024))),
+                                        C.byref(P.c_search(P.GoodputSearch())), P.c_candidates(cands), len(cands),
+                                        out) == 0
+        want.append([(e.config.tp, e.r_c, e.e_c, e.saturated, e.error)
+                     for e in (P.entry_from_c(out[i]) for i in range(len(cands)))])
+    assert outs[0][1] == want
