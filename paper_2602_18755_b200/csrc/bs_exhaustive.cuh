@@ -174,6 +174,47 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
   return base + __popc(mask & ((1u << lane) - 1u));
 }
 
+// Block-aggregated appends to two counters (one atomic per counter per
+// block instead of per warp): each lane that wants a slot gets one.  Every
+// thread of the block must call it.
+__device__ __forceinline__ void block_append2(unsigned long long* c0, bool w0, unsigned long long* c1, bool w1,
+                                              unsigned long long* s0, unsigned long long* s1) {
+  __shared__ unsigned wc0[32], wc1[32];
+  __shared__ unsigned long long b0, b1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned m0 = __ballot_sync(0xffffffffu, w0), m1 = __ballot_sync(0xffffffffu, w1);
+  if (lane == 0) {
+    wc0[warp] = __popc(m0);
+    wc1[warp] = __popc(m1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the per-warp counts, then one atomic per counter
+    unsigned v0 = threadIdx.x < nw ? wc0[threadIdx.x] : 0u, v1 = threadIdx.x < nw ? wc1[threadIdx.x] : 0u;
+    unsigned i0 = v0, i1 = v1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned a = __shfl_up_sync(0xffffffffu, i0, o), b = __shfl_up_sync(0xffffffffu, i1, o);
+      if (threadIdx.x >= o) {
+        i0 += a;
+        i1 += b;
+      }
+    }
+    if (threadIdx.x == 31) {
+      b0 = i0 ? atomicAdd(c0, static_cast<unsigned long long>(i0)) : 0ull;
+      b1 = i1 ? atomicAdd(c1, static_cast<unsigned long long>(i1)) : 0ull;
+    }
+    if (threadIdx.x < nw) {
+      wc0[threadIdx.x] = i0 - v0;
+      wc1[threadIdx.x] = i1 - v1;
+    }
+  }
+  __syncthreads();
+  const unsigned below = (1u << lane) - 1u;
+  *s0 = b0 + wc0[warp] + __popc(m0 & below);
+  *s1 = b1 + wc1[warp] + __popc(m1 & below);
+  __syncthreads();  // the shared slots are reused by the next call
+}
+
 // Level k: every (depth-k node, digit) pair; feasible children at depth
 // k + 1 go to the next list, or to the final list at their problem's FD.
 __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl, Frontier in,
@@ -204,8 +245,8 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
         to_final = (k + 1) == T->K - sweep_levels(T->K, nc);
       }
     }
-    const unsigned long long sf = warp_append(&ctl->final_count, ok && to_final);
-    const unsigned long long so = warp_append(&ctl->level_count[k + 1], ok && !to_final);
+    unsigned long long sf, so;
+    block_append2(&ctl->final_count, ok && to_final, &ctl->level_count[k + 1], ok && !to_final, &sf, &so);
     if (ok && to_final) {
       if (sf < cap_final) {
         fin.d[sf] = d;
