@@ -174,6 +174,25 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
   return base + __popc(mask & ((1u << lane) - 1u));
 }
 
+// Number of candidates at level k whose switched step passes meets_slo's
+// check from parent clock t (t unused at level 0, where the keys are T1):
+// by monotonicity of correctly rounded add/subtract in the step, the
+// passing candidates form a prefix of the sorted order ord[k].
+__device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, int k, int nc, double t) {
+  const double m = T->minarr[k], ttft = T->ttft;
+  const double* __restrict__ sb = T->sb[k];
+  int lo = 0, hi = nc;  // first failing position
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const double tl = k == 0 ? sb[mid] : __dadd_rn(t, sb[mid]);
+    if (__dsub_rn(tl, m) > ttft)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
 // Block-aggregated appends to two counters (one atomic per counter per
 // block instead of per warp): each lane that wants a slot gets one.  Every
 // thread of the block must call it.
@@ -243,6 +262,13 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
         ok = child_state(T, k, in.t[node], in.num[node], in.den[node], in.last[node], f, ct, cn, cd);
         cc = in.code[node] * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
         to_final = (k + 1) == T->K - sweep_levels(T->K, nc);
+        // a final node none of whose children passes meets_slo has no feasible
+        // leaf (meets_slo stops at the first violation): drop it here
+        if (ok && to_final && T->sorted_ok && k + 1 < T->K) {
+          const int kk = k + 1;
+          ok = feasible_prefix(T, kk, nc, ct) > 0 ||
+               !(__dsub_rn(__dadd_rn(ct, T->B0[kk][f]), T->minarr[kk]) > T->ttft);
+        }
       }
     }
     unsigned long long sf, so;
@@ -340,25 +366,6 @@ __device__ __forceinline__ void sweep_last(const DTables* __restrict__ T, int k,
       set_threshold(a, hint);
     }
   }
-}
-
-// Number of candidates at level k whose switched step passes meets_slo's
-// check from parent clock t (t unused at level 0, where the keys are T1):
-// by monotonicity of correctly rounded add/subtract in the step, the
-// passing candidates form a prefix of the sorted order ord[k].
-__device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, int k, int nc, double t) {
-  const double m = T->minarr[k], ttft = T->ttft;
-  const double* __restrict__ sb = T->sb[k];
-  int lo = 0, hi = nc;  // first failing position
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    const double tl = k == 0 ? sb[mid] : __dadd_rn(t, sb[mid]);
-    if (__dsub_rn(tl, m) > ttft)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  return lo;
 }
 
 // Calls fn(f, ct, cn, cd) for every child of (t, num, den, last) at level k
