@@ -88,9 +88,10 @@ __device__ __forceinline__ Resident heap_pop(Resident* h, int& n) {
 // whose frac is exactly 0 (a fixed value on a knot -- ladder rungs always
 // are) or that has a single knot contributes the factor 1.0 - 0 = 1.0 to
 // every low corner and weight 0 to every high corner, which
-// NdGrid::interpolate then skips (perfmodel.hpp:183-190); dropping such axes
-// therefore leaves every weight product, the corner order and the sum
-// bit-identical while the corner loop shrinks from 2^D to 2^(active axes).
+// NdGrid::interpolate then skips (perfmodel.hpp:183-190); at the last knot
+// (frac exactly 1) the roles swap.  Dropping such axes therefore leaves every
+// weight product, the corner order and the sum bit-identical while the
+// corner loop shrinks from 2^D to 2^(active axes).
 // sum_len / n_requests are bracketed per call by binary search (the index
 // std::upper_bound finds).
 struct FastGrid {
@@ -149,6 +150,12 @@ __device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double fre
       bracket(g.knots[d], g.n[d], g.role[d] == BS_AXIS_TP ? static_cast<double>(tp) : freq, &lo, &fr);
       if (fr == 0.0) {  // on a knot: drop the axis, keep its lo in the base offset
         f.base += lo * stride[d];
+        continue;
+      }
+      if (fr == 1.0) {  // on the axis' last knot (hi = lo + 1, frac 1): every low corner has weight
+        // 1 - 1 = 0 and is skipped, every high corner's weight is multiplied by exactly 1.0 -- drop
+        // the axis with its high knot in the base offset (same values, same corner order)
+        f.base += (lo + 1) * stride[d];
         continue;
       }
     }
