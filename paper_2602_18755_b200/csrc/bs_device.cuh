@@ -193,6 +193,8 @@ struct DProblem {
   int cfg;
   int run_ncomp;      // completing members of the running batch (when n_run < 0)
   double run_minarr;  // their smallest arrival, +inf if none (when n_run < 0)
+  int fgi;            // index of the problem's (configuration, tp) reduced-grid pair
+  int _pad2;
 };
 
 // Per-problem projection + (k, f) tables, built on device.

@@ -82,7 +82,7 @@ __host__ __device__ inline FinalList final_at(void* base, unsigned long long cap
 
 __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
                                                                const DWaiting* W, const DRunning* R, DTables* tables,
-                                                               ExCtl* ctl, int n) {
+                                                               ExCtl* ctl, int n, const DFastPair* fg) {
   __shared__ int s_status;
   const int d = blockIdx.x;
   if (d >= n) return;
@@ -97,7 +97,9 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const 
   const DProblem pr = probs[d];
   const DMpcCfg& c = cfgs[pr.cfg];
   DTables* T = &tables[d];
-  build_tables(m, pr, c, W + pr.wait_off, R + pr.run_off, T, &s_status);
+  const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
+  build_tables(m, pr, c, W + pr.wait_off, R + pr.run_off, T, &s_status, fp ? fp->lat : nullptr,
+               fp ? fp->pw : nullptr, fp && fp->share);
   if (threadIdx.x == 0) {
     int st = s_status;
     if (st == BS_OK) {

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -43,6 +44,8 @@ struct bs_models_s {
   void* dmem = nullptr;  // one allocation: knots, values, idle arrays
   size_t bytes = 0;
   bool grid_positive[4] = {false, false, false, false};  // every value > 0 and finite
+  std::vector<double> hbuf;  // host mirror of dmem's doubles
+  bs::DGrid hgrid[4]{};      // dm.grid with pointers into hbuf (host-side FastGrid construction)
 };
 
 namespace bs {
@@ -61,6 +64,8 @@ enum Slot : int {
   kSlotCounts = 9,
   kSlotMisc = 10,
   kSlotMisc2 = 11,
+  kSlotReplay = 12,
+  kSlotFastGrids = 13,
 };
 
 int set_error(bs_ctx_t ctx, int code, const char* fmt, ...);
@@ -104,6 +109,7 @@ struct PackedProblems {
   size_t h2d_bytes = 0;
   int max_horizon = 0;
   int max_nc = 0;
+  std::vector<std::pair<int, int>> fg_pairs;  // distinct (configuration, tp); DProblem::fgi indexes them
   void rebase(char* b) {
     base = b;
     cfgs = reinterpret_cast<DMpcCfg*>(b + off_cfg);

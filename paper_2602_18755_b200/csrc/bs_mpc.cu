@@ -98,7 +98,7 @@ __host__ __device__ inline size_t greedy_warp_bytes(int max_h, int max_nc) {
 __global__ void __launch_bounds__(kGreedyWarps * 32) greedy_kernel(DModels m, const DMpcCfg* cfgs,
                                                                   const DProblem* probs, const DWaiting* W,
                                                                   const DRunning* R, DMpcOut* out, DLevel* levels,
-                                                                  int n, int max_h, int max_nc) {
+                                                                  int n, int max_h, int max_nc, const DFastPair* fg) {
   extern __shared__ __align__(16) unsigned char gdsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int d = blockIdx.x * kGreedyWarps + wib;
@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) greedy_kernel(DModels m, co
   const DMpcCfg& c = cfgs[pr.cfg];
   if (lane == 0) wtables_bind(S.T, tab, c.horizon, c.nc);
   __syncwarp();
+  const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
   greedy_warp(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o, levels + static_cast<size_t>(d) * BS_MAX_LEVELS,
-              nullptr, nullptr);
+              fp ? fp->lat : nullptr, fp ? fp->pw : nullptr, fp && fp->share);
   if (lane == 0) out[d] = *o;
 }
 
@@ -237,6 +238,8 @@ struct MpcRun {
   DLevel* dLv = nullptr;
   int bfs_grid = 0, sweep_grid = 0;
   ExCtl ctl_host{};  // counters of an overflowed run (exact totals of the levels before the first overflow)
+  const DFastPair* dFG = nullptr;       // reduced grids per (configuration, tp) pair (pk.fg_pairs)
+  std::vector<DFastPair> hFG;           // their host build
   cudaEvent_t ev[kNumEvents] = {};
   bool have_events = false;
 };
@@ -347,6 +350,31 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
   return BS_OK;
 }
 
+// The reduced grids of every (configuration, tp) pair of a packed batch,
+// built on the host from the models' mirror (fast_grid2) with device
+// pointers; copied into `dst` (device) on the context stream.
+int upload_fast_pairs(bs_ctx_t ctx, bs_models_t models, MpcRun* run, DFastPair* dst) {
+  const auto& pairs = run->pk.fg_pairs;
+  run->hFG.assign(pairs.size(), DFastPair{});
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    const DMpcCfg& c = run->hc[pairs[p].first];
+    const int tp = pairs[p].second;
+    DFastPair& fp = run->hFG[p];
+    std::memset(&fp, 0, sizeof fp);
+    fp.share = 1;
+    for (int f = 0; f < c.nc; ++f) {
+      fp.lat[f] = fast_grid2(models->hgrid[0], models->dm.grid[0], tp, c.cand[f]);
+      fp.pw[f] = fast_grid2(models->hgrid[2], models->dm.grid[2], tp, c.cand[f]);
+      if (!fast_same_brackets(fp.lat[0], fp.lat[f]) || !fast_same_brackets(fp.pw[0], fp.pw[f])) fp.share = 0;
+    }
+  }
+  if (!pairs.empty())
+    BS_CUDA_TRY(ctx, cudaMemcpyAsync(dst, run->hFG.data(), sizeof(DFastPair) * pairs.size(), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+  run->dFG = pairs.empty() ? nullptr : dst;
+  return BS_OK;
+}
+
 #define BS_REC(i)                                                         \
   do {                                                                    \
     if (timing) BS_CUDA_TRY(ctx, cudaEventRecord(run->ev[i], ctx->stream)); \
@@ -374,7 +402,7 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
                                           static_cast<int>(smem)));
     greedy_kernel<<<(n + kGreedyWarps - 1) / kGreedyWarps, kGreedyWarps * 32, smem, ctx->stream>>>(
         models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running, run->dOut, run->dLv, n, pk.max_horizon,
-        pk.max_nc);
+        pk.max_nc, run->dFG);
     BS_LAUNCH_CHECK(ctx);
     BS_REC(1);
     return BS_OK;
@@ -386,7 +414,7 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   const Frontier lev[2] = {frontier_at(run->dLev[0], run->cap_level), frontier_at(run->dLev[1], run->cap_level)};
   const FinalList fin = final_at(run->dFin, run->cap_final);
   prepare_kernel<<<n, kPrepThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
-                                                      run->dT, run->dCtl, n);
+                                                      run->dT, run->dCtl, n, run->dFG);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
   seed_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, n, run->dBest, run->dFeas, run->dCtl, lev[0], fin,
@@ -453,6 +481,14 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
     ctx->last_h2d = run.pk.h2d_bytes;
     ctx->last_d2h = 0;
     if (n == 0) return BS_OK;
+    {
+      DFastPair* dfg = static_cast<DFastPair*>(
+          ctx->dev_buf(kSlotFastGrids, sizeof(DFastPair) * std::max<size_t>(run.pk.fg_pairs.size(), 1)));
+      if (!dfg) return set_error(ctx, BS_CUDA_ERROR, "mpc: allocation of the reduced grids failed");
+      rc = upload_fast_pairs(ctx, models, &run, dfg);
+      if (rc) return rc;
+      ctx->last_h2d += sizeof(DFastPair) * run.pk.fg_pairs.size();
+    }
     if (mode == kExhaustive) {
       const ExLayout L = ex_layout(run, 0);
       char* base = static_cast<char*>(ctx->dev_buf(kSlotWork, L.total));
@@ -565,7 +601,8 @@ int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cf
     delete plan;
     return rc;
   }
-  const size_t blob = up256(run.pk.h2d_bytes);
+  const size_t fg_bytes = up256(sizeof(DFastPair) * run.pk.fg_pairs.size());
+  const size_t blob = up256(run.pk.h2d_bytes) + fg_bytes;
   size_t total = blob, o_o = 0, o_l = 0;
   ExLayout L;
   if (mode == kExhaustive) {
@@ -589,6 +626,12 @@ int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cf
     return set_error(ctx, BS_CUDA_ERROR, "mpc plan: staging copy failed");
   }
   run.pk.rebase(m);
+  if (upload_fast_pairs(ctx, models, &run, reinterpret_cast<DFastPair*>(m + up256(run.pk.h2d_bytes))) != BS_OK ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    cudaFree(plan->mem);
+    delete plan;
+    return set_error(ctx, BS_CUDA_ERROR, "mpc plan: reduced-grid upload failed");
+  }
   if (mode == kExhaustive) {
     bind_exhaustive(&run, m, L);
   } else {

@@ -106,12 +106,23 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
 }
 
 // Tables for one problem, written by a CTA.  Projection by thread 0.
+// The controller's latency / power grids reduced to one (configuration, tp)
+// for every candidate (FastGrid, bs_sim.cuh), built on the host from the
+// model's mirror; share: every candidate's grid brackets like candidate 0's.
+struct DFastPair {
+  FastGrid lat[kMaxCand];
+  FastGrid pw[kMaxCand];
+  int share;
+  int _pad;
+};
+
 // fl / fp (optional): the latency / power grids reduced to (pr.tp, cand[f])
-// for every candidate f (FastGrid, bs_sim.cuh) -- bit-identical values with
-// 2^(active axes) corners instead of 2^rank.
+// for every candidate f -- bit-identical values with 2^(active axes) corners
+// instead of 2^rank; share: each batch is bracketed once for all candidates.
 __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
                              const DRunning* R, DTables* T, int* s_status, const FastGrid* fl = nullptr,
-                             const FastGrid* fp = nullptr) {
+                             const FastGrid* fp = nullptr, bool share = false) {
+  __shared__ FastBrk s_bl[kMaxK], s_bp[kMaxK];
   if (threadIdx.x == 0) {
     T->nc = c.nc;
     T->ttft = c.ttft;
@@ -127,10 +138,21 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
   const int K = T->K;
   const int nc = c.nc;
   if (*s_status != BS_OK) return;
+  const bool shared_brk = fl && share;
+  if (shared_brk) {
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      fast_brackets(fl[0], T->n_req[k], T->sum_len[k], s_bl[k]);
+      fast_brackets(fp[0], T->n_req[k], T->sum_len[k], s_bp[k]);
+    }
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
     const int k = e / nc, f = e - k * nc;
     double L, P;
-    if (fl) {
+    if (shared_brk) {
+      L = fast_corners(fl[f], s_bl[k]);
+      P = fast_corners(fp[f], s_bp[k]);
+    } else if (fl) {
       L = fast_interp(fl[f], T->n_req[k], T->sum_len[k]);
       P = fast_interp(fp[f], T->n_req[k], T->sum_len[k]);
     } else {

@@ -133,6 +133,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
                   const bs_mpc_problem* problems, int n, PackedProblems* out) {
+  out->fg_pairs.clear();
   if (n_cfgs < 1 || cfgs == nullptr || policies == nullptr)
     return set_error(ctx, BS_PARAMETER_ERROR, "mpc: no controller configuration");
   if (n < 0) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: negative problem count");
@@ -181,6 +182,12 @@ int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_po
     p.n_wait = s.n_waiting;
     p.n_run = s.running_active ? s.n_running : 0;
     p.cfg = problems[i].cfg_index;
+    {
+      const std::pair<int, int> key(problems[i].cfg_index, s.tp);
+      auto it = std::find(out->fg_pairs.begin(), out->fg_pairs.end(), key);
+      p.fgi = static_cast<int>(it - out->fg_pairs.begin());
+      if (it == out->fg_pairs.end()) out->fg_pairs.push_back(key);
+    }
     p.wait_off = static_cast<long long>(wo);
     p.run_off = static_cast<long long>(ro);
     for (int j = 0; j < s.n_waiting; ++j) {
@@ -475,6 +482,17 @@ int bs_models_upload(bs_ctx_t ctx, const bs_model_set* m, bs_models_t* out) {
     cudaFree(mm->dmem);
     delete mm;
     return set_error(ctx, BS_CUDA_ERROR, "model upload copy failed");
+  }
+  // host mirror for host-built FastGrids (bs_sim.cuh fast_grid2)
+  mm->hbuf.assign(reinterpret_cast<const double*>(host.data()),
+                  reinterpret_cast<const double*>(host.data()) + bytes / sizeof(double));
+  for (int i = 0; i < 4; ++i) {
+    mm->hgrid[i] = mm->dm.grid[i];
+    auto rebase = [&](const double* p) {
+      return mm->hbuf.data() + (reinterpret_cast<const char*>(p) - dbase) / sizeof(double);
+    };
+    for (int d = 0; d < mm->dm.grid[i].rank; ++d) mm->hgrid[i].knots[d] = rebase(mm->dm.grid[i].knots[d]);
+    mm->hgrid[i].values = rebase(mm->dm.grid[i].values);
   }
   *out = mm;
   return BS_OK;

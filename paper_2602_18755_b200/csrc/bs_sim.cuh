@@ -108,7 +108,7 @@ struct FastGrid {
   const double* values;
 };
 
-__device__ __forceinline__ void bracket(const double* k, int n, double x, int* lo, double* frac) {
+__host__ __device__ __forceinline__ void bracket(const double* k, int n, double x, int* lo, double* frac) {
   const double k0 = k[0], kn = k[n - 1];
   if (x < k0 || x > kn) x = x < k0 ? k0 : (kn < x ? kn : x);
   if (n == 1) {
@@ -126,14 +126,21 @@ __device__ __forceinline__ void bracket(const double* k, int n, double x, int* l
   }
   int hi = a < 1 ? 1 : (a > n - 1 ? n - 1 : a);
   *lo = hi - 1;
+#ifdef __CUDA_ARCH__
   *frac = __ddiv_rn(__dsub_rn(x, k[hi - 1]), __dsub_rn(k[hi], k[hi - 1]));
+#else  // the same correctly rounded IEEE operations on the host (-ffp-contract=off)
+  *frac = (x - k[hi - 1]) / (k[hi] - k[hi - 1]);
+#endif
 }
 
-__device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double freq) {
+// rd: the grid whose knots are read (the device grid, or its host mirror);
+// st: the grid whose pointers the FastGrid keeps (always the device grid).
+__host__ __device__ inline FastGrid fast_grid2(const DGrid& rd, const DGrid& st_grid, int tp, double freq) {
+  const DGrid& g = rd;
   FastGrid f;
   f.na = 0;
   f.bad = g.bad_axis;
-  f.values = g.values;
+  f.values = st_grid.values;
   f.base = 0;
   long long stride[kMaxRank];
   long long st = 1;
@@ -162,7 +169,7 @@ __device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double fre
     const int a = f.na++;
     f.role[a] = g.role[d];
     f.n[a] = g.n[d];
-    f.knots[a] = g.knots[d];
+    f.knots[a] = st_grid.knots[d];
     f.stride[a] = stride[d];
     f.fixed[a] = fixed_axis ? 1 : 0;
     f.lo[a] = lo;
@@ -170,6 +177,8 @@ __device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double fre
   }
   return f;
 }
+
+__device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double freq) { return fast_grid2(g, g, tp, freq); }
 
 // bracket() without a dependent load chain: std::upper_bound's index in a
 // sorted knot vector is the number of knots k with !(x < k); the loads are
@@ -255,7 +264,7 @@ __device__ __forceinline__ double fast_interp(const FastGrid& g, long long n_req
 // Two reductions of the same grid whose active axes, knots and fixed-axis
 // brackets coincide (only the dropped axes' offsets differ, e.g. the same tp
 // at two on-knot frequencies): brackets of one serve the other.
-__device__ __forceinline__ bool fast_same_brackets(const FastGrid& a, const FastGrid& b) {
+__host__ __device__ inline bool fast_same_brackets(const FastGrid& a, const FastGrid& b) {
   if (a.na != b.na || a.bad != b.bad || a.values != b.values) return false;
   for (int i = 0; i < a.na; ++i) {
     if (a.role[i] != b.role[i] || a.n[i] != b.n[i] || a.knots[i] != b.knots[i] || a.stride[i] != b.stride[i] ||
