@@ -20,13 +20,15 @@ per-decision argmin.
 
 Extra keys, one object per other BASELINE.json configuration (each with its
 own device timing, the reference on the host cores and a parity check):
+  c1_demo        configs[0]: 1P + 1D demo-shaped replay, decisions/s by trigger,
+                 plus per-decision controller-call latency (p50 / p99)
   c3_placement   configs[2]: config table + ILP, placement configs/s
   c4_replay      configs[3]-shaped what-if replay sweep, scenarios/s
   c4_experiment  configs[3]'s window loop: run_experiment over a bursty hour
                  (plan per window + 3 policies replayed), window runs/s
   c5_greedy      configs[4] greedy MPC (H8 x 24 levels), decisions/s
   c5_exhaustive  configs[4] exhaustive MPC (24^8 per decision), decisions/s
-(`--only c3|c4|c4x|c5g|c5x` runs one alone; `--no-extras` skips them.)
+(`--only c1|c3|c4|c4x|c5g|c5x` runs one alone; `--no-extras` skips them.)
 
 Multi-GPU (torchrun): weak scaling, every rank evaluates its own corpus
 (independent decisions), no data-path collective; max-over-ranks time.  The
@@ -68,7 +70,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU baseline sample duration")
     ap.add_argument("--no-extras", action="store_true", help="skip the C3/C4/C5 sub-benchmarks")
-    ap.add_argument("--only", choices=["c3", "c4", "c4x", "c5g", "c5x"], default=None,
+    ap.add_argument("--only", choices=["c1", "c3", "c4", "c4x", "c5g", "c5x"], default=None,
                     help="run one sub-benchmark alone and print its JSON object")
     ap.add_argument("--c4-scenarios", type=int, default=1024)
     ap.add_argument("--c5x-decisions", type=int, default=4096)
@@ -372,6 +374,112 @@ def bench_c4(dev, rank: int, world: int, local: int, n_scen: int, with_cpu: bool
     return out
 
 
+def bench_c1(dev, with_cpu: bool, n_rep: int = 296) -> dict:
+    """configs[0]: the demo-shaped 1P + 1D replay with per-iteration two-tier
+    decisions (one scenario, so latency-bound: the serial chain of one
+    prefill instance's event loop), decisions/s split by trigger; plus the
+    per-decision latency of the drop-in controller call (one greedy decision
+    per bs_mpc_greedy call with host buffers, as GpuPrefillMpcController::
+    decide makes it) over the C1 snapshot corpus."""
+    import ctypes as C
+
+    from paper_2602_18755_b200 import _abi as A
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import workloads as Wk
+
+    models, sc = Wk.c1_scenario()
+    lib = dev._lib
+    keep: list = []
+    cfgs, cscs, _ = P.c_replay_inputs([sc], keep)
+    out = (A.bs_replay_summary * 1)()
+    mh = dev.models(models)
+    dev.check(lib.bs_replay(dev.handle, mh, mh, cfgs, 1, cscs, 1, out, None, None))  # warm-up
+    st = (C.c_double * 8)()
+    times, kern = [], []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        dev.check(lib.bs_replay(dev.handle, mh, mh, cfgs, 1, cscs, 1, out, None, None))
+        times.append(time.perf_counter() - t0)
+        lib.bs_ctx_stats(dev.handle, st, 8)
+        kern.append([st[i] for i in range(4)])
+    kms, e2e = statistics.median(sum(k) for k in kern), statistics.median(times)
+    dec = out[0].n_decisions
+    res = {"workload": "C1: demo trace parameters (14 rps, 600 s, seed 7, lognormal 6.2/0.4 in, 2.9/0.5 out) with "
+                       "Poisson arrivals, 1P(tp2)+1D(tp4), greedy MPC K=8 N=7 of the 8-rung ladder + decode slack "
+                       "DVFS, one scenario",
+           "value": dec / (kms / 1e3), "unit": "decisions/s", "kernel_ms": kms, "decisions": int(dec),
+           "decisions_by_trigger": dict(zip(["boundary", "arrival", "safety"],
+                                            (int(x) for x in out[0].decisions_by_trigger))),
+           "phase_ms": dict(zip(["prefill", "route", "decode", "report"],
+                                [statistics.median(k[i] for k in kern) for i in range(4)])),
+           "e2e": {"value": dec / e2e, "unit": "decisions/s"}, "status": int(out[0].status)}
+    # throughput: C1 replicas over trace seeds 7, 8, ... (independent scenarios, one launch)
+    reps = [sc] + [Wk.c1_scenario(seed=7 + i)[1] for i in range(1, n_rep)]
+    k3: list = []
+    r_cfgs, r_scs, _ = P.c_replay_inputs(reps, k3)
+    rout_all = (A.bs_replay_summary * n_rep)()
+    dev.check(lib.bs_replay(dev.handle, mh, mh, r_cfgs, n_rep, r_scs, n_rep, rout_all, None, None))
+    rk = []
+    for _ in range(3):
+        dev.check(lib.bs_replay(dev.handle, mh, mh, r_cfgs, n_rep, r_scs, n_rep, rout_all, None, None))
+        lib.bs_ctx_stats(dev.handle, st, 8)
+        rk.append(sum(st[i] for i in range(4)))
+    rdec = sum(rout_all[i].n_decisions for i in range(n_rep))
+    res["replicas"] = {"scenarios": n_rep, "value": rdec / (statistics.median(rk) / 1e3), "unit": "decisions/s",
+                       "kernel_ms": statistics.median(rk), "decisions": int(rdec),
+                       "all_ok": all(rout_all[i].status == 0 for i in range(n_rep)),
+                       "first_matches_single": all(getattr(rout_all[0], f) == getattr(out[0], f)
+                                                   for f in ("n_decisions", "prefill_energy_j", "decode_energy_j"))}
+    # per-decision latency of the controller call (pack + H2D + one warp + D2H)
+    mc, cfg, pol, snaps = Wk.c1_corpus(n=256)
+    for q in snaps[:8]:
+        P.greedy_freq_select(q, cfg, mc, pol, dev)
+    lat = []
+    for q in snaps:
+        t0 = time.perf_counter()
+        P.greedy_freq_select(q, cfg, mc, pol, dev)
+        lat.append((time.perf_counter() - t0) * 1e6)
+    lat.sort()
+    res["decision_latency_us"] = {"p50": lat[len(lat) // 2], "p99": lat[int(0.99 * (len(lat) - 1))],
+                                  "calls": len(lat), "path": "pdsim.greedy_freq_select -> bs_mpc_greedy, n=1"}
+    # the same calls with the snapshots pre-marshalled: the C ABI alone (pack + H2D + kernel + D2H + sync)
+    carr = (A.bs_mpc_config * 1)(P.c_mpc_config(cfg, keep))
+    parr = (A.bs_scheduler_policy * 1)(P.c_policy(pol))
+    probs = [P.c_problems([q], None, keep) for q in snaps]
+    one = (A.bs_mpc_result * 1)()
+    mch = dev.models(mc)
+    raw = []
+    for pr in probs:
+        t0 = time.perf_counter()
+        dev.check(lib.bs_mpc_greedy(dev.handle, mch, carr, parr, 1, pr, 1, one))
+        raw.append((time.perf_counter() - t0) * 1e6)
+    raw.sort()
+    res["decision_latency_us"]["c_abi_p50"] = raw[len(raw) // 2]
+    res["decision_latency_us"]["c_abi_p99"] = raw[int(0.99 * (len(raw) - 1))]
+    if with_cpu:
+        import oracle
+
+        ref = oracle.load_ref()
+        k2: list = []
+        rc_cfgs, rc_scs, _ = P.c_replay_inputs([sc], k2)
+        rout = (A.bs_replay_summary * 1)()
+        cm = P.c_model_set(models, k2)
+        t0 = time.perf_counter()
+        rc = ref.ref_replay(C.byref(cm), C.byref(cm), rc_cfgs, rc_scs, 1, rout, None, None, 1)
+        t_cpu = time.perf_counter() - t0
+        names = [f for f, _ in A.bs_replay_summary._fields_ if f not in ("_pad", "decisions_by_trigger")]
+        same = rc == 0 and all(getattr(out[0], f) == getattr(rout[0], f) or
+                               (getattr(out[0], f) != getattr(out[0], f) and getattr(rout[0], f) !=
+                                getattr(rout[0], f)) for f in names) and \
+            list(out[0].decisions_by_trigger) == list(rout[0].decisions_by_trigger)
+        res["cpu_baseline"] = {"value": rout[0].n_decisions / t_cpu, "unit": "decisions/s", "cores": 1,
+                               "kind": "reference", "seconds": t_cpu,
+                               "sample": "the whole C1 scenario: pdsim::simulate_cluster with TwoTierFactory "
+                                         "controllers + trim_steady_state + make_report, one thread"}
+        res["identical"] = bool(same)
+    return res
+
+
 def bench_c5(dev, mode: str, rank: int, world: int, local: int, n_dec: int, with_cpu: bool) -> dict:
     """configs[4]: horizon-8 MPC on a 24-level grid, greedy or exhaustive,
     decisions sharded across ranks."""
@@ -540,10 +648,13 @@ def bench_c4_experiment(dev, with_cpu: bool) -> dict:
 
 def run_extras(args, dev, rank, world, local) -> dict:
     with_cpu = world == 1 and not args.no_cpu_baseline
-    todo = [args.only] if args.only else ["c3", "c4", "c4x", "c5g", "c5x"]
+    todo = [args.only] if args.only else ["c1", "c3", "c4", "c4x", "c5g", "c5x"]
     out = {}
     for k in todo:
-        if k == "c3":
+        if k == "c1":
+            if world == 1:
+                out["c1_demo"] = bench_c1(dev, with_cpu)
+        elif k == "c3":
             out["c3_placement"] = bench_c3(dev, with_cpu, rank=rank, world=world, local=local)
         elif k == "c4":
             out["c4_replay"] = bench_c4(dev, rank, world, local, args.c4_scenarios, with_cpu)

@@ -368,9 +368,13 @@ int upload_fast_pairs(bs_ctx_t ctx, bs_models_t models, MpcRun* run, DFastPair* 
       if (!fast_same_brackets(fp.lat[0], fp.lat[f]) || !fast_same_brackets(fp.pw[0], fp.pw[f])) fp.share = 0;
     }
   }
-  if (!pairs.empty())
-    BS_CUDA_TRY(ctx, cudaMemcpyAsync(dst, run->hFG.data(), sizeof(DFastPair) * pairs.size(), cudaMemcpyHostToDevice,
-                                     ctx->stream));
+  if (!pairs.empty()) {  // staged through pinned memory: an asynchronous copy
+    const size_t bytes = sizeof(DFastPair) * pairs.size();
+    void* h = ctx->host_buf(kSlotFastGrids, bytes);
+    if (!h) return set_error(ctx, BS_CUDA_ERROR, "mpc: pinned staging of the reduced grids failed");
+    std::memcpy(h, run->hFG.data(), bytes);
+    BS_CUDA_TRY(ctx, cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
   run->dFG = pairs.empty() ? nullptr : dst;
   return BS_OK;
 }

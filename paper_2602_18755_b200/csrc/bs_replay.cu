@@ -157,6 +157,8 @@ struct DReplay {
   DIdlX* idlx;       // null unless logs
   DDec* dec;
   DResident* res;
+  double* rec_c;     // report scratch: clipped busy energies in merged (start, instance) order
+  double* idl_c;     // the same for idle records
 };
 
 // --- shared instance machinery ---------------------------------------------------
@@ -219,6 +221,23 @@ __device__ __forceinline__ bool predict_fast(const FastGrid& g, long long n, lon
     return false;
   }
   const double v = fast_interp(g, n, sum);
+  if (!model_value_ok(v)) {
+    *err = kind;
+    return false;
+  }
+  *out = v;
+  return true;
+}
+
+// predict_fast with the iteration's cached brackets when the slot's grid
+// shares them (`shared`), else its own.
+__device__ __forceinline__ bool predict_slot(const FastGrid& g, int shared, const FastBrk& b, long long n, long long sum,
+                                             double* out, int* err, int kind) {
+  if (g.bad) {
+    *err = kErrAxis;
+    return false;
+  }
+  const double v = shared ? fast_corners(g, b) : fast_interp(g, n, sum);
   if (!model_value_ok(v)) {
     *err = kind;
     return false;
@@ -372,7 +391,14 @@ struct DecSlot {
   double f;
   double idle;
   int idle_err;
+  int share;  // bit 0: lat, bit 1: clat use the iteration's latency brackets; bit 2: pw the power brackets
   FastGrid lat, pw, clat;  // simulator latency / power, controller latency (decode)
+};
+
+// One decode iteration's brackets (its (n_requests, sum_len) query is fixed
+// from start_iteration to the emissions): latency axes and power axes.
+struct DecBrk {
+  FastBrk lat, pw;
 };
 
 __device__ __forceinline__ int find_slot(const double* fs, int ns, double f) {
@@ -903,8 +929,9 @@ __global__ void route_kernel(DReplay R, int n_scen) {
 // select_decode_freq_ex (dvfs.hpp:274-293) as a warp ladder walk (lane j
 // evaluates rung j of each 32-rung chunk; a ballot finds where the
 // reference's ascending walk stops).  Warp-uniform; false on ModelError.
-__device__ bool decode_pick(const DReplay& R, const DRCfg* C, const DecSlot* slots, long long n, long long sum, int tp,
-                            long long cap, long long used, double* f, long long* eval, int* err) {
+__device__ bool decode_pick(const DReplay& R, const DRCfg* C, const DecSlot* slots, const DecBrk* B, long long n,
+                            long long sum, int tp, long long cap, long long used, double* f, long long* eval,
+                            int* err) {
   const int lane = threadIdx.x & 31;
   const double util = cap > 0 ? __ddiv_rn(static_cast<double>(used), static_cast<double>(cap)) : 0.0;
   *f = C->ladder[C->n_ladder - 1];
@@ -920,7 +947,8 @@ __device__ bool decode_pick(const DReplay& R, const DRCfg* C, const DecSlot* slo
     const int j = j0 + lane;
     bool fits = false, bad = false;
     if (j < C->n_ladder) {
-      const double v = fast_interp(slots[j].clat, n, sum);  // slot j = rung j
+      const double v = (slots[j].share & 2) ? fast_corners(slots[j].clat, B->lat)
+                                            : fast_interp(slots[j].clat, n, sum);  // slot j = rung j
       bad = !model_value_ok(v);
       fits = !bad && __dmul_rn(v, C->dec_one_plus_margin) <= C->dec_tbt;  // dvfs.hpp:285-286
     }
@@ -971,6 +999,7 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
   const DGrid& pow_g = R.sim.grid[3];
   // per-frequency caches: slots [0, n_ladder) = the decode ladder, slot n_ladder = base
   DecSlot* slots = reinterpret_cast<DecSlot*>(dsm) + (threadIdx.x >> 5) * max_slots;
+  DecBrk* brk = reinterpret_cast<DecBrk*>(reinterpret_cast<DecSlot*>(dsm) + 4 * max_slots) + (threadIdx.x >> 5);
   const int nl = C->controlled ? C->n_ladder : 0;
   const int ns = nl + 1;
   for (int t = lane; t < ns; t += 32) {
@@ -989,6 +1018,12 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
     else if (g == 1) slots[k].pw = fg;
     else slots[k].clat = fg;
   }
+  __syncwarp();
+  // bracket sharing against slot 0 (the reference of the iteration's brackets)
+  for (int t = lane; t < ns; t += 32)
+    slots[t].share = (fast_same_axes(slots[t].lat, slots[0].lat) ? 1 : 0) |
+                     (fast_same_axes(slots[t].clat, slots[0].lat) ? 2 : 0) |
+                     (fast_same_axes(slots[t].pw, slots[0].pw) ? 4 : 0);
   __syncwarp();
   auto slot_of = [&](double f) {
     for (int i = 0; i < ns; ++i)
@@ -1026,7 +1061,7 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
   int slot = slot_of(fb.in_force);
   auto exec_latency = [&]() -> bool {
     int err = 0;
-    if (slot >= 0 ? !predict_fast(slots[slot].lat, fn, fsum, &L, &err, kErrLatency)
+    if (slot >= 0 ? !predict_slot(slots[slot].lat, slots[slot].share & 1, brk->lat, fn, fsum, &L, &err, kErrLatency)
                   : !predict(lat_g, fn, fsum, I.tp, fb.in_force, &L, &err, kErrLatency)) {
       w.fail(BS_MODEL_ERROR, err);
       return false;
@@ -1037,7 +1072,7 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
     if (to > seg_start) {
       double p;
       int err = 0;
-      if (slot >= 0 ? !predict_fast(slots[slot].pw, fn, fsum, &p, &err, kErrPower)
+      if (slot >= 0 ? !predict_slot(slots[slot].pw, slots[slot].share & 4, brk->pw, fn, fsum, &p, &err, kErrPower)
                     : !predict(pow_g, fn, fsum, I.tp, fb.in_force, &p, &err, kErrPower)) {
         w.fail(BS_MODEL_ERROR, err);
         return false;
@@ -1096,6 +1131,8 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
       // start_iteration (simulator.hpp:472-492)
       fn = n_res;
       fsum = sum_ctx;
+      if (!slots[0].lat.bad) warp_brackets(slots[0].lat, fn, fsum, &brk->lat);
+      if (!slots[0].pw.bad) warp_brackets(slots[0].pw, fn, fsum, &brk->pw);
       active = 1;
       started = now;
       seg_start = now;
@@ -1105,7 +1142,7 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
         double f;
         long long eval;
         int err = 0;
-        if (!decode_pick(R, C, slots, fn, fsum, I.tp, C->kv_cap, sum_ctx, &f, &eval, &err)) {
+        if (!decode_pick(R, C, slots, brk, fn, fsum, I.tp, C->kv_cap, sum_ctx, &f, &eval, &err)) {
           w.fail(BS_MODEL_ERROR, err);
           break;
         }
@@ -1119,7 +1156,7 @@ __global__ void __launch_bounds__(128, BS_DECODE_MINB) decode_kernel(DReplay R, 
         double pl;
         int err = 0;
         const int ks = slot_of(decided);
-        if (ks >= 0 ? !predict_fast(slots[ks].clat, fn, fsum, &pl, &err, kErrLatency)
+        if (ks >= 0 ? !predict_slot(slots[ks].clat, slots[ks].share & 2, brk->lat, fn, fsum, &pl, &err, kErrLatency)
                     : !predict(R.ctl.grid[1], fn, fsum, I.tp, decided, &pl, &err, kErrLatency)) {
           w.fail(BS_MODEL_ERROR, err);
           break;
@@ -1259,44 +1296,61 @@ __device__ __forceinline__ long long nearest_rank_index(double p, long long n) {
   return rank - 1;
 }
 
-// One fold of TrimmedResult::busy/idle_energy_j (metrics.hpp:38-56) over one
-// phase's records in SimResult order: stable by (start, instance) across the
-// phase's instances (each instance's records are in strictly increasing
-// start order), clipped to the span.
-__device__ double phase_fold(const DReplay& R, const DScen& sc, int phase, bool idle, double s0, double s1) {
-  long long pos[kMaxInstances];
-  int ids[kMaxInstances];
-  int k = 0;
-  for (int i = 0; i < sc.ni; ++i) {
-    const int g = sc.i0 + i;
-    if (R.inst[g].phase != phase) continue;
-    ids[k] = g;
-    pos[k++] = 0;
-  }
-  double e = 0.0;
-  for (;;) {
-    int best = -1;
-    double bs = 0.0;
-    for (int j = 0; j < k; ++j) {
-      const DInst& I = R.inst[ids[j]];
-      const long long cnt = idle ? R.st[ids[j]].n_idl : R.st[ids[j]].n_rec;
-      if (pos[j] >= cnt) continue;
-      const double st = (idle ? R.idl[I.idl0 + pos[j]] : R.rec[I.rec0 + pos[j]]).start;
-      if (best < 0 || st < bs) {  // ties keep the lower instance id (scan order)
-        best = j;
-        bs = st;
+// TrimmedResult::busy/idle_energy_j (metrics.hpp:38-56) folds each phase's
+// records in SimResult order: stable by (start, instance) across the phase's
+// instances (each instance's records are in start order), clipped to the
+// span.  The order is data-independent of the sums, so the block first
+// scatters every record's clipped energy to its merged position (its own
+// index plus, per other instance of the phase, a binary-search count of the
+// records that precede it: start <= s for lower instance ids, start < s for
+// higher), then one thread per fold adds the contiguous array in order.
+__device__ __forceinline__ double clip_energy(const DRec& r, double s0, double s1) {  // metrics.hpp:60-66
+  const double a = fmax(r.start, s0);
+  const double b = fmin(r.end, s1);
+  return b <= a ? 0.0 : __ddiv_rn(__dmul_rn(r.energy, __dsub_rn(b, a)), __dsub_rn(r.end, r.start));
+}
+
+__device__ void scatter_phase(const DReplay& R, const DScen& sc, int phase, bool idle, double* dst, double s0,
+                              double s1) {
+  for (int a = 0; a < sc.ni; ++a) {
+    const int ga = sc.i0 + a;
+    const DInst& Ia = R.inst[ga];
+    if (Ia.phase != phase) continue;
+    const long long na = idle ? R.st[ga].n_idl : R.st[ga].n_rec;
+    const DRec* la = idle ? R.idl + Ia.idl0 : R.rec + Ia.rec0;
+    for (long long j = threadIdx.x; j < na; j += blockDim.x) {
+      const DRec r = la[j];
+      long long pos = j;
+      for (int b = 0; b < sc.ni; ++b) {
+        const int gb = sc.i0 + b;
+        const DInst& Ib = R.inst[gb];
+        if (b == a || Ib.phase != phase) continue;
+        const DRec* lb = idle ? R.idl + Ib.idl0 : R.rec + Ib.rec0;
+        long long lo = 0, hi = idle ? R.st[gb].n_idl : R.st[gb].n_rec;
+        while (lo < hi) {
+          const long long mid = lo + (hi - lo) / 2;
+          const double t = lb[mid].start;
+          if (b < a ? !(r.start < t) : t < r.start) lo = mid + 1;
+          else hi = mid;
+        }
+        pos += lo;
       }
+      dst[pos] = clip_energy(r, s0, s1);
     }
-    if (best < 0) break;
-    const DInst& I = R.inst[ids[best]];
-    const DRec r = idle ? R.idl[I.idl0 + pos[best]] : R.rec[I.rec0 + pos[best]];
-    ++pos[best];
-    // clip_energy (metrics.hpp:60-66)
-    const double a = fmax(r.start, s0);
-    const double b = fmin(r.end, s1);
-    const double c = b <= a ? 0.0 : __ddiv_rn(__dmul_rn(r.energy, __dsub_rn(b, a)), __dsub_rn(r.end, r.start));
-    e = __dadd_rn(e, c);
   }
+}
+
+__device__ double fold_in_order(const double* c, long long n) {
+  double e = 0.0;
+  long long i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = c[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) e = __dadd_rn(e, v[u]);
+  }
+  for (; i < n; ++i) e = __dadd_rn(e, c[i]);
   return e;
 }
 
@@ -1355,9 +1409,22 @@ __global__ void __launch_bounds__(kReportThreads) report_kernel(DReplay R, bs_re
   const double s0 = C->span_start;
   const double s1 = sc.issuance_end;
   const bool empty = sc.n == 0 || s1 <= s0;
-  if (threadIdx.x < 4 && !empty) {
-    const int phase = threadIdx.x < 2 ? BS_PHASE_PREFILL : BS_PHASE_DECODE;
-    s_energy[threadIdx.x] = phase_fold(R, sc, phase, threadIdx.x & 1, s0, s1);
+  if (!empty) {
+    long long cnt[4] = {0, 0, 0, 0};  // prefill busy, prefill idle, decode busy, decode idle
+    for (int i = 0; i < sc.ni; ++i) {
+      const int g = sc.i0 + i;
+      const int d = R.inst[g].phase == BS_PHASE_PREFILL ? 0 : 2;
+      cnt[d] += R.st[g].n_rec;
+      cnt[d + 1] += R.st[g].n_idl;
+    }
+    // merged arrays: prefill at the scenario's first record slot, decode after it
+    double* base[4] = {R.rec_c + R.inst[sc.i0].rec0, R.idl_c + R.inst[sc.i0].idl0, nullptr, nullptr};
+    base[2] = base[0] + cnt[0];
+    base[3] = base[1] + cnt[1];
+    for (int f = 0; f < 4; ++f)
+      scatter_phase(R, sc, f < 2 ? BS_PHASE_PREFILL : BS_PHASE_DECODE, f & 1, base[f], s0, s1);
+    __syncthreads();
+    if (threadIdx.x < 4) s_energy[threadIdx.x] = fold_in_order(base[threadIdx.x], cnt[threadIdx.x]);
   }
   // request statistics
   long long completed = 0, generated = 0, rc = 0, rg = 0, tv = 0, pv = 0, nttft = 0, ntpot = 0;
@@ -1843,7 +1910,8 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
                  o_mslot = take(4 * NR), o_mr = take(8 * NR), o_rec = take(sizeof(DRec) * nrec),
                  o_recx = want_logs ? take(sizeof(DRecX) * nrec) : 0, o_idl = take(sizeof(DRec) * nidl),
                  o_idlx = want_logs ? take(sizeof(DIdlX) * nidl) : 0, o_decr = take(sizeof(DDec) * ndec),
-                 o_res = take(sizeof(DResident) * std::max<long long>(nres, 1));
+                 o_res = take(sizeof(DResident) * std::max<long long>(nres, 1)),
+                 o_recc = take(8 * nrec), o_idlc = take(8 * nidl);
     const size_t total = o;
     char* h = static_cast<char*>(ctx->host_buf(12, h2d));
     char* d = static_cast<char*>(ctx->dev_buf(12, total));
@@ -1911,6 +1979,8 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
     R.idlx = want_logs ? reinterpret_cast<DIdlX*>(d + o_idlx) : nullptr;
     R.dec = reinterpret_cast<DDec*>(d + o_decr);
     R.res = reinterpret_cast<DResident*>(d + o_res);
+    R.rec_c = reinterpret_cast<double*>(d + o_recc);
+    R.idl_c = reinterpret_cast<double*>(d + o_idlc);
     bs_replay_summary* dsum = reinterpret_cast<bs_replay_summary*>(d + o_sum);
     const int* dpre = reinterpret_cast<const int*>(d + o_pre);
     const int* ddec = reinterpret_cast<const int*>(d + o_dec);
@@ -1942,7 +2012,7 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
       const int nd = static_cast<int>(dec_ids.size());
       int max_slots = 1;
       for (const DRCfg& c : hcfg) max_slots = std::max(max_slots, (c.controlled ? c.n_ladder : 0) + 1);
-      const size_t smem = sizeof(DecSlot) * static_cast<size_t>(max_slots) * 4;
+      const size_t smem = (sizeof(DecSlot) * static_cast<size_t>(max_slots) + sizeof(DecBrk)) * 4;
       if (smem > 48 * 1024)
         BS_CUDA_TRY(ctx, cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));

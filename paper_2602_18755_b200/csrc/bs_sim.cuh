@@ -275,6 +275,55 @@ __host__ __device__ inline bool fast_same_brackets(const FastGrid& a, const Fast
   return true;
 }
 
+// Same bracket inputs (active axes, their knots and the fixed axes'
+// brackets) regardless of values, strides and offsets: one FastBrk serves
+// both reductions (e.g. the latency grids of two rungs, or of the simulator's
+// and the controller's models when they share knot storage).
+__host__ __device__ inline bool fast_same_axes(const FastGrid& a, const FastGrid& b) {
+  if (a.na != b.na || a.bad != b.bad) return false;
+  for (int i = 0; i < a.na; ++i) {
+    if (a.role[i] != b.role[i] || a.n[i] != b.n[i] || a.knots[i] != b.knots[i] || a.fixed[i] != b.fixed[i])
+      return false;
+    if (a.fixed[i] && (a.lo[i] != b.lo[i] || a.frac[i] != b.frac[i])) return false;
+  }
+  return true;
+}
+
+// fast_brackets by one warp (all lanes call it with the same query): lane i
+// tests knot i of each varying axis and a ballot counts the knots <= x, the
+// same (lo, frac) as bracket_count.  Lane 0 stores into `out` (shared memory).
+__device__ __forceinline__ void warp_brackets(const FastGrid& g, long long n_req, long long sum_len, FastBrk* out) {
+  const int lane = threadIdx.x & 31;
+  for (int a = 0; a < g.na; ++a) {
+    int lo;
+    double fr;
+    if (g.fixed[a]) {
+      lo = g.lo[a];
+      fr = g.frac[a];
+    } else {
+      const double* __restrict__ k = g.knots[a];
+      const int n = g.n[a];
+      double x = static_cast<double>(g.role[a] == BS_AXIS_SUM_LEN ? sum_len : n_req);
+      const double k0 = __ldg(k), kn = __ldg(k + n - 1);
+      if (x < k0 || x > kn) x = x < k0 ? k0 : (kn < x ? kn : x);
+      int cnt = 0;
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, i < n && !(x < __ldg(k + i))));
+      }
+      const int hi = cnt < 1 ? 1 : (cnt > n - 1 ? n - 1 : cnt);
+      lo = hi - 1;
+      const double klo = __ldg(k + hi - 1), khi = __ldg(k + hi);
+      fr = __ddiv_rn(__dsub_rn(x, klo), __dsub_rn(khi, klo));
+    }
+    if (lane == 0) {
+      out->lo[a] = lo;
+      out->frac[a] = fr;
+    }
+  }
+  __syncwarp();
+}
+
 // predict_latency / predict_power at the instance's (tp, freq); false on
 // ModelError (perfmodel.hpp:264, 270).
 __device__ __forceinline__ bool predict_at(const FastGrid& g, long long n_req, long long sum_len, double* out) {

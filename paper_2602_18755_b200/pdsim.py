@@ -825,7 +825,7 @@ def _mpc_batch(fn_name: str, snaps: Sequence[QueueSnapshot], cfgs: Sequence[MpcC
 
 def greedy_freq_select(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy,
                        device: Device | None = None) -> GreedyResult:
-    """greedy_freq_select (dvfs.hpp:185-259), one CTA on the GPU."""
+    """greedy_freq_select (dvfs.hpp:185-259), one warp on the GPU."""
     return _mpc_batch("bs_mpc_greedy", [q], [cfg], [policy], None, models, device)[0]
 
 

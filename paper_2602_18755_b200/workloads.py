@@ -7,6 +7,9 @@ the reference's own generators restated in ``pdsim`` (bit-identical).
   1e-7 f^3 + 60 W per GPU, TP knots {1, 2, 4, 8}).
 * ``c1_corpus`` -- C1-style snapshots for the greedy MPC (horizon 8, N = 7 of
   the 8-rung H100-style ladder).
+* ``c1_scenario`` -- C1 itself: the demo's trace parameters
+  (demos/two_tier_demo.sh:16-18) with Poisson arrivals, one prefill + one
+  decode instance under the two-tier controllers.
 """
 from __future__ import annotations
 
@@ -66,6 +69,27 @@ def c1_corpus(seed: int = 0xC1, n: int = 256):
     rng = random.Random(seed)
     snaps = [synthetic_snapshot(rng, lad, n_lo=8, n_hi=32, arrival_window_ms=100.0) for _ in range(n)]
     return models, cfg, pol, snaps
+
+
+def c1_scenario(duration_s: float = 600.0, rps: float = 14.0, seed: int = 7):
+    """C1 (BASELINE.json configs[0]): the demo's trace
+    (mean 14 rps, 600 s, seed 7, input lognormal(6.2, 0.4), output
+    lognormal(2.9, 0.5); demos/two_tier_demo.sh:16-18) but Poisson (gamma
+    shape 1), on a 1P(tp2) + 1D(tp4) cluster at max frequency with the
+    two-tier controllers: greedy MPC mpc_k 8, mpc_n 7 of the 8-rung ladder,
+    decode slack DVFS (margin 0.05), 600 / 100 ms SLOs, 30 s ramp-up."""
+    lad = ladder(8)
+    models = llama_models(lad)
+    fmax = lad.max_mhz()
+    pol = P.SchedulerPolicy(max_batch_tokens=2048, max_batch_requests=16)
+    slo = P.SLOSpec(600.0, 100.0)
+    tr = P.gen_gamma_trace(rps, 1.0, duration_s * 1000.0,
+                           P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.4, 2.9, 0.5)), seed)
+    inst = [P.ClusterInstance(P.InstanceConfig(P.Phase.prefill, 2, fmax), 1.0),
+            P.ClusterInstance(P.InstanceConfig(P.Phase.decode, 4, fmax), 1.0)]
+    fac = P.TwoTierFactory(P.MpcConfig(horizon_K=8, ladder_N=7, ladder=lad, slo=slo),
+                           P.DecodePolicyConfig(tbt_slo_ms=slo.tpot_ms, ladder=lad, margin=0.05), models, pol)
+    return models, P.ReplayScenario(tr, P.ClusterSpec(inst), pol, fac, P.SimOptions(30.0, -1.0), slo, 30.0)
 
 
 def c5_corpus(seed: int = 0xC5, n: int = 4096, ttft_ms: float = 600.0):
