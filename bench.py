@@ -284,7 +284,11 @@ def bench_c3(dev, with_cpu: bool, repeats: int = 3, rank: int = 0, world: int = 
            "single_table_configs_per_s": len(cands) / t_table, "table_s": t_table,
            "probes_per_s": k_max * len(cands) / t_table, "ilp_s": t_ilp, "gpus_used": plan.gpus_used,
            "objective_w": plan.objective_w, "phase_ms": {"mask": st[0], "probe": st[1], "energy": st[2]},
-           "events_simulated": st[4], "e2e_note": "value is end to end through pdsim.build_config_table "
+           "events_simulated": st[4],
+           "probes": {"grid": st[5], "skipped_off_path": st[6], "abandoned_off_path": st[7],
+                      "note": "every (candidate, rate step) probe is launched in search-tree order; probes the "
+                              "reference's binary search can no longer visit are skipped or abandoned"},
+           "e2e_note": "value is end to end through pdsim.build_config_table "
                                                  "(host trace in, table out)"}
     if with_cpu:
         import oracle

@@ -166,6 +166,8 @@ __device__ __forceinline__ SimParams make_params(const DCand& c, const PolicyDev
   p.ttft_bound = pol.ttft;
   p.tpot_bound = pol.tpot;
   p.early_exit = early;
+  p.search = nullptr;
+  p.k = 0;
   return p;
 }
 
@@ -220,15 +222,19 @@ struct TableDev {
 
 __global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, TraceDev tr, const TableDev* tabs, const DCand* cands, const int* kept,
                              const long long* kept_count, PolicyDev pol, Resident* heaps, int heap_cap,
-                             int heap_in_smem, const ProbeId* order, long long n_probes, ProbeOut* out) {
+                             int heap_in_smem, const ProbeId* order, long long n_probes, ProbeOut* out, int* pst,
+                             int reps) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long slot = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (slot >= n_probes) return;
-  const ProbeId id = order[slot];  // launch order: likely-long probes first, across every table
+  const ProbeId id = order[slot];  // launch order: the search tree's top levels first, across every table
   const TableDev tb = tabs[id.t];
-  const long long gid = tb.probe_off + static_cast<long long>(id.c) * tb.n_streams + id.s;
+  const long long cbase = tb.probe_off + static_cast<long long>(id.c) * tb.n_streams;
+  const long long gid = cbase + id.s;
   const DCand cd = cands[id.c];
+  const SearchView sv{pst + cbase, tb.n_streams / reps, reps};
+  const long long k = id.s / reps + 1;
   ProbeOut o;
   o.status = BS_OK;
   o.model_err = 0;
@@ -238,10 +244,23 @@ __global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, Tr
   o.completed = 0;
   o.busy_j = 0.0;
   o.idle_j = 0.0;
+  auto publish = [&](int code) {  // the outcome record first, then its code for the other probes
+    out[gid] = o;
+    __threadfence();
+    *reinterpret_cast<volatile int*>(pst + gid) = code;
+  };
+  int alive = lane == 0 ? (search_alive(sv, k) ? 1 : 0) : 0;
+  alive = __shfl_sync(0xffffffffu, alive, 0);
+  if (!alive) {  // off the search path already: never run
+    o.status = kSimAborted;
+    o.completed = -1;  // marks "skipped at start" in the statistics
+    if (lane == 0) publish(kProbeSkipped);
+    return;
+  }
   const long long nk = kept_count[tb.stream_off + id.s];
   if (nk == 0) {  // placement.hpp:169: an empty probe passes
     o.empty = 1;
-    if (lane == 0) out[gid] = o;
+    if (lane == 0) publish(kProbePass);
     return;
   }
   SimTrace st;
@@ -251,7 +270,9 @@ __global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, Tr
   st.kept = kept + tb.kept_off + static_cast<size_t>(id.s) * tb.n;
   st.n = nk;
   st.duration_ms = tb.duration_ms;
-  const SimParams p = make_params(cd, pol, cd.safe);
+  SimParams p = make_params(cd, pol, cd.safe);
+  p.search = &sv;
+  p.k = k;
   SimOut r;
   if (cd.phase == BS_PHASE_PREFILL) {
     if (lane != 0) return;
@@ -269,7 +290,12 @@ __global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, Tr
   o.completed = r.completed;
   o.busy_j = r.busy_j;
   o.idle_j = r.idle_j;
-  out[gid] = o;
+  // feasible(k) (placement.hpp:172-176): SimulationError counts as a failure
+  publish(r.status == kSimAborted           ? kProbeSkipped
+          : r.status == BS_MODEL_ERROR      ? kProbeErr
+          : r.status == BS_PARAMETER_ERROR  ? kProbeErr
+          : (r.status == BS_OK && r.meets_slo) ? kProbePass
+                                               : kProbeFail);
 }
 
 // Whole-trace simulations (bs_simulate_instance): thread i runs trace i.
@@ -646,7 +672,8 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
   const size_t o_order = o_koff + up(8ull * n_tables);
   const size_t in_bytes = o_order + up(sizeof(ProbeId) * probe_total);
   const size_t o_kept = in_bytes, o_kc = o_kept + up(4ull * kept_total), o_probe = o_kc + up(8ull * stream_total);
-  const size_t o_heap = o_probe + up(sizeof(ProbeOut) * probe_total);
+  const size_t o_pst = o_probe + up(sizeof(ProbeOut) * probe_total);
+  const size_t o_heap = o_pst + up(4ull * probe_total);
   const size_t heap_rows = any_decode ? static_cast<size_t>(probe_total) : 0;
   const size_t total = o_heap + up(sizeof(Resident) * heap_rows * heap_cap);
   char* d = static_cast<char*>(ctx->dev_buf(kSlotWork, total));
@@ -673,21 +700,45 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
     }
     so[n_tables] = stream_total;
   }
-  {  // launch order, across tables: decode probes at high rate steps run longest (feasible ones never
-     // stop early), then by rate step; long ones first
+  {  // launch order, across tables: the levels of max_goodput's search tree (k_max; 1; the midpoints of
+     // (1, k_max) level by level), so the probes the search needs start first and the deeper ones run
+     // only where the published outcomes still leave them on the path; within a level decode probes
+     // (the long ones), higher rate steps first
     ProbeId* po = reinterpret_cast<ProbeId*>(h + o_order);
+    std::vector<std::vector<std::pair<int, long long>>> by_depth;  // (table, k)
+    for (int t = 0; t < n_tables; ++t) {
+      const long long km = tabs[t].n_streams / std::max(1, reps);
+      if (km < 1) continue;
+      auto put = [&](int depth, long long k) {
+        if (static_cast<int>(by_depth.size()) <= depth) by_depth.resize(depth + 1);
+        by_depth[depth].push_back({t, k});
+      };
+      put(0, km);
+      if (km > 1) put(1, 1);
+      std::vector<std::pair<long long, long long>> lv{{1, km}}, nx;
+      for (int depth = 2; !lv.empty(); ++depth) {
+        nx.clear();
+        for (const auto& iv : lv) {
+          if (iv.second - iv.first <= 1) continue;
+          const long long mid = iv.first + (iv.second - iv.first) / 2;
+          put(depth, mid);
+          nx.push_back({iv.first, mid});
+          nx.push_back({mid, iv.second});
+        }
+        lv.swap(nx);
+      }
+    }
     long long w = 0;
-    long long kmax_all = 0;
-    for (int t = 0; t < n_tables; ++t) kmax_all = std::max(kmax_all, tabs[t].n_streams / std::max(1, reps));
-    for (int pass = 0; pass < 2; ++pass)
-      for (long long k = kmax_all; k >= 1; --k)
-        for (int t = 0; t < n_tables; ++t) {
-          if (k > tabs[t].n_streams / std::max(1, reps)) continue;
+    for (auto& lvl : by_depth) {
+      std::stable_sort(lvl.begin(), lvl.end(), [](const auto& a, const auto& b) { return a.second > b.second; });
+      for (int pass = 0; pass < 2; ++pass)
+        for (const auto& tk : lvl)
           for (int c = 0; c < n_cand; ++c) {
             if ((cands[c].phase == BS_PHASE_DECODE) != (pass == 0)) continue;
-            for (int j = 0; j < reps; ++j) po[w++] = ProbeId{t, c, (k - 1) * reps + j};
+            for (int j = 0; j < reps; ++j) po[w++] = ProbeId{tk.first, c, (tk.second - 1) * reps + j};
           }
-        }
+    }
+    if (w != probe_total) return set_error(ctx, BS_CUDA_ERROR, "config table: probe order incomplete");
   }
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
   ctx->last_h2d = in_bytes;
@@ -708,13 +759,15 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
                 slo->ttft_ms, slo->tpot_ms};
   ProbeOut* dprobe = reinterpret_cast<ProbeOut*>(d + o_probe);
   Resident* dheap = reinterpret_cast<Resident*>(d + o_heap);
+  int* dpst = reinterpret_cast<int*>(d + o_pst);
+  BS_CUDA_TRY(ctx, cudaMemsetAsync(dpst, 0, 4ull * probe_total, ctx->stream));
   const bool heap_smem = heap_cap <= 1024;
   const size_t smem4 = 4 * warp_scratch_bytes(static_cast<int>(heap_cap), heap_smem);
   BS_CUDA_TRY(ctx, set_smem_limit(reinterpret_cast<const void*>(probe_kernel), smem4));
   probe_kernel<<<static_cast<unsigned>((probe_total * 32 + 127) / 128), 128, smem4, ctx->stream>>>(
       models->dm, tr, reinterpret_cast<const TableDev*>(d + o_tabs), reinterpret_cast<const DCand*>(d + o_cand),
       dkept, dkc, pol, dheap, static_cast<int>(heap_cap), heap_smem ? 1 : 0,
-      reinterpret_cast<const ProbeId*>(d + o_order), probe_total, dprobe);
+      reinterpret_cast<const ProbeId*>(d + o_order), probe_total, dprobe, dpst, reps);
   BS_LAUNCH_CHECK(ctx);
   BS_CUDA_TRY(ctx, cudaEventRecord(ev[2], ctx->stream));
   ProbeOut* hp = reinterpret_cast<ProbeOut*>(h + in_bytes);
@@ -725,17 +778,21 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
-    long long mx = 0, sum = 0;
+    long long mx = 0, sum = 0, skipped = 0, abandoned = 0;
     for (long long i = 0; i < probe_total; ++i) {
       mx = std::max(mx, hp[i].events);
       sum += hp[i].events;
+      if (hp[i].status == kSimAborted) (hp[i].completed < 0 ? skipped : abandoned) += 1;
     }
     ctx->stats[0] = a;
     ctx->stats[1] = b;
     ctx->stats[2] = 0.0;
     ctx->stats[3] = static_cast<double>(mx);
     ctx->stats[4] = static_cast<double>(sum);
-    ctx->n_stats = 5;
+    ctx->stats[5] = static_cast<double>(probe_total);
+    ctx->stats[6] = static_cast<double>(skipped);
+    ctx->stats[7] = static_cast<double>(abandoned);
+    ctx->n_stats = 8;
     for (auto& e : ev) cudaEventDestroy(e);
   }
 
@@ -750,6 +807,7 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
       auto outcome = [&](long long k) -> int {
         for (int j = 0; j < reps; ++j) {
           const ProbeOut& p = hpt[static_cast<size_t>(c) * tb.n_streams + (k - 1) * reps + j];
+          if (p.status == kSimAborted) return -101;  // the path never leaves the probes that ran
           if (p.empty) continue;
           if (p.status == BS_MODEL_ERROR) return -p.model_err;
           if (p.status == BS_PARAMETER_ERROR) return -100;
@@ -759,6 +817,7 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
       };
       const SearchResult sr = replay_search(k_max[t], outcome);
       if (sr.model_err == 100) return set_error(ctx, BS_CUDA_ERROR, "config table: device resident scratch too small");
+      if (sr.model_err == 101) return set_error(ctx, BS_CUDA_ERROR, "config table: search path reached a pruned probe");
       if (sr.model_err) {
         ot[c].error_code = BS_MODEL_ERROR;
         std::snprintf(ot[c].error, sizeof ot[c].error, "%s", model_err_msg(sr.model_err));

@@ -27,6 +27,66 @@ struct SimTrace {
   double duration_ms;
 };
 
+// Goodput-search pruning.  max_goodput (placement.hpp:154-199) visits k_max,
+// then 1, then lo + (hi - lo) / 2 until hi - lo <= 1; which k it visits
+// depends only on the outcomes along that path.  A probe grid evaluates all k
+// at once, so every probe publishes its outcome, and a probe whose k can no
+// longer be on the path, given the outcomes published so far, is skipped (at
+// start) or abandoned (polled during the run).  Outcomes only accumulate and
+// each is final, so "off the path" is final too, and the probes the host
+// replay reads (the path, and (k*, replicate 0) for E_c) always run to their
+// exact end.
+enum : int { kProbePending = 0, kProbePass = 1, kProbeFail = 2, kProbeErr = 3, kProbeSkipped = 4 };
+constexpr int kSimAborted = -7;  // SimOut.status of an abandoned probe
+
+struct SearchView {
+  const int* st;  // outcome codes of one candidate's probes, index (k - 1) * reps + j
+  long long k_max;
+  int reps;
+};
+
+// feasible(k) of max_goodput as far as published: every replicate in order
+// (placement.hpp:165-178): 1 pass, 0 fail, -1 ModelError, 2 not known yet.
+__device__ __forceinline__ int search_outcome(const SearchView& v, long long k) {
+  const volatile int* s = v.st + (k - 1) * v.reps;
+  for (int j = 0; j < v.reps; ++j) {
+    const int c = s[j];
+    if (c == kProbePass) continue;
+    if (c == kProbeFail) return 0;
+    if (c == kProbeErr) return -1;
+    return 2;
+  }
+  return 1;
+}
+
+// Can the reference's search still visit k?  Walks the path through the
+// published outcomes; an unknown outcome leaves every k of its open interval
+// possible.
+__device__ inline bool search_alive(const SearchView& v, long long k) {
+  if (k == v.k_max) return true;
+  int o = search_outcome(v, v.k_max);
+  if (o == 2) return true;
+  if (o != 0) return false;  // saturated, or a ModelError ended the search
+  if (k == 1) return true;
+  o = search_outcome(v, 1);
+  if (o == 2) return true;
+  if (o != 1) return false;
+  long long lo = 1, hi = v.k_max;
+  while (hi - lo > 1) {
+    if (k <= lo || k >= hi) return false;
+    const long long mid = lo + (hi - lo) / 2;
+    if (k == mid) return true;
+    o = search_outcome(v, mid);
+    if (o == 2) return true;
+    if (o < 0) return false;
+    if (o == 1)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return false;
+}
+
 struct SimParams {
   int tp;
   double freq;
@@ -37,7 +97,12 @@ struct SimParams {
   double ttft_bound;
   double tpot_bound;
   int early_exit;  // stop at the first SLO violation (feasibility only)
+  const SearchView* search;  // non-null: abandon the run once rate step k is off the search path
+  long long k;
 };
+
+constexpr int kSearchPollPrefill = 64;  // batches between polls (scalar event loop)
+constexpr int kSearchPollDecode = 8;    // event windows between polls (warp simulator)
 
 struct SimOut {
   int status;      // BS_OK, BS_SIMULATION_ERROR, BS_MODEL_ERROR
@@ -369,8 +434,16 @@ __device__ inline SimOut simulate_prefill(const DModels& m, const SimTrace& tr, 
     return true;
   };
 
+  int poll = 0;
   for (;;) {
     if (!active && qhead < arr) {
+      if (p.search && ++poll == kSearchPollPrefill) {
+        poll = 0;
+        if (!search_alive(*p.search, p.k)) {
+          o.status = kSimAborted;
+          return o;
+        }
+      }
       while (arr < tr.n && tr.arrival[tr.kept[arr]] <= now) ++arr;  // simulator.hpp:350-353
       // form_prefill_batch (scheduler.hpp:40-66) over the queue
       long long tokens = 0, npick = 0, sum = 0;
@@ -658,7 +731,17 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
     return true;
   };
 
+  int poll = 0;
   while (arr < tr.n || whead < arr || n_res > 0) {
+    if (p.search && ++poll == kSearchPollDecode) {  // warp-uniform: lane 0's view decides
+      poll = 0;
+      int alive = lane == 0 ? (search_alive(*p.search, p.k) ? 1 : 0) : 0;
+      alive = __shfl_sync(0xffffffffu, alive, 0);
+      if (!alive) {
+        o.status = kSimAborted;
+        return o;
+      }
+    }
     // ---- boundary: pull arrivals, admit (simulator.hpp:515-519, 455-470)
     while (arr < tr.n && tr.arrival[tr.kept[arr]] <= now) ++arr;
     int n_new = 0;
