@@ -195,6 +195,24 @@ __device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, in
   return lo;
 }
 
+// Does the non-switching child (step B0[k][last], k >= 1) pass meets_slo's check?
+__device__ __forceinline__ bool diag_passes(const DTables* __restrict__ T, int k, double t, int last) {
+  return !(__dsub_rn(__dadd_rn(t, T->B0[k][last]), T->minarr[k]) > T->ttft);
+}
+
+// Number of children of (t, last) at level k that pass the check, without
+// visiting them: the sorted prefix, less f == last if it lies in it (its
+// real step is B0), plus the non-switching child if it passes.
+__device__ __forceinline__ int count_feasible_children(const DTables* __restrict__ T, int k, int nc, double t,
+                                                       int last) {
+  int c = feasible_prefix(T, k, nc, t);
+  if (k > 0) {
+    if (T->rank[k][last] < c) c -= 1;
+    if (diag_passes(T, k, t, last)) c += 1;
+  }
+  return c;
+}
+
 // Block-aggregated appends to two counters (one atomic per counter per
 // block instead of per warp): each lane that wants a slot gets one.  Every
 // thread of the block must call it.
@@ -268,8 +286,7 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
         // leaf (meets_slo stops at the first violation): drop it here
         if (ok && to_final && T->sorted_ok && k + 1 < T->K) {
           const int kk = k + 1;
-          ok = feasible_prefix(T, kk, nc, ct) > 0 ||
-               !(__dsub_rn(__dadd_rn(ct, T->B0[kk][f]), T->minarr[kk]) > T->ttft);
+          ok = feasible_prefix(T, kk, nc, ct) > 0 || diag_passes(T, kk, ct, f);
         }
       }
     }
@@ -390,12 +407,9 @@ __device__ __forceinline__ int for_feasible_children(const DTables* __restrict__
     fn(f, ct, __dadd_rn(num, E[f]), __dadd_rn(den, A[f]));
     ++passed;
   }
-  if (k > 0) {
-    const double ct = __dadd_rn(t, T->B0[k][last]);
-    if (!(__dsub_rn(ct, T->minarr[k]) > T->ttft)) {
-      fn(last, ct, __dadd_rn(num, E[last]), __dadd_rn(den, A[last]));
-      ++passed;
-    }
+  if (k > 0 && diag_passes(T, k, t, last)) {
+    fn(last, __dadd_rn(t, T->B0[k][last]), __dadd_rn(num, E[last]), __dadd_rn(den, A[last]));
+    ++passed;
   }
   return passed;
 }
@@ -425,8 +439,7 @@ __device__ __forceinline__ void leaves_sorted(const DTables* __restrict__ T, int
     int passed = nc;
     bool diag = true;
     if (k > 0) {  // the non-switching leaf f == last is re-tested with its own step
-      const double td = __dadd_rn(t, T->B0[k][last]);
-      diag = !(__dsub_rn(td, m) > ttft);
+      diag = diag_passes(T, k, t, last);
       if (!diag) passed -= 1;
     }
     a.count += static_cast<unsigned long long>(passed);
@@ -439,8 +452,7 @@ __device__ __forceinline__ void leaves_sorted(const DTables* __restrict__ T, int
     return;
   }
   if (filt && row_dominated(a, num, den)) {  // count only
-    a.count += static_cast<unsigned long long>(
-        for_feasible_children(T, k, nc, t, num, den, last, [&](int, double, double, double) {}));
+    a.count += static_cast<unsigned long long>(count_feasible_children(T, k, nc, t, last));
     return;
   }
   a.count += static_cast<unsigned long long>(
