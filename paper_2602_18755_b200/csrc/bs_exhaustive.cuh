@@ -414,16 +414,19 @@ __device__ __forceinline__ int for_feasible_children(const DTables* __restrict__
   return passed;
 }
 
-// Leaves (level k = K-1) under a parent, sorted path: only passing leaves
-// are visited; each needs just its objective.
-__device__ __forceinline__ void leaves_sorted(const DTables* __restrict__ T, int k, int nc, double t, double num,
-                                              double den, int last, unsigned long long code_base, bool filt,
-                                              double hint, LeafAcc& a) {
-  const double m = T->minarr[k], ttft = T->ttft;
-  const double* __restrict__ sb = T->sb[k];
+// Leaves (level k >= 1) under a parent with clock t whose sorted-prefix
+// count c = feasible_prefix(T, k, nc, t) is known: count them in closed form,
+// skip a dominated row, else visit only the passing leaves.
+__device__ __forceinline__ void leaves_counted(const DTables* __restrict__ T, int k, int nc, double t, double num,
+                                               double den, int last, int c, unsigned long long code_base, bool filt,
+                                               double hint, LeafAcc& a) {
+  const bool diag = diag_passes(T, k, t, last);
+  a.count += static_cast<unsigned long long>(c - (T->rank[k][last] < c ? 1 : 0) + (diag ? 1 : 0));
+  if (filt && row_dominated(a, num, den)) return;
   const double* __restrict__ E = T->E[k];
   const double* __restrict__ A = T->A[k];
-  auto leaf = [&](int f, double nl, double dl) {
+  auto leaf = [&](int f) {
+    const double nl = __dadd_rn(num, E[f]), dl = __dadd_rn(den, A[f]);
     if (filt && nl > __dmul_rn(a.thr_scaled, dl)) return;  // provably worse than a known feasible key
     const double obj = dl > 0.0 ? __ddiv_rn(nl, dl) : 0.0;  // dvfs.hpp:170
     const unsigned long long code = code_base + static_cast<unsigned long long>(f);
@@ -433,40 +436,57 @@ __device__ __forceinline__ void leaves_sorted(const DTables* __restrict__ T, int
       set_threshold(a, hint);
     }
   };
-  // all switched leaves pass when the largest step does (monotonicity)
-  const double tmax = k == 0 ? sb[nc - 1] : __dadd_rn(t, sb[nc - 1]);
-  if (!(__dsub_rn(tmax, m) > ttft)) {
-    int passed = nc;
-    bool diag = true;
-    if (k > 0) {  // the non-switching leaf f == last is re-tested with its own step
-      diag = diag_passes(T, k, t, last);
-      if (!diag) passed -= 1;
-    }
-    a.count += static_cast<unsigned long long>(passed);
-    if (filt && row_dominated(a, num, den)) return;
+  if (c == nc) {  // every switched leaf passes: natural order, no index loads
 #pragma unroll 4
-    for (int f = 0; f < nc; ++f) {
-      if (k > 0 && f == last && !diag) continue;
-      leaf(f, __dadd_rn(num, E[f]), __dadd_rn(den, A[f]));
-    }
+    for (int f = 0; f < nc; ++f)
+      if (f != last || diag) leaf(f);
     return;
   }
-  if (filt && row_dominated(a, num, den)) {  // count only
-    a.count += static_cast<unsigned long long>(count_feasible_children(T, k, nc, t, last));
-    return;
+  const unsigned char* __restrict__ ord = T->ord[k];
+  for (int j = 0; j < c; ++j) {
+    const int f = ord[j];
+    if (f != last) leaf(f);
   }
-  a.count += static_cast<unsigned long long>(
-      for_feasible_children(T, k, nc, t, num, den, last, [&](int f, double, double nl, double dl) { leaf(f, nl, dl); }));
+  if (diag) leaf(last);
 }
 
-// Two bottom levels below a node at depth K-2, sorted path.
+// Two bottom levels below a node at depth K-2, sorted path.  The switched
+// children are visited in step order, so their clocks never decrease and the
+// leaf level's sorted-prefix count never increases: one binary search for
+// the first child, then a downward walk.
 __device__ __forceinline__ void two_sorted(const DTables* __restrict__ T, int k, int nc, double t, double num,
                                            double den, int last, unsigned long long code_base, double hint,
                                            LeafAcc& a) {
-  for_feasible_children(T, k, nc, t, num, den, last, [&](int g, double t2, double n2, double d2) {
-    const bool filt = T->filter_ok && d2 >= kFilterMinDen;
-    leaves_sorted(T, k + 1, nc, t2, n2, d2, g, (code_base + static_cast<unsigned long long>(g)) * nc, filt, hint, a);
-  });
+  const int c = feasible_prefix(T, k, nc, t);
+  const unsigned char* __restrict__ ord = T->ord[k];
+  const double* __restrict__ sb = T->sb[k];
+  const double* __restrict__ E = T->E[k];
+  const double* __restrict__ A = T->A[k];
+  const int kl = k + 1;
+  const double ml = T->minarr[kl], ttft = T->ttft;
+  const double* __restrict__ sbl = T->sb[kl];
+  int cl = -1;
+  for (int j = 0; j < c; ++j) {
+    const int g = ord[j];
+    if (k > 0 && g == last) continue;
+    const double t2 = k == 0 ? sb[j] : __dadd_rn(t, sb[j]);
+    if (cl < 0) {
+      cl = feasible_prefix(T, kl, nc, t2);
+    } else {
+      while (cl > 0 && __dsub_rn(__dadd_rn(t2, sbl[cl - 1]), ml) > ttft) --cl;
+    }
+    const double d2 = __dadd_rn(den, A[g]);
+    leaves_counted(T, kl, nc, t2, __dadd_rn(num, E[g]), d2, g, cl,
+                   (code_base + static_cast<unsigned long long>(g)) * nc, T->filter_ok && d2 >= kFilterMinDen, hint,
+                   a);
+  }
+  if (k > 0 && diag_passes(T, k, t, last)) {
+    const double t2 = __dadd_rn(t, T->B0[k][last]);
+    const double d2 = __dadd_rn(den, A[last]);
+    leaves_counted(T, kl, nc, t2, __dadd_rn(num, E[last]), d2, last, feasible_prefix(T, kl, nc, t2),
+                   (code_base + static_cast<unsigned long long>(last)) * nc, T->filter_ok && d2 >= kFilterMinDen,
+                   hint, a);
+  }
 }
 
 // Two bottom levels (K-2, K-1) below a node at depth K-2.
