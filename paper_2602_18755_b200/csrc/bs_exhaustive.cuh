@@ -80,72 +80,6 @@ __host__ __device__ inline FinalList final_at(void* base, unsigned long long cap
   return f;
 }
 
-__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
-                                                               const DWaiting* W, const DRunning* R, DTables* tables,
-                                                               ExCtl* ctl, int n, const DFastPair* fg) {
-  __shared__ int s_status;
-  const int d = blockIdx.x;
-  if (d >= n) return;
-  if (d == 0 && threadIdx.x < kMaxK + 3) {  // counters of this run
-    if (threadIdx.x <= kMaxK)
-      ctl->level_count[threadIdx.x] = 0;
-    else if (threadIdx.x == kMaxK + 1)
-      ctl->final_count = 0;
-    else
-      ctl->overflow = 0;
-  }
-  const DProblem pr = probs[d];
-  const DMpcCfg& c = cfgs[pr.cfg];
-  DTables* T = &tables[d];
-  const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
-  build_tables(m, pr, c, W + pr.wait_off, R + pr.run_off, T, &s_status, fp ? fp->lat : nullptr,
-               fp ? fp->pw : nullptr, fp && fp->share);
-  if (threadIdx.x == 0) {
-    int st = s_status;
-    if (st == BS_OK) {
-      unsigned any = 0;
-      for (int k = 0; k < T->K; ++k) any |= T->bad_lat[k] | T->bad_pow[k];
-      if (any) st = BS_MODEL_ERROR;
-    }
-    T->status = st;
-  }
-}
-
-// One thread per problem: reset the argmin slots, seed the roots.
-__global__ void seed_kernel(const DTables* __restrict__ tables, int n, Key128* best, unsigned long long* feas,
-                            ExCtl* ctl, Frontier L0, FinalList fin, unsigned long long cap0,
-                            unsigned long long cap_final) {
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= n) return;
-  best[d].obj = ~0ull;
-  best[d].code = ~0ull;
-  feas[d] = 0ull;
-  const DTables* T = &tables[d];
-  if (T->status != BS_OK || T->K == 0) return;
-  const int FD = T->K - sweep_levels(T->K, T->nc);
-  if (FD == 0) {
-    const unsigned long long s = atomicAdd(&ctl->final_count, 1ull);
-    if (s < cap_final) {
-      fin.d[s] = d;
-      fin.code[s] = 0;
-    } else {
-      atomicAdd(&ctl->overflow, 1ull);
-    }
-  } else {
-    const unsigned long long s = atomicAdd(&ctl->level_count[0], 1ull);
-    if (s < cap0) {
-      L0.d[s] = d;
-      L0.code[s] = 0;
-      L0.t[s] = 0.0;
-      L0.num[s] = 0.0;
-      L0.den[s] = 0.0;
-      L0.last[s] = -1;
-    } else {
-      atomicAdd(&ctl->overflow, 1ull);
-    }
-  }
-}
-
 // Child of node (t, num, den, last) at level k, digit f: meets_slo's step
 // (dvfs.hpp:111-118) and the time_weighted_power accumulation (167-168).
 // Returns feasibility at level k.
@@ -257,7 +191,8 @@ __device__ __forceinline__ void block_append2(unsigned long long* c0, bool w0, u
 // Level k: every (depth-k node, digit) pair; feasible children at depth
 // k + 1 go to the next list, or to the final list at their problem's FD.
 __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl, Frontier in,
-                                                  Frontier out, FinalList fin, int nc_max, unsigned long long cap_out,
+                                                  Frontier out, FinalList fin, int nc_max, unsigned long long div_magic,
+                                                  unsigned long long cap_out,
                                                   unsigned long long cap_final) {
   // an overflowed level still counts every append (the exact need of the
   // retry); the levels below it are not expanded
@@ -273,7 +208,9 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
     double ct = 0.0, cn = 0.0, cd = 0.0;
     unsigned long long cc = 0;
     if (j < total) {
-      const unsigned long long node = j / static_cast<unsigned long long>(nc_max);
+      // j / nc_max by a multiply-high: with M = ceil(2^64 / d) the quotient
+      // is exact for j < 2^58 and d <= 32 (error < j / 2^64 < 1 / d)
+      const unsigned long long node = nc_max == 1 ? j : __umul64hi(j, div_magic);
       f = static_cast<int>(j - node * nc_max);
       d = in.d[node];
       const DTables* __restrict__ T = &tables[d];
@@ -307,6 +244,102 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
         out.num[so] = cn;
         out.den[so] = cd;
         out.last[so] = f;
+      } else {
+        atomicAdd(&ctl->overflow, 1ull);
+      }
+    }
+  }
+}
+
+// One CTA per decision: the tables, the argmin slot reset, and the first
+// levels of the search.  The prefixes of depth D0 = min(2, FD) are expanded
+// here (nc^D0 per decision) and appended to the depth-D0 list (or, at FD, to
+// the final list), so the BFS starts at depth 2.  The run's counters are
+// zeroed by the host before this launch.
+__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
+                                                               const DWaiting* W, const DRunning* R, DTables* tables,
+                                                               ExCtl* ctl, int n, const DFastPair* fg, Key128* best,
+                                                               unsigned long long* feas, Frontier L2,
+                                                               FinalList fin, unsigned long long cap_level,
+                                                               unsigned long long cap_final) {
+  __shared__ int s_status;
+  const int d = blockIdx.x;
+  if (d >= n) return;
+  const DProblem pr = probs[d];
+  const DMpcCfg& c = cfgs[pr.cfg];
+  DTables* T = &tables[d];
+  const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
+  build_tables(m, pr, c, W + pr.wait_off, R + pr.run_off, T, &s_status, fp ? fp->lat : nullptr,
+               fp ? fp->pw : nullptr, fp && fp->share);
+  if (threadIdx.x == 0) {
+    int st = s_status;
+    if (st == BS_OK) {
+      unsigned any = 0;
+      for (int k = 0; k < T->K; ++k) any |= T->bad_lat[k] | T->bad_pow[k];
+      if (any) st = BS_MODEL_ERROR;
+    }
+    T->status = st;
+    s_status = st;
+    best[d].obj = ~0ull;
+    best[d].code = ~0ull;
+    feas[d] = 0ull;
+  }
+  __syncthreads();
+  const int K = T->K, nc = T->nc;
+  if (s_status != BS_OK || K == 0) return;
+  const int FD = K - sweep_levels(K, nc);
+  if (FD == 0) {
+    if (threadIdx.x == 0) {
+      const unsigned long long sl = atomicAdd(&ctl->final_count, 1ull);
+      if (sl < cap_final) {
+        fin.d[sl] = d;
+        fin.code[sl] = 0;
+      } else {
+        atomicAdd(&ctl->overflow, 1ull);
+      }
+    }
+    return;
+  }
+  const int D0 = FD < 2 ? FD : 2;
+  const int width = D0 == 1 ? nc : nc * nc;
+  const bool to_final = D0 == FD;
+  for (int base = 0; base < width; base += blockDim.x) {  // uniform trip count: block_append2 needs every thread
+    const int e = base + threadIdx.x;
+    bool ok = false;
+    double t = 0.0, num = 0.0, den = 0.0;
+    int last = -1;
+    if (e < width) {
+      const int f0 = D0 == 1 ? e : e / nc, f1 = D0 == 1 ? -1 : e - f0 * nc;
+      ok = child_state(T, 0, 0.0, 0.0, 0.0, -1, f0, t, num, den);
+      last = f0;
+      if (ok && D0 == 2) {
+        double t1, n1, d1;
+        ok = child_state(T, 1, t, num, den, f0, f1, t1, n1, d1);
+        t = t1;
+        num = n1;
+        den = d1;
+        last = f1;
+      }
+      // a final node none of whose children passes has no feasible leaf (as in bfs_kernel)
+      if (ok && to_final && T->sorted_ok && FD < K) ok = feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
+    }
+    unsigned long long sf, so;
+    block_append2(&ctl->final_count, ok && to_final, &ctl->level_count[D0], ok && !to_final, &sf, &so);
+    if (ok && to_final) {
+      if (sf < cap_final) {
+        fin.d[sf] = d;
+        fin.code[sf] = static_cast<unsigned long long>(e);
+      } else {
+        atomicAdd(&ctl->overflow, 1ull);
+      }
+    } else if (ok) {
+      if (so < cap_level) {
+        L2.d[so] = d;
+        L2.code[so] = static_cast<unsigned long long>(e);
+        L2.t[so] = t;
+        L2.num[so] = num;
+        L2.den[so] = den;
+        L2.last[so] = last;
       } else {
         atomicAdd(&ctl->overflow, 1ull);
       }

@@ -6,9 +6,10 @@
 // until the final copy-out):
 //   prepare_kernel   1 CTA / problem: project_batches (dvfs.hpp:63-100) by
 //                    one thread, then the K x N (lat, pow) tables by all
-//                    threads through the bit-exact interpolator.
-//   seed_kernel      1 thread / problem: reset argmin slots, seed the roots.
-//   bfs_kernel       x (max depth of final nodes): level-synchronous
+//                    threads through the bit-exact interpolator; resets the
+//                    argmin slot and expands the first two levels (N^2
+//                    prefixes) straight into the depth-2 list.
+//   bfs_kernel       x (max depth of final nodes - 2): level-synchronous
 //                    expansion of every feasible prefix of every decision,
 //                    compacted with warp-aggregated appends (meets_slo fails
 //                    at the first violated batch, so violated prefixes have
@@ -417,17 +418,17 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   }
   const Frontier lev[2] = {frontier_at(run->dLev[0], run->cap_level), frontier_at(run->dLev[1], run->cap_level)};
   const FinalList fin = final_at(run->dFin, run->cap_final);
+  BS_CUDA_TRY(ctx, cudaMemsetAsync(run->dCtl, 0, sizeof(ExCtl), ctx->stream));
   prepare_kernel<<<n, kPrepThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
-                                                      run->dT, run->dCtl, n, run->dFG);
+                                                      run->dT, run->dCtl, n, run->dFG, run->dBest, run->dFeas, lev[0],
+                                                      fin, run->cap_level, run->cap_final);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
-  seed_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, n, run->dBest, run->dFeas, run->dCtl, lev[0], fin,
-                                                        run->cap_level, run->cap_final);
-  BS_LAUNCH_CHECK(ctx);
-  BS_REC(2);
-  for (int k = 0; k < run->bfs_levels; ++k) {
+  BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel
+  for (int k = 2; k < run->bfs_levels; ++k) {  // depth-2 lists come from prepare_kernel
     bfs_kernel<<<run->bfs_grid, 256, 0, ctx->stream>>>(run->dT, k, run->dCtl, lev[k & 1], lev[(k + 1) & 1], fin,
-                                                       run->max_nc, run->cap_level, run->cap_final);
+                                                       run->max_nc, ~0ull / static_cast<unsigned>(run->max_nc) + 1,
+                                                       run->cap_level, run->cap_final);
     BS_LAUNCH_CHECK(ctx);
   }
   BS_REC(3);
