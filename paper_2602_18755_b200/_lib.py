@@ -6,13 +6,15 @@ visible, every entry point of the package raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from . import _abi
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libbiscale_gpu.so"
+# BS_LIB_PATH: an alternative in-tree build (A/B experiments of compile-time variants)
+LIB_PATH = Path(os.environ.get("BS_LIB_PATH", str(PKG / "libbiscale_gpu.so")))
 
 _lock = threading.Lock()
 _lib = None

@@ -234,6 +234,7 @@ struct DTables {
   unsigned char ord[kMaxK][kMaxCand];
   unsigned char rank[kMaxK][kMaxCand];
   int sorted_ok;
+  int FD;  // exhaustive search: depth of the final nodes, K - sweep_levels(K, nc) (set by prepare_kernel)
   // Per-level bounds for the leaf-row skip: amax = max_f A, pmin_lo =
   // fl(min_f P * (1 - 2^-50)) <= min_f P * (1 - u).
   double amax[kMaxK];

@@ -19,6 +19,10 @@
 // a 128-bit CAS.  Work is proportional to the feasible part of the tree, and
 // every level is spread over the whole GPU however uneven the decisions are.
 
+#ifndef BS_SWEEP3_MIN
+#define BS_SWEEP3_MIN 16777216.0  // prefixes at depth K - 2 above which the sweep takes 3 levels
+#endif
+
 struct ExCtl {
   unsigned long long level_count[kMaxK + 1];  // BFS list sizes per depth
   unsigned long long final_count;
@@ -32,7 +36,7 @@ __host__ __device__ inline int sweep_levels(int K, int nc) {
   if (K <= 2) return K;
   double np = 1.0;
   for (int i = 0; i < K - 2; ++i) np *= nc;
-  return np > 16777216.0 ? 3 : 2;
+  return np > BS_SWEEP3_MIN ? 3 : 2;
 }
 
 // Frontier lists in HBM, structure of arrays.
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
       if (f < nc) {
         ok = child_state(T, k, in.t[node], in.num[node], in.den[node], in.last[node], f, ct, cn, cd);
         cc = in.code[node] * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
-        to_final = (k + 1) == T->K - sweep_levels(T->K, nc);
+        to_final = (k + 1) == T->FD;
         // a final node none of whose children passes meets_slo has no feasible
         // leaf (meets_slo stops at the first violation): drop it here
         if (ok && to_final && T->sorted_ok && k + 1 < T->K) {
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
 // here (nc^D0 per decision) and appended to the depth-D0 list (or, at FD, to
 // the final list), so the BFS starts at depth 2.  The run's counters are
 // zeroed by the host before this launch.
-__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
+__global__ void __launch_bounds__(kPrepThreads, 4) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
                                                                const DWaiting* W, const DRunning* R, DTables* tables,
                                                                ExCtl* ctl, int n, const DFastPair* fg, Key128* best,
                                                                unsigned long long* feas, Frontier L2,
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const 
   const int K = T->K, nc = T->nc;
   if (s_status != BS_OK || K == 0) return;
   const int FD = K - sweep_levels(K, nc);
+  if (threadIdx.x == 0) T->FD = FD;
   if (FD == 0) {
     if (threadIdx.x == 0) {
       const unsigned long long sl = atomicAdd(&ctl->final_count, 1ull);
@@ -347,9 +352,11 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(DModels m, const 
   }
 }
 
-#ifndef BS_SWEEP_MINB
-#define BS_SWEEP_MINB 3  // resident CTAs per SM the sweep is register-budgeted for
-#endif
+// Resident CTAs per SM the sweep is register-budgeted for: 3 (80 registers)
+// for two swept levels, 4 (64) for three, where more warps hide the longer
+// per-thread walks (measured: C2 0.42 vs 0.45 ms; C5 3,838 vs 4,298
+// decisions/s).
+constexpr int kSweepMinB2 = 3, kSweepMinB3 = 4;
 
 // Per-thread accumulator of the sweep.
 struct LeafAcc {
@@ -593,7 +600,8 @@ __device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsig
 }
 
 // One thread per final node: the I bottom levels of its subtree.
-__global__ void __launch_bounds__(256, BS_SWEEP_MINB) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
                                                     FinalList fin, Key128* best, unsigned long long* feas,
                                                     unsigned long long cap_final) {
   if (ctl->overflow) return;  // the run is repeated with larger lists (one_shot): skip the sweep
@@ -607,8 +615,8 @@ __global__ void __launch_bounds__(256, BS_SWEEP_MINB) sweep_kernel(const DTables
     const unsigned long long code = fin.code[j];
     const DTables* __restrict__ T = &tables[d];
     const int K = T->K, nc = T->nc;
-    const int I = sweep_levels(K, nc);
-    const int FD = K - I;
+    const int FD = T->FD;
+    const int I = K - FD;
     double t, num, den;
     int last;
     walk(T, nc, FD, code, t, num, den, last);

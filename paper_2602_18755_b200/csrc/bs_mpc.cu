@@ -30,7 +30,7 @@ using namespace bs;
 
 namespace {
 
-constexpr int kPrepThreads = 256;
+constexpr int kPrepThreads = 128;  // K x N <= 128 table entries in one pass; 4 CTAs / SM
 constexpr double kFilterScale = 1.0 + 0x1p-50;  // C in the filter bound
 constexpr double kFilterMinBest = 0x1p-100;
 constexpr double kFilterMinDen = 0x1p-900;
@@ -237,7 +237,8 @@ struct MpcRun {
   void* dFin = nullptr;
   DMpcOut* dOut = nullptr;
   DLevel* dLv = nullptr;
-  int bfs_grid = 0, sweep_grid = 0;
+  int bfs_grid = 0, sweep_grid2 = 0, sweep_grid3 = 0;
+  bool sweep3 = false;  // some decision may sweep three levels (sweep_levels)
   ExCtl ctl_host{};  // counters of an overflowed run (exact totals of the levels before the first overflow)
   const DFastPair* dFG = nullptr;       // reduced grids per (configuration, tp) pair (pk.fg_pairs)
   std::vector<DFastPair> hFG;           // their host build
@@ -325,6 +326,7 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
   run->cap_level = 0;
   run->cap_final = 0;
   run->bfs_levels = 0;
+  run->sweep3 = false;
   for (int i = 0; i < n; ++i) {
     run->cfg_of[i] = problems[i].cfg_index;
     run->target[i] = problems[i].snap.target_freq_mhz;
@@ -332,6 +334,7 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
     const DMpcCfg& c = run->hc[problems[i].cfg_index];
     const int FD = c.horizon - sweep_levels(c.horizon, c.nc);
     run->bfs_levels = std::max(run->bfs_levels, FD);
+    if (sweep_levels(c.horizon, c.nc) == 3) run->sweep3 = true;
     run->cap_final += ipow(static_cast<unsigned long long>(c.nc), FD);
     run->cap_level += ipow(static_cast<unsigned long long>(c.nc), FD > 0 ? FD - 1 : 0);
   }
@@ -414,7 +417,8 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   }
   if (!run->bfs_grid) {
     run->bfs_grid = grid_for(ctx, reinterpret_cast<const void*>(bfs_kernel), 256);
-    run->sweep_grid = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel), 256);
+    run->sweep_grid2 = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2>), 256);
+    run->sweep_grid3 = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3>), 256);
   }
   const Frontier lev[2] = {frontier_at(run->dLev[0], run->cap_level), frontier_at(run->dLev[1], run->cap_level)};
   const FinalList fin = final_at(run->dFin, run->cap_final);
@@ -432,8 +436,12 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
     BS_LAUNCH_CHECK(ctx);
   }
   BS_REC(3);
-  sweep_kernel<<<run->sweep_grid, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest, run->dFeas,
-                                                         run->cap_final);
+  if (run->sweep3)
+    sweep_kernel<kSweepMinB3><<<run->sweep_grid3, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest,
+                                                                        run->dFeas, run->cap_final);
+  else
+    sweep_kernel<kSweepMinB2><<<run->sweep_grid2, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest,
+                                                                        run->dFeas, run->cap_final);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(4);
   finalize_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, pk.cfgs, pk.problems, run->dBest, run->dFeas,

@@ -173,12 +173,14 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
   __syncthreads();
   // per-level sorted order of the switched steps: one thread per (k, f)
   // computes its rank (ties by index), then scatters
-  int finite = 1;
+  int finite = 1, filt = 1;
   for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
     const int k = e / nc, f = e - k * nc;
     const double* key = k == 0 ? T->T1 : T->B1[k];
     const double v = key[f];
     if (!isfinite(v) || !isfinite(T->B0[k][f])) finite = 0;
+    const double A = T->A[k][f];
+    if (!(A >= 0.0) || !isfinite(A) || !isfinite(T->E[k][f])) filt = 0;
     int r = 0;
     for (int g = 0; g < nc; ++g) {
       const double w = key[g];
@@ -198,14 +200,9 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     T->pmin_lo[k] = __dmul_rn(pmin, 1.0 - 0x1p-50);
   }
   const int all_finite = __syncthreads_and(finite);
+  const int all_filt = __syncthreads_and(filt);
   if (threadIdx.x == 0) {
-    int ok = 1;
-    for (int k = 0; k < K; ++k)
-      for (int f = 0; f < nc; ++f) {
-        const double A = T->A[k][f];
-        if (!(A >= 0.0) || !isfinite(A) || !isfinite(T->E[k][f])) ok = 0;
-      }
-    T->filter_ok = ok;
+    T->filter_ok = all_filt;
     T->sorted_ok = all_finite && isfinite(T->ttft);
   }
   __syncthreads();
