@@ -326,6 +326,31 @@ __device__ __forceinline__ double fast_interp(const FastGrid& g, long long n_req
   return fast_corners(g, b);
 }
 
+// fast_brackets in two parts: the fixed axes and the n_requests axis (fixed
+// over a decode event window, where the batch size is constant), then the
+// sum_len axis per query.  Together they equal fast_brackets.
+__device__ __forceinline__ void fast_brackets_nreq(const FastGrid& g, long long n_req, FastBrk& b) {
+#pragma unroll
+  for (int a = 0; a < kMaxRank; ++a) {
+    if (a >= g.na) break;
+    if (g.fixed[a]) {
+      b.lo[a] = g.lo[a];
+      b.frac[a] = g.frac[a];
+    } else if (g.role[a] != BS_AXIS_SUM_LEN) {
+      bracket_count(g.knots[a], g.n[a], static_cast<double>(n_req), &b.lo[a], &b.frac[a]);
+    }
+  }
+}
+
+__device__ __forceinline__ void fast_brackets_sum(const FastGrid& g, long long sum_len, FastBrk& b) {
+#pragma unroll
+  for (int a = 0; a < kMaxRank; ++a) {
+    if (a >= g.na) break;
+    if (!g.fixed[a] && g.role[a] == BS_AXIS_SUM_LEN)
+      bracket_count(g.knots[a], g.n[a], static_cast<double>(sum_len), &b.lo[a], &b.frac[a]);
+  }
+}
+
 // Two reductions of the same grid whose active axes, knots and fixed-axis
 // brackets coincide (only the dropped axes' offsets differ, e.g. the same tp
 // at two on-knot frequencies): brackets of one serve the other.
@@ -711,6 +736,7 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
   o.batches = 0;
   const FastGrid lat = fast_grid(m.grid[1], p.tp, p.freq);
   const FastGrid pw = fast_grid(m.grid[3], p.tp, p.freq);
+  const bool share = fast_same_axes(lat, pw);  // one bracket set serves both models
   double idle_w = 0.0;
   const bool have_idle = idle_power(m.idle, p.tp, p.freq, &idle_w);
   double now = 0.0;
@@ -802,6 +828,10 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
     }
     bool first_chunk = true, cut = false;
     long long it0 = it;
+    // brackets of the window's constant axes (fixed ones and n_requests = n_res)
+    FastBrk bl, bp;
+    if (!lat.bad) fast_brackets_nreq(lat, n_res, bl);
+    if (!pw.bad && !share) fast_brackets_nreq(pw, n_res, bp);
     while (!cut) {
       const long long left = R - it0 + 1;
       const int mcount = left < 32 ? static_cast<int>(left) : 32;
@@ -813,8 +843,25 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
       if (lane < mcount) {
         const long long s = sum_ctx + static_cast<long long>(lane) * n_res;
         double Lv = 0.0, Pv = 0.0;
-        if (!predict_at(lat, n_res, s, &Lv)) bad = true;
-        if (!predict_at(pw, n_res, s, &Pv)) pbad = true;
+        // predict_at(lat / pw, n_res, s) with the window's brackets
+        if (lat.bad) {
+          bad = true;
+        } else {
+          fast_brackets_sum(lat, s, bl);
+          Lv = fast_corners(lat, bl);
+          bad = !model_value_ok(Lv);
+        }
+        if (pw.bad) {
+          pbad = true;
+        } else {
+          if (share) {
+            Pv = fast_corners(pw, bl);
+          } else {
+            fast_brackets_sum(pw, s, bp);
+            Pv = fast_corners(pw, bp);
+          }
+          pbad = !model_value_ok(Pv);
+        }
         ws.L[lane] = Lv;
         ws.P[lane] = Pv;
       }
