@@ -293,6 +293,46 @@ __global__ void __launch_bounds__(kPrepThreads, 4) prepare_kernel(DModels m, con
   if (s_status != BS_OK || K == 0) return;
   const int FD = K - sweep_levels(K, nc);
   if (threadIdx.x == 0) T->FD = FD;
+  // Seed the argmin with the best feasible uniform assignment (every batch
+  // at one rung), evaluated with the sweep's exact op sequence: a genuine
+  // (objective, code) key of the tree, so the minimum is unchanged, while
+  // every sweep thread starts with a tight filter threshold.
+  if (threadIdx.x < 32) {
+    const int f = threadIdx.x;
+    unsigned long long ko = ~0ull, kc = ~0ull;
+    if (f < nc) {
+      double t = 0.0, num = 0.0, den = 0.0;
+      int last = -1;
+      bool ok = true;
+      unsigned long long code = 0;
+      for (int k = 0; k < K && ok; ++k) {
+        double ct, cn, cd;
+        ok = child_state(T, k, t, num, den, last, f, ct, cn, cd);
+        t = ct;
+        num = cn;
+        den = cd;
+        last = f;
+        code = code * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
+      }
+      if (ok) {
+        const double obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;  // dvfs.hpp:170
+        ko = static_cast<unsigned long long>(__double_as_longlong(obj));
+        kc = code;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long oo = __shfl_xor_sync(0xffffffffu, ko, o), oc = __shfl_xor_sync(0xffffffffu, kc, o);
+      if (key_less(oo, oc, ko, kc)) {
+        ko = oo;
+        kc = oc;
+      }
+    }
+    if (threadIdx.x == 0 && ko != ~0ull) {  // after this thread's reset above (program order)
+      best[d].obj = ko;
+      best[d].code = kc;
+    }
+  }
   if (FD == 0) {
     if (threadIdx.x == 0) {
       const unsigned long long sl = atomicAdd(&ctl->final_count, 1ull);
