@@ -255,6 +255,8 @@ __global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ ta
   }
 }
 
+constexpr int kSeedRounds = 3;  // single-move improvement rounds of the argmin seed
+
 // One CTA per decision: the tables, the argmin slot reset, and the first
 // levels of the search.  The prefixes of depth D0 = min(2, FD) are expanded
 // here (nc^D0 per decision) and appended to the depth-D0 list (or, at FD, to
@@ -293,40 +295,83 @@ __global__ void __launch_bounds__(kPrepThreads, 4) prepare_kernel(DModels m, con
   if (s_status != BS_OK || K == 0) return;
   const int FD = K - sweep_levels(K, nc);
   if (threadIdx.x == 0) T->FD = FD;
-  // Seed the argmin with the best feasible uniform assignment (every batch
-  // at one rung), evaluated with the sweep's exact op sequence: a genuine
-  // (objective, code) key of the tree, so the minimum is unchanged, while
-  // every sweep thread starts with a tight filter threshold.
-  if (threadIdx.x < 32) {
-    const int f = threadIdx.x;
-    unsigned long long ko = ~0ull, kc = ~0ull;
-    if (f < nc) {
+  // Seed the argmin with a good feasible assignment: the best uniform one
+  // (every batch at one rung), then rounds of single-position moves (every
+  // (k, f) replacement of the current assignment, best feasible taken).
+  // Each is evaluated with the sweep's exact op sequence, so the seed is a
+  // genuine (objective, code) key of the tree and the minimum is unchanged,
+  // while every sweep thread filters against a tight threshold from its
+  // first leaf.
+  {
+    __shared__ unsigned long long s_ko[kPrepThreads / 32], s_kc[kPrepThreads / 32];
+    __shared__ unsigned char s_cur[kMaxK];
+    auto eval = [&](int kk, int ff, unsigned long long& ko, unsigned long long& kc) {
+      // assignment s_cur with position kk set to ff (kk < 0: all positions ff)
       double t = 0.0, num = 0.0, den = 0.0;
       int last = -1;
-      bool ok = true;
       unsigned long long code = 0;
-      for (int k = 0; k < K && ok; ++k) {
+      for (int k = 0; k < K; ++k) {
+        const int f = kk < 0 ? ff : (k == kk ? ff : s_cur[k]);
         double ct, cn, cd;
-        ok = child_state(T, k, t, num, den, last, f, ct, cn, cd);
+        if (!child_state(T, k, t, num, den, last, f, ct, cn, cd)) return;
         t = ct;
         num = cn;
         den = cd;
         last = f;
         code = code * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
       }
-      if (ok) {
-        const double obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;  // dvfs.hpp:170
-        ko = static_cast<unsigned long long>(__double_as_longlong(obj));
-        kc = code;
-      }
-    }
+      const double obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;  // dvfs.hpp:170
+      ko = static_cast<unsigned long long>(__double_as_longlong(obj));
+      kc = code;
+    };
+    auto block_min = [&](unsigned long long& ko, unsigned long long& kc) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long oo = __shfl_xor_sync(0xffffffffu, ko, o), oc = __shfl_xor_sync(0xffffffffu, kc, o);
-      if (key_less(oo, oc, ko, kc)) {
-        ko = oo;
-        kc = oc;
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long oo = __shfl_xor_sync(0xffffffffu, ko, o), oc = __shfl_xor_sync(0xffffffffu, kc, o);
+        if (key_less(oo, oc, ko, kc)) {
+          ko = oo;
+          kc = oc;
+        }
       }
+      if ((threadIdx.x & 31) == 0) {
+        s_ko[threadIdx.x >> 5] = ko;
+        s_kc[threadIdx.x >> 5] = kc;
+      }
+      __syncthreads();
+      ko = s_ko[0];
+      kc = s_kc[0];
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+        if (key_less(s_ko[w], s_kc[w], ko, kc)) {
+          ko = s_ko[w];
+          kc = s_kc[w];
+        }
+      __syncthreads();
+    };
+    unsigned long long ko = ~0ull, kc = ~0ull;
+    if (threadIdx.x < nc) eval(-1, threadIdx.x, ko, kc);
+    block_min(ko, kc);
+    for (int round = 0; round < kSeedRounds && ko != ~0ull; ++round) {
+      if (threadIdx.x < K) {  // digits of the current best, batch 0 most significant
+        unsigned long long c = kc;
+        for (int k = K - 1; k > static_cast<int>(threadIdx.x); --k) c /= static_cast<unsigned long long>(nc);
+        s_cur[threadIdx.x] = static_cast<unsigned char>(c % static_cast<unsigned long long>(nc));
+      }
+      __syncthreads();
+      unsigned long long mo = ko, mc = kc;
+      for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
+        const int kk = e / nc, ff = e - kk * nc;
+        if (ff == s_cur[kk]) continue;
+        unsigned long long eo = ~0ull, ec = ~0ull;
+        eval(kk, ff, eo, ec);
+        if (key_less(eo, ec, mo, mc)) {
+          mo = eo;
+          mc = ec;
+        }
+      }
+      block_min(mo, mc);
+      if (!key_less(mo, mc, ko, kc)) break;  // a local minimum of single moves (uniform across the block)
+      ko = mo;
+      kc = mc;
     }
     if (threadIdx.x == 0 && ko != ~0ull) {  // after this thread's reset above (program order)
       best[d].obj = ko;
