@@ -192,65 +192,154 @@ __device__ __forceinline__ void block_append2(unsigned long long* c0, bool w0, u
   __syncthreads();  // the shared slots are reused by the next call
 }
 
-// Level k: every (depth-k node, digit) pair; feasible children at depth
-// k + 1 go to the next list, or to the final list at their problem's FD.
-__global__ void __launch_bounds__(256) bfs_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl, Frontier in,
-                                                  Frontier out, FinalList fin, int nc_max, unsigned long long div_magic,
-                                                  unsigned long long cap_out,
-                                                  unsigned long long cap_final) {
-  // an overflowed level still counts every append (the exact need of the
-  // retry); the levels below it are not expanded
+// Block-aggregated appends of variable counts to two counters: thread i
+// reserves n0 slots of c0 and n1 of c1 (contiguous per thread, threads in
+// order within the block), one atomic per counter per block.  Every thread
+// of the block must call it.
+__device__ __forceinline__ void block_append2n(unsigned long long* c0, unsigned n0, unsigned long long* c1, unsigned n1,
+                                               unsigned long long* s0, unsigned long long* s1) {
+  __shared__ unsigned wc0[32], wc1[32];
+  __shared__ unsigned long long b0, b1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned i0 = n0, i1 = n1;  // inclusive warp scans
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned a = __shfl_up_sync(0xffffffffu, i0, o), b = __shfl_up_sync(0xffffffffu, i1, o);
+    if (lane >= o) {
+      i0 += a;
+      i1 += b;
+    }
+  }
+  if (lane == 31) {
+    wc0[warp] = i0;
+    wc1[warp] = i1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the per-warp totals, then one atomic per counter
+    const unsigned v0 = threadIdx.x < nw ? wc0[threadIdx.x] : 0u, v1 = threadIdx.x < nw ? wc1[threadIdx.x] : 0u;
+    unsigned j0 = v0, j1 = v1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned a = __shfl_up_sync(0xffffffffu, j0, o), b = __shfl_up_sync(0xffffffffu, j1, o);
+      if (threadIdx.x >= o) {
+        j0 += a;
+        j1 += b;
+      }
+    }
+    if (threadIdx.x == 31) {
+      b0 = j0 ? atomicAdd(c0, static_cast<unsigned long long>(j0)) : 0ull;
+      b1 = j1 ? atomicAdd(c1, static_cast<unsigned long long>(j1)) : 0ull;
+    }
+    if (threadIdx.x < nw) {
+      wc0[threadIdx.x] = j0 - v0;
+      wc1[threadIdx.x] = j1 - v1;
+    }
+  }
+  __syncthreads();
+  *s0 = b0 + wc0[warp] + (i0 - n0);
+  *s1 = b1 + wc1[warp] + (i1 - n1);
+  __syncthreads();  // the shared slots are reused by the next call
+}
+
+// Level k >= 2, one thread per depth-k node: its children that pass
+// meets_slo's check are the sorted prefix of the level (feasible_prefix, by
+// monotonicity), less f == last, plus the non-switching child when it passes
+// -- so no (node, digit) pair that fails is touched.  Children at the
+// problem's FD go to the final list, and only when one of their own children
+// passes (no feasible leaf below otherwise); visited in step order, their
+// clocks never decrease, so that test walks one sorted-prefix count down.
+// Pass 1 marks the kept children by digit, pass 2 writes them in digit order
+// (the layout of a (node, digit) expansion: siblings contiguous, in code
+// order) after a block-aggregated append.
+__global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl,
+                                                       Frontier in, Frontier out, FinalList fin,
+                                                       unsigned long long cap_out, unsigned long long cap_final) {
   if (ctl->overflow) return;
   const unsigned long long n_in = ctl->level_count[k];
-  const unsigned long long total = n_in * static_cast<unsigned long long>(nc_max);
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < total;
+  for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < n_in;
        base += stride) {
-    const unsigned long long j = base + threadIdx.x;
-    bool ok = false, to_final = false;
-    int d = 0, f = 0;
-    double ct = 0.0, cn = 0.0, cd = 0.0;
-    unsigned long long cc = 0;
-    if (j < total) {
-      // j / nc_max by a multiply-high: with M = ceil(2^64 / d) the quotient
-      // is exact for j < 2^58 and d <= 32 (error < j / 2^64 < 1 / d)
-      const unsigned long long node = nc_max == 1 ? j : __umul64hi(j, div_magic);
-      f = static_cast<int>(j - node * nc_max);
-      d = in.d[node];
-      const DTables* __restrict__ T = &tables[d];
-      const int nc = T->nc;
-      if (f < nc) {
-        ok = child_state(T, k, in.t[node], in.num[node], in.den[node], in.last[node], f, ct, cn, cd);
-        cc = in.code[node] * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
-        to_final = (k + 1) == T->FD;
-        // a final node none of whose children passes meets_slo has no feasible
-        // leaf (meets_slo stops at the first violation): drop it here
-        if (ok && to_final && T->sorted_ok && k + 1 < T->K) {
-          const int kk = k + 1;
-          ok = feasible_prefix(T, kk, nc, ct) > 0 || diag_passes(T, kk, ct, f);
+    const unsigned long long i = base + threadIdx.x;
+    unsigned keep = 0u;  // bit f: child f kept
+    bool to_final = false;
+    int d = 0, last = 0, nc = 0;
+    double t = 0.0, num = 0.0, den = 0.0;
+    unsigned long long code = 0;
+    const DTables* __restrict__ T = tables;
+    if (i < n_in) {
+      d = in.d[i];
+      T = &tables[d];
+      t = in.t[i];
+      num = in.num[i];
+      den = in.den[i];
+      last = in.last[i];
+      code = in.code[i];
+      nc = T->nc;
+      to_final = (k + 1) == T->FD;
+      if (T->sorted_ok) {
+        const bool prune = to_final && k + 1 < T->K;
+        const int c = feasible_prefix(T, k, nc, t);
+        const unsigned char* __restrict__ ord = T->ord[k];
+        const double* __restrict__ sb = T->sb[k];
+        const int kl = k + 1;
+        int cl = -1;
+        for (int j = 0; j < c; ++j) {
+          const int f = ord[j];
+          if (f == last) continue;
+          bool ok = true;
+          if (prune) {
+            const double ct = __dadd_rn(t, sb[j]);
+            if (cl < 0) {
+              cl = feasible_prefix(T, kl, nc, ct);
+            } else {
+              const double ml = T->minarr[kl], ttft = T->ttft;
+              const double* __restrict__ sbl = T->sb[kl];
+              while (cl > 0 && __dsub_rn(__dadd_rn(ct, sbl[cl - 1]), ml) > ttft) --cl;
+            }
+            ok = cl > 0 || diag_passes(T, kl, ct, f);
+          }
+          if (ok) keep |= 1u << f;
+        }
+        if (diag_passes(T, k, t, last)) {
+          bool ok = true;
+          if (prune) {
+            const double ct = __dadd_rn(t, T->B0[k][last]);
+            ok = feasible_prefix(T, kl, nc, ct) > 0 || diag_passes(T, kl, ct, last);
+          }
+          if (ok) keep |= 1u << last;
+        }
+      } else {  // unsorted tables: every digit
+        for (int f = 0; f < nc; ++f) {
+          double ct, cn, cd;
+          if (child_state(T, k, t, num, den, last, f, ct, cn, cd)) keep |= 1u << f;
         }
       }
     }
+    const unsigned m = static_cast<unsigned>(__popc(keep));
     unsigned long long sf, so;
-    block_append2(&ctl->final_count, ok && to_final, &ctl->level_count[k + 1], ok && !to_final, &sf, &so);
-    if (ok && to_final) {
-      if (sf < cap_final) {
-        fin.d[sf] = d;
-        fin.code[sf] = cc;
-      } else {
+    block_append2n(&ctl->final_count, to_final ? m : 0u, &ctl->level_count[k + 1], to_final ? 0u : m, &sf, &so);
+    unsigned long long slot = to_final ? sf : so;
+    const unsigned long long cap = to_final ? cap_final : cap_out;
+    const unsigned long long cb = code * static_cast<unsigned long long>(nc);
+    while (keep) {
+      const int f = __ffs(keep) - 1;
+      keep &= keep - 1u;
+      if (slot >= cap) {
         atomicAdd(&ctl->overflow, 1ull);
-      }
-    } else if (ok) {
-      if (so < cap_out) {
-        out.d[so] = d;
-        out.code[so] = cc;
-        out.t[so] = ct;
-        out.num[so] = cn;
-        out.den[so] = cd;
-        out.last[so] = f;
+      } else if (to_final) {
+        fin.d[slot] = d;
+        fin.code[slot] = cb + static_cast<unsigned long long>(f);
       } else {
-        atomicAdd(&ctl->overflow, 1ull);
+        double ct, cn, cd;
+        child_state(T, k, t, num, den, last, f, ct, cn, cd);
+        out.d[slot] = d;
+        out.code[slot] = cb + static_cast<unsigned long long>(f);
+        out.t[slot] = ct;
+        out.num[slot] = cn;
+        out.den[slot] = cd;
+        out.last[slot] = f;
       }
+      ++slot;
     }
   }
 }
@@ -410,7 +499,7 @@ __global__ void __launch_bounds__(kPrepThreads, 4) prepare_kernel(DModels m, con
         den = d1;
         last = f1;
       }
-      // a final node none of whose children passes has no feasible leaf (as in bfs_kernel)
+      // a final node none of whose children passes has no feasible leaf (as in bfs_node_kernel)
       if (ok && to_final && T->sorted_ok && FD < K) ok = feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
     }
     unsigned long long sf, so;

@@ -9,17 +9,21 @@
 //                    threads through the bit-exact interpolator; resets the
 //                    argmin slot and expands the first two levels (N^2
 //                    prefixes) straight into the depth-2 list.
-//   bfs_kernel       x (max depth of final nodes - 2): level-synchronous
+//   bfs_node_kernel  x (max depth of final nodes - 2): level-synchronous
 //                    expansion of every feasible prefix of every decision,
-//                    compacted with warp-aggregated appends (meets_slo fails
-//                    at the first violated batch, so violated prefixes have
-//                    no feasible completion and are dropped for good).
+//                    one thread per node (its passing children are a sorted
+//                    prefix), compacted with block-aggregated appends
+//                    (meets_slo fails at the first violated batch, so
+//                    violated prefixes have no feasible completion and are
+//                    dropped for good).
 //   sweep_kernel     one thread per final node sweeps its bottom 2 (or 3)
 //                    levels in increasing code order with a division-free
 //                    objective filter; (objective, code) minima merge
 //                    through a 128-bit CAS.  See bs_exhaustive.cuh.
 //   finalize_kernel  1 thread / problem: decode the argmin code.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -416,7 +420,7 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
     return BS_OK;
   }
   if (!run->bfs_grid) {
-    run->bfs_grid = grid_for(ctx, reinterpret_cast<const void*>(bfs_kernel), 256);
+    run->bfs_grid = grid_for(ctx, reinterpret_cast<const void*>(bfs_node_kernel), 256);
     run->sweep_grid2 = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2>), 256);
     run->sweep_grid3 = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3>), 256);
   }
@@ -430,9 +434,8 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   BS_REC(1);
   BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel
   for (int k = 2; k < run->bfs_levels; ++k) {  // depth-2 lists come from prepare_kernel
-    bfs_kernel<<<run->bfs_grid, 256, 0, ctx->stream>>>(run->dT, k, run->dCtl, lev[k & 1], lev[(k + 1) & 1], fin,
-                                                       run->max_nc, ~0ull / static_cast<unsigned>(run->max_nc) + 1,
-                                                       run->cap_level, run->cap_final);
+    bfs_node_kernel<<<run->bfs_grid, 256, 0, ctx->stream>>>(run->dT, k, run->dCtl, lev[k & 1], lev[(k + 1) & 1],
+                                                            fin, run->cap_level, run->cap_final);
     BS_LAUNCH_CHECK(ctx);
   }
   BS_REC(3);
@@ -663,6 +666,15 @@ int bs_mpc_plan_run(bs_ctx_t ctx, bs_mpc_plan_t plan, int record_kernel_times) {
 int bs_mpc_plan_results(bs_ctx_t ctx, bs_mpc_plan_t plan, bs_mpc_result* out) {
   if (!ctx || !plan) return set_error(ctx, BS_PARAMETER_ERROR, "bs_mpc_plan_results: null argument");
   const int rc = run_results(ctx, &plan->run, out);
+  if (std::getenv("BS_DEBUG_COUNTS") && plan->run.mode == kExhaustive) {  // list sizes of the last run (diagnostics)
+    ExCtl c;
+    if (cudaMemcpy(&c, plan->run.dCtl, sizeof c, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      std::fprintf(stderr, "bs_mpc lists:");
+      for (int k = 0; k <= kMaxK; ++k)
+        if (c.level_count[k]) std::fprintf(stderr, " depth%d=%llu", k, c.level_count[k]);
+      std::fprintf(stderr, " final=%llu overflow=%llu\n", c.final_count, c.overflow);
+    }
+  }
   // a resident plan's frontiers are fixed at creation: report an overflow as
   // a parameter problem of the batch (one-shot calls re-run or split instead)
   return rc == kOverflowStatus ? set_error(ctx, BS_PARAMETER_ERROR, "%s", ctx->err.c_str()) : rc;
