@@ -318,28 +318,64 @@ __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict
     const unsigned m = static_cast<unsigned>(__popc(keep));
     unsigned long long sf, so;
     block_append2n(&ctl->final_count, to_final ? m : 0u, &ctl->level_count[k + 1], to_final ? 0u : m, &sf, &so);
-    unsigned long long slot = to_final ? sf : so;
-    const unsigned long long cap = to_final ? cap_final : cap_out;
-    const unsigned long long cb = code * static_cast<unsigned long long>(nc);
-    while (keep) {
-      const int f = __ffs(keep) - 1;
-      keep &= keep - 1u;
-      if (slot >= cap) {
-        atomicAdd(&ctl->overflow, 1ull);
-      } else if (to_final) {
-        fin.d[slot] = d;
-        fin.code[slot] = cb + static_cast<unsigned long long>(f);
-      } else {
-        double ct, cn, cd;
-        child_state(T, k, t, num, den, last, f, ct, cn, cd);
-        out.d[slot] = d;
-        out.code[slot] = cb + static_cast<unsigned long long>(f);
-        out.t[slot] = ct;
-        out.num[slot] = cn;
-        out.den[slot] = cd;
-        out.last[slot] = f;
+    // Pass 2, warp-cooperative so the stores coalesce: the warp's children of
+    // each list occupy one contiguous slot range (block_append2n keeps lanes
+    // in order), and lane l writes items l, l + 32, ... of it, fetching the
+    // owner node's state by shuffles.
+    const int lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (int list = 0; list < 2; ++list) {
+      const bool mine = (list == 0) == to_final;
+      const unsigned cnt = mine ? m : 0u;
+      unsigned inc = cnt;  // inclusive warp scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
       }
-      ++slot;
+      const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+      if (total == 0u) continue;
+      // the warp's first slot of this list (every lane with cnt > 0 agrees; take the first)
+      const unsigned long long my_start = (list == 0 ? sf : so) - (inc - cnt);
+      const int first = __ffs(__ballot_sync(0xffffffffu, cnt > 0u)) - 1;
+      const unsigned long long wbase = __shfl_sync(0xffffffffu, my_start, first);
+      const unsigned long long cap = list == 0 ? cap_final : cap_out;
+      for (unsigned b0 = 0; b0 < total; b0 += 32u) {
+        const unsigned idx = b0 + static_cast<unsigned>(lane);
+        int o = 0;  // owner: the first lane whose inclusive count exceeds idx
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const unsigned probe = __shfl_sync(0xffffffffu, inc, o + step - 1);
+          if (probe <= idx) o += step;
+        }
+        const unsigned o_inc = __shfl_sync(0xffffffffu, inc, o), o_cnt = __shfl_sync(0xffffffffu, cnt, o);
+        const unsigned o_keep = __shfl_sync(0xffffffffu, keep, o);
+        const int o_d = __shfl_sync(0xffffffffu, d, o), o_last = __shfl_sync(0xffffffffu, last, o);
+        const int o_nc = __shfl_sync(0xffffffffu, nc, o);
+        const unsigned long long o_code = __shfl_sync(0xffffffffu, code, o);
+        const double o_t = __shfl_sync(0xffffffffu, t, o), o_num = __shfl_sync(0xffffffffu, num, o),
+                     o_den = __shfl_sync(0xffffffffu, den, o);
+        if (idx >= total) continue;
+        const int r = static_cast<int>(idx - (o_inc - o_cnt));
+        const int f = static_cast<int>(__fns(o_keep, 0, r + 1));
+        const unsigned long long slot = wbase + idx;
+        const unsigned long long cc = o_code * static_cast<unsigned long long>(o_nc) + static_cast<unsigned long long>(f);
+        if (slot >= cap) {
+          atomicAdd(&ctl->overflow, 1ull);
+        } else if (list == 0) {
+          fin.d[slot] = o_d;
+          fin.code[slot] = cc;
+        } else {
+          double ct, cn, cd;
+          child_state(&tables[o_d], k, o_t, o_num, o_den, o_last, f, ct, cn, cd);
+          out.d[slot] = o_d;
+          out.code[slot] = cc;
+          out.t[slot] = ct;
+          out.num[slot] = cn;
+          out.den[slot] = cd;
+          out.last[slot] = f;
+        }
+      }
     }
   }
 }
