@@ -235,6 +235,7 @@ struct DTables {
   unsigned char rank[kMaxK][kMaxCand];
   int sorted_ok;
   int FD;  // exhaustive search: depth of the final nodes, K - sweep_levels(K, nc) (set by prepare_kernel)
+  unsigned nc_magic;  // ceil(2^32 / nc): code / nc by a multiply-high for codes < 2^27 (set by prepare_kernel)
   // Per-level bounds for the leaf-row skip: amax = max_f A, pmin_lo =
   // fl(min_f P * (1 - 2^-50)) <= min_f P * (1 - u).
   double amax[kMaxK];

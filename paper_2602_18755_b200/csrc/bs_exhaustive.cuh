@@ -419,7 +419,10 @@ __global__ void __launch_bounds__(kPrepThreads, 4) prepare_kernel(DModels m, con
   const int K = T->K, nc = T->nc;
   if (s_status != BS_OK || K == 0) return;
   const int FD = K - sweep_levels(K, nc);
-  if (threadIdx.x == 0) T->FD = FD;
+  if (threadIdx.x == 0) {
+    T->FD = FD;
+    T->nc_magic = nc > 1 ? 0xffffffffu / static_cast<unsigned>(nc) + 1u : 0u;
+  }
   // Seed the argmin with a good feasible assignment: the best uniform one
   // (every batch at one rung), then rounds of single-position moves (every
   // (k, f) replacement of the current assignment, best feasible taken).
@@ -759,6 +762,28 @@ __device__ __forceinline__ void walk(const DTables* __restrict__ T, int nc, int 
   num = 0.0;
   den = 0.0;
   last = -1;
+  if (nc > 1 && P <= 12 && code < (1ull << 27)) {
+    // digits least significant first by a multiply-high (q = umulhi(c,
+    // ceil(2^32 / nc)) is exact for c < 2^32 / nc), packed 5 bits each
+    const unsigned M = T->nc_magic;
+    unsigned c = static_cast<unsigned>(code);
+    unsigned long long packed = 0;
+    for (int k = P - 1; k >= 0; --k) {
+      const unsigned q = __umulhi(c, M);
+      packed |= static_cast<unsigned long long>(c - q * static_cast<unsigned>(nc)) << (5 * k);
+      c = q;
+    }
+    for (int k = 0; k < P; ++k) {
+      const int f = static_cast<int>((packed >> (5 * k)) & 31u);
+      double ct, cn, cd;
+      child_state(T, k, t, num, den, last, f, ct, cn, cd);
+      t = ct;
+      num = cn;
+      den = cd;
+      last = f;
+    }
+    return;
+  }
   unsigned long long div = ipow(static_cast<unsigned long long>(nc), P > 0 ? P - 1 : 0);
   for (int k = 0; k < P; ++k) {
     int f;
@@ -817,12 +842,22 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
   if (ctl->overflow) return;  // the run is repeated with larger lists (one_shot): skip the sweep
   const unsigned long long n_fin = ctl->final_count < cap_final ? ctl->final_count : cap_final;
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-  for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < n_fin;
-       base += stride) {
-    const unsigned long long j = base + threadIdx.x;
-    if (j >= n_fin) continue;  // only the last round is partial
-    const int d = fin.d[j];
-    const unsigned long long code = fin.code[j];
+  unsigned long long j = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int d_next = 0;
+  unsigned long long code_next = 0;
+  if (j < n_fin) {
+    d_next = fin.d[j];
+    code_next = fin.code[j];
+  }
+  for (; j < n_fin; j += stride) {
+    const int d = d_next;
+    const unsigned long long code = code_next;
+    if (j + stride < n_fin) {  // the next node's entry, in flight during this one
+      d_next = fin.d[j + stride];
+      code_next = fin.code[j + stride];
+    }
+    const double hint = __longlong_as_double(static_cast<long long>(
+        *reinterpret_cast<volatile unsigned long long*>(&best[d].obj)));
     const DTables* __restrict__ T = &tables[d];
     const int K = T->K, nc = T->nc;
     const int FD = T->FD;
@@ -830,8 +865,6 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
     double t, num, den;
     int last;
     walk(T, nc, FD, code, t, num, den, last);
-    const double hint = __longlong_as_double(static_cast<long long>(
-        *reinterpret_cast<volatile unsigned long long*>(&best[d].obj)));
     LeafAcc a;
     a.best = INFINITY;
     a.code = ~0ull;

@@ -25,6 +25,7 @@ struct bs_ctx_s {
   int64_t launches = 0;
   double stats[16] = {};  // phase timings / counters of the last entry point
   int n_stats = 0;
+  int grid_cache[8] = {};  // occupancy-sized persistent grids, computed once per context (bs_mpc.cu)
 
   struct Buf {
     void* p = nullptr;

@@ -419,10 +419,15 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
     BS_REC(1);
     return BS_OK;
   }
-  if (!run->bfs_grid) {
-    run->bfs_grid = grid_for(ctx, reinterpret_cast<const void*>(bfs_node_kernel), 256);
-    run->sweep_grid2 = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2>), 256);
-    run->sweep_grid3 = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3>), 256);
+  if (!run->bfs_grid) {  // occupancy queries once per context
+    if (!ctx->grid_cache[0]) {
+      ctx->grid_cache[0] = grid_for(ctx, reinterpret_cast<const void*>(bfs_node_kernel), 256);
+      ctx->grid_cache[1] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2>), 256);
+      ctx->grid_cache[2] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3>), 256);
+    }
+    run->bfs_grid = ctx->grid_cache[0];
+    run->sweep_grid2 = ctx->grid_cache[1];
+    run->sweep_grid3 = ctx->grid_cache[2];
   }
   const Frontier lev[2] = {frontier_at(run->dLev[0], run->cap_level), frontier_at(run->dLev[1], run->cap_level)};
   const FinalList fin = final_at(run->dFin, run->cap_final);
