@@ -380,14 +380,20 @@ __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict
   }
 }
 
-constexpr int kSeedRounds = 3;  // single-move improvement rounds of the argmin seed
+#ifndef BS_SEED_ROUNDS
+#define BS_SEED_ROUNDS 3  // single-move improvement rounds of the argmin seed (1: C2 sweep 0.239 ms; 3: 0.219; 6: 0.221)
+#endif
+#ifndef BS_PREP_MINB
+#define BS_PREP_MINB 8  // 64 registers: the 1024-decision batch in one wave (C2: 0.055 -> 0.040 ms)
+#endif
+constexpr int kSeedRounds = BS_SEED_ROUNDS;
 
 // One CTA per decision: the tables, the argmin slot reset, and the first
 // levels of the search.  The prefixes of depth D0 = min(2, FD) are expanded
 // here (nc^D0 per decision) and appended to the depth-D0 list (or, at FD, to
 // the final list), so the BFS starts at depth 2.  The run's counters are
 // zeroed by the host before this launch.
-__global__ void __launch_bounds__(kPrepThreads, 4) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
+__global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
                                                                const DWaiting* W, const DRunning* R, DTables* tables,
                                                                ExCtl* ctl, int n, const DFastPair* fg, Key128* best,
                                                                unsigned long long* feas, Frontier L2,

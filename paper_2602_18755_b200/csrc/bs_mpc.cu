@@ -62,9 +62,12 @@ __global__ void finalize_kernel(const DTables* __restrict__ tables, const DMpcCf
       o.objective = __longlong_as_double(static_cast<long long>(best[d].obj));
       unsigned long long code = best[d].code;
       o.best_code = code;
+      // code / nc by a multiply-high with ceil(2^64 / nc): exact for codes < 2^58
+      const unsigned long long M = nc > 1 ? ~0ull / static_cast<unsigned>(nc) + 1 : 0ull;
       for (int k = K - 1; k >= 0; --k) {
-        o.idx[k] = static_cast<unsigned char>(code % nc);
-        code /= nc;
+        const unsigned long long q = nc == 1 ? code : code < (1ull << 58) ? __umul64hi(code, M) : code / nc;
+        o.idx[k] = static_cast<unsigned char>(code - q * static_cast<unsigned long long>(nc));
+        code = q;
       }
     } else {  // nothing feasible: all-max and its objective
       o.feasible = 0;
