@@ -205,7 +205,7 @@ typedef struct bs_mpc_result {
   uint64_t feasible_count;    /* exhaustive: # feasible trajectories */
   uint64_t trajectories;      /* exhaustive: N^K */
   uint64_t best_code;         /* exhaustive: argmin code, batch 0 most significant */
-  bs_level_stats levels[BS_MAX_LEVELS];
+  bs_level_stats levels[BS_MAX_LEVELS]; /* [0, n_levels) written; later entries are left untouched */
 } bs_mpc_result;
 
 /* ProjectedBatch (dvfs.hpp:54-59), device-side summary. */

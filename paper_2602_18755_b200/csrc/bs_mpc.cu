@@ -22,6 +22,8 @@
 //                    through a 128-bit CAS.  See bs_exhaustive.cuh.
 //   finalize_kernel  1 thread / problem: decode the argmin code.
 #include <algorithm>
+#include <cstddef>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -170,7 +172,9 @@ __global__ void project_kernel(const DMpcCfg* cfgs, const DProblem* probs, const
 
 void expand_result(const DMpcOut& o, const DLevel* lv, const DMpcCfg& c, double target_freq, bs_mpc_result* r,
                    bool exhaustive) {
-  std::memset(r, 0, sizeof *r);
+  // everything before the level list; levels[n_levels..) are not written
+  // (GreedyResult::levels has n_levels entries, dvfs.hpp:133-139)
+  std::memset(r, 0, offsetof(bs_mpc_result, levels));
   r->status = o.status;
   r->K = o.K;
   if (o.status != BS_OK) {
@@ -498,9 +502,15 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
              int n_cfgs, const bs_mpc_problem* problems, int n, bs_mpc_result* out, int mode) {
   if (!ctx || !models) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: null context or models");
   unsigned long long cap_level = 0, cap_final = 0;  // 0: worst case (clamped)
+  const bool dbg_t = std::getenv("BS_DEBUG_TIMING") != nullptr;  // host phase timings (diagnostics)
+  auto now_us = []() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
   for (int attempt = 0;; ++attempt) {
     MpcRun run;
+    const double t0 = dbg_t ? now_us() : 0.0;
     int rc = run_pack(ctx, cfgs, policies, n_cfgs, problems, n, mode, &run, cap_level, cap_final);
+    const double t1 = dbg_t ? now_us() : 0.0;
     if (rc) return rc;
     ctx->last_h2d = run.pk.h2d_bytes;
     ctx->last_d2h = 0;
@@ -523,9 +533,16 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
       run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n)));
       if (!run.dOut || !run.dLv) return set_error(ctx, BS_CUDA_ERROR, "mpc greedy: allocation failed");
     }
+    const double t2 = dbg_t ? now_us() : 0.0;
     rc = run_enqueue(ctx, models, &run, false);
     if (rc) return rc;
+    const double t3 = dbg_t ? now_us() : 0.0;
+    if (dbg_t) cudaStreamSynchronize(ctx->stream);
+    const double t4 = dbg_t ? now_us() : 0.0;
     rc = run_results(ctx, &run, out);
+    if (dbg_t)
+      std::fprintf(stderr, "bs_mpc one_shot us: pack %.1f upload %.1f enqueue %.1f device %.1f results %.1f\n", t1 - t0,
+                   t2 - t1, t3 - t2, t4 - t3, now_us() - t4);
     if (rc != kOverflowStatus) return rc;
     // Overflow: counts up to the first overflowing level are exact totals;
     // retry with room for them, or split the batch when they exceed the budget.
