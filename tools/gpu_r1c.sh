@@ -8,7 +8,7 @@ L="ncu --metrics gpu__time_duration.sum --clock-control none --csv"
 F="ncu --set full --clock-control none --import-source on"
 $L --log-file gpurun_out/c2_launches.csv python bench.py --no-extras --no-cpu-baseline --steps 2 --warmup 3 > gpurun_out/c2_launches.log 2>&1
 $F -k regex:sweep_kernel -s 3 -c 1 -o gpurun_out/sweep_full python bench.py --no-extras --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/sweep_full.log 2>&1
-$F -k regex:bfs_kernel -s 6 -c 2 -o gpurun_out/bfs_full python bench.py --no-extras --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/bfs_full.log 2>&1
+$F -k regex:bfs_node_kernel -s 6 -c 2 -o gpurun_out/bfs_full python bench.py --no-extras --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/bfs_full.log 2>&1
 $F -k regex:prepare_kernel -s 3 -c 1 -o gpurun_out/prepare_full python bench.py --no-extras --no-cpu-baseline --steps 1 --warmup 3 > gpurun_out/prepare_full.log 2>&1
 $L --log-file gpurun_out/c3_launches.csv python bench.py --only c3 --no-cpu-baseline > gpurun_out/c3_launches.log 2>&1
 $L --log-file gpurun_out/c5x_launches.csv python bench.py --only c5x --no-cpu-baseline --c5x-decisions 1024 > gpurun_out/c5x_launches.log 2>&1
