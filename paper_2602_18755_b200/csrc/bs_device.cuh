@@ -206,6 +206,10 @@ struct DProblem {
 //   T1[f]    = now + (cand[f] != current ? B1 : B0)[0][f]
 //   minarr[k]= min completing arrival (+inf if none): monotone-subtraction
 //              reduction of meets_slo's per-request test (SURVEY.md appx. 5)
+struct __align__(16) SRec {
+  double sb, E, A, B0n;
+};
+
 struct DTables {
   int K;
   int nc;
@@ -233,6 +237,12 @@ struct DTables {
   double sb[kMaxK][kMaxCand];
   unsigned char ord[kMaxK][kMaxCand];
   unsigned char rank[kMaxK][kMaxCand];
+  // The same order as records for the sweep's children loop (one vector
+  // load per child, independent of the index load): srec[k][j] = {sb[k][j],
+  // E[k][f], A[k][f], B0[k+1][f]} and sinfo[k][j] = f | rank[k+1][f] << 8
+  // with f = ord[k][j] (next-level fields 0 at the last level).
+  SRec srec[kMaxK][kMaxCand];
+  unsigned short sinfo[kMaxK][kMaxCand];
   int sorted_ok;
   int FD;  // exhaustive search: depth of the final nodes, K - sweep_levels(K, nc) (set by prepare_kernel)
   unsigned nc_magic;  // ceil(2^32 / nc): code / nc by a multiply-high for codes < 2^27 (set by prepare_kernel)

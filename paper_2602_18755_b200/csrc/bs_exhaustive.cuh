@@ -675,12 +675,13 @@ __device__ __forceinline__ int for_feasible_children(const DTables* __restrict__
 
 // Leaves (level k >= 1) under a parent with clock t whose sorted-prefix
 // count c = feasible_prefix(T, k, nc, t) is known: count them in closed form,
-// skip a dominated row, else visit only the passing leaves.
+// skip a dominated row, else visit only the passing leaves.  rank_last /
+// b0_last: rank[k][last] and B0[k][last] (from the parent's record).
 __device__ __forceinline__ void leaves_counted(const DTables* __restrict__ T, int k, int nc, double t, double num,
-                                               double den, int last, int c, unsigned long long code_base, bool filt,
-                                               double hint, LeafAcc& a) {
-  const bool diag = diag_passes(T, k, t, last);
-  a.count += static_cast<unsigned long long>(c - (T->rank[k][last] < c ? 1 : 0) + (diag ? 1 : 0));
+                                               double den, int last, int rank_last, double b0_last, int c,
+                                               unsigned long long code_base, bool filt, double hint, LeafAcc& a) {
+  const bool diag = !(__dsub_rn(__dadd_rn(t, b0_last), T->minarr[k]) > T->ttft);  // diag_passes
+  a.count += static_cast<unsigned long long>(c - (rank_last < c ? 1 : 0) + (diag ? 1 : 0));
   if (filt && row_dominated(a, num, den)) return;
   const double* __restrict__ E = T->E[k];
   const double* __restrict__ A = T->A[k];
@@ -717,34 +718,34 @@ __device__ __forceinline__ void two_sorted(const DTables* __restrict__ T, int k,
                                            double den, int last, unsigned long long code_base, double hint,
                                            LeafAcc& a) {
   const int c = feasible_prefix(T, k, nc, t);
-  const unsigned char* __restrict__ ord = T->ord[k];
-  const double* __restrict__ sb = T->sb[k];
-  const double* __restrict__ E = T->E[k];
-  const double* __restrict__ A = T->A[k];
+  const SRec* __restrict__ sr = T->srec[k];
+  const unsigned short* __restrict__ si = T->sinfo[k];
   const int kl = k + 1;
   const double ml = T->minarr[kl], ttft = T->ttft;
   const double* __restrict__ sbl = T->sb[kl];
   int cl = -1;
   for (int j = 0; j < c; ++j) {
-    const int g = ord[j];
+    const unsigned info = si[j];
+    const int g = static_cast<int>(info & 0xffu);
     if (k > 0 && g == last) continue;
-    const double t2 = k == 0 ? sb[j] : __dadd_rn(t, sb[j]);
+    const SRec r = sr[j];
+    const double t2 = k == 0 ? r.sb : __dadd_rn(t, r.sb);
     if (cl < 0) {
       cl = feasible_prefix(T, kl, nc, t2);
     } else {
       while (cl > 0 && __dsub_rn(__dadd_rn(t2, sbl[cl - 1]), ml) > ttft) --cl;
     }
-    const double d2 = __dadd_rn(den, A[g]);
-    leaves_counted(T, kl, nc, t2, __dadd_rn(num, E[g]), d2, g, cl,
+    const double d2 = __dadd_rn(den, r.A);
+    leaves_counted(T, kl, nc, t2, __dadd_rn(num, r.E), d2, g, static_cast<int>(info >> 8), r.B0n, cl,
                    (code_base + static_cast<unsigned long long>(g)) * nc, T->filter_ok && d2 >= kFilterMinDen, hint,
                    a);
   }
   if (k > 0 && diag_passes(T, k, t, last)) {
     const double t2 = __dadd_rn(t, T->B0[k][last]);
-    const double d2 = __dadd_rn(den, A[last]);
-    leaves_counted(T, kl, nc, t2, __dadd_rn(num, E[last]), d2, last, feasible_prefix(T, kl, nc, t2),
-                   (code_base + static_cast<unsigned long long>(last)) * nc, T->filter_ok && d2 >= kFilterMinDen,
-                   hint, a);
+    const double d2 = __dadd_rn(den, T->A[k][last]);
+    leaves_counted(T, kl, nc, t2, __dadd_rn(num, T->E[k][last]), d2, last, T->rank[kl][last], T->B0[kl][last],
+                   feasible_prefix(T, kl, nc, t2), (code_base + static_cast<unsigned long long>(last)) * nc,
+                   T->filter_ok && d2 >= kFilterMinDen, hint, a);
   }
 }
 

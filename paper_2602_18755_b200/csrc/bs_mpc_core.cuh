@@ -189,6 +189,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     T->sb[k][r] = v;
     T->ord[k][r] = static_cast<unsigned char>(f);
     T->rank[k][f] = static_cast<unsigned char>(r);
+    T->srec[k][r] = SRec{v, T->E[k][f], A, k + 1 < K ? T->B0[k + 1][f] : 0.0};
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     double amax = 0.0, pmin = INFINITY;
@@ -201,6 +202,11 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
   }
   const int all_finite = __syncthreads_and(finite);
   const int all_filt = __syncthreads_and(filt);
+  for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {  // ranks of every level are in place
+    const int k = e / nc, f = e - k * nc;
+    T->sinfo[k][T->rank[k][f]] =
+        static_cast<unsigned short>(f | (k + 1 < K ? static_cast<int>(T->rank[k + 1][f]) << 8 : 0));
+  }
   if (threadIdx.x == 0) {
     T->filter_ok = all_filt;
     T->sorted_ok = all_finite && isfinite(T->ttft);
