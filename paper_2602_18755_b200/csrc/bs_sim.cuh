@@ -757,6 +757,23 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
     return true;
   };
 
+  // the next not-yet-pulled request (index arr), cached: its arrival and KV
+  // need are read once per request instead of at every event window
+  int r_nx = -1;
+  double a_nx = INFINITY;
+  long long need_nx = 0;
+  auto refresh_next = [&]() {
+    if (arr < tr.n) {
+      r_nx = tr.kept[arr];
+      a_nx = tr.arrival[r_nx];
+      need_nx = tr.input[r_nx] + tr.output[r_nx];
+    } else {
+      r_nx = -1;
+      a_nx = INFINITY;
+      need_nx = 0;
+    }
+  };
+  refresh_next();
   int poll = 0;
   while (arr < tr.n || whead < arr || n_res > 0) {
     if (p.search && ++poll == kSearchPollDecode) {  // warp-uniform: lane 0's view decides
@@ -769,7 +786,10 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
       }
     }
     // ---- boundary: pull arrivals, admit (simulator.hpp:515-519, 455-470)
-    while (arr < tr.n && tr.arrival[tr.kept[arr]] <= now) ++arr;
+    while (arr < tr.n && a_nx <= now) {
+      ++arr;
+      refresh_next();
+    }
     int n_new = 0;
     double new_min_arr = 0.0;
     while (whead < arr) {
@@ -807,7 +827,7 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
         o.meets_slo = 0;
         return o;
       }
-      const double t_next = fmax(tr.arrival[tr.kept[arr]], now);
+      const double t_next = fmax(a_nx, now);
       if (!record_idle(now, t_next)) return o;
       now = t_next;
       continue;
@@ -821,10 +841,9 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
     bool arrival_cuts = false;
     double t_a = INFINITY;
     if (whead == arr && arr < tr.n) {
-      const int r = tr.kept[arr];
-      const long long need = tr.input[r] + tr.output[r];
-      arrival_cuts = need > p.kv_capacity || (n_res < p.max_batch_requests && reserved + need <= p.kv_capacity);
-      t_a = tr.arrival[r];
+      arrival_cuts =
+          need_nx > p.kv_capacity || (n_res < p.max_batch_requests && reserved + need_nx <= p.kv_capacity);
+      t_a = a_nx;
     }
     bool first_chunk = true, cut = false;
     long long it0 = it;
