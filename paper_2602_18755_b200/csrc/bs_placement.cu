@@ -23,6 +23,7 @@
 //   ILP            exact branch and bound (host), reference fold order and
 //                  tie-breaks.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstddef>
 #include <cstring>
@@ -140,6 +141,7 @@ struct ProbeOut {
   long long completed;
   double busy_j;
   double idle_j;
+  long long ns;  // wall time of the probe (%globaltimer; diagnostics)
 };
 
 struct TraceDev {
@@ -244,6 +246,9 @@ __global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, Tr
   o.completed = 0;
   o.busy_j = 0.0;
   o.idle_j = 0.0;
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  o.ns = 0;
   auto publish = [&](int code) {  // the outcome record first, then its code for the other probes
     out[gid] = o;
     __threadfence();
@@ -290,6 +295,11 @@ __global__ void __launch_bounds__(128, BS_PROBE_MINB) probe_kernel(DModels m, Tr
   o.completed = r.completed;
   o.busy_j = r.busy_j;
   o.idle_j = r.idle_j;
+  {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    o.ns = static_cast<long long>(t_end - t_start);
+  }
   // feasible(k) (placement.hpp:172-176): SimulationError counts as a failure
   publish(r.status == kSimAborted           ? kProbeSkipped
           : r.status == BS_MODEL_ERROR      ? kProbeErr
@@ -793,6 +803,21 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
     ctx->stats[6] = static_cast<double>(skipped);
     ctx->stats[7] = static_cast<double>(abandoned);
     ctx->n_stats = 8;
+    if (std::getenv("BS_DEBUG_PROBES")) {  // the longest probes (diagnostics)
+      std::vector<long long> idx(probe_total);
+      for (long long i = 0; i < probe_total; ++i) idx[i] = i;
+      std::partial_sort(idx.begin(), idx.begin() + std::min<long long>(8, probe_total), idx.end(),
+                        [&](long long a, long long b) { return hp[a].ns > hp[b].ns; });
+      for (long long q = 0; q < std::min<long long>(8, probe_total); ++q) {
+        const long long i = idx[q];
+        int t = 0;
+        while (t + 1 < n_tables && tabs[t + 1].probe_off <= i) ++t;
+        const long long rel = i - tabs[t].probe_off, c = rel / tabs[t].n_streams, st = rel % tabs[t].n_streams;
+        std::fprintf(stderr, "probe t%d c%lld (phase %d tp %d f %.0f) k %lld: %.1f ms, %lld events, status %d meets %d\n",
+                     t, c, cands[c].phase, cands[c].tp, cands[c].base_freq_mhz, st / std::max(1, reps) + 1,
+                     hp[i].ns / 1e6, hp[i].events, hp[i].status, hp[i].meets);
+      }
+    }
     for (auto& e : ev) cudaEventDestroy(e);
   }
 
