@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--only", choices=["c1", "c3", "c4", "c4x", "c5g", "c5x"], default=None,
                     help="run one sub-benchmark alone and print its JSON object")
     ap.add_argument("--c4-scenarios", type=int, default=1024)
+    ap.add_argument("--c3-windows", type=int, default=24, help="1-hour windows in the C3 table stream")
     ap.add_argument("--c5x-decisions", type=int, default=4096)
     return ap.parse_args()
 
@@ -227,7 +228,8 @@ def _barrier(world: int):
         dist.barrier()
 
 
-def bench_c3(dev, with_cpu: bool, repeats: int = 3, rank: int = 0, world: int = 1, local: int = 0) -> dict:
+def bench_c3(dev, with_cpu: bool, repeats: int = 3, rank: int = 0, world: int = 1, local: int = 0,
+             n_windows: int = 24) -> dict:
     """configs[2]: coarse-tier placement for a 16-GPU cluster over a bursty
     1-hour window: the config table (goodput search + E_c of every
     candidate, build_config_table placement.hpp:240-260) + the ILP."""
@@ -255,9 +257,9 @@ def bench_c3(dev, with_cpu: bool, repeats: int = 3, rank: int = 0, world: int = 
     t_ilp = time.perf_counter() - t0
     t_table = statistics.median(times)
     k_max = int(base.mean_rps() // search.tolerance_rps)
-    # the stream of bursty 1-hour windows (configs[2]: "over bursty 1-hour trace windows"): four
+    # the stream of bursty 1-hour windows (configs[2]: "over bursty 1-hour trace windows"): a day of
     # consecutive windows, their tables built concurrently on one GPU
-    day = P.gen_gamma_trace(12.0, 0.5, 4 * 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)),
+    day = P.gen_gamma_trace(12.0, 0.5, n_windows * 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)),
                             7)
     wins = P.split_windows(day, 3600e3)
     if world > 1:  # windows sharded across ranks, tables all-gathered
@@ -659,7 +661,8 @@ def run_extras(args, dev, rank, world, local) -> dict:
             if world == 1:
                 out["c1_demo"] = bench_c1(dev, with_cpu)
         elif k == "c3":
-            out["c3_placement"] = bench_c3(dev, with_cpu, rank=rank, world=world, local=local)
+            out["c3_placement"] = bench_c3(dev, with_cpu, rank=rank, world=world, local=local,
+                                           n_windows=args.c3_windows)
         elif k == "c4":
             out["c4_replay"] = bench_c4(dev, rank, world, local, args.c4_scenarios, with_cpu)
         elif k == "c4x":

@@ -684,7 +684,9 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
   const size_t o_kept = in_bytes, o_kc = o_kept + up(4ull * kept_total), o_probe = o_kc + up(8ull * stream_total);
   const size_t o_pst = o_probe + up(sizeof(ProbeOut) * probe_total);
   const size_t o_heap = o_pst + up(4ull * probe_total);
-  const size_t heap_rows = any_decode ? static_cast<size_t>(probe_total) : 0;
+  // decode residents live in shared memory when they fit (heap_cap <= 1024, see the launch); global
+  // heaps only otherwise
+  const size_t heap_rows = any_decode && heap_cap > 1024 ? static_cast<size_t>(probe_total) : 0;
   const size_t total = o_heap + up(sizeof(Resident) * heap_rows * heap_cap);
   char* d = static_cast<char*>(ctx->dev_buf(kSlotWork, total));
   char* h = static_cast<char*>(ctx->host_buf(kSlotWork, in_bytes + sizeof(ProbeOut) * probe_total + 256));
