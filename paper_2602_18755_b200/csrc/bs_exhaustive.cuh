@@ -587,20 +587,20 @@ struct LeafAcc {
   // with (num, den) is provably worse than thr when
   //   fl(num - fl(beta * den)) > s_last + num * 2^-40,
   // beta = fl(thr * (1 + 2^-47)), s_last >= amax * (beta - pmin (1 - u))^+.
-  double amax_last;
-  double pmin_lo_last;
   double beta;
   double s_last;
 };
 
-__device__ __forceinline__ void set_threshold(LeafAcc& a, double hint) {
+// (the last level's amax / pmin_lo are re-read from the tables: fewer live registers)
+__device__ __forceinline__ void set_threshold(LeafAcc& a, double hint, const DTables* __restrict__ T) {
   // hint is NaN while the slot still holds its (~0, ~0) reset value
   const double thr = (a.best < hint || hint != hint) ? a.best : hint;
   a.thr_scaled = thr >= kFilterMinBest ? __dmul_rn(thr, kFilterScale) : (thr == 0.0 ? 0.0 : INFINITY);
   if (thr >= kFilterMinBest && thr < INFINITY) {
     a.beta = __dmul_rn(thr, 1.0 + 0x1p-47);
-    const double gap = __dsub_rn(a.beta, a.pmin_lo_last);
-    a.s_last = gap > 0.0 ? __dmul_rn(__dmul_rn(gap, a.amax_last), 1.0 + 0x1p-40) : 0.0;
+    const int kl = T->K - 1;
+    const double gap = __dsub_rn(a.beta, T->pmin_lo[kl]);
+    a.s_last = gap > 0.0 ? __dmul_rn(__dmul_rn(gap, T->amax[kl]), 1.0 + 0x1p-40) : 0.0;
   } else {
     a.beta = INFINITY;
     a.s_last = INFINITY;
@@ -641,7 +641,7 @@ __device__ __forceinline__ void sweep_last(const DTables* __restrict__ T, int k,
     if (obj < a.best || (obj == a.best && code < a.code)) {
       a.best = obj;
       a.code = code;
-      set_threshold(a, hint);
+      set_threshold(a, hint, T);
     }
   }
 }
@@ -693,7 +693,7 @@ __device__ __forceinline__ void leaves_counted(const DTables* __restrict__ T, in
     if (obj < a.best || (obj == a.best && code < a.code)) {
       a.best = obj;
       a.code = code;
-      set_threshold(a, hint);
+      set_threshold(a, hint, T);
     }
   };
   if (c == nc) {  // every switched leaf passes: natural order, no index loads
@@ -876,9 +876,7 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
     a.best = INFINITY;
     a.code = ~0ull;
     a.count = 0;
-    a.amax_last = T->amax[K - 1];
-    a.pmin_lo_last = T->pmin_lo[K - 1];
-    set_threshold(a, hint);
+    set_threshold(a, hint, T);
     const unsigned long long cb = code * static_cast<unsigned long long>(nc);
     if (I == 1) {  // K == 1
       sweep_last(T, FD, nc, t, num, den, last, cb, false, hint, a);
