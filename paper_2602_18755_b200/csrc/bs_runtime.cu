@@ -1,5 +1,6 @@
 // bs_runtime.cu — context, model upload, packing and the model-query entry
 // points of the C ABI (include/biscale_gpu.h).
+#include <cstddef>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -131,6 +132,12 @@ int pack_mpc_cfg(bs_ctx_t ctx, const bs_mpc_config& c, const bs_scheduler_policy
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+static_assert(sizeof(DWaiting) == sizeof(bs_waiting) && offsetof(DWaiting, id) == offsetof(bs_waiting, id) &&
+                  offsetof(DWaiting, arrival) == offsetof(bs_waiting, arrival_ms) &&
+                  offsetof(DWaiting, total) == offsetof(bs_waiting, total_len) &&
+                  offsetof(DWaiting, remaining) == offsetof(bs_waiting, remaining_len),
+              "DWaiting mirrors bs_waiting");
+
 int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
                   const bs_mpc_problem* problems, int n, PackedProblems* out) {
   out->fg_pairs.clear();
@@ -190,13 +197,9 @@ int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_po
     }
     p.wait_off = static_cast<long long>(wo);
     p.run_off = static_cast<long long>(ro);
-    for (int j = 0; j < s.n_waiting; ++j) {
-      hw[wo].id = s.waiting[j].id;
-      hw[wo].arrival = s.waiting[j].arrival_ms;
-      hw[wo].total = s.waiting[j].total_len;
-      hw[wo].remaining = s.waiting[j].remaining_len;
-      ++wo;
-    }
+    // bs_waiting and DWaiting share one layout (static_asserts below): one copy per snapshot
+    if (s.n_waiting > 0) std::memcpy(hw + wo, s.waiting, sizeof(DWaiting) * static_cast<size_t>(s.n_waiting));
+    wo += static_cast<size_t>(s.n_waiting);
     if (s.running_active) {
       for (int j = 0; j < s.n_running; ++j) {
         hr[ro].arrival = s.running_arrivals_ms[j];
