@@ -253,3 +253,39 @@ def test_batched_tables_match_reference(gpu_device, ref_lib):
         for w, table in zip(wins, tables):
             want = _ref_table(ref_lib, m, w, slo, pol, search, cands)
             assert [_cmp(e) for e in table] == [_cmp(e) for e in want]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_search_pruning_random_tables_match_reference(gpu_device, ref_lib, seed):
+    """Search-path pruning under stress: random grids whose latency or power
+    turns non-positive above a random batch size (ModelError part-way through
+    some probes, so outcomes mix pass / fail / error along the search path),
+    1-3 replicates, tight and loose SLOs, traces whose feasibility is not
+    monotone in the rate step -- every table entry equals the reference's."""
+    rng = random.Random(seed)
+    m = probe_models()
+    cut = rng.choice([3000.0, 4000.0, 6000.0])
+    knots = P.Axis("sum_len", [0.0, 1000.0, cut, 1.5 * cut])  # values cross zero just above `cut`
+    lat = [2.0, 40.0, 300.0, -1.0 if seed % 2 else 900.0]
+    pw = [100.0, 150.0, 180.0, -5.0 if seed % 4 == 0 else 200.0]
+    m.latency_prefill = P.LatencyTable(PF, P.NdGrid([knots], lat))
+    m.power_prefill = P.PowerTable(PF, P.NdGrid([P.Axis("sum_len", [0.0, 1000.0, cut, 1.5 * cut])], pw))
+    m.latency_decode = P.LatencyTable(DE, P.NdGrid([P.Axis("n_requests", [1.0, 8.0, 64.0]),
+                                                    P.Axis("freq_mhz", [500.0, 1000.0])],
+                                                   [2.0, 1.0, 8.0, 5.0, -3.0 if seed % 2 == 0 else 40.0, 25.0]))
+    m.idle = P.IdlePowerModel([P.TpEntry(1, [500.0, 1000.0], [10.0, 10.0]), P.TpEntry(2, [500.0, 1000.0], [12.0, 14.0])])
+    reqs, t = [], 0.0
+    for i in range(rng.randint(150, 400)):
+        t += rng.expovariate(1.0 / rng.choice([5.0, 20.0, 80.0]))
+        reqs.append(P.Request(i, t, rng.randint(50, 3000), rng.randint(1, 60)))
+    base = P.Trace(reqs, t + 1000.0)
+    cands = P.enumerate_candidates(P.FrequencyLadder([500.0, 750.0, 1000.0]), [1, 2])
+    # batches big enough to reach the non-positive region (prefill: odd seeds; decode: even seeds)
+    pol = P.SchedulerPolicy(max_batch_tokens=8192 if seed % 2 else rng.choice([2048, 8192]),
+                            max_batch_requests=256 if seed % 2 == 0 else rng.choice([16, 256]))
+    for slo in (P.SLOSpec(rng.uniform(30.0, 300.0), rng.uniform(3.0, 20.0)), P.SLOSpec(5000.0, 500.0)):
+        search = P.GoodputSearch(tolerance_rps=rng.choice([0.25, 0.5, 1.0]), probe_count=rng.randint(1, 3),
+                                 seed=rng.getrandbits(63))
+        got = P.build_config_table(cands, base, slo, m, pol, search)
+        want = _ref_table(ref_lib, m, base, slo, pol, search, cands)
+        assert [_cmp(e) for e in got] == [_cmp(e) for e in want]
