@@ -251,6 +251,134 @@ __device__ __forceinline__ void block_append2n(unsigned long long* c0, unsigned 
 // Pass 1 marks the kept children by digit, pass 2 writes them in digit order
 // (the layout of a (node, digit) expansion: siblings contiguous, in code
 // order) after a block-aggregated append.
+// Expansion of one depth-k node per thread (valid: the thread holds one);
+// every thread of the block must call it.  Its children that pass
+// meets_slo's check are the sorted prefix of the level (feasible_prefix, by
+// monotonicity), less f == last, plus the non-switching child when it passes
+// -- so no (node, digit) pair that fails is touched.  Children at the
+// problem's FD go to the final list, and only when one of their own children
+// passes (no feasible leaf below otherwise); visited in step order, their
+// clocks never decrease, so that test walks one sorted-prefix count down.
+// Pass 1 marks the kept children by digit, pass 2 writes them in digit order
+// (the layout of a (node, digit) expansion: siblings contiguous, in code
+// order) after a block-aggregated append.
+__device__ __forceinline__ void expand_node(const DTables* __restrict__ tables, int k, ExCtl* ctl, bool valid, int d,
+                                            double t, double num, double den, int last, unsigned long long code,
+                                            Frontier out, FinalList fin, unsigned long long cap_out,
+                                            unsigned long long cap_final) {
+  unsigned keep = 0u;  // bit f: child f kept
+  bool to_final = false;
+  int nc = 0;
+  const DTables* __restrict__ T = tables;
+  if (valid) {
+    T = &tables[d];
+    nc = T->nc;
+    to_final = (k + 1) == T->FD;
+    if (T->sorted_ok) {
+      const bool prune = to_final && k + 1 < T->K;
+      const int c = feasible_prefix(T, k, nc, t);
+      const unsigned char* __restrict__ ord = T->ord[k];
+      const double* __restrict__ sb = T->sb[k];
+      const int kl = k + 1;
+      int cl = -1;
+      for (int j = 0; j < c; ++j) {
+        const int f = ord[j];
+        if (f == last) continue;
+        bool ok = true;
+        if (prune) {
+          const double ct = __dadd_rn(t, sb[j]);
+          if (cl < 0) {
+            cl = feasible_prefix(T, kl, nc, ct);
+          } else {
+            const double ml = T->minarr[kl], ttft = T->ttft;
+            const double* __restrict__ sbl = T->sb[kl];
+            while (cl > 0 && __dsub_rn(__dadd_rn(ct, sbl[cl - 1]), ml) > ttft) --cl;
+          }
+          ok = cl > 0 || diag_passes(T, kl, ct, f);
+        }
+        if (ok) keep |= 1u << f;
+      }
+      if (diag_passes(T, k, t, last)) {
+        bool ok = true;
+        if (prune) {
+          const double ct = __dadd_rn(t, T->B0[k][last]);
+          ok = feasible_prefix(T, kl, nc, ct) > 0 || diag_passes(T, kl, ct, last);
+        }
+        if (ok) keep |= 1u << last;
+      }
+    } else {  // unsorted tables: every digit
+      for (int f = 0; f < nc; ++f) {
+        double ct, cn, cd;
+        if (child_state(T, k, t, num, den, last, f, ct, cn, cd)) keep |= 1u << f;
+      }
+    }
+  }
+  const unsigned m = static_cast<unsigned>(__popc(keep));
+  unsigned long long sf, so;
+  block_append2n(&ctl->final_count, to_final ? m : 0u, &ctl->level_count[k + 1], to_final ? 0u : m, &sf, &so);
+  // Pass 2, warp-cooperative so the stores coalesce: the warp's children of
+  // each list occupy one contiguous slot range (block_append2n keeps lanes
+  // in order), and lane l writes items l, l + 32, ... of it, fetching the
+  // owner node's state by shuffles.
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int list = 0; list < 2; ++list) {
+    const bool mine = (list == 0) == to_final;
+    const unsigned cnt = mine ? m : 0u;
+    unsigned inc = cnt;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+    if (total == 0u) continue;
+    // the warp's first slot of this list (every lane with cnt > 0 agrees; take the first)
+    const unsigned long long my_start = (list == 0 ? sf : so) - (inc - cnt);
+    const int first = __ffs(__ballot_sync(0xffffffffu, cnt > 0u)) - 1;
+    const unsigned long long wbase = __shfl_sync(0xffffffffu, my_start, first);
+    const unsigned long long cap = list == 0 ? cap_final : cap_out;
+    for (unsigned b0 = 0; b0 < total; b0 += 32u) {
+      const unsigned idx = b0 + static_cast<unsigned>(lane);
+      int o = 0;  // owner: the first lane whose inclusive count exceeds idx
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const unsigned probe = __shfl_sync(0xffffffffu, inc, o + step - 1);
+        if (probe <= idx) o += step;
+      }
+      const unsigned o_inc = __shfl_sync(0xffffffffu, inc, o), o_cnt = __shfl_sync(0xffffffffu, cnt, o);
+      const unsigned o_keep = __shfl_sync(0xffffffffu, keep, o);
+      const int o_d = __shfl_sync(0xffffffffu, d, o), o_last = __shfl_sync(0xffffffffu, last, o);
+      const int o_nc = __shfl_sync(0xffffffffu, nc, o);
+      const unsigned long long o_code = __shfl_sync(0xffffffffu, code, o);
+      const double o_t = __shfl_sync(0xffffffffu, t, o), o_num = __shfl_sync(0xffffffffu, num, o),
+                   o_den = __shfl_sync(0xffffffffu, den, o);
+      if (idx >= total) continue;
+      const int r = static_cast<int>(idx - (o_inc - o_cnt));
+      const int f = static_cast<int>(__fns(o_keep, 0, r + 1));
+      const unsigned long long slot = wbase + idx;
+      const unsigned long long cc = o_code * static_cast<unsigned long long>(o_nc) + static_cast<unsigned long long>(f);
+      if (slot >= cap) {
+        atomicAdd(&ctl->overflow, 1ull);
+      } else if (list == 0) {
+        fin.d[slot] = o_d;
+        fin.code[slot] = cc;
+      } else {
+        double ct, cn, cd;
+        child_state(&tables[o_d], k, o_t, o_num, o_den, o_last, f, ct, cn, cd);
+        out.d[slot] = o_d;
+        out.code[slot] = cc;
+        out.t[slot] = ct;
+        out.num[slot] = cn;
+        out.den[slot] = cd;
+        out.last[slot] = f;
+      }
+    }
+  }
+}
+
+// Level k >= 3 of the search (prepare_kernel expands depths 1-3): one
+// thread per depth-k node, expand_node.
 __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl,
                                                        Frontier in, Frontier out, FinalList fin,
                                                        unsigned long long cap_out, unsigned long long cap_final) {
@@ -260,123 +388,10 @@ __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict
   for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < n_in;
        base += stride) {
     const unsigned long long i = base + threadIdx.x;
-    unsigned keep = 0u;  // bit f: child f kept
-    bool to_final = false;
-    int d = 0, last = 0, nc = 0;
-    double t = 0.0, num = 0.0, den = 0.0;
-    unsigned long long code = 0;
-    const DTables* __restrict__ T = tables;
-    if (i < n_in) {
-      d = in.d[i];
-      T = &tables[d];
-      t = in.t[i];
-      num = in.num[i];
-      den = in.den[i];
-      last = in.last[i];
-      code = in.code[i];
-      nc = T->nc;
-      to_final = (k + 1) == T->FD;
-      if (T->sorted_ok) {
-        const bool prune = to_final && k + 1 < T->K;
-        const int c = feasible_prefix(T, k, nc, t);
-        const unsigned char* __restrict__ ord = T->ord[k];
-        const double* __restrict__ sb = T->sb[k];
-        const int kl = k + 1;
-        int cl = -1;
-        for (int j = 0; j < c; ++j) {
-          const int f = ord[j];
-          if (f == last) continue;
-          bool ok = true;
-          if (prune) {
-            const double ct = __dadd_rn(t, sb[j]);
-            if (cl < 0) {
-              cl = feasible_prefix(T, kl, nc, ct);
-            } else {
-              const double ml = T->minarr[kl], ttft = T->ttft;
-              const double* __restrict__ sbl = T->sb[kl];
-              while (cl > 0 && __dsub_rn(__dadd_rn(ct, sbl[cl - 1]), ml) > ttft) --cl;
-            }
-            ok = cl > 0 || diag_passes(T, kl, ct, f);
-          }
-          if (ok) keep |= 1u << f;
-        }
-        if (diag_passes(T, k, t, last)) {
-          bool ok = true;
-          if (prune) {
-            const double ct = __dadd_rn(t, T->B0[k][last]);
-            ok = feasible_prefix(T, kl, nc, ct) > 0 || diag_passes(T, kl, ct, last);
-          }
-          if (ok) keep |= 1u << last;
-        }
-      } else {  // unsorted tables: every digit
-        for (int f = 0; f < nc; ++f) {
-          double ct, cn, cd;
-          if (child_state(T, k, t, num, den, last, f, ct, cn, cd)) keep |= 1u << f;
-        }
-      }
-    }
-    const unsigned m = static_cast<unsigned>(__popc(keep));
-    unsigned long long sf, so;
-    block_append2n(&ctl->final_count, to_final ? m : 0u, &ctl->level_count[k + 1], to_final ? 0u : m, &sf, &so);
-    // Pass 2, warp-cooperative so the stores coalesce: the warp's children of
-    // each list occupy one contiguous slot range (block_append2n keeps lanes
-    // in order), and lane l writes items l, l + 32, ... of it, fetching the
-    // owner node's state by shuffles.
-    const int lane = threadIdx.x & 31;
-#pragma unroll 1
-    for (int list = 0; list < 2; ++list) {
-      const bool mine = (list == 0) == to_final;
-      const unsigned cnt = mine ? m : 0u;
-      unsigned inc = cnt;  // inclusive warp scan
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
-      if (total == 0u) continue;
-      // the warp's first slot of this list (every lane with cnt > 0 agrees; take the first)
-      const unsigned long long my_start = (list == 0 ? sf : so) - (inc - cnt);
-      const int first = __ffs(__ballot_sync(0xffffffffu, cnt > 0u)) - 1;
-      const unsigned long long wbase = __shfl_sync(0xffffffffu, my_start, first);
-      const unsigned long long cap = list == 0 ? cap_final : cap_out;
-      for (unsigned b0 = 0; b0 < total; b0 += 32u) {
-        const unsigned idx = b0 + static_cast<unsigned>(lane);
-        int o = 0;  // owner: the first lane whose inclusive count exceeds idx
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const unsigned probe = __shfl_sync(0xffffffffu, inc, o + step - 1);
-          if (probe <= idx) o += step;
-        }
-        const unsigned o_inc = __shfl_sync(0xffffffffu, inc, o), o_cnt = __shfl_sync(0xffffffffu, cnt, o);
-        const unsigned o_keep = __shfl_sync(0xffffffffu, keep, o);
-        const int o_d = __shfl_sync(0xffffffffu, d, o), o_last = __shfl_sync(0xffffffffu, last, o);
-        const int o_nc = __shfl_sync(0xffffffffu, nc, o);
-        const unsigned long long o_code = __shfl_sync(0xffffffffu, code, o);
-        const double o_t = __shfl_sync(0xffffffffu, t, o), o_num = __shfl_sync(0xffffffffu, num, o),
-                     o_den = __shfl_sync(0xffffffffu, den, o);
-        if (idx >= total) continue;
-        const int r = static_cast<int>(idx - (o_inc - o_cnt));
-        const int f = static_cast<int>(__fns(o_keep, 0, r + 1));
-        const unsigned long long slot = wbase + idx;
-        const unsigned long long cc = o_code * static_cast<unsigned long long>(o_nc) + static_cast<unsigned long long>(f);
-        if (slot >= cap) {
-          atomicAdd(&ctl->overflow, 1ull);
-        } else if (list == 0) {
-          fin.d[slot] = o_d;
-          fin.code[slot] = cc;
-        } else {
-          double ct, cn, cd;
-          child_state(&tables[o_d], k, o_t, o_num, o_den, o_last, f, ct, cn, cd);
-          out.d[slot] = o_d;
-          out.code[slot] = cc;
-          out.t[slot] = ct;
-          out.num[slot] = cn;
-          out.den[slot] = cd;
-          out.last[slot] = f;
-        }
-      }
-    }
+    const bool valid = i < n_in;
+    expand_node(tables, k, ctl, valid, valid ? in.d[i] : 0, valid ? in.t[i] : 0.0, valid ? in.num[i] : 0.0,
+                valid ? in.den[i] : 0.0, valid ? in.last[i] : 0, valid ? in.code[i] : 0ull, out, fin, cap_out,
+                cap_final);
   }
 }
 
@@ -389,14 +404,15 @@ __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict
 constexpr int kSeedRounds = BS_SEED_ROUNDS;
 
 // One CTA per decision: the tables, the argmin slot reset, and the first
-// levels of the search.  The prefixes of depth D0 = min(2, FD) are expanded
-// here (nc^D0 per decision) and appended to the depth-D0 list (or, at FD, to
-// the final list), so the BFS starts at depth 2.  The run's counters are
+// levels of the search.  The prefixes of depth D0 = min(2, FD) are evaluated
+// here (nc^D0 per decision); at FD they go to the final list, otherwise the
+// depth-2 ones are expanded once more (expand_node) into the depth-3 list
+// (or the final list), so the BFS starts at depth 3.  The run's counters are
 // zeroed by the host before this launch.
 __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
                                                                const DWaiting* W, const DRunning* R, DTables* tables,
                                                                ExCtl* ctl, int n, const DFastPair* fg, Key128* best,
-                                                               unsigned long long* feas, Frontier L2,
+                                                               unsigned long long* feas, Frontier L2, Frontier L3,
                                                                FinalList fin, unsigned long long cap_level,
                                                                unsigned long long cap_final) {
   __shared__ int s_status;
@@ -546,6 +562,11 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       }
       // a final node none of whose children passes has no feasible leaf (as in bfs_node_kernel)
       if (ok && to_final && T->sorted_ok && FD < K) ok = feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
+    }
+    if (FD > 2) {  // one more level here: the depth-2 nodes never reach global memory (FD is uniform per CTA)
+      expand_node(tables, 2, ctl, ok, d, t, num, den, last, static_cast<unsigned long long>(e), L3, fin, cap_level,
+                  cap_final);
+      continue;
     }
     unsigned long long sf, so;
     block_append2(&ctl->final_count, ok && to_final, &ctl->level_count[D0], ok && !to_final, &sf, &so);

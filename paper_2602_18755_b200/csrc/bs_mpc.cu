@@ -7,8 +7,9 @@
 //   prepare_kernel   1 CTA / problem: project_batches (dvfs.hpp:63-100) by
 //                    one thread, then the K x N (lat, pow) tables by all
 //                    threads through the bit-exact interpolator; resets the
-//                    argmin slot and expands the first two levels (N^2
-//                    prefixes) straight into the depth-2 list.
+//                    argmin slot and expands the first three levels (N^2
+//                    prefixes, then their passing children) straight into
+//                    the depth-3 list.
 //   bfs_node_kernel  x (max depth of final nodes - 2): level-synchronous
 //                    expansion of every feasible prefix of every decision,
 //                    one thread per node (its passing children are a sorted
@@ -441,11 +442,11 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   BS_CUDA_TRY(ctx, cudaMemsetAsync(run->dCtl, 0, sizeof(ExCtl), ctx->stream));
   prepare_kernel<<<n, kPrepThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
                                                       run->dT, run->dCtl, n, run->dFG, run->dBest, run->dFeas, lev[0],
-                                                      fin, run->cap_level, run->cap_final);
+                                                      lev[1], fin, run->cap_level, run->cap_final);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
   BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel
-  for (int k = 2; k < run->bfs_levels; ++k) {  // depth-2 lists come from prepare_kernel
+  for (int k = 3; k < run->bfs_levels; ++k) {  // depths up to 3 come from prepare_kernel
     bfs_node_kernel<<<run->bfs_grid, 256, 0, ctx->stream>>>(run->dT, k, run->dCtl, lev[k & 1], lev[(k + 1) & 1],
                                                             fin, run->cap_level, run->cap_final);
     BS_LAUNCH_CHECK(ctx);
