@@ -740,17 +740,23 @@ def main():
         clocks.start()
         launches0 = dev.kernel_launches()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        leaf_ms, phase_ms = [], []  # leaf_ms: the sweep kernel (dominant)
         for s in range(args.steps):
-            step(evs[s], kernel_times=True)
-            ms = (C.c_float * 5)()
-            lib.bs_mpc_plan_kernel_ms(dev.handle, plan, ms, 5)  # syncs the stream
-            phase_ms.append(list(ms))
-            leaf_ms.append(ms[3])
+            step(evs[s])
+            evs[s][1].synchronize()
             flush.zero_()  # untimed L2 flush between timed steps
         torch.cuda.synchronize()
         launches = dev.kernel_launches() - launches0
         step_ms = [a.elapsed_time(b) for a, b in evs]
+        # per-kernel times from the same number of extra, untimed steps (events between the kernels
+        # would serialise the programmatic dependent launches of the timed ones)
+        leaf_ms, phase_ms = [], []  # leaf_ms: the sweep kernel (dominant)
+        for s in range(args.steps):
+            step(None, kernel_times=True)
+            ms = (C.c_float * 5)()
+            lib.bs_mpc_plan_kernel_ms(dev.handle, plan, ms, 5)  # syncs the stream
+            phase_ms.append(list(ms))
+            leaf_ms.append(ms[3])
+            flush.zero_()
         total_ms = sum(step_ms)
         if world > 1:
             t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")

@@ -382,6 +382,7 @@ __device__ __forceinline__ void expand_node(const DTables* __restrict__ tables, 
 __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl,
                                                        Frontier in, Frontier out, FinalList fin,
                                                        unsigned long long cap_out, unsigned long long cap_final) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous level (programmatic dependent launch)
   if (ctl->overflow) return;
   const unsigned long long n_in = ctl->level_count[k];
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
@@ -867,6 +868,7 @@ template <int MINB>
 __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
                                                     FinalList fin, Key128* best, unsigned long long* feas,
                                                     unsigned long long cap_final) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the BFS lists (programmatic dependent launch)
   if (ctl->overflow) return;  // the run is repeated with larger lists (one_shot): skip the sweep
   const unsigned long long n_fin = ctl->final_count < cap_final ? ctl->final_count : cap_final;
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;

@@ -49,6 +49,7 @@ constexpr double kFilterMinDen = 0x1p-900;
 
 __global__ void finalize_kernel(const DTables* __restrict__ tables, const DMpcCfg* cfgs, const DProblem* probs,
                                 const Key128* best, const unsigned long long* feas, DMpcOut* out, int n) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the sweep's results (programmatic dependent launch)
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= n) return;
   const DTables* T = &tables[d];
@@ -406,6 +407,23 @@ int grid_for(bs_ctx_t ctx, const void* kernel, int threads) {
   return ctx->sm_count * b;
 }
 
+// A launch with programmatic stream serialization (the kernel calls
+// griddepcontrol.wait before reading its predecessor's results).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Enqueues the kernels of one run on the context stream (no host sync).
 int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   const int n = run->n;
@@ -446,22 +464,31 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
   BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel
+  // The kernels after prepare are launched as programmatic dependents: each
+  // may be scheduled while its predecessor drains and waits for it in
+  // griddepcontrol.wait before touching its data (phase events, when
+  // recorded, serialise them again).
   for (int k = 3; k < run->bfs_levels; ++k) {  // depths up to 3 come from prepare_kernel
-    bfs_node_kernel<<<run->bfs_grid, 256, 0, ctx->stream>>>(run->dT, k, run->dCtl, lev[k & 1], lev[(k + 1) & 1],
-                                                            fin, run->cap_level, run->cap_final);
+    BS_CUDA_TRY(ctx, launch_pdl(bfs_node_kernel, dim3(run->bfs_grid), dim3(256), ctx->stream,
+                                static_cast<const DTables*>(run->dT), k, run->dCtl, lev[k & 1], lev[(k + 1) & 1], fin,
+                                run->cap_level, run->cap_final));
     BS_LAUNCH_CHECK(ctx);
   }
   BS_REC(3);
   if (run->sweep3)
-    sweep_kernel<kSweepMinB3><<<run->sweep_grid3, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest,
-                                                                        run->dFeas, run->cap_final);
+    BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB3>, dim3(run->sweep_grid3), dim3(256), ctx->stream,
+                                static_cast<const DTables*>(run->dT), static_cast<const ExCtl*>(run->dCtl), fin,
+                                run->dBest, run->dFeas, run->cap_final));
   else
-    sweep_kernel<kSweepMinB2><<<run->sweep_grid2, 256, 0, ctx->stream>>>(run->dT, run->dCtl, fin, run->dBest,
-                                                                        run->dFeas, run->cap_final);
+    BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB2>, dim3(run->sweep_grid2), dim3(256), ctx->stream,
+                                static_cast<const DTables*>(run->dT), static_cast<const ExCtl*>(run->dCtl), fin,
+                                run->dBest, run->dFeas, run->cap_final));
   BS_LAUNCH_CHECK(ctx);
   BS_REC(4);
-  finalize_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(run->dT, pk.cfgs, pk.problems, run->dBest, run->dFeas,
-                                                            run->dOut, n);
+  BS_CUDA_TRY(ctx, launch_pdl(finalize_kernel, dim3((n + 127) / 128), dim3(128), ctx->stream,
+                              static_cast<const DTables*>(run->dT), static_cast<const DMpcCfg*>(pk.cfgs),
+                              static_cast<const DProblem*>(pk.problems), static_cast<const Key128*>(run->dBest),
+                              static_cast<const unsigned long long*>(run->dFeas), run->dOut, n));
   BS_LAUNCH_CHECK(ctx);
   BS_REC(5);
   return BS_OK;
