@@ -6,7 +6,9 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -121,5 +123,26 @@ struct PackedProblems {
 };
 int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
                   const bs_mpc_problem* problems, int n, PackedProblems* out);
+
+// fn(begin, end) over [0, n) split into contiguous chunks on up to `threads`
+// host threads (the caller runs the first chunk); serial below `grain` items
+// per thread.  Used for the per-problem host work of large batches (packing,
+// result expansion), which is independent per item.
+template <class Fn>
+void parallel_chunks(int n, int grain, Fn&& fn) {
+  const int hw = static_cast<int>(std::thread::hardware_concurrency());
+  const int threads = std::max(1, std::min({hw > 0 ? hw : 1, 8, n / std::max(1, grain)}));
+  if (threads <= 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(threads - 1);
+  for (int t = 1; t < threads; ++t)
+    pool.emplace_back([&, t] { fn(static_cast<int>(static_cast<long long>(n) * t / threads),
+                                  static_cast<int>(static_cast<long long>(n) * (t + 1) / threads)); });
+  fn(0, static_cast<int>(static_cast<long long>(n) / threads));
+  for (auto& th : pool) th.join();
+}
 
 }  // namespace bs

@@ -520,9 +520,11 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
     return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
                      "batch; split it into smaller calls", *hOverflow);
   }
-  for (int i = 0; i < n; ++i)
-    expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
-                  run->target[i], &out[i], run->mode == kExhaustive);
+  parallel_chunks(n, 1024, [&](int lo, int hi) {
+    for (int i = lo; i < hi; ++i)
+      expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
+                    run->target[i], &out[i], run->mode == kExhaustive);
+  });
   return report_status(ctx, out, n);
 }
 

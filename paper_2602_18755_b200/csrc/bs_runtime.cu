@@ -174,40 +174,47 @@ int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_po
   DProblem* hp = reinterpret_cast<DProblem*>(h + o_prob);
   DWaiting* hw = reinterpret_cast<DWaiting*>(h + o_wait);
   DRunning* hr = reinterpret_cast<DRunning*>(h + o_run);
-  size_t wo = 0, ro = 0;
+  // serial: offsets and the distinct (configuration, tp) pairs; then the
+  // independent per-problem copies, in parallel for large batches
+  std::vector<size_t> woff(static_cast<size_t>(n) + 1), roff(static_cast<size_t>(n) + 1);
+  std::vector<int> fgi(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) {
     const bs_snapshot& s = problems[i].snap;
-    DProblem& p = hp[i];
-    p.now = s.now_ms;
-    p.cur_freq = s.current_freq_mhz;
-    p.target_freq = s.target_freq_mhz;
-    p.run_wr = s.running_work_remaining;
-    p.run_n = s.running_features.n_requests;
-    p.run_sum = s.running_features.sum_len;
-    p.tp = s.tp;
-    p.run_active = s.running_active ? 1 : 0;
-    p.n_wait = s.n_waiting;
-    p.n_run = s.running_active ? s.n_running : 0;
-    p.cfg = problems[i].cfg_index;
-    {
-      const std::pair<int, int> key(problems[i].cfg_index, s.tp);
-      auto it = std::find(out->fg_pairs.begin(), out->fg_pairs.end(), key);
-      p.fgi = static_cast<int>(it - out->fg_pairs.begin());
-      if (it == out->fg_pairs.end()) out->fg_pairs.push_back(key);
-    }
-    p.wait_off = static_cast<long long>(wo);
-    p.run_off = static_cast<long long>(ro);
-    // bs_waiting and DWaiting share one layout (static_asserts below): one copy per snapshot
-    if (s.n_waiting > 0) std::memcpy(hw + wo, s.waiting, sizeof(DWaiting) * static_cast<size_t>(s.n_waiting));
-    wo += static_cast<size_t>(s.n_waiting);
-    if (s.running_active) {
-      for (int j = 0; j < s.n_running; ++j) {
-        hr[ro].arrival = s.running_arrivals_ms[j];
-        hr[ro].completes = s.running_completes[j] ? 1 : 0;
-        ++ro;
+    woff[i + 1] = woff[i] + static_cast<size_t>(s.n_waiting);
+    roff[i + 1] = roff[i] + (s.running_active ? static_cast<size_t>(s.n_running) : 0);
+    const std::pair<int, int> key(problems[i].cfg_index, s.tp);
+    auto it = std::find(out->fg_pairs.begin(), out->fg_pairs.end(), key);
+    fgi[i] = static_cast<int>(it - out->fg_pairs.begin());
+    if (it == out->fg_pairs.end()) out->fg_pairs.push_back(key);
+  }
+  parallel_chunks(n, 1024, [&](int lo, int hi) {
+    for (int i = lo; i < hi; ++i) {
+      const bs_snapshot& s = problems[i].snap;
+      DProblem& p = hp[i];
+      p.now = s.now_ms;
+      p.cur_freq = s.current_freq_mhz;
+      p.target_freq = s.target_freq_mhz;
+      p.run_wr = s.running_work_remaining;
+      p.run_n = s.running_features.n_requests;
+      p.run_sum = s.running_features.sum_len;
+      p.tp = s.tp;
+      p.run_active = s.running_active ? 1 : 0;
+      p.n_wait = s.n_waiting;
+      p.n_run = s.running_active ? s.n_running : 0;
+      p.cfg = problems[i].cfg_index;
+      p.fgi = fgi[i];
+      p.wait_off = static_cast<long long>(woff[i]);
+      p.run_off = static_cast<long long>(roff[i]);
+      // bs_waiting and DWaiting share one layout (static_asserts above): one copy per snapshot
+      if (s.n_waiting > 0) std::memcpy(hw + woff[i], s.waiting, sizeof(DWaiting) * static_cast<size_t>(s.n_waiting));
+      if (s.running_active) {
+        for (int j = 0; j < s.n_running; ++j) {
+          hr[roff[i] + j].arrival = s.running_arrivals_ms[j];
+          hr[roff[i] + j].completes = s.running_completes[j] ? 1 : 0;
+        }
       }
     }
-  }
+  });
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, ctx->stream));
   out->off_cfg = o_cfg;
   out->off_prob = o_prob;
