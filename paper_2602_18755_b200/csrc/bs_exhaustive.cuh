@@ -27,6 +27,9 @@ struct ExCtl {
   unsigned long long level_count[kMaxK + 1];  // BFS list sizes per depth
   unsigned long long final_count;
   unsigned long long overflow;  // appends dropped for lack of capacity (must stay 0)
+#ifdef BS_SWEEP_STATS
+  unsigned long long st_nodes, st_children, st_rows_eval, st_leaves_eval, st_div;
+#endif
 };
 
 // Bottom levels swept per final node: 2, or 3 for trees wider than 2^24
@@ -605,6 +608,9 @@ struct LeafAcc {
   unsigned long long code;   // its code
   double thr_scaled;         // fl(min(local, global hint) * C), +inf disables the filter
   unsigned long long count;  // feasible leaves
+#ifdef BS_SWEEP_STATS
+  unsigned long long st_rows, st_leaves, st_div, st_children;
+#endif
   // leaf-row skip ("row bound"): a row of leaves under a parent
   // with (num, den) is provably worse than thr when
   //   fl(num - fl(beta * den)) > s_last + num * 2^-40,
@@ -699,17 +705,33 @@ __device__ __forceinline__ int for_feasible_children(const DTables* __restrict__
 // count c = feasible_prefix(T, k, nc, t) is known: count them in closed form,
 // skip a dominated row, else visit only the passing leaves.  rank_last /
 // b0_last: rank[k][last] and B0[k][last] (from the parent's record).
-__device__ __forceinline__ void leaves_counted(const DTables* __restrict__ T, int k, int nc, double t, double num,
-                                               double den, int last, int rank_last, double b0_last, int c,
-                                               unsigned long long code_base, bool filt, double hint, LeafAcc& a) {
+// The row's (num, den) = parent's + (e_row, a_row) are formed only for rows
+// with a feasible leaf (most rows have none: the last batch's deadline binds).
+__device__ __forceinline__ void leaves_counted(const DTables* __restrict__ T, int k, int nc, double t, double num_p,
+                                               double den_p, double e_row, double a_row, int last, int rank_last,
+                                               double b0_last, int c, unsigned long long code_base, double hint,
+                                               LeafAcc& a) {
   const bool diag = !(__dsub_rn(__dadd_rn(t, b0_last), T->minarr[k]) > T->ttft);  // diag_passes
-  a.count += static_cast<unsigned long long>(c - (rank_last < c ? 1 : 0) + (diag ? 1 : 0));
+  const int passed = c - (rank_last < c ? 1 : 0) + (diag ? 1 : 0);
+  if (passed == 0) return;
+  a.count += static_cast<unsigned long long>(passed);
+  const double num = __dadd_rn(num_p, e_row), den = __dadd_rn(den_p, a_row);
+  const bool filt = T->filter_ok && den >= kFilterMinDen;
   if (filt && row_dominated(a, num, den)) return;
+#ifdef BS_SWEEP_STATS
+  a.st_rows += 1;
+#endif
   const double* __restrict__ E = T->E[k];
   const double* __restrict__ A = T->A[k];
   auto leaf = [&](int f) {
     const double nl = __dadd_rn(num, E[f]), dl = __dadd_rn(den, A[f]);
+#ifdef BS_SWEEP_STATS
+    a.st_leaves += 1;
+#endif
     if (filt && nl > __dmul_rn(a.thr_scaled, dl)) return;  // provably worse than a known feasible key
+#ifdef BS_SWEEP_STATS
+    a.st_div += 1;
+#endif
     const double obj = dl > 0.0 ? __ddiv_rn(nl, dl) : 0.0;  // dvfs.hpp:170
     const unsigned long long code = code_base + static_cast<unsigned long long>(f);
     if (obj < a.best || (obj == a.best && code < a.code)) {
@@ -757,17 +779,16 @@ __device__ __forceinline__ void two_sorted(const DTables* __restrict__ T, int k,
     } else {
       while (cl > 0 && __dsub_rn(__dadd_rn(t2, sbl[cl - 1]), ml) > ttft) --cl;
     }
-    const double d2 = __dadd_rn(den, r.A);
-    leaves_counted(T, kl, nc, t2, __dadd_rn(num, r.E), d2, g, static_cast<int>(info >> 8), r.B0n, cl,
-                   (code_base + static_cast<unsigned long long>(g)) * nc, T->filter_ok && d2 >= kFilterMinDen, hint,
-                   a);
+#ifdef BS_SWEEP_STATS
+    a.st_children += 1;
+#endif
+    leaves_counted(T, kl, nc, t2, num, den, r.E, r.A, g, static_cast<int>(info >> 8), r.B0n, cl,
+                   (code_base + static_cast<unsigned long long>(g)) * nc, hint, a);
   }
   if (k > 0 && diag_passes(T, k, t, last)) {
     const double t2 = __dadd_rn(t, T->B0[k][last]);
-    const double d2 = __dadd_rn(den, T->A[k][last]);
-    leaves_counted(T, kl, nc, t2, __dadd_rn(num, T->E[k][last]), d2, last, T->rank[kl][last], T->B0[kl][last],
-                   feasible_prefix(T, kl, nc, t2), (code_base + static_cast<unsigned long long>(last)) * nc,
-                   T->filter_ok && d2 >= kFilterMinDen, hint, a);
+    leaves_counted(T, kl, nc, t2, num, den, T->E[k][last], T->A[k][last], last, T->rank[kl][last], T->B0[kl][last],
+                   feasible_prefix(T, kl, nc, t2), (code_base + static_cast<unsigned long long>(last)) * nc, hint, a);
   }
 }
 
@@ -899,6 +920,9 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
     a.best = INFINITY;
     a.code = ~0ull;
     a.count = 0;
+#ifdef BS_SWEEP_STATS
+    a.st_rows = a.st_leaves = a.st_div = a.st_children = 0;
+#endif
     set_threshold(a, hint, T);
     const unsigned long long cb = code * static_cast<unsigned long long>(nc);
     if (I == 1) {  // K == 1
@@ -928,5 +952,13 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
       }
     }
     flush_acc(d, a, best, feas);
+#ifdef BS_SWEEP_STATS
+    ExCtl* wctl = const_cast<ExCtl*>(ctl);
+    atomicAdd(&wctl->st_nodes, 1ull);
+    atomicAdd(&wctl->st_children, a.st_children);
+    atomicAdd(&wctl->st_rows_eval, a.st_rows);
+    atomicAdd(&wctl->st_leaves_eval, a.st_leaves);
+    atomicAdd(&wctl->st_div, a.st_div);
+#endif
   }
 }

@@ -728,6 +728,10 @@ int bs_mpc_plan_results(bs_ctx_t ctx, bs_mpc_plan_t plan, bs_mpc_result* out) {
       for (int k = 0; k <= kMaxK; ++k)
         if (c.level_count[k]) std::fprintf(stderr, " depth%d=%llu", k, c.level_count[k]);
       std::fprintf(stderr, " final=%llu overflow=%llu\n", c.final_count, c.overflow);
+#ifdef BS_SWEEP_STATS
+      std::fprintf(stderr, "bs_mpc sweep: nodes %llu children %llu rows evaluated %llu leaves %llu divisions %llu\n",
+                   c.st_nodes, c.st_children, c.st_rows_eval, c.st_leaves_eval, c.st_div);
+#endif
     }
   }
   // a resident plan's frontiers are fixed at creation: report an overflow as
