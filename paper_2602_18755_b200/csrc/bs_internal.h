@@ -7,6 +7,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <utility>
@@ -16,6 +20,11 @@
 
 #include "biscale_gpu.h"
 #include "bs_device.cuh"
+
+namespace bs {
+struct HostPool;
+constexpr int kHostWorkers = 3;  // host pool workers (plus the calling thread)
+}  // namespace bs
 
 struct bs_ctx_s {
   int device = 0;
@@ -28,6 +37,8 @@ struct bs_ctx_s {
   double stats[16] = {};  // phase timings / counters of the last entry point
   int n_stats = 0;
   int grid_cache[8] = {};  // occupancy-sized persistent grids, computed once per context (bs_mpc.cu)
+  std::unique_ptr<bs::HostPool> host_pool;  // started on first use (parallel_chunks)
+  bs::HostPool& pool();
 
   struct Buf {
     void* p = nullptr;
@@ -124,25 +135,82 @@ struct PackedProblems {
 int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
                   const bs_mpc_problem* problems, int n, PackedProblems* out);
 
-// fn(begin, end) over [0, n) split into contiguous chunks on up to `threads`
-// host threads (the caller runs the first chunk); serial below `grain` items
-// per thread.  Used for the per-problem host work of large batches (packing,
-// result expansion), which is independent per item.
+// A small pool of host worker threads owned by a context, started on first
+// use and blocked on a condition variable between jobs (they never spin, so
+// they take no cores from anything else the process runs).  run(tasks, fn)
+// calls fn(i) for i in [0, tasks) on the workers and the calling thread and
+// returns when all are done.
+struct HostPool {
+  std::vector<std::thread> th;
+  std::mutex m;
+  std::condition_variable cv, done_cv;
+  std::function<void(int)> job;
+  int tasks = 0, next = 0, finished = 0;
+  unsigned long long gen = 0;
+  bool stop = false;
+
+  void start(int workers) {
+    for (int w = 0; w < workers; ++w)
+      th.emplace_back([this] {
+        unsigned long long seen = 0;
+        for (;;) {
+          std::unique_lock<std::mutex> lk(m);
+          cv.wait(lk, [&] { return stop || gen != seen; });
+          if (stop) return;
+          seen = gen;
+          while (next < tasks) {
+            const int i = next++;
+            lk.unlock();
+            job(i);
+            lk.lock();
+            if (++finished == tasks) done_cv.notify_all();
+          }
+        }
+      });
+  }
+  void run(int n_tasks, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> lk(m);
+    job = fn;
+    tasks = n_tasks;
+    next = 0;
+    finished = 0;
+    ++gen;
+    cv.notify_all();
+    while (next < tasks) {  // the caller takes tasks too
+      const int i = next++;
+      lk.unlock();
+      job(i);
+      lk.lock();
+      ++finished;
+    }
+    done_cv.wait(lk, [&] { return finished == tasks; });
+    job = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+  }
+};
+
+// fn(begin, end) over [0, n) in contiguous chunks of at least `grain` items
+// on the context's host pool (serial for small n).  Used for the per-problem
+// host work of large batches (packing, result expansion), independent per item.
 template <class Fn>
-void parallel_chunks(int n, int grain, Fn&& fn) {
-  const int hw = static_cast<int>(std::thread::hardware_concurrency());
-  const int threads = std::max(1, std::min({hw > 0 ? hw : 1, 8, n / std::max(1, grain)}));
-  if (threads <= 1) {
+void parallel_chunks(bs_ctx_t ctx, int n, int grain, Fn&& fn) {
+  const int chunks = std::min(kHostWorkers + 1, n / std::max(1, grain));
+  if (chunks <= 1 || !ctx) {
     fn(0, n);
     return;
   }
-  std::vector<std::thread> pool;
-  pool.reserve(threads - 1);
-  for (int t = 1; t < threads; ++t)
-    pool.emplace_back([&, t] { fn(static_cast<int>(static_cast<long long>(n) * t / threads),
-                                  static_cast<int>(static_cast<long long>(n) * (t + 1) / threads)); });
-  fn(0, static_cast<int>(static_cast<long long>(n) / threads));
-  for (auto& th : pool) th.join();
+  HostPool& pool = ctx->pool();
+  pool.run(chunks, [&](int c) {
+    fn(static_cast<int>(static_cast<long long>(n) * c / chunks),
+       static_cast<int>(static_cast<long long>(n) * (c + 1) / chunks));
+  });
 }
 
 }  // namespace bs

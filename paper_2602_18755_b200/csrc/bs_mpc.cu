@@ -520,7 +520,7 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
     return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
                      "batch; split it into smaller calls", *hOverflow);
   }
-  parallel_chunks(n, 1024, [&](int lo, int hi) {
+  parallel_chunks(ctx, n, 1024, [&](int lo, int hi) {
     for (int i = lo; i < hi; ++i)
       expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
                     run->target[i], &out[i], run->mode == kExhaustive);

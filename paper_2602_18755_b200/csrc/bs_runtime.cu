@@ -46,6 +46,14 @@ void* bs_ctx_s::host_buf(int slot, size_t bytes) {
   return b.p;
 }
 
+bs::HostPool& bs_ctx_s::pool() {
+  if (!host_pool) {
+    host_pool = std::make_unique<bs::HostPool>();
+    host_pool->start(bs::kHostWorkers);
+  }
+  return *host_pool;
+}
+
 bs_ctx_s::~bs_ctx_s() {
   for (auto& b : dev)
     if (b.p) cudaFree(b.p);
@@ -187,7 +195,7 @@ int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_po
     fgi[i] = static_cast<int>(it - out->fg_pairs.begin());
     if (it == out->fg_pairs.end()) out->fg_pairs.push_back(key);
   }
-  parallel_chunks(n, 1024, [&](int lo, int hi) {
+  parallel_chunks(ctx, n, 256, [&](int lo, int hi) {
     for (int i = lo; i < hi; ++i) {
       const bs_snapshot& s = problems[i].snap;
       DProblem& p = hp[i];
