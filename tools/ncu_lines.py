@@ -1,6 +1,10 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-usage: python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [LIB.so] [TOP]
+usage: python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX[@SASS_REGEX] [LIB.so] [TOP]
+
+SASS_REGEX selects the kernel's section in the library when several
+instantiations share the name (e.g. sweep_kernel@sweep_kernelILi3E for
+sweep_kernel<3>): offsets from another instantiation would mislabel lines.
 
 ncu's source page gives per-SASS-instruction samples with runtime
 addresses; nvdisasm -g on the library's cubin gives per-instruction source
@@ -67,10 +71,11 @@ def line_map(lib: str, kernel: str):
 
 def main():
     rep, kernel = sys.argv[1], sys.argv[2]
+    kernel, _, sass_kernel = kernel.partition("@")
     lib = sys.argv[3] if len(sys.argv) > 3 else "paper_2602_18755_b200/libbiscale_gpu.so"
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     samples = sass_samples(rep, kernel)
-    lines = line_map(lib, kernel)
+    lines = line_map(lib, sass_kernel or kernel)
     tot = sum(s for _, s, _ in samples) or 1.0
     agg = collections.Counter()
     for off, s, _ in samples:
