@@ -87,3 +87,24 @@ def test_gpu_decode_golden(gpu_device):
     for (m, cfg, batch, kv), rec in zip(decode_instances(d["seed"], d["count"]), d["records"]):
         g = P.select_decode_freq_ex(batch, kv, cfg, m, 1)
         assert [0, g.freq_mhz, g.eval_count, int(g.kv_override)] == rec
+
+
+def test_placement_golden_inputs_regenerate():
+    """The C3-shaped windows regenerate with the recorded request counts (the
+    host trace generator is bit-identical to gen_gamma_trace, workload.hpp)."""
+    from make_golden import placement_inputs
+    for t in GOLDEN["placement"]:
+        _, base, cands, _, _ = placement_inputs(t["seed"])
+        assert len(base.requests) == t["n_requests"] and len(cands) == len(t["rows"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("t", GOLDEN["placement"], ids=lambda t: f"seed{t['seed']}-probes{t['probe_count']}")
+def test_gpu_config_table_golden(gpu_device, t):
+    """build_config_table (placement.hpp:240-260) on the GPU probe grid equals
+    the reference's table entry for entry (r_c, E_c, G_c, saturated, error)."""
+    from make_golden import placement_inputs, table_row
+    m, base, cands, pol, slo = placement_inputs(t["seed"])
+    search = P.GoodputSearch(probe_count=t["probe_count"], tolerance_rps=t["tolerance_rps"])
+    got = P.build_config_table(cands, base, slo, m, pol, search)
+    assert [table_row(e) for e in got] == t["rows"]

@@ -80,7 +80,28 @@ def record(kind, r) -> dict:
     return d
 
 
+# Config tables (build_config_table, placement.hpp:240-260) of C3-shaped
+# 1-minute gamma(0.5) windows at 12 rps: TP {1,2,4,8} x 8 rungs x 2 phases.
+PLACEMENT_SEEDS = [7, 8, 11]
+PLACEMENT_WINDOW_MS = 60_000.0
+
+
+def placement_inputs(seed: int):
+    from paper_2602_18755_b200 import workloads as W
+    lad = W.ladder(8)
+    m = W.llama_models(lad)
+    base = P.gen_gamma_trace(12.0, 0.5, PLACEMENT_WINDOW_MS,
+                             P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), seed)
+    cands = P.enumerate_candidates(lad, [1, 2, 4, 8])
+    return m, base, cands, P.SchedulerPolicy(max_batch_tokens=2048), P.SLOSpec(600.0, 100.0)
+
+
+def table_row(e) -> list:
+    return [int(e.config.phase), e.config.tp, e.config.base_freq_mhz, e.r_c, e.e_c, e.g_c, bool(e.saturated), e.error]
+
+
 def main() -> None:
+    from test_gpu_placement import _ref_table
     ref = oracle.load_ref()
     sets = []
     for kind, gen, seed, count, kw in MPC_SETS:
@@ -98,10 +119,18 @@ def main() -> None:
     for m, cfg, batch, kv in decode_instances(DECODE_SEED, DECODE_COUNT):
         d = cpu_decode(ref, m, cfg, batch, kv, 1)
         dec.append([d.status, d.freq_mhz, d.eval_count, d.kv_override])
+    tables = []
+    for seed in PLACEMENT_SEEDS:
+        for search in (P.GoodputSearch(), P.GoodputSearch(probe_count=2, tolerance_rps=0.5)):
+            m, base, cands, pol, slo = placement_inputs(seed)
+            want = _ref_table(ref, m, base, slo, pol, search, cands)
+            tables.append({"seed": seed, "probe_count": search.probe_count, "tolerance_rps": search.tolerance_rps,
+                           "n_requests": len(base.requests), "rows": [table_row(e) for e in want]})
     OUT.parent.mkdir(parents=True, exist_ok=True)
     doc = {"generated_by": "tools/make_golden.py from oracle/_ref/libpdsim_ref.so (the unmodified reference)",
            "mpc_sets": sets, "c2": {"seed": C2_SEED, "count": C2_COUNT, "records": c2},
-           "decode": {"seed": DECODE_SEED, "count": DECODE_COUNT, "records": dec}}
+           "decode": {"seed": DECODE_SEED, "count": DECODE_COUNT, "records": dec},
+           "placement": tables}
     OUT.write_text(json.dumps(doc, indent=1) + "\n")
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes)")
 
