@@ -495,6 +495,11 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
 }
 
 // Copies results back (one or two D2H copies), syncs, expands.
+// Problems per host-pool chunk of the result expansion.
+#ifndef BS_RESULT_GRAIN
+#define BS_RESULT_GRAIN 256
+#endif
+
 int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   const int n = run->n;
   if (n == 0) return BS_OK;
@@ -520,7 +525,7 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
     return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
                      "batch; split it into smaller calls", *hOverflow);
   }
-  parallel_chunks(ctx, n, 1024, [&](int lo, int hi) {
+  parallel_chunks(ctx, n, BS_RESULT_GRAIN, [&](int lo, int hi) {
     for (int i = lo; i < hi; ++i)
       expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
                     run->target[i], &out[i], run->mode == kExhaustive);
