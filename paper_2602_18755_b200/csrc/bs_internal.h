@@ -23,7 +23,10 @@
 
 namespace bs {
 struct HostPool;
-constexpr int kHostWorkers = 3;  // host pool workers (plus the calling thread)
+#ifndef BS_HOST_WORKERS
+#define BS_HOST_WORKERS 3
+#endif
+constexpr int kHostWorkers = BS_HOST_WORKERS;  // host pool workers (plus the calling thread)
 }  // namespace bs
 
 struct bs_ctx_s {

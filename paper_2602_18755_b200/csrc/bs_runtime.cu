@@ -146,6 +146,11 @@ static_assert(sizeof(DWaiting) == sizeof(bs_waiting) && offsetof(DWaiting, id) =
                   offsetof(DWaiting, remaining) == offsetof(bs_waiting, remaining_len),
               "DWaiting mirrors bs_waiting");
 
+// Problems per host-pool chunk of the pack copies.
+#ifndef BS_PACK_GRAIN
+#define BS_PACK_GRAIN 256
+#endif
+
 int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
                   const bs_mpc_problem* problems, int n, PackedProblems* out) {
   out->fg_pairs.clear();
@@ -195,7 +200,7 @@ int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_po
     fgi[i] = static_cast<int>(it - out->fg_pairs.begin());
     if (it == out->fg_pairs.end()) out->fg_pairs.push_back(key);
   }
-  parallel_chunks(ctx, n, 256, [&](int lo, int hi) {
+  parallel_chunks(ctx, n, BS_PACK_GRAIN, [&](int lo, int hi) {
     for (int i = lo; i < hi; ++i) {
       const bs_snapshot& s = problems[i].snap;
       DProblem& p = hp[i];
