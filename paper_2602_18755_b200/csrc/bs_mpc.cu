@@ -110,7 +110,8 @@ __host__ __device__ inline size_t greedy_warp_bytes(int max_h, int max_nc) {
 __global__ void __launch_bounds__(kGreedyWarps * 32) greedy_kernel(DModels m, const DMpcCfg* cfgs,
                                                                   const DProblem* probs, const DWaiting* W,
                                                                   const DRunning* R, DMpcOut* out, DLevel* levels,
-                                                                  int n, int max_h, int max_nc, const DFastPair* fg) {
+                                                                  int n, int max_h, int max_nc, const DFastPair* fg,
+                                                                  int lv_stride) {
   extern __shared__ __align__(16) unsigned char gdsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int d = blockIdx.x * kGreedyWarps + wib;
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) greedy_kernel(DModels m, co
   if (lane == 0) wtables_bind(S.T, tab, c.horizon, c.nc);
   __syncwarp();
   const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
-  greedy_warp(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o, levels + static_cast<size_t>(d) * BS_MAX_LEVELS,
+  greedy_warp(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o, levels + static_cast<size_t>(d) * lv_stride,
               fp ? fp->lat : nullptr, fp ? fp->pw : nullptr, fp && fp->share);
   if (lane == 0) out[d] = *o;
 }
@@ -239,6 +240,7 @@ struct MpcRun {
   std::vector<int> cfg_of;          // per-problem configuration index
   std::vector<double> target;       // per-problem target_freq (controller fallback)
   int max_nc = 1;                   // largest candidate count in the batch
+  int lv_stride = BS_MAX_LEVELS;    // greedy level records per problem: max(1, max_nc - 2) (dvfs.hpp:205)
   int bfs_levels = 0;               // deepest final-node depth over the batch
   unsigned long long cap_level = 0;  // BFS list capacity (per ping-pong buffer)
   unsigned long long cap_final = 0;  // final list capacity
@@ -263,7 +265,7 @@ size_t up256(size_t x) { return (x + 255) / 256 * 256; }
 size_t tables_bytes(int n) { return sizeof(DTables) * static_cast<size_t>(n); }
 size_t best_bytes(int n) { return (sizeof(Key128) + 8ull) * static_cast<size_t>(n); }
 size_t out_bytes(int n) { return sizeof(DMpcOut) * static_cast<size_t>(n); }
-size_t levels_bytes(int n) { return sizeof(DLevel) * BS_MAX_LEVELS * static_cast<size_t>(n); }
+size_t levels_bytes(int n, int stride) { return sizeof(DLevel) * static_cast<size_t>(stride) * static_cast<size_t>(n); }
 
 // Device scratch layout of an exhaustive run (offsets from one base).
 struct ExLayout {
@@ -334,6 +336,7 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
   }
   run->max_nc = 1;
   for (const DMpcCfg& c : run->hc) run->max_nc = std::max(run->max_nc, c.nc);
+  run->lv_stride = std::min(BS_MAX_LEVELS, std::max(1, run->max_nc - 2));
   run->cfg_of.resize(n);
   run->target.resize(n);
   run->cap_level = 0;
@@ -440,7 +443,7 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
                                           static_cast<int>(smem)));
     greedy_kernel<<<(n + kGreedyWarps - 1) / kGreedyWarps, kGreedyWarps * 32, smem, ctx->stream>>>(
         models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running, run->dOut, run->dLv, n, pk.max_horizon,
-        pk.max_nc, run->dFG);
+        pk.max_nc, run->dFG, run->lv_stride);
     BS_LAUNCH_CHECK(ctx);
     BS_REC(1);
     return BS_OK;
@@ -511,10 +514,11 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut, run->dOut, out_bytes(n), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->last_d2h = out_bytes(n);
   if (run->mode == kGreedy) {
-    hLv = static_cast<DLevel*>(ctx->host_buf(kSlotLevels, levels_bytes(n)));
+    hLv = static_cast<DLevel*>(ctx->host_buf(kSlotLevels, levels_bytes(n, run->lv_stride)));
     if (!hLv) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
-    BS_CUDA_TRY(ctx, cudaMemcpyAsync(hLv, run->dLv, levels_bytes(n), cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->last_d2h += levels_bytes(n);
+    BS_CUDA_TRY(ctx, cudaMemcpyAsync(hLv, run->dLv, levels_bytes(n, run->lv_stride), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    ctx->last_d2h += levels_bytes(n, run->lv_stride);
   } else {
     BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOverflow, &run->dCtl->overflow, 8, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->last_d2h += 8;
@@ -527,7 +531,7 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   }
   parallel_chunks(ctx, n, BS_RESULT_GRAIN, [&](int lo, int hi) {
     for (int i = lo; i < hi; ++i)
-      expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * BS_MAX_LEVELS : nullptr, run->hc[run->cfg_of[i]],
+      expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * run->lv_stride : nullptr, run->hc[run->cfg_of[i]],
                     run->target[i], &out[i], run->mode == kExhaustive);
   });
   return report_status(ctx, out, n);
@@ -565,7 +569,7 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
       bind_exhaustive(&run, base, L);
     } else {
       run.dOut = static_cast<DMpcOut*>(ctx->dev_buf(kSlotOut, out_bytes(n)));
-      run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n)));
+      run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n, run.lv_stride)));
       if (!run.dOut || !run.dLv) return set_error(ctx, BS_CUDA_ERROR, "mpc greedy: allocation failed");
     }
     const double t2 = dbg_t ? now_us() : 0.0;
@@ -686,7 +690,7 @@ int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cf
     total = L.total;
   } else {
     o_l = total;
-    total += up256(levels_bytes(n));
+    total += up256(levels_bytes(n, run.lv_stride));
     o_o = total;
     total += up256(out_bytes(n));
   }
