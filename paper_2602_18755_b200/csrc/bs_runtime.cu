@@ -150,6 +150,13 @@ static_assert(sizeof(DWaiting) == sizeof(bs_waiting) && offsetof(DWaiting, id) =
 #ifndef BS_PACK_GRAIN
 #define BS_PACK_GRAIN 256
 #endif
+// Problems per pipelined pack slice (H2D of a slice overlaps the next slice's packing).
+#ifndef BS_PACK_SLICE
+#define BS_PACK_SLICE 1024
+#endif
+#ifndef BS_PACK_SLICES_MAX
+#define BS_PACK_SLICES_MAX 4
+#endif
 
 int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
                   const bs_mpc_problem* problems, int n, PackedProblems* out) {
@@ -200,35 +207,55 @@ int pack_problems(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_po
     fgi[i] = static_cast<int>(it - out->fg_pairs.begin());
     if (it == out->fg_pairs.end()) out->fg_pairs.push_back(key);
   }
-  parallel_chunks(ctx, n, BS_PACK_GRAIN, [&](int lo, int hi) {
-    for (int i = lo; i < hi; ++i) {
-      const bs_snapshot& s = problems[i].snap;
-      DProblem& p = hp[i];
-      p.now = s.now_ms;
-      p.cur_freq = s.current_freq_mhz;
-      p.target_freq = s.target_freq_mhz;
-      p.run_wr = s.running_work_remaining;
-      p.run_n = s.running_features.n_requests;
-      p.run_sum = s.running_features.sum_len;
-      p.tp = s.tp;
-      p.run_active = s.running_active ? 1 : 0;
-      p.n_wait = s.n_waiting;
-      p.n_run = s.running_active ? s.n_running : 0;
-      p.cfg = problems[i].cfg_index;
-      p.fgi = fgi[i];
-      p.wait_off = static_cast<long long>(woff[i]);
-      p.run_off = static_cast<long long>(roff[i]);
-      // bs_waiting and DWaiting share one layout (static_asserts above): one copy per snapshot
-      if (s.n_waiting > 0) std::memcpy(hw + woff[i], s.waiting, sizeof(DWaiting) * static_cast<size_t>(s.n_waiting));
-      if (s.running_active) {
-        for (int j = 0; j < s.n_running; ++j) {
-          hr[roff[i] + j].arrival = s.running_arrivals_ms[j];
-          hr[roff[i] + j].completes = s.running_completes[j] ? 1 : 0;
+  // Large batches are packed in slices of problems; each slice's ranges of
+  // the problem / waiting / running regions are copied as soon as the slice
+  // is packed, so the H2D transfer overlaps the packing of the next slice.
+  const int n_slices = std::max(1, std::min(BS_PACK_SLICES_MAX, n / BS_PACK_SLICE));
+  for (int sl = 0; sl < n_slices; ++sl) {
+    const int s_lo = static_cast<int>(static_cast<long long>(n) * sl / n_slices);
+    const int s_hi = static_cast<int>(static_cast<long long>(n) * (sl + 1) / n_slices);
+    parallel_chunks(ctx, s_hi - s_lo, BS_PACK_GRAIN, [&](int lo, int hi) {
+      for (int i = s_lo + lo; i < s_lo + hi; ++i) {
+        const bs_snapshot& s = problems[i].snap;
+        DProblem& p = hp[i];
+        p.now = s.now_ms;
+        p.cur_freq = s.current_freq_mhz;
+        p.target_freq = s.target_freq_mhz;
+        p.run_wr = s.running_work_remaining;
+        p.run_n = s.running_features.n_requests;
+        p.run_sum = s.running_features.sum_len;
+        p.tp = s.tp;
+        p.run_active = s.running_active ? 1 : 0;
+        p.n_wait = s.n_waiting;
+        p.n_run = s.running_active ? s.n_running : 0;
+        p.cfg = problems[i].cfg_index;
+        p.fgi = fgi[i];
+        p.wait_off = static_cast<long long>(woff[i]);
+        p.run_off = static_cast<long long>(roff[i]);
+        // bs_waiting and DWaiting share one layout (static_asserts above): one copy per snapshot
+        if (s.n_waiting > 0) std::memcpy(hw + woff[i], s.waiting, sizeof(DWaiting) * static_cast<size_t>(s.n_waiting));
+        if (s.running_active) {
+          for (int j = 0; j < s.n_running; ++j) {
+            hr[roff[i] + j].arrival = s.running_arrivals_ms[j];
+            hr[roff[i] + j].completes = s.running_completes[j] ? 1 : 0;
+          }
         }
       }
+    });
+    if (n_slices == 1) {
+      BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, ctx->stream));
+      break;
     }
-  });
-  BS_CUDA_TRY(ctx, cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, ctx->stream));
+    auto h2d = [&](size_t off, size_t bytes) -> int {
+      if (bytes) BS_CUDA_TRY(ctx, cudaMemcpyAsync(d + off, h + off, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      return BS_OK;
+    };
+    if (sl == 0 && h2d(o_cfg, o_prob - o_cfg)) return BS_CUDA_ERROR;
+    if (h2d(o_prob + sizeof(DProblem) * s_lo, sizeof(DProblem) * (s_hi - s_lo)) ||
+        h2d(o_wait + sizeof(DWaiting) * woff[s_lo], sizeof(DWaiting) * (woff[s_hi] - woff[s_lo])) ||
+        h2d(o_run + sizeof(DRunning) * roff[s_lo], sizeof(DRunning) * (roff[s_hi] - roff[s_lo])))
+      return BS_CUDA_ERROR;
+  }
   out->off_cfg = o_cfg;
   out->off_prob = o_prob;
   out->off_wait = o_wait;
