@@ -150,9 +150,9 @@ static_assert(sizeof(DWaiting) == sizeof(bs_waiting) && offsetof(DWaiting, id) =
 #ifndef BS_PACK_GRAIN
 #define BS_PACK_GRAIN 256
 #endif
-// Problems per pipelined pack slice (H2D of a slice overlaps the next slice's packing).
+// Minimum problems per pipelined pack slice (H2D of a slice overlaps the next slice's packing).
 #ifndef BS_PACK_SLICE
-#define BS_PACK_SLICE 1024
+#define BS_PACK_SLICE 256
 #endif
 #ifndef BS_PACK_SLICES_MAX
 #define BS_PACK_SLICES_MAX 4

@@ -1,4 +1,4 @@
-# A/B of the pipelined pack (4 slices of >= 1024 problems) vs libbiscale_gpu_s1.so (one slice).
+# A/B of the pipelined pack (up to 4 slices of >= 256 problems) vs libbiscale_gpu_s1.so (one slice).
 V=$PWD/paper_2602_18755_b200/libbiscale_gpu_s1.so
 timeout 600 python -m pytest tests/test_gpu_mpc.py tests/test_golden.py tests/test_gpu_experiment.py tests/test_gpu_cluster_replay.py -m gpu -q > gpurun_out/ab_slices_pytest.log 2>&1; echo pytest=$?
 for i in 1 2 3; do
