@@ -497,11 +497,27 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   return BS_OK;
 }
 
-// Copies results back (one or two D2H copies), syncs, expands.
-// Problems per host-pool chunk of the result expansion.
+// Copies results back, syncs, expands.  Batches of >= 512 problems are
+// copied in up to 4 slices, each followed by an event, so the expansion of a
+// slice overlaps the D2H copy of the next.
+// Problems per host-pool chunk of the result expansion; minimum problems per slice.
 #ifndef BS_RESULT_GRAIN
 #define BS_RESULT_GRAIN 256
 #endif
+#ifndef BS_RESULT_SLICE
+#define BS_RESULT_SLICE 256
+#endif
+#ifndef BS_RESULT_SLICES_MAX
+#define BS_RESULT_SLICES_MAX 4
+#endif
+
+struct SliceEvents {
+  cudaEvent_t ev[BS_RESULT_SLICES_MAX > 0 ? BS_RESULT_SLICES_MAX : 1] = {};
+  int made = 0;
+  ~SliceEvents() {
+    for (int i = 0; i < made; ++i) cudaEventDestroy(ev[i]);
+  }
+};
 
 int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   const int n = run->n;
@@ -511,29 +527,48 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   if (!hOut) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
   unsigned long long* hOverflow = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(hOut) + out_bytes(n));
   *hOverflow = 0;
-  BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut, run->dOut, out_bytes(n), cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->last_d2h = out_bytes(n);
+  const int stride = run->lv_stride;
   if (run->mode == kGreedy) {
-    hLv = static_cast<DLevel*>(ctx->host_buf(kSlotLevels, levels_bytes(n, run->lv_stride)));
+    hLv = static_cast<DLevel*>(ctx->host_buf(kSlotLevels, levels_bytes(n, stride)));
     if (!hLv) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
-    BS_CUDA_TRY(ctx, cudaMemcpyAsync(hLv, run->dLv, levels_bytes(n, run->lv_stride), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-    ctx->last_d2h += levels_bytes(n, run->lv_stride);
-  } else {
+  } else {  // the overflow flag first: it is checked before any slice is expanded
     BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOverflow, &run->dCtl->overflow, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->last_d2h += 8;
   }
-  BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  if (*hOverflow) {
-    BS_CUDA_TRY(ctx, cudaMemcpy(&run->ctl_host, run->dCtl, sizeof(ExCtl), cudaMemcpyDeviceToHost));
-    return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
-                     "batch; split it into smaller calls", *hOverflow);
+  const int n_slices = std::max(1, std::min(BS_RESULT_SLICES_MAX, n / BS_RESULT_SLICE));
+  auto slice_lo = [&](int sl) { return static_cast<int>(static_cast<long long>(n) * sl / n_slices); };
+  SliceEvents se;
+  for (int sl = 0; sl < n_slices; ++sl) {
+    const int lo = slice_lo(sl), hi = slice_lo(sl + 1);
+    BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut + lo, run->dOut + lo, out_bytes(hi - lo), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    if (hLv)
+      BS_CUDA_TRY(ctx, cudaMemcpyAsync(hLv + static_cast<size_t>(lo) * stride, run->dLv + static_cast<size_t>(lo) * stride,
+                                       levels_bytes(hi - lo, stride), cudaMemcpyDeviceToHost, ctx->stream));
+    if (n_slices > 1) {
+      BS_CUDA_TRY(ctx, cudaEventCreateWithFlags(&se.ev[sl], cudaEventDisableTiming));
+      se.made = sl + 1;
+      BS_CUDA_TRY(ctx, cudaEventRecord(se.ev[sl], ctx->stream));
+    }
   }
-  parallel_chunks(ctx, n, BS_RESULT_GRAIN, [&](int lo, int hi) {
-    for (int i = lo; i < hi; ++i)
-      expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * run->lv_stride : nullptr, run->hc[run->cfg_of[i]],
-                    run->target[i], &out[i], run->mode == kExhaustive);
-  });
+  ctx->last_d2h = out_bytes(n) + (hLv ? levels_bytes(n, stride) : 8);
+  for (int sl = 0; sl < n_slices; ++sl) {
+    if (n_slices > 1)
+      BS_CUDA_TRY(ctx, cudaEventSynchronize(se.ev[sl]));
+    else
+      BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (sl == 0 && *hOverflow) {
+      BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      BS_CUDA_TRY(ctx, cudaMemcpy(&run->ctl_host, run->dCtl, sizeof(ExCtl), cudaMemcpyDeviceToHost));
+      return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
+                       "batch; split it into smaller calls", *hOverflow);
+    }
+    const int s_lo = slice_lo(sl), s_hi = slice_lo(sl + 1);
+    parallel_chunks(ctx, s_hi - s_lo, BS_RESULT_GRAIN, [&](int lo, int hi) {
+      for (int i = s_lo + lo; i < s_lo + hi; ++i)
+        expand_result(hOut[i], hLv ? hLv + static_cast<size_t>(i) * stride : nullptr, run->hc[run->cfg_of[i]],
+                      run->target[i], &out[i], run->mode == kExhaustive);
+    });
+  }
   return report_status(ctx, out, n);
 }
 
