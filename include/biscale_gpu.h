@@ -325,6 +325,14 @@ void bs_ctx_destroy(bs_ctx_t ctx);
 const char* bs_last_error(bs_ctx_t ctx);
 /* Device the context runs on and its SM count (for host-side grid sizing). */
 int bs_ctx_info(bs_ctx_t ctx, int* device, int* sm_count);
+/* Exhaustive-MPC limits of the context (tuning and test hook; 0 restores a
+ * default): the number of prefixes at depth K - 2 above which the sweep walks
+ * three bottom levels instead of two (default 2^24), and the frontier
+ * capacities in entries -- per BFS ping-pong list (default 2.5e8, 40 B each)
+ * and for the final list (default 2e9, 12 B each).  A batch whose frontiers
+ * exceed them is split into smaller launches; one decision that exceeds them
+ * fails with BS_PARAMETER_ERROR.  Results never depend on these settings. */
+int bs_ctx_set_exhaustive_limits(bs_ctx_t ctx, double sweep3_min_prefixes, uint64_t level_cap, uint64_t final_cap);
 /* Synchronise the context's stream. */
 int bs_ctx_sync(bs_ctx_t ctx);
 /* Number of kernels the context launched since creation (instrumentation). */
@@ -383,6 +391,27 @@ int bs_mpc_greedy(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
 int bs_mpc_exhaustive(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
                       const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems,
                       int n, bs_mpc_result* out);
+
+/* One slice of every decision's code space, for splitting a single large
+ * decision across GPUs: the assignments whose first `digits`
+ * digits (batch 0 most significant, base |cand|) form a number in [lo, hi);
+ * digits is 0 (whole tree), 1 or 2, hi <= |cand|^digits.  A projection
+ * shorter than `digits` reads its missing digits as 0, so the slices of any
+ * partition of [0, |cand|^digits) partition every decision.  Per slice the
+ * result holds the slice's feasible count, its (objective, code) minimum
+ * (feasible = 0 and the all-max fallback when it has no feasible
+ * assignment) and trajectories = eval_count = the slice's size; the
+ * decision is the minimum over slices (sharding.argmin_over_ranks) and the
+ * feasible counts add up. */
+typedef struct bs_slice {
+  int32_t digits;
+  int32_t _pad;
+  uint64_t lo;
+  uint64_t hi;
+} bs_slice;
+int bs_mpc_exhaustive_slice(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
+                            const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems,
+                            int n, const bs_slice* slice, bs_mpc_result* out);
 
 /* Resident batches (the throughput path): upload a batch of problems once
  * (one H2D copy), then enqueue its kernels any number of times on the

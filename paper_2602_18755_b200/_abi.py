@@ -120,6 +120,10 @@ class bs_level_stats(C.Structure):
     ]
 
 
+class bs_slice(C.Structure):
+    _fields_ = [("digits", C.c_int32), ("_pad", C.c_int32), ("lo", C.c_uint64), ("hi", C.c_uint64)]
+
+
 class bs_mpc_result(C.Structure):
     _fields_ = [
         ("status", C.c_int32),
@@ -330,6 +334,7 @@ PROTOTYPES = [
     ("bs_ctx_destroy", None, [ctx_t]),
     ("bs_last_error", C.c_char_p, [ctx_t]),
     ("bs_ctx_info", C.c_int, [ctx_t, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("bs_ctx_set_exhaustive_limits", C.c_int, [ctx_t, C.c_double, C.c_uint64, C.c_uint64]),
     ("bs_ctx_sync", C.c_int, [ctx_t]),
     ("bs_ctx_kernel_launches", C.c_int64, [ctx_t]),
     ("bs_ctx_stats", C.c_int, [ctx_t, C.POINTER(C.c_double), C.c_int]),
@@ -348,6 +353,9 @@ PROTOTYPES = [
                                 C.POINTER(bs_mpc_problem), C.c_int, C.POINTER(bs_mpc_result)]),
     ("bs_mpc_exhaustive", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy),
                                     C.c_int, C.POINTER(bs_mpc_problem), C.c_int, C.POINTER(bs_mpc_result)]),
+    ("bs_mpc_exhaustive_slice", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config),
+                                          C.POINTER(bs_scheduler_policy), C.c_int, C.POINTER(bs_mpc_problem),
+                                          C.c_int, C.POINTER(bs_slice), C.POINTER(bs_mpc_result)]),
     ("bs_mpc_plan_create", C.c_int, [ctx_t, models_t, C.POINTER(bs_mpc_config), C.POINTER(bs_scheduler_policy),
                                      C.c_int, C.POINTER(bs_mpc_problem), C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     ("bs_mpc_plan_run", C.c_int, [ctx_t, C.c_void_p, C.c_int]),

@@ -20,7 +20,7 @@
 // every level is spread over the whole GPU however uneven the decisions are.
 
 #ifndef BS_SWEEP3_MIN
-#define BS_SWEEP3_MIN 16777216.0  // prefixes at depth K - 2 above which the sweep takes 3 levels
+#define BS_SWEEP3_MIN 16777216.0  // default: prefixes at depth K - 2 above which the sweep takes 3 levels
 #endif
 
 struct ExCtl {
@@ -32,14 +32,60 @@ struct ExCtl {
 #endif
 };
 
-// Bottom levels swept per final node: 2, or 3 for trees wider than 2^24
-// prefixes at depth K - 2 (measured at C5, 24^8: the deeper final list of
-// I = 2 costs more traffic and frontier work than the longer sweep saves).
-__host__ __device__ inline int sweep_levels(int K, int nc) {
+// Bottom levels swept per final node: 2, or 3 for trees wider than
+// `sweep3_min` prefixes at depth K - 2 (default 2^24, measured at C5, 24^8:
+// the deeper final list of I = 2 costs more traffic and frontier work than
+// the longer sweep saves).  The threshold is a context setting
+// (bs_ctx_set_exhaustive_limits) so the tests can drive small trees through
+// the three-level sweep.
+__host__ __device__ inline int sweep_levels(int K, int nc, double sweep3_min) {
   if (K <= 2) return K;
   double np = 1.0;
   for (int i = 0; i < K - 2; ++i) np *= nc;
-  return np > BS_SWEEP3_MIN ? 3 : 2;
+  return np > sweep3_min ? 3 : 2;
+}
+
+// A slice of one decision's code space (bs_slice): the assignments whose
+// first `digits` digits (batch 0 most significant), read as a base-nc
+// number, lie in [lo, hi).  digits == 0: the whole tree.  A projection
+// shorter than `digits` reads its missing digits as 0, so the slices of a
+// partition of [0, nc^digits) partition every tree.
+struct DSlice {
+  int digits;
+  int _pad;
+  unsigned long long lo, hi;
+};
+
+// Leading-digit value of a prefix of `depth` digits (depth >= digits), or of
+// a complete assignment of K < digits digits (missing digits 0).
+__host__ __device__ inline unsigned long long slice_key(unsigned long long code, int depth, int digits, int nc) {
+  unsigned long long v = code;
+  if (depth >= digits) {
+    for (int i = digits; i < depth; ++i) v /= static_cast<unsigned long long>(nc);
+  } else {
+    for (int i = depth; i < digits; ++i) v *= static_cast<unsigned long long>(nc);
+  }
+  return v;
+}
+
+__host__ __device__ inline bool in_slice(const DSlice& s, unsigned long long code, int depth, int nc) {
+  if (s.digits == 0) return true;
+  const unsigned long long v = slice_key(code, depth, s.digits, nc);
+  return v >= s.lo && v < s.hi;
+}
+
+// Number of K-digit assignments in the slice.
+__host__ __device__ inline unsigned long long slice_size(const DSlice& s, int K, int nc) {
+  unsigned long long total = 1;
+  for (int i = 0; i < K; ++i) total *= static_cast<unsigned long long>(nc);
+  if (s.digits == 0) return total;
+  unsigned long long lead = 1;
+  for (int i = 0; i < s.digits; ++i) lead *= static_cast<unsigned long long>(nc);
+  const unsigned long long lo = s.lo < lead ? s.lo : lead, hi = s.hi < lead ? s.hi : lead;
+  if (hi <= lo) return 0;
+  if (K >= s.digits) return (hi - lo) * (total / lead);
+  const unsigned long long m = lead / total;  // codes c with c * m in [lo, hi)
+  return (hi + m - 1) / m - (lo + m - 1) / m;
 }
 
 // Frontier lists in HBM, structure of arrays.
@@ -399,6 +445,72 @@ __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict
   }
 }
 
+// Every leaf of a sliced tree whose leading digits lie below prepare's
+// first list (K <= 3, or a final depth < digits): one CTA evaluates the
+// slice's assignments in code order with meets_slo's early exit, counts the
+// feasible ones and merges the (objective, code) minimum -- the same op
+// sequence as the sweep (child_state chain, then den > 0 ? num / den : 0).
+__device__ __noinline__ void small_tree_slice(const DTables* __restrict__ T, int d, int K, int nc, DSlice sl,
+                                              Key128* best, unsigned long long* feas) {
+  __shared__ unsigned long long s_o[32], s_c[32], s_n[32];
+  const unsigned long long total = ipow(static_cast<unsigned long long>(nc), K);
+  unsigned long long ko = ~0ull, kc = ~0ull, cnt = 0;
+  for (unsigned long long code = threadIdx.x; code < total; code += blockDim.x) {
+    if (!in_slice(sl, code, K, nc)) continue;
+    double t = 0.0, num = 0.0, den = 0.0;
+    int last = -1;
+    bool ok = true;
+    unsigned long long div = total / static_cast<unsigned long long>(nc);
+    for (int k = 0; k < K && ok; ++k) {
+      const int f = static_cast<int>((code / div) % static_cast<unsigned long long>(nc));
+      div /= static_cast<unsigned long long>(nc);
+      double ct, cn, cd;
+      ok = child_state(T, k, t, num, den, last, f, ct, cn, cd);
+      t = ct;
+      num = cn;
+      den = cd;
+      last = f;
+    }
+    if (!ok) continue;
+    ++cnt;
+    const double obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;  // dvfs.hpp:170
+    const unsigned long long o = static_cast<unsigned long long>(__double_as_longlong(obj));
+    if (key_less(o, code, ko, kc)) {
+      ko = o;
+      kc = code;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const unsigned long long oo = __shfl_xor_sync(0xffffffffu, ko, o), oc = __shfl_xor_sync(0xffffffffu, kc, o);
+    if (key_less(oo, oc, ko, kc)) {
+      ko = oo;
+      kc = oc;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_o[threadIdx.x >> 5] = ko;
+    s_c[threadIdx.x >> 5] = kc;
+    s_n[threadIdx.x >> 5] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      cnt += s_n[w];
+      if (key_less(s_o[w], s_c[w], ko, kc)) {
+        ko = s_o[w];
+        kc = s_c[w];
+      }
+    }
+    feas[d] = cnt;
+    if (ko != ~0ull) {
+      best[d].obj = ko;
+      best[d].code = kc;
+    }
+  }
+}
+
 #ifndef BS_SEED_ROUNDS
 #define BS_SEED_ROUNDS 3  // single-move improvement rounds of the argmin seed (1: C2 sweep 0.239 ms; 3: 0.219; 6: 0.221)
 #endif
@@ -418,7 +530,8 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
                                                                ExCtl* ctl, int n, const DFastPair* fg, Key128* best,
                                                                unsigned long long* feas, Frontier L2, Frontier L3,
                                                                FinalList fin, unsigned long long cap_level,
-                                                               unsigned long long cap_final) {
+                                                               unsigned long long cap_final, double sweep3_min,
+                                                               DSlice sl) {
   __shared__ int s_status;
   const int d = blockIdx.x;
   if (d >= n) return;
@@ -444,10 +557,17 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   __syncthreads();
   const int K = T->K, nc = T->nc;
   if (s_status != BS_OK || K == 0) return;
-  const int FD = K - sweep_levels(K, nc);
+  const int FD = K - sweep_levels(K, nc, sweep3_min);
   if (threadIdx.x == 0) {
     T->FD = FD;
     T->nc_magic = nc > 1 ? 0xffffffffu / static_cast<unsigned>(nc) + 1u : 0u;
+  }
+  // A slice whose leading digits lie below the first list this kernel
+  // writes (trees of at most 3 levels, or shallow final depths): every leaf
+  // of the slice evaluated here, in the sweep's op sequence.
+  if (sl.digits > (FD < 2 ? FD : 2)) {
+    small_tree_slice(T, d, K, nc, sl, best, feas);
+    return;
   }
   // Seed the argmin with a good feasible assignment: the best uniform one
   // (every batch at one rung), then rounds of single-position moves (every
@@ -459,13 +579,21 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   {
     __shared__ unsigned long long s_ko[kPrepThreads / 32], s_kc[kPrepThreads / 32];
     __shared__ unsigned char s_cur[kMaxK];
+    // the slice's leading digits (seeds must be keys of the slice)
+    const int sd = sl.digits < K ? sl.digits : K;
+    auto lead_digit = [&](int k) {
+      unsigned long long v = sl.lo;
+      for (int i = k + 1; i < sl.digits; ++i) v /= static_cast<unsigned long long>(nc);
+      return static_cast<int>(v % static_cast<unsigned long long>(nc));
+    };
     auto eval = [&](int kk, int ff, unsigned long long& ko, unsigned long long& kc) {
-      // assignment s_cur with position kk set to ff (kk < 0: all positions ff)
+      // assignment s_cur with position kk set to ff (kk < 0: the slice's
+      // leading digits, then every position ff)
       double t = 0.0, num = 0.0, den = 0.0;
       int last = -1;
       unsigned long long code = 0;
       for (int k = 0; k < K; ++k) {
-        const int f = kk < 0 ? ff : (k == kk ? ff : s_cur[k]);
+        const int f = kk < 0 ? (k < sd ? lead_digit(k) : ff) : (k == kk ? ff : s_cur[k]);
         double ct, cn, cd;
         if (!child_state(T, k, t, num, den, last, f, ct, cn, cd)) return;
         t = ct;
@@ -474,6 +602,7 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
         last = f;
         code = code * static_cast<unsigned long long>(nc) + static_cast<unsigned long long>(f);
       }
+      if (!in_slice(sl, code, K, nc)) return;
       const double obj = den > 0.0 ? __ddiv_rn(num, den) : 0.0;  // dvfs.hpp:170
       ko = static_cast<unsigned long long>(__double_as_longlong(obj));
       kc = code;
@@ -564,6 +693,7 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
         den = d1;
         last = f1;
       }
+      if (ok && sl.digits) ok = in_slice(sl, static_cast<unsigned long long>(e), D0, nc);  // sl.digits <= D0 here
       // a final node none of whose children passes has no feasible leaf (as in bfs_node_kernel)
       if (ok && to_final && T->sorted_ok && FD < K) ok = feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
     }

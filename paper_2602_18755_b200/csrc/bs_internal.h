@@ -40,6 +40,12 @@ struct bs_ctx_s {
   double stats[16] = {};  // phase timings / counters of the last entry point
   int n_stats = 0;
   int grid_cache[8] = {};  // occupancy-sized persistent grids, computed once per context (bs_mpc.cu)
+  // exhaustive-MPC limits (bs_ctx_set_exhaustive_limits): the sweep-depth
+  // threshold and the frontier capacities (12 B per final entry: 24 GB; 40 B
+  // per level entry, two ping-pong lists: 20 GB)
+  double ex_sweep3_min = 16777216.0;
+  unsigned long long ex_level_cap = 250000000ull;
+  unsigned long long ex_final_cap = 2000000000ull;
   std::unique_ptr<bs::HostPool> host_pool;  // started on first use (parallel_chunks)
   bs::HostPool& pool();
 

@@ -48,7 +48,7 @@ constexpr double kFilterMinDen = 0x1p-900;
 #include "bs_exhaustive.cuh"
 
 __global__ void finalize_kernel(const DTables* __restrict__ tables, const DMpcCfg* cfgs, const DProblem* probs,
-                                const Key128* best, const unsigned long long* feas, DMpcOut* out, int n) {
+                                const Key128* best, const unsigned long long* feas, DMpcOut* out, int n, DSlice sl) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the sweep's results (programmatic dependent launch)
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= n) return;
@@ -60,7 +60,7 @@ __global__ void finalize_kernel(const DTables* __restrict__ tables, const DMpcCf
   if (o.status == BS_OK && T->K > 0) {
     const int K = T->K, nc = T->nc;
     o.feasible_count = feas[d];
-    o.eval_count = static_cast<long long>(ipow(static_cast<unsigned long long>(nc), K));
+    o.eval_count = static_cast<long long>(slice_size(sl, K, nc));  // nc^K unsliced
     if (best[d].obj != ~0ull) {
       o.feasible = 1;
       o.objective = __longlong_as_double(static_cast<long long>(best[d].obj));
@@ -254,6 +254,8 @@ struct MpcRun {
   DLevel* dLv = nullptr;
   int bfs_grid = 0, sweep_grid2 = 0, sweep_grid3 = 0;
   bool sweep3 = false;  // some decision may sweep three levels (sweep_levels)
+  double sweep3_min = BS_SWEEP3_MIN;  // the context's threshold (bs_ctx_set_exhaustive_limits)
+  DSlice slice{};                     // the code-space slice of every decision (digits 0: whole trees)
   ExCtl ctl_host{};  // counters of an overflowed run (exact totals of the levels before the first overflow)
   const DFastPair* dFG = nullptr;       // reduced grids per (configuration, tp) pair (pk.fg_pairs)
   std::vector<DFastPair> hFG;           // their host build
@@ -311,14 +313,14 @@ constexpr size_t kMaxExhaustiveScratch = 48ull << 30;
 // Frontier capacities: the worst case (every prefix feasible), clamped to a
 // scratch budget; a run whose appends overflow is re-run with capacities
 // from the observed counts, or split (one_shot).
-constexpr unsigned long long kFinalCapMax = 2000000000ull;  // 12 B each: 24 GB
-constexpr unsigned long long kLevelCapMax = 250000000ull;   // 40 B each, two ping-pong lists: 20 GB
+// (defaults of the context's limits, bs_ctx_s::ex_final_cap / ex_level_cap)
 
 int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies, int n_cfgs,
              const bs_mpc_problem* problems, int n, int mode, MpcRun* run, unsigned long long cap_level_hint = 0,
              unsigned long long cap_final_hint = 0) {
   run->mode = mode;
   run->n = n;
+  run->sweep3_min = ctx->ex_sweep3_min;
   if (n > (1 << 24)) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: at most 2^24 problems per call");
   int rc = pack_problems(ctx, cfgs, policies, n_cfgs, problems, n, &run->pk);
   if (rc) return rc;
@@ -348,17 +350,19 @@ int run_pack(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_scheduler_policy*
     run->target[i] = problems[i].snap.target_freq_mhz;
     if (mode != kExhaustive) continue;
     const DMpcCfg& c = run->hc[problems[i].cfg_index];
-    const int FD = c.horizon - sweep_levels(c.horizon, c.nc);
+    const int FD = c.horizon - sweep_levels(c.horizon, c.nc, ctx->ex_sweep3_min);
     run->bfs_levels = std::max(run->bfs_levels, FD);
-    if (sweep_levels(c.horizon, c.nc) == 3) run->sweep3 = true;
+    // a shorter projection (K < horizon) may take three levels where the horizon takes two
+    for (int K = 3; K <= c.horizon; ++K)
+      if (sweep_levels(K, c.nc, ctx->ex_sweep3_min) == 3) run->sweep3 = true;
     run->cap_final += ipow(static_cast<unsigned long long>(c.nc), FD);
     run->cap_level += ipow(static_cast<unsigned long long>(c.nc), FD > 0 ? FD - 1 : 0);
   }
   if (mode == kExhaustive) {
     if (cap_level_hint) run->cap_level = std::min(run->cap_level, cap_level_hint);
     if (cap_final_hint) run->cap_final = std::min(run->cap_final, cap_final_hint);
-    run->cap_level = std::min(run->cap_level, kLevelCapMax);
-    run->cap_final = std::min(run->cap_final, kFinalCapMax);
+    run->cap_level = std::min(run->cap_level, ctx->ex_level_cap);
+    run->cap_final = std::min(run->cap_final, ctx->ex_final_cap);
     run->cap_level = std::max<unsigned long long>(run->cap_level, static_cast<unsigned long long>(n));
     run->cap_final = std::max<unsigned long long>(run->cap_final, static_cast<unsigned long long>(n));
     const ExLayout L = ex_layout(*run, 0);
@@ -463,7 +467,8 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   BS_CUDA_TRY(ctx, cudaMemsetAsync(run->dCtl, 0, sizeof(ExCtl), ctx->stream));
   prepare_kernel<<<n, kPrepThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
                                                       run->dT, run->dCtl, n, run->dFG, run->dBest, run->dFeas, lev[0],
-                                                      lev[1], fin, run->cap_level, run->cap_final);
+                                                      lev[1], fin, run->cap_level, run->cap_final,
+                                                      run->sweep3_min, run->slice);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
   BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel
@@ -491,7 +496,7 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   BS_CUDA_TRY(ctx, launch_pdl(finalize_kernel, dim3((n + 127) / 128), dim3(128), ctx->stream,
                               static_cast<const DTables*>(run->dT), static_cast<const DMpcCfg*>(pk.cfgs),
                               static_cast<const DProblem*>(pk.problems), static_cast<const Key128*>(run->dBest),
-                              static_cast<const unsigned long long*>(run->dFeas), run->dOut, n));
+                              static_cast<const unsigned long long*>(run->dFeas), run->dOut, n, run->slice));
   BS_LAUNCH_CHECK(ctx);
   BS_REC(5);
   return BS_OK;
@@ -573,7 +578,8 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
 }
 
 int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,
-             int n_cfgs, const bs_mpc_problem* problems, int n, bs_mpc_result* out, int mode) {
+             int n_cfgs, const bs_mpc_problem* problems, int n, bs_mpc_result* out, int mode,
+             const DSlice& slice = DSlice{}) {
   if (!ctx || !models) return set_error(ctx, BS_PARAMETER_ERROR, "mpc: null context or models");
   unsigned long long cap_level = 0, cap_final = 0;  // 0: worst case (clamped)
   const bool dbg_t = std::getenv("BS_DEBUG_TIMING") != nullptr;  // host phase timings (diagnostics)
@@ -584,6 +590,7 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
     MpcRun run;
     const double t0 = dbg_t ? now_us() : 0.0;
     int rc = run_pack(ctx, cfgs, policies, n_cfgs, problems, n, mode, &run, cap_level, cap_final);
+    run.slice = slice;
     const double t1 = dbg_t ? now_us() : 0.0;
     if (rc) return rc;
     ctx->last_h2d = run.pk.h2d_bytes;
@@ -625,7 +632,7 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
     const unsigned long long need_final = run.ctl_host.final_count;
     const unsigned long long grow_level = need_level + need_level / 4 + 1024;
     const unsigned long long grow_final = need_final + need_final / 4 + 1024;
-    const bool fits = grow_level <= kLevelCapMax && grow_final <= kFinalCapMax;
+    const bool fits = grow_level <= ctx->ex_level_cap && grow_final <= ctx->ex_final_cap;
     if (fits && attempt < kMaxK + 2 && (grow_level > run.cap_level || grow_final > run.cap_final)) {
       cap_level = std::max(grow_level, run.cap_level);
       cap_final = std::max(grow_final, run.cap_final);
@@ -633,14 +640,14 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
     }
     if (n == 1) return set_error(ctx, BS_PARAMETER_ERROR, "mpc exhaustive: one decision exceeds the frontier budget");
     // split into pieces sized from the observed (lower-bound) need
-    const double over = std::max(static_cast<double>(grow_level) / kLevelCapMax,
-                                 static_cast<double>(grow_final) / kFinalCapMax);
+    const double over = std::max(static_cast<double>(grow_level) / ctx->ex_level_cap,
+                                 static_cast<double>(grow_final) / ctx->ex_final_cap);
     const int pieces = std::min(n, std::max(2, static_cast<int>(std::ceil(over * 1.25))));
     uint64_t h2d = ctx->last_h2d, d2h = ctx->last_d2h;
     for (int p = 0; p < pieces; ++p) {
       const int a = static_cast<int>(static_cast<long long>(n) * p / pieces);
       const int b = static_cast<int>(static_cast<long long>(n) * (p + 1) / pieces);
-      rc = one_shot(ctx, models, cfgs, policies, n_cfgs, problems + a, b - a, out + a, mode);
+      rc = one_shot(ctx, models, cfgs, policies, n_cfgs, problems + a, b - a, out + a, mode, slice);
       if (rc) return rc;
       h2d += ctx->last_h2d;
       d2h += ctx->last_d2h;
@@ -695,6 +702,30 @@ int bs_mpc_exhaustive(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfg
                       const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
                       bs_mpc_result* out) {
   return one_shot(ctx, models, cfgs, policies, n_cfgs, problems, n, out, kExhaustive);
+}
+
+int bs_mpc_exhaustive_slice(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
+                            const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
+                            const bs_slice* slice, bs_mpc_result* out) {
+  if (!slice) return set_error(ctx, BS_PARAMETER_ERROR, "bs_mpc_exhaustive_slice: null slice");
+  if (slice->digits < 0 || slice->digits > 2)
+    return set_error(ctx, BS_PARAMETER_ERROR, "mpc slice: digits must be 0, 1 or 2 (got %d)", slice->digits);
+  DSlice s{};
+  s.digits = slice->digits;
+  s.lo = slice->lo;
+  s.hi = slice->hi;
+  if (s.digits > 0) {
+    if (s.lo > s.hi) return set_error(ctx, BS_PARAMETER_ERROR, "mpc slice: bad range [%llu, %llu)", s.lo, s.hi);
+    for (int c = 0; c < n_cfgs; ++c) {
+      double cand[BS_MAX_CAND];
+      const int nc = ladder_select(ctx, cfgs[c].ladder_mhz, cfgs[c].n_ladder, cfgs[c].ladder_N, cand, BS_MAX_CAND);
+      if (nc < 0) return nc;
+      if (static_cast<double>(s.hi) > std::pow(static_cast<double>(nc), s.digits))
+        return set_error(ctx, BS_PARAMETER_ERROR, "mpc slice: hi %llu exceeds %d^%d leading-digit values", s.hi, nc,
+                         s.digits);
+    }
+  }
+  return one_shot(ctx, models, cfgs, policies, n_cfgs, problems, n, out, kExhaustive, s);
 }
 
 int bs_mpc_greedy(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const bs_scheduler_policy* policies,

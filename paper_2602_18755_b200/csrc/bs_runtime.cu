@@ -389,6 +389,16 @@ int bs_ctx_info(bs_ctx_t ctx, int* device, int* sm_count) {
   return BS_OK;
 }
 
+int bs_ctx_set_exhaustive_limits(bs_ctx_t ctx, double sweep3_min_prefixes, uint64_t level_cap, uint64_t final_cap) {
+  if (!ctx) return BS_PARAMETER_ERROR;
+  if (!(sweep3_min_prefixes >= 0.0))
+    return bs::set_error(ctx, BS_PARAMETER_ERROR, "exhaustive limits: sweep threshold must be >= 0");
+  ctx->ex_sweep3_min = sweep3_min_prefixes > 0.0 ? sweep3_min_prefixes : 16777216.0;
+  ctx->ex_level_cap = level_cap ? level_cap : 250000000ull;
+  ctx->ex_final_cap = final_cap ? final_cap : 2000000000ull;
+  return BS_OK;
+}
+
 int bs_ctx_sync(bs_ctx_t ctx) {
   if (!ctx) return BS_PARAMETER_ERROR;
   BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));

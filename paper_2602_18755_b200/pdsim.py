@@ -720,6 +720,15 @@ class Device:
         self._models[key] = (mh, m)
         return mh
 
+    def set_exhaustive_limits(self, sweep3_min_prefixes: float = 0.0, level_cap: int = 0, final_cap: int = 0) -> None:
+        """Exhaustive-MPC limits of this context (0 restores a default): the
+        prefixes at depth K - 2 above which the sweep walks three levels
+        (2^24), and the frontier capacities in entries (2.5e8 per BFS list,
+        2e9 final).  Batches that exceed them are split; results never
+        depend on them."""
+        self.check(self._lib.bs_ctx_set_exhaustive_limits(self.handle, float(sweep3_min_prefixes), int(level_cap),
+                                                          int(final_cap)))
+
     def interpolate(self, grid: NdGrid, coords: Sequence[Sequence[float]]) -> tuple:
         grid.validate_structure()
         keep: list = []
@@ -808,7 +817,7 @@ def project_batches(q: QueueSnapshot, policy: SchedulerPolicy, horizon_K: int,
 
 def _mpc_batch(fn_name: str, snaps: Sequence[QueueSnapshot], cfgs: Sequence[MpcConfig],
                policies: Sequence[SchedulerPolicy], cfg_index: Sequence[int] | None, models: ModelSet,
-               device: Device | None) -> list:
+               device: Device | None, code_slice: tuple | None = None) -> list:
     dev = device or default_device()
     for c in cfgs:
         c.validate()
@@ -819,7 +828,13 @@ def _mpc_batch(fn_name: str, snaps: Sequence[QueueSnapshot], cfgs: Sequence[MpcC
     n = len(snaps)
     out = (_abi.bs_mpc_result * max(1, n))()
     fn = getattr(dev._lib, fn_name)
-    dev.check(fn(dev.handle, dev.models(models), carr, parr, len(cfgs), probs, n, out))
+    if code_slice is None:
+        dev.check(fn(dev.handle, dev.models(models), carr, parr, len(cfgs), probs, n, out))
+    else:
+        digits, lo, hi = code_slice
+        sl = _abi.bs_slice(int(digits), 0, int(lo), int(hi))
+        dev.check(dev._lib.bs_mpc_exhaustive_slice(dev.handle, dev.models(models), carr, parr, len(cfgs), probs, n,
+                                                   C.byref(sl), out))
     return [greedy_from_c(out[i]) for i in range(n)]
 
 
@@ -842,8 +857,14 @@ def exhaustive_freq_select(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, p
 
 
 def exhaustive_freq_select_batch(snaps: Sequence[QueueSnapshot], cfg: MpcConfig, models: ModelSet,
-                                 policy: SchedulerPolicy, device: Device | None = None) -> list:
-    return _mpc_batch("bs_mpc_exhaustive", snaps, [cfg], [policy], None, models, device)
+                                 policy: SchedulerPolicy, device: Device | None = None,
+                                 code_slice: tuple | None = None) -> list:
+    """Exhaustive MPC of many decisions in one launch.  code_slice = (digits,
+    lo, hi) restricts every decision to the assignments whose first `digits`
+    digits (batch 0 most significant) lie in [lo, hi) (bs_mpc_exhaustive_slice);
+    the decision is then the minimum over a partition's slices
+    (sharding.argmin_over_ranks) and the feasible counts add up."""
+    return _mpc_batch("bs_mpc_exhaustive", snaps, [cfg], [policy], None, models, device, code_slice)
 
 
 def mpc_tables(q: QueueSnapshot, cfg: MpcConfig, models: ModelSet, policy: SchedulerPolicy,

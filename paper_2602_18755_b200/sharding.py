@@ -58,6 +58,37 @@ def code_slice(n_cand: int, K: int, rank: int, world: int) -> tuple[int, int]:
     return lo_p * sub, hi_p * sub
 
 
+def prefix_slice(n_cand: int, rank: int, world: int) -> tuple[int, int, int]:
+    """rank's slice of one exhaustive decision as bs_slice's (digits, lo, hi):
+    the assignments whose first `digits` digits (batch 0 most significant)
+    form a number in [lo, hi).  One leading digit when there are at least as
+    many rungs as ranks, else two; ranks beyond the |cand|^2 leading values
+    get an empty slice.  Independent of the projection length, so ranks need
+    not know K (bs_mpc_exhaustive_slice reads a shorter projection's missing
+    digits as 0)."""
+    digits = 1 if n_cand >= world else 2
+    lo, hi = shard_bounds(n_cand ** digits, rank, world)
+    return digits, lo, hi
+
+
+def combine_slices(parts: list) -> tuple:
+    """Single-process counterpart of argmin_over_ranks for one decision:
+    parts = [(feasible, objective, code, feasible_count)] of a partition's
+    slices; returns (objective, code, feasible_count) with objective/code
+    None when no slice has a feasible assignment."""
+    best = None
+    count = 0
+    for feasible, obj, code, n in parts:
+        count += n
+        if feasible:
+            key = (_obj_bits(obj), code)
+            if best is None or key < best:
+                best = key
+    if best is None:
+        return None, None, count
+    return struct.unpack("<d", struct.pack("<q", best[0]))[0], best[1], count
+
+
 def _obj_bits(x: float) -> int:
     if not x >= 0.0:
         raise ValueError("argmin_over_ranks: objectives are non-negative")

@@ -35,6 +35,22 @@ def test_code_slices_cover_whole_subtrees():
         assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
 
 
+def test_prefix_slices_partition_leading_digits():
+    for nc, world in ((16, 2), (16, 8), (24, 8), (5, 8), (2, 8), (3, 3)):
+        spans = [S.prefix_slice(nc, r, world) for r in range(world)]
+        digits = spans[0][0]
+        assert all(d == digits for d, _, _ in spans) and digits == (1 if nc >= world else 2)
+        assert spans[0][1] == 0 and spans[-1][2] == nc ** digits
+        assert all(spans[i][2] == spans[i + 1][1] for i in range(world - 1))
+
+
+def test_combine_slices_takes_lexicographic_minimum():
+    assert S.combine_slices([(False, 9.0, 5, 0), (False, 1.0, 2, 0)]) == (None, None, 0)
+    # equal objectives: the smaller code wins whatever the slice order
+    assert S.combine_slices([(True, 2.5, 40, 3), (True, 2.5, 7, 4), (True, 3.0, 1, 1)]) == (2.5, 7, 8)
+    assert S.combine_slices([(True, 0.0, 99, 1), (False, 0.0, 0, 0)]) == (0.0, 99, 1)
+
+
 def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
