@@ -498,9 +498,11 @@ int bs_simulate_instance(bs_ctx_t ctx, bs_models_t models, const bs_trace* trace
                          const bs_instance_config* cfg, const bs_scheduler_policy* policy, const bs_slo* slo,
                          bs_sim_summary* out);
 
-/* solve_placement (placement.hpp:357-416): counts[n] (lexicographically
- * smallest among equal-cost optima), objective, GPUs used.
- * BS_INFEASIBLE_ERROR: bs_last_error is "<binding constraint>|<message>". */
+/* solve_placement (placement.hpp:357-416) on the device: counts[n]
+ * (lexicographically smallest among equal-cost optima), objective, GPUs used.
+ * BS_INFEASIBLE_ERROR: bs_last_error is "<binding constraint>|<message>".
+ * ctx may be NULL: the calling thread's default context on device 0 is used
+ * and the message is read with bs_last_error(NULL). */
 int bs_placement_solve(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target_rps,
                        double alpha, int64_t* counts, double* objective_w, int32_t* gpus_used);
 
@@ -509,6 +511,32 @@ int bs_placement_solve(bs_ctx_t ctx, const bs_table_entry* table, int n, int tot
 int bs_placement_max_throughput(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus,
                                 double target_rps, double alpha, double max_freq_mhz, int64_t* counts,
                                 double* objective_w, int32_t* gpus_used);
+
+/* Many placement problems (e.g. every window of run_experiment) in one set
+ * of device launches.  max_throughput != 0 selects solve_max_throughput with
+ * max_freq_mhz.  Per problem: status (BS_OK, BS_INFEASIBLE_ERROR with error =
+ * "<constraint>|<message>", or BS_PARAMETER_ERROR), counts written to the
+ * caller's array, objective and GPUs used.  Limits of the device search: at
+ * most 256 table entries, 2047 GPUs and 64 non-zero counts per plan. */
+typedef struct bs_placement_problem {
+  const bs_table_entry* table;
+  int32_t n;
+  int32_t total_gpus;
+  double target_rps;
+  double alpha;
+  int32_t max_throughput;
+  int32_t _pad;
+  double max_freq_mhz;
+  int64_t* counts; /* out: n entries */
+} bs_placement_problem;
+typedef struct bs_placement_solution {
+  int32_t status;
+  int32_t gpus_used;
+  double objective_w;
+  char error[192];
+} bs_placement_solution;
+int bs_placement_solve_batch(bs_ctx_t ctx, const bs_placement_problem* problems, int n,
+                             bs_placement_solution* out);
 
 /* --- cluster replay ---------------------------------------------------------- */
 

@@ -710,6 +710,50 @@ inline std::vector<ReplayRun> replay_policies(const DeviceModels& dm, const std:
   return runs;
 }
 
+// solve_placement (max_freq[i] < 0) / solve_max_throughput (max_freq[i] =
+// the ladder's maximum) for many problems in ONE device call
+// (bs_placement_solve_batch).  The first failing problem, in order, throws
+// what the reference's call would throw.
+inline std::vector<pdsim::PlacementPlan> solve_placements(const Device& dev,
+                                                          const std::vector<pdsim::PlacementProblem>& ps,
+                                                          const std::vector<double>& max_freq) {
+  const std::size_t n = ps.size();
+  std::vector<std::vector<bs_table_entry>> tabs(n);
+  std::vector<std::vector<int64_t>> counts(n);
+  std::vector<bs_placement_problem> in(n);
+  for (std::size_t k = 0; k < n; ++k) {
+    ps[k].validate();
+    for (const auto& e : ps[k].table) tabs[k].push_back(detail::to_entry(e));
+    counts[k].assign(ps[k].table.size(), 0);
+    in[k] = bs_placement_problem{tabs[k].data(), static_cast<int32_t>(tabs[k].size()), ps[k].total_gpus,
+                                 ps[k].target_rps, ps[k].alpha, max_freq[k] >= 0.0 ? 1 : 0, 0,
+                                 max_freq[k] >= 0.0 ? max_freq[k] : 0.0, counts[k].data()};
+  }
+  std::vector<bs_placement_solution> out(n);
+  dev.check(bs_placement_solve_batch(dev.get(), in.data(), static_cast<int>(n), out.data()));
+  std::vector<pdsim::PlacementPlan> plans(n);
+  for (std::size_t k = 0; k < n; ++k) {
+    if (out[k].status != BS_OK) rethrow(out[k].status, out[k].error);
+    pdsim::PlacementPlan& plan = plans[k];
+    plan.counts.assign(counts[k].begin(), counts[k].end());
+    plan.table = ps[k].table;
+    if (max_freq[k] >= 0.0)  // the restricted table (placement.hpp:423-430, 486)
+      for (auto& e : plan.table)
+        if (e.config.base_freq_mhz != max_freq[k]) {
+          e.r_c = 0.0;
+          e.e_c.reset();
+          e.error = "below maximum frequency";
+        }
+    plan.objective_w = out[k].objective_w;
+    plan.target_rps = ps[k].target_rps;
+    plan.alpha = ps[k].alpha;
+    plan.total_gpus = ps[k].total_gpus;
+    plan.gpus_used = out[k].gpus_used;
+    plan.instances = pdsim::derive_routing_weights(plan.counts, plan.table);
+  }
+  return plans;
+}
+
 // run_experiment (runner.hpp:155-172): window w planned from window w-1 on
 // the GPU, then every (window, policy) replayed in one device call.  Result
 // as the reference's; runs[i].sim holds SimResult's counters, plus the
@@ -735,14 +779,23 @@ inline pdsim::ExperimentResult run_experiment(const DeviceModels& dm, const pdsi
   const std::vector<pdsim::InstanceConfig> candidates = pdsim::enumerate_candidates(cfg.ladder, cfg.tp_options);
   std::vector<std::vector<pdsim::ConfigTableEntry>> tables =
       pdsim_gpu::build_config_tables(dm, candidates, probes, cfg.slo, cfg.plan.policy, cfg.plan.search);
+  // every window's ILP and max-throughput baseline in one device call
   std::vector<pdsim::WindowPlans> plans(windows.size());
+  std::vector<pdsim::PlacementProblem> problems;
+  std::vector<double> max_freq;
   for (std::size_t w = 0; w < windows.size(); ++w) {
     pdsim::WindowPlans& wp = plans[w];
     wp.target_rps = pdsim::peak_rps(predicted[w], cfg.plan.peak_subwindow_s);
     wp.table = std::move(tables[w]);
-    pdsim::PlacementProblem p{wp.table, cfg.total_gpus, wp.target_rps, cfg.plan.alpha};
-    wp.ilp = pdsim_gpu::solve_placement(p);
-    wp.maxfreq = pdsim_gpu::solve_max_throughput(p, cfg.ladder.max_mhz());
+    problems.push_back(pdsim::PlacementProblem{wp.table, cfg.total_gpus, wp.target_rps, cfg.plan.alpha});
+    problems.push_back(problems.back());
+    max_freq.push_back(-1.0);
+    max_freq.push_back(cfg.ladder.max_mhz());
+  }
+  std::vector<pdsim::PlacementPlan> solved = pdsim_gpu::solve_placements(dm.device(), problems, max_freq);
+  for (std::size_t w = 0; w < windows.size(); ++w) {
+    plans[w].ilp = std::move(solved[2 * w]);
+    plans[w].maxfreq = std::move(solved[2 * w + 1]);
   }
   std::vector<const pdsim::Trace*> wins;
   std::vector<const pdsim::PlacementPlan*> pls;

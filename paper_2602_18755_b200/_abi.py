@@ -124,6 +124,17 @@ class bs_slice(C.Structure):
     _fields_ = [("digits", C.c_int32), ("_pad", C.c_int32), ("lo", C.c_uint64), ("hi", C.c_uint64)]
 
 
+class bs_placement_problem(C.Structure):
+    _fields_ = [("table", C.c_void_p), ("n", C.c_int32), ("total_gpus", C.c_int32), ("target_rps", C.c_double),
+                ("alpha", C.c_double), ("max_throughput", C.c_int32), ("_pad", C.c_int32),
+                ("max_freq_mhz", C.c_double), ("counts", C.POINTER(C.c_int64))]
+
+
+class bs_placement_solution(C.Structure):
+    _fields_ = [("status", C.c_int32), ("gpus_used", C.c_int32), ("objective_w", C.c_double),
+                ("error", C.c_char * 192)]
+
+
 class bs_mpc_result(C.Structure):
     _fields_ = [
         ("status", C.c_int32),
@@ -387,6 +398,8 @@ PROTOTYPES = [
     ("bs_placement_max_throughput", C.c_int, [ctx_t, C.POINTER(bs_table_entry), C.c_int, C.c_int, C.c_double,
                                               C.c_double, C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                               C.POINTER(C.c_int32)]),
+    ("bs_placement_solve_batch", C.c_int, [ctx_t, C.POINTER(bs_placement_problem), C.c_int,
+                                           C.POINTER(bs_placement_solution)]),
     ("bs_replay", C.c_int, [ctx_t, models_t, models_t, C.POINTER(bs_replay_config), C.c_int, C.POINTER(bs_scenario),
                             C.c_int, C.POINTER(bs_replay_summary), C.POINTER(bs_replay_request),
                             C.POINTER(bs_replay_logs)]),

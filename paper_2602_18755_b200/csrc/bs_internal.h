@@ -47,6 +47,7 @@ struct bs_ctx_s {
   unsigned long long ex_level_cap = 250000000ull;
   unsigned long long ex_final_cap = 2000000000ull;
   std::unique_ptr<bs::HostPool> host_pool;  // started on first use (parallel_chunks)
+  cudaEvent_t slice_ev[4] = {};  // per-slice D2H events of the MPC result copy (created once, bs_mpc.cu)
   bs::HostPool& pool();
 
   struct Buf {
@@ -89,9 +90,15 @@ enum Slot : int {
   kSlotMisc2 = 11,
   kSlotReplay = 12,
   kSlotFastGrids = 13,
+  kSlotIlp = 14,
 };
 
 int set_error(bs_ctx_t ctx, int code, const char* fmt, ...);
+
+// The calling thread's default context on device 0 (created on first use;
+// nullptr when no device is usable): what the entry points that accept a
+// NULL context run on.
+bs_ctx_t default_ctx();
 
 #define BS_CUDA_TRY(ctx, expr)                                                                     \
   do {                                                                                             \

@@ -516,13 +516,7 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
 #define BS_RESULT_SLICES_MAX 4
 #endif
 
-struct SliceEvents {
-  cudaEvent_t ev[BS_RESULT_SLICES_MAX > 0 ? BS_RESULT_SLICES_MAX : 1] = {};
-  int made = 0;
-  ~SliceEvents() {
-    for (int i = 0; i < made; ++i) cudaEventDestroy(ev[i]);
-  }
-};
+static_assert(BS_RESULT_SLICES_MAX >= 1 && BS_RESULT_SLICES_MAX <= 4, "bs_ctx_s::slice_ev holds 4 events");
 
 int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   const int n = run->n;
@@ -541,7 +535,9 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   }
   const int n_slices = std::max(1, std::min(BS_RESULT_SLICES_MAX, n / BS_RESULT_SLICE));
   auto slice_lo = [&](int sl) { return static_cast<int>(static_cast<long long>(n) * sl / n_slices); };
-  SliceEvents se;
+  if (n_slices > 1)  // the context's slice events, created on first use and reused by every call
+    for (int sl = 0; sl < n_slices; ++sl)
+      if (!ctx->slice_ev[sl]) BS_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->slice_ev[sl], cudaEventDisableTiming));
   for (int sl = 0; sl < n_slices; ++sl) {
     const int lo = slice_lo(sl), hi = slice_lo(sl + 1);
     BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut + lo, run->dOut + lo, out_bytes(hi - lo), cudaMemcpyDeviceToHost,
@@ -549,16 +545,12 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
     if (hLv)
       BS_CUDA_TRY(ctx, cudaMemcpyAsync(hLv + static_cast<size_t>(lo) * stride, run->dLv + static_cast<size_t>(lo) * stride,
                                        levels_bytes(hi - lo, stride), cudaMemcpyDeviceToHost, ctx->stream));
-    if (n_slices > 1) {
-      BS_CUDA_TRY(ctx, cudaEventCreateWithFlags(&se.ev[sl], cudaEventDisableTiming));
-      se.made = sl + 1;
-      BS_CUDA_TRY(ctx, cudaEventRecord(se.ev[sl], ctx->stream));
-    }
+    if (n_slices > 1) BS_CUDA_TRY(ctx, cudaEventRecord(ctx->slice_ev[sl], ctx->stream));
   }
   ctx->last_d2h = out_bytes(n) + (hLv ? levels_bytes(n, stride) : 8);
   for (int sl = 0; sl < n_slices; ++sl) {
     if (n_slices > 1)
-      BS_CUDA_TRY(ctx, cudaEventSynchronize(se.ev[sl]));
+      BS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->slice_ev[sl]));
     else
       BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     if (sl == 0 && *hOverflow) {

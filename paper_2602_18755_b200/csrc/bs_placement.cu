@@ -27,7 +27,6 @@
 #include <cmath>
 #include <cstddef>
 #include <cstring>
-#include <functional>
 #include <string>
 #include <vector>
 
@@ -417,103 +416,6 @@ SearchResult replay_search(long long k_max, const std::function<int(long long)>&
 
 }  // namespace
 
-namespace bs {
-
-// --- ILP (placement.hpp:282-499), exact, host ---------------------------------------
-
-struct IlpEntry {
-  int phase;
-  int g;
-  double r;
-  double e;
-  bool usable;
-};
-
-static bool entry_usable(const bs_table_entry& e) { return e.error_code == 0 && e.r_c > 0.0 && e.has_e_c; }
-
-// SolverCtx::dfs (placement.hpp:297-334), same pruning, fold order, strict <.
-struct SolverCtx {
-  const std::vector<IlpEntry>* t;
-  double need;
-  std::vector<long long> counts, best_counts;
-  double best_cost = INFINITY;
-  bool found = false;
-  std::vector<double> min_e_p, min_e_d, max_rpg_p, max_rpg_d;
-
-  void dfs(size_t i, int gpus_left, double cost, double rp, double rd) {
-    const double def_p = std::max(0.0, need - rp);
-    const double def_d = std::max(0.0, need - rd);
-    if (def_p > 0.0 && min_e_p[i] == INFINITY) return;
-    if (def_d > 0.0 && min_e_d[i] == INFINITY) return;
-    double lb = cost;
-    if (def_p > 0.0) lb += def_p * min_e_p[i];
-    if (def_d > 0.0) lb += def_d * min_e_d[i];
-    if (lb >= best_cost && found) return;
-    double gpus_needed = 0.0;
-    if (def_p > 0.0) gpus_needed += def_p / max_rpg_p[i];
-    if (def_d > 0.0) gpus_needed += def_d / max_rpg_d[i];
-    if (gpus_needed > static_cast<double>(gpus_left) + 1e-9) return;
-    if (i == t->size()) {
-      if (def_p > 1e-9 || def_d > 1e-9) return;
-      if (!found || cost < best_cost) {
-        found = true;
-        best_cost = cost;
-        best_counts = counts;
-      }
-      return;
-    }
-    const IlpEntry& e = (*t)[i];
-    const long long max_n = e.usable ? gpus_left / e.g : 0;
-    const double ec = e.e;
-    for (long long n = 0; n <= max_n; ++n) {
-      counts[i] = n;
-      const double add_r = static_cast<double>(n) * e.r;
-      const double add_cost = static_cast<double>(n) * ec * e.r;
-      dfs(i + 1, gpus_left - static_cast<int>(n) * e.g, cost + add_cost, rp + (e.phase == BS_PHASE_PREFILL ? add_r : 0.0),
-          rd + (e.phase == BS_PHASE_DECODE ? add_r : 0.0));
-    }
-    counts[i] = 0;
-  }
-};
-
-// min_gpus_for_phase (placement.hpp:339-351)
-static int min_gpus_for_phase(const std::vector<IlpEntry>& t, int phase, double need, int budget) {
-  std::vector<double> best(static_cast<size_t>(budget) + 1, 0.0);
-  for (int g = 1; g <= budget; ++g) {
-    double v = 0.0;
-    for (const auto& e : t) {
-      if (e.phase != phase || !e.usable || e.g > g) continue;
-      v = std::max(v, best[static_cast<size_t>(g - e.g)] + e.r);
-    }
-    best[static_cast<size_t>(g)] = std::max(best[static_cast<size_t>(g - 1)], v);
-    if (best[static_cast<size_t>(g)] >= need - 1e-9) return g;
-  }
-  return -1;
-}
-
-static std::string capacity_msg(const std::vector<IlpEntry>& t, double need, int total) {
-  const int gp = min_gpus_for_phase(t, BS_PHASE_PREFILL, need, total);
-  const int gd = min_gpus_for_phase(t, BS_PHASE_DECODE, need, total);
-  auto s = [&](int g) { return g < 0 ? std::string(">" + std::to_string(total)) : std::to_string(g); };
-  return "prefill needs " + s(gp) + " GPUs, decode needs " + s(gd) + ", available " + std::to_string(total);
-}
-
-static int validate_problem(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target,
-                            double alpha) {  // PlacementProblem::validate (placement.hpp:42-51)
-  if (total_gpus < 1) return set_error(ctx, BS_PARAMETER_ERROR, "placement: total_gpus must be >= 1");
-  if (target <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: target_rps must be > 0");
-  if (alpha < 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: alpha must be >= 0");
-  for (int i = 0; i < n; ++i) {
-    const bs_table_entry& e = table[i];
-    if (e.g_c != e.config.tp) return set_error(ctx, BS_PARAMETER_ERROR, "placement: G_c must equal tp");
-    if (e.r_c < 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: R_c must be >= 0");
-    if (e.r_c > 0.0 && e.has_e_c && e.e_c <= 0.0) return set_error(ctx, BS_PARAMETER_ERROR, "placement: E_c must be > 0");
-  }
-  return BS_OK;
-}
-
-}  // namespace bs
-
 extern "C" {
 
 int bs_downsample_keep(bs_ctx_t ctx, const bs_trace* trace, const bs_goodput_search* search, int64_t k,
@@ -861,11 +763,9 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
       // An empty probe trace only records the idle span [0, duration] (simulator.hpp:731-733).
       const ProbeOut& e = hpt[static_cast<size_t>(c) * tb.n_streams + (sr.k_star - 1) * reps];
       if (e.empty) {
-        if (!idle_tp_ok[c]) {
+        if (!idle_tp_ok[c]) {  // evaluate_candidate's catch (placement.hpp:233-236): r_c = 0, saturated kept
           ot[c].error_code = BS_MODEL_ERROR;
           ot[c].r_c = 0.0;
-          ot[c].k_star = 0;
-          ot[c].saturated = 0;
           std::snprintf(ot[c].error, sizeof ot[c].error, "idle model: tp %d not present", cands[c].tp);
         } else {
           ot[c].error_code = -1;
@@ -963,118 +863,6 @@ int bs_simulate_instance(bs_ctx_t ctx, bs_models_t models, const bs_trace* trace
     out[i].idle_energy_j = hr[i].idle_j;
     out[i].horizon_ms = hr[i].horizon_ms;
   }
-  return BS_OK;
-}
-
-int bs_placement_solve(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target_rps,
-                       double alpha, int64_t* counts, double* objective_w, int32_t* gpus_used) {
-  if ((!table && n > 0) || !counts) return set_error(ctx, BS_PARAMETER_ERROR, "bs_placement_solve: null argument");
-  int rc = validate_problem(ctx, table, n, total_gpus, target_rps, alpha);
-  if (rc) return rc;
-  std::vector<IlpEntry> t(n);
-  bool has_p = false, has_d = false;
-  for (int i = 0; i < n; ++i) {
-    t[i] = IlpEntry{table[i].config.phase, table[i].g_c, table[i].r_c, table[i].has_e_c ? table[i].e_c : 0.0,
-                    entry_usable(table[i])};
-    if (t[i].usable) (t[i].phase == BS_PHASE_PREFILL ? has_p : has_d) = true;
-  }
-  if (!has_p) return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-prefill|no usable prefill configuration in the table");
-  if (!has_d) return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-decode|no usable decode configuration in the table");
-  SolverCtx s;
-  s.t = &t;
-  s.need = (1.0 + alpha) * target_rps;
-  s.counts.assign(n, 0);
-  s.min_e_p.assign(n + 1, INFINITY);
-  s.min_e_d.assign(n + 1, INFINITY);
-  s.max_rpg_p.assign(n + 1, 0.0);
-  s.max_rpg_d.assign(n + 1, 0.0);
-  for (int i = n; i-- > 0;) {  // placement.hpp:376-390
-    s.min_e_p[i] = s.min_e_p[i + 1];
-    s.min_e_d[i] = s.min_e_d[i + 1];
-    s.max_rpg_p[i] = s.max_rpg_p[i + 1];
-    s.max_rpg_d[i] = s.max_rpg_d[i + 1];
-    if (!t[i].usable) continue;
-    if (t[i].phase == BS_PHASE_PREFILL) {
-      s.min_e_p[i] = std::min(s.min_e_p[i], t[i].e);
-      s.max_rpg_p[i] = std::max(s.max_rpg_p[i], t[i].r / t[i].g);
-    } else {
-      s.min_e_d[i] = std::min(s.min_e_d[i], t[i].e);
-      s.max_rpg_d[i] = std::max(s.max_rpg_d[i], t[i].r / t[i].g);
-    }
-  }
-  s.dfs(0, total_gpus, 0.0, 0.0, 0.0);
-  if (!s.found) return set_error(ctx, BS_INFEASIBLE_ERROR, "capacity|%s", capacity_msg(t, s.need, total_gpus).c_str());
-  int used = 0;
-  for (int i = 0; i < n; ++i) {
-    counts[i] = s.best_counts[i];
-    used += static_cast<int>(s.best_counts[i]) * t[i].g;
-  }
-  if (objective_w) *objective_w = s.best_cost;
-  if (gpus_used) *gpus_used = used;
-  return BS_OK;
-}
-
-int bs_placement_max_throughput(bs_ctx_t ctx, const bs_table_entry* table, int n, int total_gpus, double target_rps,
-                                double alpha, double max_freq_mhz, int64_t* counts, double* objective_w,
-                                int32_t* gpus_used) {
-  if ((!table && n > 0) || !counts)
-    return set_error(ctx, BS_PARAMETER_ERROR, "bs_placement_max_throughput: null argument");
-  int rc = validate_problem(ctx, table, n, total_gpus, target_rps, alpha);
-  if (rc) return rc;
-  std::vector<IlpEntry> t(n);
-  bool has_p = false, has_d = false;
-  for (int i = 0; i < n; ++i) {  // restricted table (placement.hpp:423-430)
-    const bool keep = table[i].config.base_freq_mhz == max_freq_mhz;
-    t[i] = IlpEntry{table[i].config.phase, table[i].g_c, keep ? table[i].r_c : 0.0,
-                    keep && table[i].has_e_c ? table[i].e_c : 0.0, keep && entry_usable(table[i])};
-    if (t[i].usable) (t[i].phase == BS_PHASE_PREFILL ? has_p : has_d) = true;
-  }
-  if (!has_p)
-    return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-prefill|no usable max-frequency prefill configuration");
-  if (!has_d)
-    return set_error(ctx, BS_INFEASIBLE_ERROR, "goodput-decode|no usable max-frequency decode configuration");
-  const double need = (1.0 + alpha) * target_rps;
-  std::vector<long long> cur(n, 0), best;
-  bool found = false;
-  double best_score = -1.0;
-  int best_gpus = 0;
-  std::function<void(size_t, int, double, double)> rec = [&](size_t i, int left, double rp, double rd) {
-    if (i == static_cast<size_t>(n)) {  // placement.hpp:448-461
-      if (rp < need - 1e-9 || rd < need - 1e-9) return;
-      const int used = total_gpus - left;
-      if (used <= 0) return;
-      const double score = std::min(rp, rd) / static_cast<double>(used);
-      const bool better = !found || score > best_score + 1e-12 || (std::abs(score - best_score) <= 1e-12 && used < best_gpus);
-      if (better) {
-        found = true;
-        best_score = score;
-        best_gpus = used;
-        best = cur;
-      }
-      return;
-    }
-    const IlpEntry& e = t[i];
-    const long long max_n = e.usable ? left / e.g : 0;
-    for (long long c = 0; c <= max_n; ++c) {
-      cur[i] = c;
-      rec(i + 1, left - static_cast<int>(c) * e.g,
-          rp + (e.phase == BS_PHASE_PREFILL ? static_cast<double>(c) * e.r : 0.0),
-          rd + (e.phase == BS_PHASE_DECODE ? static_cast<double>(c) * e.r : 0.0));
-    }
-    cur[i] = 0;
-  };
-  rec(0, total_gpus, 0.0, 0.0);
-  if (!found) return set_error(ctx, BS_INFEASIBLE_ERROR, "capacity|%s", capacity_msg(t, need, total_gpus).c_str());
-  int used = 0;
-  double obj = 0.0;
-  for (int i = 0; i < n; ++i) {  // placement.hpp:490-495
-    counts[i] = best[i];
-    used += static_cast<int>(best[i]) * t[i].g;
-    if (table[i].config.base_freq_mhz == max_freq_mhz && table[i].has_e_c)
-      obj += static_cast<double>(best[i]) * table[i].e_c * table[i].r_c;
-  }
-  if (objective_w) *objective_w = obj;
-  if (gpus_used) *gpus_used = used;
   return BS_OK;
 }
 

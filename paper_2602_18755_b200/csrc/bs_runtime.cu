@@ -55,6 +55,8 @@ bs::HostPool& bs_ctx_s::pool() {
 }
 
 bs_ctx_s::~bs_ctx_s() {
+  for (cudaEvent_t e : slice_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& b : dev)
     if (b.p) cudaFree(b.p);
   for (auto& b : host)
@@ -65,6 +67,22 @@ bs_ctx_s::~bs_ctx_s() {
 namespace bs {
 
 thread_local std::string g_host_err;
+
+bs_ctx_t default_ctx() {
+  struct Holder {
+    bs_ctx_t c = nullptr;
+    bool tried = false;
+    ~Holder() {
+      if (c) bs_ctx_destroy(c);
+    }
+  };
+  thread_local Holder h;
+  if (!h.tried) {
+    h.tried = true;
+    if (bs_ctx_create(0, &h.c) != BS_OK) h.c = nullptr;
+  }
+  return h.c;
+}
 
 int set_error(bs_ctx_t ctx, int code, const char* fmt, ...) {
   char buf[1024];

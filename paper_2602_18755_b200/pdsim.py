@@ -1381,6 +1381,49 @@ def _solve(fn_name: str, p: PlacementProblem, extra: tuple, device: Device | Non
     return plan
 
 
+def solve_placement_batch(problems: Sequence[tuple], device: Device | None = None) -> list:
+    """Many placement problems in one device call (bs_placement_solve_batch):
+    problems = [(PlacementProblem, max_freq_mhz or None)], None selecting
+    solve_placement and a frequency solve_max_throughput.  Returns, per
+    problem, its PlacementPlan or the exception the single call would raise."""
+    dev = device or default_device()
+    n = len(problems)
+    arr = (_abi.bs_placement_problem * max(1, n))()
+    keep: list = []
+    for k, (p, mf) in enumerate(problems):
+        tab = c_table(p.table)
+        cnt = (C.c_int64 * max(1, len(p.table)))()
+        keep += [tab, cnt]
+        arr[k].table = C.cast(tab, C.c_void_p)
+        arr[k].n = len(p.table)
+        arr[k].total_gpus = p.total_gpus
+        arr[k].target_rps = p.target_rps
+        arr[k].alpha = p.alpha
+        arr[k].max_throughput = 0 if mf is None else 1
+        arr[k].max_freq_mhz = 0.0 if mf is None else mf
+        arr[k].counts = cnt
+    out = (_abi.bs_placement_solution * max(1, n))()
+    dev.check(dev._lib.bs_placement_solve_batch(dev.handle, arr, n, out))
+    res = []
+    for k, (p, mf) in enumerate(problems):
+        o = out[k]
+        if o.status != _abi.BS_OK:
+            try:
+                raise_status(o.status, o.error.decode())
+            except PdsimError as e:
+                res.append(e)
+            continue
+        counts = [arr[k].counts[i] for i in range(len(p.table))]
+        plan = PlacementPlan(counts, list(p.table), o.objective_w, p.target_rps, p.alpha, p.total_gpus, o.gpus_used)
+        if mf is not None:
+            plan.table = [e if e.config.base_freq_mhz == mf else
+                          ConfigTableEntry(e.config, 0.0, None, e.g_c, e.saturated, "below maximum frequency", e.k_star)
+                          for e in p.table]
+        plan.instances = derive_routing_weights(plan.counts, plan.table)
+        res.append(plan)
+    return res
+
+
 def solve_placement(p: PlacementProblem, device: Device | None = None) -> PlacementPlan:
     """solve_placement (placement.hpp:357-416): exact branch and bound."""
     return _solve("bs_placement_solve", p, (), device)
@@ -1776,9 +1819,9 @@ def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, 
                    device: Device | None = None) -> ExperimentResult:
     """run_experiment (runner.hpp:155-172): window w is planned from window
     w-1 (the first from itself): every window's config table in ONE
-    bs_goodput_tables call, then the ILP and the max-throughput baseline;
-    then every (window, policy) replay in ONE bs_replay call (windows are
-    independent once planned).  Reports, SLO verdicts and their order follow
+    bs_goodput_tables call, every window's ILP and max-throughput baseline in
+    ONE bs_placement_solve_batch call, then every (window, policy) replay in
+    ONE bs_replay call (windows are independent once planned).  Reports, SLO verdicts and their order follow
     the reference."""
     dev = device or default_device()
     cfg.validate()
@@ -1805,13 +1848,19 @@ def run_experiment(trace: Trace, window_ms: float, policies, cfg: RunnerConfig, 
     probes = [opts.probe_trace if opts.probe_trace is not None else p for p in predicted]
     candidates = enumerate_candidates(cfg.ladder, cfg.tp_options)
     tables = build_config_tables(probes, candidates, cfg.slo, models, opts.policy, opts.search, dev)
-    plans = []
-    for p, table in zip(predicted, tables):
-        target = peak_rps(p, opts.peak_subwindow_s)
-        ilp = solve_placement(PlacementProblem(table, cfg.total_gpus, target, opts.alpha), dev)
-        mx = solve_max_throughput(PlacementProblem(table, cfg.total_gpus, target, opts.alpha), cfg.ladder.max_mhz(),
-                                  dev)
-        plans.append(WindowPlans(target, table, ilp, mx))
+    # every window's ILP and max-throughput baseline in ONE device call
+    # (bs_placement_solve_batch); errors surface in the reference's order
+    # (window by window, solve_placement before solve_max_throughput)
+    targets = [peak_rps(p, opts.peak_subwindow_s) for p in predicted]
+    probs = []
+    for table, target in zip(tables, targets):
+        probs.append((PlacementProblem(table, cfg.total_gpus, target, opts.alpha), None))
+        probs.append((PlacementProblem(table, cfg.total_gpus, target, opts.alpha), cfg.ladder.max_mhz()))
+    solved = solve_placement_batch(probs, dev)
+    for x in solved:
+        if isinstance(x, Exception):
+            raise x
+    plans = [WindowPlans(targets[w], tables[w], solved[2 * w], solved[2 * w + 1]) for w in range(len(tables))]
     scs, keys = [], []
     for w, win in enumerate(windows):
         for pol in policies:

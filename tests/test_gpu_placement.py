@@ -289,3 +289,31 @@ def test_search_pruning_random_tables_match_reference(gpu_device, ref_lib, seed)
         got = P.build_config_table(cands, base, slo, m, pol, search)
         want = _ref_table(ref_lib, m, base, slo, pol, search, cands)
         assert [_cmp(e) for e in got] == [_cmp(e) for e in want]
+
+
+def test_empty_saturated_probe_without_idle_tp_matches_reference(gpu_device, ref_lib):
+    """evaluate_candidate (placement.hpp:217-238) when the search ends on an
+    EMPTY probe (an empty probe counts as a pass, placement.hpp:169) and the
+    idle model lacks the candidate's tp: the E_c simulation throws ModelError,
+    the catch clears r_c but keeps saturated.  Seeds are searched on the
+    reference's own down-sampler until the k_max probe of replicate 0 keeps
+    nothing."""
+    m = probe_models()  # idle model: tp 1 only
+    base = P.Trace([P.Request(0, 100.0, 200, 5), P.Request(1, 2500.0, 300, 5)], 3000.0)  # 0.667 rps: k_max 2
+    keep: list = []
+    ct = P.c_trace(base, keep)
+    kept = (C.c_int32 * 2)()
+    nk = C.c_int64()
+    found = None
+    for seed in range(1, 400):
+        search = P.GoodputSearch(seed=seed)
+        assert ref_lib.ref_downsample_keep(C.byref(ct), C.byref(P.c_search(search)), 2, 0, kept, C.byref(nk)) == 0
+        if nk.value == 0:
+            found = search
+            break
+    assert found is not None
+    cands = [P.InstanceConfig(PF, 4, 1000.0), P.InstanceConfig(PF, 1, 1000.0), P.InstanceConfig(DE, 4, 500.0)]
+    got = P.build_config_table(cands, base, P.SLOSpec(600.0, 100.0), m, P.SchedulerPolicy(), found)
+    want = _ref_table(ref_lib, m, base, P.SLOSpec(600.0, 100.0), P.SchedulerPolicy(), found, cands)
+    assert [_cmp(e) for e in got] == [_cmp(e) for e in want]
+    assert want[0].saturated and want[0].r_c == 0.0 and "tp 4" in want[0].error

@@ -43,6 +43,7 @@ MPC_SETS = [
     ("exhaustive", "sandwich", 0x6020, 30, {}),
     ("exhaustive", "llama", 0x6021, 20, {"levels": 8, "ladder_n": 5, "horizon": 4}),
     ("exhaustive", "llama", 0x6022, 8, {"levels": 16, "ladder_n": 16, "horizon": 3}),
+    ("exhaustive", "llama", 0x6023, 4, {"levels": 24, "ladder_n": 24, "horizon": 5}),  # C5 grid, 24^5 = 8M each
 ]
 C2_SEED, C2_COUNT = 0xC2, 2
 
