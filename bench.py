@@ -959,7 +959,7 @@ def main():
             "decisions_per_s": world * D * args.steps / (total_ms * 1e-3),
             "feasible_fraction": feasible / max(1, trajectories),
             "phase_ms_avg": {k: statistics.mean(p[i] for p in phase_ms)
-                             for i, k in enumerate(["prepare", "seed", "bfs", "sweep", "finalize"])},
+                             for i, k in enumerate(["prepare", "thresholds", "bfs", "sweep", "finalize"])},
             "e2e": {"value": world * D * TRAJ_PER_DECISION / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
                     "matches_resident": bool(same)},

@@ -418,7 +418,7 @@ int bs_mpc_exhaustive_slice(bs_ctx_t ctx, bs_models_t models, const bs_mpc_confi
  * context stream without host synchronisation, and copy results out.
  * mode: 0 exhaustive, 1 greedy.  bs_mpc_plan_kernel_ms returns the number
  * of phases and their durations from the last run with record_kernel_times
- * (exhaustive: prepare, scan, prefix, leaf, finalize; greedy: greedy). */
+ * (exhaustive: prepare, thresholds, bfs, sweep, finalize; greedy: greedy). */
 typedef struct bs_mpc_plan_s* bs_mpc_plan_t;
 int bs_mpc_plan_create(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
                        const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,

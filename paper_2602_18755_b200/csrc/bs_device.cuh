@@ -244,12 +244,20 @@ struct DTables {
   SRec srec[kMaxK][kMaxCand];
   unsigned short sinfo[kMaxK][kMaxCand];
   int sorted_ok;
+  int thr_ok;  // exhaustive search: the two bottom levels' leaf-count thresholds are built (DThr, bs_exhaustive.cuh)
+  int fuse;    // exhaustive search: the BFS settles dominated final nodes (thr_kernel)
+  int n_ok3;   // exhaustive search: feasible depth-3 prefixes (prepare_kernel)
   int FD;  // exhaustive search: depth of the final nodes, K - sweep_levels(K, nc) (set by prepare_kernel)
   unsigned nc_magic;  // ceil(2^32 / nc): code / nc by a multiply-high for codes < 2^27 (set by prepare_kernel)
   // Per-level bounds for the leaf-row skip: amax = max_f A, pmin_lo =
   // fl(min_f P * (1 - 2^-50)) <= min_f P * (1 - u).
   double amax[kMaxK];
   double pmin_lo[kMaxK];
+  // Node bound of the argmin seed (exhaustive search, set by prepare_kernel;
+  // nb_R = +inf disables it): a node at depth K-2 with (num, den) has every
+  // leaf worse than the seed when fl(num - fl(nb_beta den)) > fl(nb_R + fl(num 2^-40)).
+  double nb_beta;
+  double nb_R;
 };
 
 // Compact per-problem result written by the device; the host expands it

@@ -27,8 +27,10 @@ struct ExCtl {
   unsigned long long level_count[kMaxK + 1];  // BFS list sizes per depth
   unsigned long long final_count;
   unsigned long long overflow;  // appends dropped for lack of capacity (must stay 0)
+  unsigned long long n_loose;   // decisions prepare_kernel found loose (candidates for BFS-settled final nodes)
+  unsigned long long n_thr;     // decisions listed for thr_kernel (three swept levels, or loose)
 #ifdef BS_SWEEP_STATS
-  unsigned long long st_nodes, st_children, st_rows_eval, st_leaves_eval, st_div;
+  unsigned long long st_nodes, st_children, st_rows_eval, st_leaves_eval, st_div, st_thr_nodes, st_slow_nodes;
 #endif
 };
 
@@ -86,6 +88,179 @@ __host__ __device__ inline unsigned long long slice_size(const DSlice& s, int K,
   if (K >= s.digits) return (hi - lo) * (total / lead);
   const unsigned long long m = lead / total;  // codes c with c * m in [lo, hi)
   return (hi + m - 1) / m - (lo + m - 1) / m;
+}
+
+// Leaf-count thresholds of the two bottom levels (K-2, K-1) of one decision.
+// A node at depth K-2 with clock t and last digit l has the leaf (g, f)
+// feasible iff both meets_slo checks pass:
+//   fl(fl(t + s1) - m[K-2]) <= ttft  and  fl(fl(fl(t + s1) + s2) - m[K-1]) <= ttft,
+// s1 = B1[K-2][g] (g != l) or B0[K-2][g] (g == l), s2 = B1[K-1][f] (f != g)
+// or B0[K-1][f].  Correctly rounded add / subtract are monotone, so each
+// test holds exactly for t <= tau, one double per (g, f, switched): found by
+// bisection over the doubles' order with the sweep's own op sequence.  The
+// node's feasible-leaf count is then
+//   #{tau_S >= t over all (g, f)} - #{tau_S[l][f] >= t} + #{tau_N[l][f] >= t},
+// three binary searches over descending arrays instead of a walk over the
+// node's children rows.
+struct DThr {
+  double cs[kMaxCand * kMaxCand];  // every switched tau_S, descending
+  double rs[kMaxCand * kMaxCand];  // row g: tau_S[g][*], descending (stride nc)
+  double rn[kMaxCand * kMaxCand];  // row g: tau_N[g][*] (g the node's last digit), descending
+};
+
+// Number of leading entries >= t of a descending array.
+__device__ __forceinline__ int count_ge(const double* __restrict__ a, int n, double t) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] >= t)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Feasible leaves below a node at depth K-2 (clock t, last digit l).
+__device__ __forceinline__ int thr_leaf_count(const DThr* __restrict__ H, int nc, double t, int l) {
+  return count_ge(H->cs, nc * nc, t) - count_ge(H->rs + l * nc, nc, t) + count_ge(H->rn + l * nc, nc, t);
+}
+
+// The seed's node bound ("seed node bound"): every leaf below a
+// node at depth K-2 with (num, den) has a rounded objective above the seed's
+// (a genuine feasible key, so none of them is the argmin).  With beta =
+// thr_seed (1 + 2^-47) and Q_k = min_x (E[k][x] - beta A[k][x]) over the two
+// bottom levels, num - beta den + Q_K-2 + Q_K-1 > 0 suffices (A >= 0);
+// nb_R >= -(Q_K-2 + Q_K-1) with its rounding margin, clamped at 0.
+// Precondition: filter_ok tables, den >= 2^-900.
+__device__ __forceinline__ bool node_dom_seed(const DTables* __restrict__ T, double num, double den) {
+  return den >= kFilterMinDen &&
+         __dsub_rn(num, __dmul_rn(T->nb_beta, den)) > __dadd_rn(T->nb_R, __dmul_rn(num, 0x1p-40));
+}
+
+// Order-preserving map of doubles to unsigned integers (and back).
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dval(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// The largest double t for which both bottom-level checks pass (-inf: none;
+// +inf: every finite t).
+__device__ double leaf_threshold(double s1, double m1, double s2, double m2, double ttft) {
+  auto ok = [&](double t) {
+    const double t2 = __dadd_rn(t, s1);
+    if (__dsub_rn(t2, m1) > ttft) return false;                 // dvfs.hpp:117 at level K-2
+    return !(__dsub_rn(__dadd_rn(t2, s2), m2) > ttft);          // and at level K-1
+  };
+  const double big = 1.7976931348623157e308;
+  if (ok(big)) return INFINITY;
+  if (!ok(-big)) return -INFINITY;
+  // bracket the boundary by galloping from the real-arithmetic estimate
+  // (within a few ulps unless an operand swamps another), then bisect
+  const unsigned long long kmin = dkey(-big), kmax = dkey(big);
+  const double x1 = __dsub_rn(__dadd_rn(ttft, m1), s1), x2 = __dsub_rn(__dsub_rn(__dadd_rn(ttft, m2), s1), s2);
+  double x0 = x1 < x2 ? x1 : x2;
+  if (!(x0 == x0)) x0 = 0.0;
+  unsigned long long k0 = dkey(x0 < -big ? -big : (x0 > big ? big : x0));
+  unsigned long long lo, hi;  // ok(lo), !ok(hi)
+  unsigned long long step = 1;
+  if (ok(dval(k0))) {
+    lo = k0;
+    for (;;) {
+      const unsigned long long nk = kmax - lo > step ? lo + step : kmax;
+      if (!ok(dval(nk))) {
+        hi = nk;
+        break;
+      }
+      lo = nk;
+      step <<= 1;
+    }
+  } else {
+    hi = k0;
+    for (;;) {
+      const unsigned long long nk = hi - kmin > step ? hi - step : kmin;
+      if (ok(dval(nk))) {
+        lo = nk;
+        break;
+      }
+      hi = nk;
+      step <<= 1;
+    }
+  }
+  while (hi - lo > 1) {
+    const unsigned long long mid = lo + ((hi - lo) >> 1);
+    if (ok(dval(mid)))
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return dval(lo);
+}
+
+// Builds H for decision T (K >= 3, sorted tables) with the whole CTA
+// (called by prepare_kernel; every thread must call it).
+// Rows need no sort: for a fixed level-(K-2) step, tau is non-increasing in
+// the leaf step s2 (rounding is monotone), and the leaf steps of a row are
+// the level's switched steps in their sorted order (ord[K-1]) with the
+// non-switching leaf f == g (B0 <= B1) moved to its place.  The switched
+// thresholds of all rows are then merged into cs by ranks counted against
+// every other threshold (broadcast shared-memory reads; equal values
+// ordered by row, then position).  Out of line: its registers and shared
+// memory stay out of the rest of prepare_kernel.
+__device__ __noinline__ void build_thresholds(const DTables* __restrict__ T, DThr* H) {
+  __shared__ double s_rows[2 * kMaxCand * kMaxCand];
+  __shared__ double s_b0k[kMaxCand], s_b1k[kMaxCand], s_b0l[kMaxCand], s_b1l[kMaxCand];
+  __shared__ unsigned char s_pos[kMaxCand], s_rank[kMaxCand], s_ord[kMaxCand];
+  const int K = T->K, nc = T->nc, k = K - 2, kl = K - 1, M = nc * nc;
+  const double m1 = T->minarr[k], m2 = T->minarr[kl], ttft = T->ttft;
+  for (int x = threadIdx.x; x < nc; x += blockDim.x) {
+    const double b0 = T->B0[kl][x];
+    s_b0k[x] = T->B0[k][x];
+    s_b1k[x] = T->B1[k][x];
+    s_b0l[x] = b0;
+    s_b1l[x] = T->B1[kl][x];
+    s_rank[x] = T->rank[kl][x];
+    s_ord[x] = T->ord[kl][x];
+    int p = 0;  // the non-switching leaf's position in row x: switched steps below B0[K-1][x] (x's own excluded)
+    for (int j = 0; j < nc; ++j) p += T->sb[kl][j] < b0 ? 1 : 0;
+    if (T->B1[kl][x] < b0) --p;  // only with a negative switch latency
+    s_pos[x] = static_cast<unsigned char>(p);
+  }
+  __syncthreads();
+  double* sS = s_rows;
+  double* sN = s_rows + M;
+  for (int e = threadIdx.x; e < 2 * M; e += blockDim.x) {
+    const bool sw = e < M;
+    const int r = sw ? e : e - M, g = r / nc, j = r - g * nc;
+    const int p = s_pos[g], rg = s_rank[g];
+    int f;  // the leaf at position j of row g
+    if (j == p) {
+      f = g;
+    } else {
+      const int i = j < p ? j : j - 1;  // index into the switched order without g
+      f = s_ord[i < rg ? i : i + 1];
+    }
+    const double tau = leaf_threshold(sw ? s_b1k[g] : s_b0k[g], m1, f == g ? s_b0l[g] : s_b1l[f], m2, ttft);
+    (sw ? sS : sN)[r] = tau;
+    (sw ? H->rs : H->rn)[r] = tau;
+  }
+  __syncthreads();
+  // cs = the switched thresholds merged, descending: rank of (g, j) counts
+  // the larger ones and the equal ones earlier in (row, position) order
+  for (int e = threadIdx.x; e < M; e += blockDim.x) {
+    const double x = sS[e];
+    int rank = 0;
+    for (int o = 0; o < M; ++o) {
+      const double y = sS[o];
+      rank += (y > x || (y == x && o < e)) ? 1 : 0;
+    }
+    H->cs[rank] = x;
+  }
+  __syncthreads();
 }
 
 // Frontier lists in HBM, structure of arrays.
@@ -311,10 +486,12 @@ __device__ __forceinline__ void block_append2n(unsigned long long* c0, unsigned 
 // Pass 1 marks the kept children by digit, pass 2 writes them in digit order
 // (the layout of a (node, digit) expansion: siblings contiguous, in code
 // order) after a block-aggregated append.
-__device__ __forceinline__ void expand_node(const DTables* __restrict__ tables, int k, ExCtl* ctl, bool valid, int d,
+template <bool FUSE>
+__device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tables, int k, ExCtl* ctl, bool valid, int d,
                                             double t, double num, double den, int last, unsigned long long code,
                                             Frontier out, FinalList fin, unsigned long long cap_out,
-                                            unsigned long long cap_final) {
+                                            unsigned long long cap_final, const DThr* __restrict__ thr,
+                                            unsigned long long* feas, bool fuse_batch = false) {
   unsigned keep = 0u;  // bit f: child f kept
   bool to_final = false;
   int nc = 0;
@@ -360,6 +537,23 @@ __device__ __forceinline__ void expand_node(const DTables* __restrict__ tables, 
         double ct, cn, cd;
         if (child_state(T, k, t, num, den, last, f, ct, cn, cd)) keep |= 1u << f;
       }
+    }
+    // Final nodes at depth K-2 whose leaves are all worse than the seed are
+    // settled here: their feasible leaves are counted from the thresholds and
+    // they never reach the final list (or the sweep).
+    if (FUSE && to_final && T->fuse && fuse_batch && k + 1 == T->K - 2) {
+      unsigned long long cnt = 0;
+      for (unsigned kk = keep; kk;) {
+        const int f = __ffs(kk) - 1;
+        kk &= kk - 1u;
+        double ct, cn, cd;
+        child_state(T, k, t, num, den, last, f, ct, cn, cd);
+        if (node_dom_seed(T, cn, cd)) {
+          cnt += static_cast<unsigned long long>(thr_leaf_count(thr + d, nc, ct, f));
+          keep &= ~(1u << f);
+        }
+      }
+      if (cnt) atomicAdd(&feas[d], cnt);
     }
   }
   const unsigned m = static_cast<unsigned>(__popc(keep));
@@ -424,24 +618,29 @@ __device__ __forceinline__ void expand_node(const DTables* __restrict__ tables, 
       }
     }
   }
+  return m;
 }
 
 // Level k >= 3 of the search (prepare_kernel expands depths 1-3): one
 // thread per depth-k node, expand_node.
 __global__ void __launch_bounds__(256) bfs_node_kernel(const DTables* __restrict__ tables, int k, ExCtl* ctl,
                                                        Frontier in, Frontier out, FinalList fin,
-                                                       unsigned long long cap_out, unsigned long long cap_final) {
+                                                       unsigned long long cap_out, unsigned long long cap_final,
+                                                       const DThr* __restrict__ thr, unsigned long long* feas,
+                                                       int n_problems) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous level (programmatic dependent launch)
   if (ctl->overflow) return;
+  // BFS-settled final nodes only when >= 10 % of the batch is loose (prepare_kernel)
+  const bool fuse_batch = true;  // T->fuse is cleared by thr_kernel unless >= 10 % of the batch is loose
   const unsigned long long n_in = ctl->level_count[k];
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
   for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < n_in;
        base += stride) {
     const unsigned long long i = base + threadIdx.x;
     const bool valid = i < n_in;
-    expand_node(tables, k, ctl, valid, valid ? in.d[i] : 0, valid ? in.t[i] : 0.0, valid ? in.num[i] : 0.0,
+    expand_node<true>(tables, k, ctl, valid, valid ? in.d[i] : 0, valid ? in.t[i] : 0.0, valid ? in.num[i] : 0.0,
                 valid ? in.den[i] : 0.0, valid ? in.last[i] : 0, valid ? in.code[i] : 0ull, out, fin, cap_out,
-                cap_final);
+                cap_final, thr, feas, fuse_batch);
   }
 }
 
@@ -527,11 +726,12 @@ constexpr int kSeedRounds = BS_SEED_ROUNDS;
 // zeroed by the host before this launch.
 __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
                                                                const DWaiting* W, const DRunning* R, DTables* tables,
-                                                               ExCtl* ctl, int n, const DFastPair* fg, Key128* best,
+                                                               DThr* thr, ExCtl* ctl, int n, const DFastPair* fg,
+                                                               Key128* best,
                                                                unsigned long long* feas, Frontier L2, Frontier L3,
                                                                FinalList fin, unsigned long long cap_level,
                                                                unsigned long long cap_final, double sweep3_min,
-                                                               DSlice sl) {
+                                                               DSlice sl, int* thr_list) {
   __shared__ int s_status;
   const int d = blockIdx.x;
   if (d >= n) return;
@@ -561,6 +761,10 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   if (threadIdx.x == 0) {
     T->FD = FD;
     T->nc_magic = nc > 1 ? 0xffffffffu / static_cast<unsigned>(nc) + 1u : 0u;
+    T->fuse = 0;
+    T->thr_ok = 0;
+    T->nb_beta = INFINITY;
+    T->nb_R = INFINITY;
   }
   // A slice whose leading digits lie below the first list this kernel
   // writes (trees of at most 3 levels, or shallow final depths): every leaf
@@ -660,6 +864,38 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       best[d].obj = ko;
       best[d].code = kc;
     }
+    // the seed's node bound over the two bottom levels (node_dom_seed), one
+    // warp: lane x takes candidate x of each level
+    const double thr_s = __longlong_as_double(static_cast<long long>(ko));
+    if (threadIdx.x < 32 && K >= 3 && T->sorted_ok && T->filter_ok && ko != ~0ull && thr_s >= kFilterMinBest &&
+        thr_s < INFINITY) {
+      const double beta = __dmul_rn(thr_s, 1.0 + 0x1p-47);
+      double qs = 0.0, mag = 0.0;
+      for (int k = K - 2; k < K; ++k) {
+        const int x = threadIdx.x;
+        double q = INFINITY, emax = 0.0, amax = 0.0;
+        if (x < nc) {
+          q = __dsub_rn(T->E[k][x], __dmul_rn(beta, T->A[k][x]));
+          emax = T->E[k][x];
+          amax = T->A[k][x];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // min / max are exact in any order
+          const double q2 = __shfl_xor_sync(0xffffffffu, q, o), e2 = __shfl_xor_sync(0xffffffffu, emax, o),
+                       a2 = __shfl_xor_sync(0xffffffffu, amax, o);
+          q = q2 < q ? q2 : q;
+          emax = e2 > emax ? e2 : emax;
+          amax = a2 > amax ? a2 : amax;
+        }
+        qs = __dadd_rn(qs, q);
+        mag = __dadd_rn(mag, __dadd_rn(emax, __dmul_rn(beta, amax)));
+      }
+      if (threadIdx.x == 0) {
+        const double R = __dadd_rn(-qs, __dmul_rn(mag, 0x1p-44));
+        T->nb_beta = beta;
+        T->nb_R = R > 0.0 ? R : 0.0;
+      }
+    }
   }
   if (FD == 0) {
     if (threadIdx.x == 0) {
@@ -675,6 +911,8 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   }
   const int D0 = FD < 2 ? FD : 2;
   const int width = D0 == 1 ? nc : nc * nc;
+  if (threadIdx.x == 0) T->n_ok3 = 0;
+  __syncthreads();
   const bool to_final = D0 == FD;
   for (int base = 0; base < width; base += blockDim.x) {  // uniform trip count: block_append2 needs every thread
     const int e = base + threadIdx.x;
@@ -698,8 +936,10 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       if (ok && to_final && T->sorted_ok && FD < K) ok = feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
     }
     if (FD > 2) {  // one more level here: the depth-2 nodes never reach global memory (FD is uniform per CTA)
-      expand_node(tables, 2, ctl, ok, d, t, num, den, last, static_cast<unsigned long long>(e), L3, fin, cap_level,
-                  cap_final);
+      const unsigned m3 = expand_node<false>(tables, 2, ctl, ok, d, t, num, den, last,
+                                             static_cast<unsigned long long>(e), L3, fin, cap_level, cap_final, thr,
+                                             feas);
+      if (m3) atomicAdd(&T->n_ok3, static_cast<int>(m3));  // feasible depth-3 prefixes (looseness, thr_kernel)
       continue;
     }
     unsigned long long sf, so;
@@ -724,6 +964,53 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       }
     }
   }
+  // Loose trees (more than 98 % of the depth-3 prefixes feasible: every
+  // decision of the 1200 ms C2 corpus, almost none of the 600 ms one, whose
+  // decisions are 0-68 % feasible at depth 3) are candidates for the BFS to
+  // settle the final nodes the seed's node bound dominates (thr_kernel
+  // decides for the whole batch).
+  //
+  // Leaf-count thresholds of the two bottom levels (build_thresholds) for
+  // the decisions that use them:
+  //  * three swept levels: the sweep counts a dominated child's leaves with
+  //    three binary searches;
+  //  * loose decisions with two swept levels: the BFS settles their dominated
+  //    final nodes when at least 10 % of the batch is loose (measured at C2
+  //    TTFT 1200 ms: 92 % of the final nodes; step 7.9 -> 1.9 ms).
+  __syncthreads();
+  const bool loose = FD >= 4 && FD == K - 2 && 50ll * T->n_ok3 > 49ll * nc * nc * nc;
+  if (threadIdx.x == 0 && K >= 3 && FD >= 1 && T->sorted_ok && T->filter_ok && sl.digits <= (FD < 2 ? FD : 2) &&
+      (K - FD == 3 || loose)) {  // listed for thr_kernel
+    if (loose) {
+      T->fuse = 1;
+      atomicAdd(&ctl->n_loose, 1ull);
+    }
+    thr_list[atomicAdd(&ctl->n_thr, 1ull)] = d;
+  }
+}
+
+// The thresholds of the listed decisions (prepare_kernel), a few CTAs per SM
+// taking list entries in turn: a batch that lists none (the 600 ms C2
+// corpus) costs one short launch; loose two-level decisions are built only
+// when at least 10 % of the batch is loose (measured at C2 TTFT 1200 ms: the
+// BFS then settles 92 % of the final nodes, step 7.9 -> 1.9 ms), since one
+// build is a ~10 us chain of dependent steps a batch with only a few loose
+// decisions would pay without gaining it back.
+__global__ void __launch_bounds__(kPrepThreads) thr_kernel(DTables* tables, DThr* thr, const ExCtl* ctl,
+                                                           const int* thr_list, int n) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // prepare_kernel's tables and list
+  const unsigned long long n_thr = ctl->n_thr;
+  const bool fuse_batch = 10ull * ctl->n_loose >= static_cast<unsigned long long>(n);
+  for (unsigned long long i = blockIdx.x; i < n_thr; i += gridDim.x) {
+    DTables* T = &tables[thr_list[i]];
+    const bool use = T->K - T->FD == 3 || fuse_batch;  // uniform per CTA
+    if (!use) {
+      if (threadIdx.x == 0) T->fuse = 0;
+      continue;
+    }
+    build_thresholds(T, &thr[thr_list[i]]);
+    if (threadIdx.x == 0) T->thr_ok = 1;
+  }
 }
 
 // Resident CTAs per SM the sweep is register-budgeted for: 3 (80 registers)
@@ -739,7 +1026,7 @@ struct LeafAcc {
   double thr_scaled;         // fl(min(local, global hint) * C), +inf disables the filter
   unsigned long long count;  // feasible leaves
 #ifdef BS_SWEEP_STATS
-  unsigned long long st_rows, st_leaves, st_div, st_children;
+  unsigned long long st_rows, st_leaves, st_div, st_children, st_thr, st_slow;
 #endif
   // leaf-row skip ("row bound"): a row of leaves under a parent
   // with (num, den) is provably worse than thr when
@@ -747,6 +1034,7 @@ struct LeafAcc {
   // beta = fl(thr * (1 + 2^-47)), s_last >= amax * (beta - pmin (1 - u))^+.
   double beta;
   double s_last;
+  double s_node;  // >= the two bottom levels' slack: a node at depth K-2 is dominated (node_dominated)
 };
 
 // (the last level's amax / pmin_lo are re-read from the tables: fewer live registers)
@@ -759,9 +1047,13 @@ __device__ __forceinline__ void set_threshold(LeafAcc& a, double hint, const DTa
     const int kl = T->K - 1;
     const double gap = __dsub_rn(a.beta, T->pmin_lo[kl]);
     a.s_last = gap > 0.0 ? __dmul_rn(__dmul_rn(gap, T->amax[kl]), 1.0 + 0x1p-40) : 0.0;
+    const double gap2 = kl >= 1 ? __dsub_rn(a.beta, T->pmin_lo[kl - 1]) : 0.0;
+    const double s2 = gap2 > 0.0 ? __dmul_rn(__dmul_rn(gap2, T->amax[kl - 1]), 1.0 + 0x1p-40) : 0.0;
+    a.s_node = __dmul_rn(__dadd_rn(s2, a.s_last), 1.0 + 0x1p-40);
   } else {
     a.beta = INFINITY;
     a.s_last = INFINITY;
+    a.s_node = INFINITY;
   }
 }
 
@@ -770,6 +1062,18 @@ __device__ __forceinline__ void set_threshold(LeafAcc& a, double hint, const DTa
 // den >= 2^-900).
 __device__ __forceinline__ bool row_dominated(const LeafAcc& a, double num, double den) {
   return __dsub_rn(num, __dmul_rn(a.beta, den)) > __dadd_rn(a.s_last, __dmul_rn(num, 0x1p-40));
+}
+
+// True when every leaf below a node at depth K-2 with (num, den) is provably
+// worse than the current threshold ("node bound"): with
+// thr' = thr (1 + 2^-50) <= beta, a leaf's rounded objective exceeds thr when
+// num + E_g + E_f > thr' (den + A_g + A_f), and E_x - thr' A_x >= -amax (thr' -
+// pmin (1 - u))^+ per level (A >= 0, E = fl(A P)), so num - thr' den > s_K-2 +
+// s_K-1 suffices; the test below is that inequality with its rounding margin
+// (num 2^-40, s_node inflated by 2^-40).  Preconditions as the leaf filter:
+// filter_ok tables, den >= 2^-900, thr >= 2^-100.
+__device__ __forceinline__ bool node_dominated(const LeafAcc& a, double num, double den) {
+  return den >= kFilterMinDen && __dsub_rn(num, __dmul_rn(a.beta, den)) > __dadd_rn(a.s_node, __dmul_rn(num, 0x1p-40));
 }
 
 // Last level k = K-1 for one parent state: every f in 0..nc-1, in order.
@@ -1016,9 +1320,10 @@ __device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsig
 
 // One thread per final node: the I bottom levels of its subtree.
 template <int MINB>
-__global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restrict__ tables, const ExCtl* ctl,
-                                                    FinalList fin, Key128* best, unsigned long long* feas,
-                                                    unsigned long long cap_final) {
+__global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restrict__ tables,
+                                                          const DThr* __restrict__ thr, const ExCtl* ctl,
+                                                          FinalList fin, Key128* best, unsigned long long* feas,
+                                                          unsigned long long cap_final) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the BFS lists (programmatic dependent launch)
   if (ctl->overflow) return;  // the run is repeated with larger lists (one_shot): skip the sweep
   const unsigned long long n_fin = ctl->final_count < cap_final ? ctl->final_count : cap_final;
@@ -1051,18 +1356,35 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
     a.code = ~0ull;
     a.count = 0;
 #ifdef BS_SWEEP_STATS
-    a.st_rows = a.st_leaves = a.st_div = a.st_children = 0;
+    a.st_rows = a.st_leaves = a.st_div = a.st_children = a.st_thr = a.st_slow = 0;
 #endif
     set_threshold(a, hint, T);
     const unsigned long long cb = code * static_cast<unsigned long long>(nc);
     if (I == 1) {  // K == 1
       sweep_last(T, FD, nc, t, num, den, last, cb, false, hint, a);
     } else if (T->sorted_ok) {
+      // a node at depth K-2 whose leaves are all provably worse than the
+      // threshold only needs its feasible-leaf count: three binary searches
+      const bool use_thr = T->thr_ok != 0;
+      const DThr* __restrict__ H = thr + d;
       if (I == 2) {
+#ifdef BS_SWEEP_STATS
+        a.st_slow += 1;
+#endif
         two_sorted(T, FD, nc, t, num, den, last, cb, hint, a);
-      } else {
+      } else if (MINB == kSweepMinB3) {  // three swept levels only occur in batches launched with MINB 4
         for_feasible_children(T, FD, nc, t, num, den, last, [&](int e, double t3, double n3, double d3) {
-          two_sorted(T, FD + 1, nc, t3, n3, d3, e, (cb + static_cast<unsigned long long>(e)) * nc, hint, a);
+          if (use_thr && (node_dom_seed(T, n3, d3) || node_dominated(a, n3, d3))) {
+            a.count += static_cast<unsigned long long>(thr_leaf_count(H, nc, t3, e));
+#ifdef BS_SWEEP_STATS
+            a.st_thr += 1;
+#endif
+          } else {
+#ifdef BS_SWEEP_STATS
+            a.st_slow += 1;
+#endif
+            two_sorted(T, FD + 1, nc, t3, n3, d3, e, (cb + static_cast<unsigned long long>(e)) * nc, hint, a);
+          }
         });
       }
     } else {
@@ -1089,6 +1411,8 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
     atomicAdd(&wctl->st_rows_eval, a.st_rows);
     atomicAdd(&wctl->st_leaves_eval, a.st_leaves);
     atomicAdd(&wctl->st_div, a.st_div);
+    atomicAdd(&wctl->st_thr_nodes, a.st_thr);
+    atomicAdd(&wctl->st_slow_nodes, a.st_slow);
 #endif
   }
 }

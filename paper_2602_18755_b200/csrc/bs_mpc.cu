@@ -245,6 +245,8 @@ struct MpcRun {
   unsigned long long cap_level = 0;  // BFS list capacity (per ping-pong buffer)
   unsigned long long cap_final = 0;  // final list capacity
   DTables* dT = nullptr;
+  DThr* dThr = nullptr;  // leaf-count thresholds per decision (exhaustive)
+  int* dThrList = nullptr;  // decisions that need them (prepare_kernel -> thr_kernel)
   ExCtl* dCtl = nullptr;
   Key128* dBest = nullptr;
   unsigned long long* dFeas = nullptr;
@@ -271,7 +273,7 @@ size_t levels_bytes(int n, int stride) { return sizeof(DLevel) * static_cast<siz
 
 // Device scratch layout of an exhaustive run (offsets from one base).
 struct ExLayout {
-  size_t tables = 0, ctl = 0, best = 0, lev0 = 0, lev1 = 0, fin = 0, out = 0, total = 0;
+  size_t tables = 0, thr = 0, thr_list = 0, ctl = 0, best = 0, lev0 = 0, lev1 = 0, fin = 0, out = 0, total = 0;
 };
 
 ExLayout ex_layout(const MpcRun& r, size_t start) {
@@ -279,6 +281,10 @@ ExLayout ex_layout(const MpcRun& r, size_t start) {
   size_t o = start;
   L.tables = o;
   o += up256(tables_bytes(r.n));
+  L.thr = o;
+  o += up256(sizeof(DThr) * static_cast<size_t>(r.n));
+  L.thr_list = o;
+  o += up256(4ull * static_cast<size_t>(r.n));
   L.ctl = o;
   o += up256(sizeof(ExCtl));
   L.best = o;
@@ -297,6 +303,8 @@ ExLayout ex_layout(const MpcRun& r, size_t start) {
 
 void bind_exhaustive(MpcRun* r, char* base, const ExLayout& L) {
   r->dT = reinterpret_cast<DTables*>(base + L.tables);
+  r->dThr = reinterpret_cast<DThr*>(base + L.thr);
+  r->dThrList = reinterpret_cast<int*>(base + L.thr_list);
   r->dCtl = reinterpret_cast<ExCtl*>(base + L.ctl);
   r->dBest = reinterpret_cast<Key128*>(base + L.best);
   r->dFeas = reinterpret_cast<unsigned long long*>(r->dBest + r->n);
@@ -466,12 +474,17 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   const FinalList fin = final_at(run->dFin, run->cap_final);
   BS_CUDA_TRY(ctx, cudaMemsetAsync(run->dCtl, 0, sizeof(ExCtl), ctx->stream));
   prepare_kernel<<<n, kPrepThreads, 0, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
-                                                      run->dT, run->dCtl, n, run->dFG, run->dBest, run->dFeas, lev[0],
+                                                      run->dT, run->dThr, run->dCtl, n, run->dFG, run->dBest,
+                                                      run->dFeas, lev[0],
                                                       lev[1], fin, run->cap_level, run->cap_final,
-                                                      run->sweep3_min, run->slice);
+                                                      run->sweep3_min, run->slice, run->dThrList);
   BS_LAUNCH_CHECK(ctx);
   BS_REC(1);
-  BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel
+  BS_CUDA_TRY(ctx, launch_pdl(thr_kernel, dim3(2 * ctx->sm_count), dim3(kPrepThreads), ctx->stream, run->dT,
+                              run->dThr, static_cast<const ExCtl*>(run->dCtl), static_cast<const int*>(run->dThrList),
+                              n));
+  BS_LAUNCH_CHECK(ctx);
+  BS_REC(2);  // the roots and first two levels are expanded by prepare_kernel; thresholds by thr_kernel
   // The kernels after prepare are launched as programmatic dependents: each
   // may be scheduled while its predecessor drains and waits for it in
   // griddepcontrol.wait before touching its data (phase events, when
@@ -479,18 +492,18 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   for (int k = 3; k < run->bfs_levels; ++k) {  // depths up to 3 come from prepare_kernel
     BS_CUDA_TRY(ctx, launch_pdl(bfs_node_kernel, dim3(run->bfs_grid), dim3(256), ctx->stream,
                                 static_cast<const DTables*>(run->dT), k, run->dCtl, lev[k & 1], lev[(k + 1) & 1], fin,
-                                run->cap_level, run->cap_final));
+                                run->cap_level, run->cap_final, static_cast<const DThr*>(run->dThr), run->dFeas, n));
     BS_LAUNCH_CHECK(ctx);
   }
   BS_REC(3);
   if (run->sweep3)
     BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB3>, dim3(run->sweep_grid3), dim3(256), ctx->stream,
-                                static_cast<const DTables*>(run->dT), static_cast<const ExCtl*>(run->dCtl), fin,
-                                run->dBest, run->dFeas, run->cap_final));
+                                static_cast<const DTables*>(run->dT), static_cast<const DThr*>(run->dThr),
+                                static_cast<const ExCtl*>(run->dCtl), fin, run->dBest, run->dFeas, run->cap_final));
   else
     BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB2>, dim3(run->sweep_grid2), dim3(256), ctx->stream,
-                                static_cast<const DTables*>(run->dT), static_cast<const ExCtl*>(run->dCtl), fin,
-                                run->dBest, run->dFeas, run->cap_final));
+                                static_cast<const DTables*>(run->dT), static_cast<const DThr*>(run->dThr),
+                                static_cast<const ExCtl*>(run->dCtl), fin, run->dBest, run->dFeas, run->cap_final));
   BS_LAUNCH_CHECK(ctx);
   BS_REC(4);
   BS_CUDA_TRY(ctx, launch_pdl(finalize_kernel, dim3((n + 127) / 128), dim3(128), ctx->stream,
@@ -796,8 +809,10 @@ int bs_mpc_plan_results(bs_ctx_t ctx, bs_mpc_plan_t plan, bs_mpc_result* out) {
         if (c.level_count[k]) std::fprintf(stderr, " depth%d=%llu", k, c.level_count[k]);
       std::fprintf(stderr, " final=%llu overflow=%llu\n", c.final_count, c.overflow);
 #ifdef BS_SWEEP_STATS
-      std::fprintf(stderr, "bs_mpc sweep: nodes %llu children %llu rows evaluated %llu leaves %llu divisions %llu\n",
-                   c.st_nodes, c.st_children, c.st_rows_eval, c.st_leaves_eval, c.st_div);
+      std::fprintf(stderr, "bs_mpc sweep: nodes %llu children %llu rows evaluated %llu leaves %llu divisions %llu "
+                   "depth-(K-2) nodes counted by thresholds %llu / walked %llu\n",
+                   c.st_nodes, c.st_children, c.st_rows_eval, c.st_leaves_eval, c.st_div, c.st_thr_nodes,
+                   c.st_slow_nodes);
 #endif
     }
   }
