@@ -118,10 +118,13 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
   unsigned long long pw[kMaxK + 1];
   pw[0] = 1;
   for (int i = 0; i < np; ++i) pw[i + 1] = pw[i] * static_cast<unsigned long long>(base);
-  unsigned long long rem = prefix;
+  // prefix < base^J <= 3^16 < 2^32: 32-bit digit extraction, division by the
+  // constant 3 (a multiply-high) or a shift
+  unsigned rem = static_cast<unsigned>(prefix);
   for (int i = 0; i < J; ++i) {
-    dig[i] = static_cast<int>(rem % base);
-    rem /= base;
+    const unsigned q = base == 3 ? rem / 3u : rem >> 1;
+    dig[i] = static_cast<int>(rem - q * static_cast<unsigned>(base));
+    rem = q;
   }
   // walk k = 0 .. (J < np ? pos[J] - 1 : K - 1) with the prefix applied
   double t = pr.now, num = 0.0, den = 0.0;
@@ -195,18 +198,35 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
   }
 }
 
-// greedy_freq_select for one decision by the calling warp (all 32 lanes).
+// greedy_freq_select for one decision by NW cooperating warps: the calling
+// warp (NW == 1: any warp of a CTA running several decisions) or the whole
+// CTA (NW > 1, blockDim.x == 32 NW: one decision per CTA, for batches too
+// small to fill the GPU one warp per decision -- latency of a single
+// controller call).  Same results for every NW: each mutation is evaluated
+// with the same op sequence; the level's (objective, lexicographic) minimum,
+// feasible count and first ModelError are exact reductions.
 // fl / fp: the controller's latency / power grids reduced per candidate
 // (FastGrid), or null for the generic interpolator.  lv (optional): level
-// stats.  Results in *o (lane 0 writes; the warp is synchronised on return).
+// stats.  Results in *o (thread 0 writes; the group is synchronised on return).
 //   share: every fl[f] (and every fp[f]) has the brackets of fl[0] (fp[0])
 //   (fast_same_brackets), so each batch is bracketed once for all candidates.
-__device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
+template <int NW>
+__device__ __forceinline__ void greedy_sync() {
+  if (NW == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+template <int NW>
+__device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
                             const DRunning* R, WGreedyShared& S, DMpcOut* o, DLevel* lv, const FastGrid* fl,
                             const FastGrid* fp, bool share = false) {
+  constexpr int NT = 32 * NW;
   const int lane = threadIdx.x & 31;
+  const int tid = NW == 1 ? lane : static_cast<int>(threadIdx.x);
   WTables& T = S.T;
-  if (lane == 0) {
+  if (tid == 0) {
     T.nc = c.nc;
     T.ttft = c.ttft;
     int st = project_dev(pr, c, W, R, &T);
@@ -217,24 +237,24 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
     o->status = st;
     o->K = T.K;
   }
-  __syncwarp();
+  greedy_sync<NW>();
   if (T.status != BS_OK) return;
   const int K = T.K, nc = c.nc;
   if (K == 0) {  // dvfs.hpp:194-197
-    if (lane == 0) o->feasible = 1;
-    __syncwarp();
+    if (tid == 0) o->feasible = 1;
+    greedy_sync<NW>();
     return;
   }
   unsigned anybad = 0;
   const bool shared_brk = fl && share;
   if (shared_brk) {
-    if (lane < K) {
-      fast_brackets(fl[0], T.n_req[lane], T.sum_len[lane], S.blat[lane]);
-      fast_brackets(fp[0], T.n_req[lane], T.sum_len[lane], S.bpow[lane]);
+    if (tid < K) {
+      fast_brackets(fl[0], T.n_req[tid], T.sum_len[tid], S.blat[tid]);
+      fast_brackets(fp[0], T.n_req[tid], T.sum_len[tid], S.bpow[tid]);
     }
-    __syncwarp();
+    greedy_sync<NW>();
   }
-  for (int e = lane; e < K * nc; e += 32) {
+  for (int e = tid; e < K * nc; e += NT) {
     const int k = e / nc, f = e - k * nc;
     double L, P;
     if (shared_brk) {
@@ -264,10 +284,15 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
     T.B1[e] = __dmul_rn(__dadd_rn(A, c.switch_ms), c.one_plus_margin);      // dvfs.hpp:114-115
     if (k == 0) T.T1[f] = __dadd_rn(pr.now, c.cand[f] != pr.cur_freq ? T.B1[e] : T.B0[e]);
   }
-  const bool bad = __any_sync(0xffffffffu, anybad);
-  __syncwarp();
+  bool bad;
+  if (NW == 1) {
+    bad = __any_sync(0xffffffffu, anybad);
+    __syncwarp();
+  } else {
+    bad = __syncthreads_or(anybad) != 0;
+  }
   // all-max initialization (dvfs.hpp:201-205)
-  if (lane == 0) {
+  if (tid == 0) {
     for (int k = 0; k < K; ++k) S.cur[k] = static_cast<unsigned char>(nc - 1);
     double obj = 0.0;
     int err;
@@ -291,7 +316,7 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
     o->eval_count = 1;
     o->objective = obj;
   }
-  __syncwarp();
+  greedy_sync<NW>();
   if (o->status != BS_OK) return;
   if (S.accepted && nc > 1) {
     const int last_level = nc >= 3 ? nc - 2 : 1;
@@ -300,33 +325,36 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
       const int r1 = nc - 1 - l;  // avail[l]
       const int r2 = l + 1 < nc ? nc - 2 - l : -1;
       const int base = r2 >= 0 ? 3 : 2;
-      const unsigned pm = __ballot_sync(0xffffffffu, lane < K && S.cur[lane] == target);
-      const int np = __popc(pm);
-      if (np == 0) break;  // dvfs.hpp:222
-      if (lane == 0) {
-        unsigned mm = pm;
-        for (int i = 0; i < np; ++i) {
-          S.pos[i] = __ffs(mm) - 1;
-          mm &= mm - 1;
+      if (threadIdx.x < 32 || NW == 1) {  // positions holding the target (warp 0; every warp when NW == 1)
+        const unsigned pm = __ballot_sync(0xffffffffu, lane < K && S.cur[lane] == target);
+        if (lane == 0) {
+          S.np = __popc(pm);
+          unsigned mm = pm;
+          for (int i = 0; mm; ++i) {
+            S.pos[i] = __ffs(mm) - 1;
+            mm &= mm - 1;
+          }
         }
       }
-      __syncwarp();
+      greedy_sync<NW>();
+      const int np = S.np;
+      if (np == 0) break;  // dvfs.hpp:222
       const unsigned long long combos = ipow(static_cast<unsigned long long>(base), np);
       unsigned long long bo = ~0ull, bc = ~0ull, feas = 0, errkey = ~0ull;
       if (!bad) {
         // prefixes of the first J digits spread over lanes
         int J = 0;
         unsigned long long tasks = 1;
-        while (J < np && tasks < 64) {
+        while (J < np && tasks < 2ull * NT) {
           tasks *= base;
           ++J;
         }
-        for (unsigned long long p = lane; p < tasks; p += 32)
+        for (unsigned long long p = tid; p < tasks; p += NT)
           wlevel_dfs(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, p, bo, bc, feas);
       } else {
         unsigned char mut[kMaxK];
         for (int k = 0; k < K; ++k) mut[k] = S.cur[k];
-        for (unsigned long long code = 1 + lane; code < combos; code += 32) {
+        for (unsigned long long code = 1 + tid; code < combos; code += NT) {
           unsigned long long cc = code, lex = 0;
           for (int i = 0; i < np; ++i) {  // digit i -> pos[i], least significant first (dvfs.hpp:233-237)
             const unsigned long long digit = cc % base;
@@ -367,7 +395,27 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
         const unsigned long long oe = __shfl_xor_sync(0xffffffffu, errkey, of);
         errkey = oe < errkey ? oe : errkey;
       }
-      if (lane == 0) {
+      if constexpr (NW > 1) {  // across the CTA's warps
+        __shared__ unsigned long long r_bo[NW], r_bc[NW], r_feas[NW], r_err[NW];
+        const int w = threadIdx.x >> 5;
+        if (lane == 0) {
+          r_bo[w] = bo;
+          r_bc[w] = bc;
+          r_feas[w] = feas;
+          r_err[w] = errkey;
+        }
+        __syncthreads();
+        if (tid == 0)
+          for (int v = 1; v < NW; ++v) {
+            if (key_less(r_bo[v], r_bc[v], bo, bc)) {
+              bo = r_bo[v];
+              bc = r_bc[v];
+            }
+            feas += r_feas[v];
+            errkey = r_err[v] < errkey ? r_err[v] : errkey;
+          }
+      }
+      if (tid == 0) {
         o->eval_count += static_cast<long long>(combos - 1);  // every mutation counts (dvfs.hpp:238)
         DLevel Lv;
         Lv.k_prime = np;
@@ -396,11 +444,18 @@ __device__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg&
         }
         S.accepted = Lv.accepted;
       }
-      __syncwarp();
+      greedy_sync<NW>();
       if (o->status != BS_OK || S.accepted == 0) break;
     }
   }
-  if (lane == 0 && o->status == BS_OK)
+  if (tid == 0 && o->status == BS_OK)
     for (int k = 0; k < K; ++k) o->idx[k] = S.cur[k];
-  __syncwarp();
+  greedy_sync<NW>();
+}
+
+// One decision per warp (the batch kernels and the cluster replay).
+__device__ __forceinline__ void greedy_warp(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
+                                            const DRunning* R, WGreedyShared& S, DMpcOut* o, DLevel* lv,
+                                            const FastGrid* fl, const FastGrid* fp, bool share = false) {
+  greedy_coop<1>(m, pr, c, W, R, S, o, lv, fl, fp, share);
 }

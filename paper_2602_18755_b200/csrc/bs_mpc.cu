@@ -131,6 +131,31 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) greedy_kernel(DModels m, co
   if (lane == 0) out[d] = *o;
 }
 
+// One decision per CTA of NW warps (greedy_coop): batches too small to fill
+// the GPU one warp per decision give each decision more warps, down to a
+// single controller call (n = 1) spread over 16 warps.
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) greedy_coop_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs,
+                                                             const DWaiting* W, const DRunning* R, DMpcOut* out,
+                                                             DLevel* levels, int n, int max_h, int max_nc,
+                                                             const DFastPair* fg, int lv_stride) {
+  extern __shared__ __align__(16) unsigned char gdsm[];
+  const int d = blockIdx.x;
+  if (d >= n) return;
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  WGreedyShared& S = *reinterpret_cast<WGreedyShared*>(gdsm);
+  DMpcOut* o = reinterpret_cast<DMpcOut*>(gdsm + a16(sizeof(WGreedyShared)));
+  double* tab = reinterpret_cast<double*>(gdsm + a16(sizeof(WGreedyShared)) + a16(sizeof(DMpcOut)));
+  const DProblem pr = probs[d];
+  const DMpcCfg& c = cfgs[pr.cfg];
+  if (threadIdx.x == 0) wtables_bind(S.T, tab, c.horizon, c.nc);
+  __syncthreads();
+  const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
+  greedy_coop<NW>(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o, levels + static_cast<size_t>(d) * lv_stride,
+                  fp ? fp->lat : nullptr, fp ? fp->pw : nullptr, fp && fp->share);
+  if (threadIdx.x == 0) out[d] = *o;
+}
+
 // ---------------------------------------------------------------------------
 // parity probes
 // ---------------------------------------------------------------------------
@@ -263,6 +288,7 @@ struct MpcRun {
   std::vector<DFastPair> hFG;           // their host build
   cudaEvent_t ev[kNumEvents] = {};
   bool have_events = false;
+  bool contig = false;  // dLv = dOut + levels_off(n) (greedy one-shot)
 };
 
 size_t up256(size_t x) { return (x + 255) / 256 * 256; }
@@ -270,6 +296,9 @@ size_t tables_bytes(int n) { return sizeof(DTables) * static_cast<size_t>(n); }
 size_t best_bytes(int n) { return (sizeof(Key128) + 8ull) * static_cast<size_t>(n); }
 size_t out_bytes(int n) { return sizeof(DMpcOut) * static_cast<size_t>(n); }
 size_t levels_bytes(int n, int stride) { return sizeof(DLevel) * static_cast<size_t>(stride) * static_cast<size_t>(n); }
+// greedy one-shot results: [out | overflow flag | levels], device and host alike
+size_t levels_off(int n) { return (out_bytes(n) + 64 + 255) / 256 * 256; }
+size_t result_region(int n, int stride) { return levels_off(n) + levels_bytes(n, stride); }
 
 // Device scratch layout of an exhaustive run (offsets from one base).
 struct ExLayout {
@@ -450,12 +479,43 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   }
   BS_REC(0);
   if (run->mode == kGreedy) {
-    const size_t smem = kGreedyWarps * greedy_warp_bytes(pk.max_horizon, pk.max_nc);
-    BS_CUDA_TRY(ctx, cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-    greedy_kernel<<<(n + kGreedyWarps - 1) / kGreedyWarps, kGreedyWarps * 32, smem, ctx->stream>>>(
-        models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running, run->dOut, run->dLv, n, pk.max_horizon,
-        pk.max_nc, run->dFG, run->lv_stride);
+    // warps per decision: one, unless the batch leaves the GPU's warp slots
+    // (16 per SM here) idle -- then up to 16 per decision (one per CTA)
+    const long long slots = 16ll * ctx->sm_count;
+    int nw = 1;
+    while (nw < 16 && static_cast<long long>(n) * nw * 2 <= slots) nw *= 2;
+    const size_t one = greedy_warp_bytes(pk.max_horizon, pk.max_nc);
+    if (nw == 1) {
+      const size_t smem = kGreedyWarps * one;
+      if (smem > ctx->greedy_smem[0]) {
+        BS_CUDA_TRY(ctx, cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem)));
+        ctx->greedy_smem[0] = smem;
+      }
+      greedy_kernel<<<(n + kGreedyWarps - 1) / kGreedyWarps, kGreedyWarps * 32, smem, ctx->stream>>>(
+          models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running, run->dOut, run->dLv, n, pk.max_horizon,
+          pk.max_nc, run->dFG, run->lv_stride);
+    } else {
+      auto go = [&](auto kernel, int slot) -> int {
+        if (one > ctx->greedy_smem[slot]) {
+          BS_CUDA_TRY(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(one)));
+          ctx->greedy_smem[slot] = one;
+        }
+        kernel<<<n, 32 * nw, one, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting, pk.running,
+                                                 run->dOut, run->dLv, n, pk.max_horizon, pk.max_nc, run->dFG,
+                                                 run->lv_stride);
+        return BS_OK;
+      };
+      int rc = BS_OK;
+      switch (nw) {
+        case 2: rc = go(greedy_coop_kernel<2>, 1); break;
+        case 4: rc = go(greedy_coop_kernel<4>, 2); break;
+        case 8: rc = go(greedy_coop_kernel<8>, 3); break;
+        default: rc = go(greedy_coop_kernel<16>, 4); break;
+      }
+      if (rc) return rc;
+    }
     BS_LAUNCH_CHECK(ctx);
     BS_REC(1);
     return BS_OK;
@@ -534,15 +594,14 @@ static_assert(BS_RESULT_SLICES_MAX >= 1 && BS_RESULT_SLICES_MAX <= 4, "bs_ctx_s:
 int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
   const int n = run->n;
   if (n == 0) return BS_OK;
-  DMpcOut* hOut = static_cast<DMpcOut*>(ctx->host_buf(kSlotOut, out_bytes(n) + 64));
+  const int stride = run->lv_stride;
+  DMpcOut* hOut = static_cast<DMpcOut*>(ctx->host_buf(kSlotOut, result_region(n, stride)));
   DLevel* hLv = nullptr;
   if (!hOut) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
   unsigned long long* hOverflow = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(hOut) + out_bytes(n));
   *hOverflow = 0;
-  const int stride = run->lv_stride;
   if (run->mode == kGreedy) {
-    hLv = static_cast<DLevel*>(ctx->host_buf(kSlotLevels, levels_bytes(n, stride)));
-    if (!hLv) return set_error(ctx, BS_CUDA_ERROR, "mpc: host allocation failed");
+    hLv = reinterpret_cast<DLevel*>(reinterpret_cast<char*>(hOut) + levels_off(n));
   } else {  // the overflow flag first: it is checked before any slice is expanded
     BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOverflow, &run->dCtl->overflow, 8, cudaMemcpyDeviceToHost, ctx->stream));
   }
@@ -553,6 +612,11 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
       if (!ctx->slice_ev[sl]) BS_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->slice_ev[sl], cudaEventDisableTiming));
   for (int sl = 0; sl < n_slices; ++sl) {
     const int lo = slice_lo(sl), hi = slice_lo(sl + 1);
+    if (hLv && run->contig && n_slices == 1) {  // results, flag and level records in one copy
+      BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut, run->dOut, result_region(n, stride), cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+      break;
+    }
     BS_CUDA_TRY(ctx, cudaMemcpyAsync(hOut + lo, run->dOut + lo, out_bytes(hi - lo), cudaMemcpyDeviceToHost,
                                      ctx->stream));
     if (hLv)
@@ -566,7 +630,7 @@ int run_results(bs_ctx_t ctx, MpcRun* run, bs_mpc_result* out) {
       BS_CUDA_TRY(ctx, cudaEventSynchronize(ctx->slice_ev[sl]));
     else
       BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    if (sl == 0 && *hOverflow) {
+    if (sl == 0 && run->mode == kExhaustive && *hOverflow) {
       BS_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
       BS_CUDA_TRY(ctx, cudaMemcpy(&run->ctl_host, run->dCtl, sizeof(ExCtl), cudaMemcpyDeviceToHost));
       return set_error(ctx, kOverflowStatus, "mpc exhaustive: %llu frontier appends exceeded the capacity of this "
@@ -605,9 +669,25 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
       DFastPair* dfg = static_cast<DFastPair*>(
           ctx->dev_buf(kSlotFastGrids, sizeof(DFastPair) * std::max<size_t>(run.pk.fg_pairs.size(), 1)));
       if (!dfg) return set_error(ctx, BS_CUDA_ERROR, "mpc: allocation of the reduced grids failed");
-      rc = upload_fast_pairs(ctx, models, &run, dfg);
-      if (rc) return rc;
-      ctx->last_h2d += sizeof(DFastPair) * run.pk.fg_pairs.size();
+      // the reduced grids depend only on (models, candidate rungs, tp) per pair:
+      // a call with the same pairs as the context's last upload (a controller
+      // deciding again) reuses them
+      std::string key(reinterpret_cast<const char*>(&models->serial), sizeof models->serial);
+      key.append(reinterpret_cast<const char*>(&dfg), sizeof dfg);
+      for (const auto& pr : run.pk.fg_pairs) {
+        const DMpcCfg& c = run.hc[pr.first];
+        key.append(reinterpret_cast<const char*>(&pr.second), sizeof pr.second);
+        key.append(reinterpret_cast<const char*>(&c.nc), sizeof c.nc);
+        key.append(reinterpret_cast<const char*>(c.cand), sizeof(double) * c.nc);
+      }
+      if (key != ctx->fg_key) {
+        rc = upload_fast_pairs(ctx, models, &run, dfg);
+        if (rc) return rc;
+        ctx->fg_key = key;
+        ctx->last_h2d += sizeof(DFastPair) * run.pk.fg_pairs.size();
+      } else {
+        run.dFG = run.pk.fg_pairs.empty() ? nullptr : dfg;
+      }
     }
     if (mode == kExhaustive) {
       const ExLayout L = ex_layout(run, 0);
@@ -615,9 +695,12 @@ int one_shot(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs, const 
       if (!base) return set_error(ctx, BS_CUDA_ERROR, "mpc exhaustive: device allocation of %zu bytes failed", L.total);
       bind_exhaustive(&run, base, L);
     } else {
-      run.dOut = static_cast<DMpcOut*>(ctx->dev_buf(kSlotOut, out_bytes(n)));
-      run.dLv = static_cast<DLevel*>(ctx->dev_buf(kSlotLevels, levels_bytes(n, run.lv_stride)));
-      if (!run.dOut || !run.dLv) return set_error(ctx, BS_CUDA_ERROR, "mpc greedy: allocation failed");
+      // results and level records in one region: one D2H copy for small batches
+      char* g = static_cast<char*>(ctx->dev_buf(kSlotOut, result_region(n, run.lv_stride)));
+      if (!g) return set_error(ctx, BS_CUDA_ERROR, "mpc greedy: allocation failed");
+      run.dOut = reinterpret_cast<DMpcOut*>(g);
+      run.dLv = reinterpret_cast<DLevel*>(g + levels_off(n));
+      run.contig = true;
     }
     const double t2 = dbg_t ? now_us() : 0.0;
     rc = run_enqueue(ctx, models, &run, false);

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <new>
 
+#include <atomic>
+
 #include "bs_internal.h"
 
 using namespace bs;
@@ -492,6 +494,8 @@ int bs_models_upload(bs_ctx_t ctx, const bs_model_set* m, bs_models_t* out) {
 
   std::vector<char> host(bytes, 0);
   bs_models_t mm = new (std::nothrow) bs_models_s();
+  static std::atomic<unsigned long long> serials{0};
+  if (mm) mm->serial = ++serials;
   if (!mm) return set_error(ctx, BS_CUDA_ERROR, "out of host memory");
   if (cudaMalloc(&mm->dmem, bytes) != cudaSuccess) {
     delete mm;
