@@ -70,9 +70,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU baseline sample duration")
     ap.add_argument("--no-extras", action="store_true", help="skip the C3/C4/C5 sub-benchmarks")
-    ap.add_argument("--only", choices=["c1", "c2l", "c3", "c4", "c4x", "c5g", "c5x"], default=None,
+    ap.add_argument("--only", choices=["c1", "c2l", "c3", "c4", "c4d", "c4x", "c5g", "c5x"], default=None,
                     help="run one sub-benchmark alone and print its JSON object")
     ap.add_argument("--c4-scenarios", type=int, default=1024)
+    ap.add_argument("--c4-day-scenarios", type=int, default=8, help="full-day C4 scenarios per rank")
     ap.add_argument("--c3-windows", type=int, default=24, help="1-hour windows in the C3 table stream")
     ap.add_argument("--c5x-decisions", type=int, default=4096)
     return ap.parse_args()
@@ -397,6 +398,90 @@ def bench_c4(dev, rank: int, world: int, local: int, n_scen: int, with_cpu: bool
                                "kind": "reference", "seconds": t_cpu,
                                "sample": f"first {m} scenarios: pdsim::simulate_cluster + trim_steady_state + "
                                          "make_report, one scenario per thread"}
+        out["identical_on_sample"] = bool(same)
+    return out
+
+
+def bench_c4_day(dev, rank: int, world: int, local: int, n_scen: int, with_cpu: bool) -> dict:
+    """configs[3] as configured, on a declared contiguous fraction of the
+    scenario set: full 24 h diurnal days (24 one-hour gamma(0.5) segments,
+    6 -> 20 rps) planned per 5-minute window (288 windows: config table from
+    the previous window, ILP, max-throughput baseline) and replayed with the
+    two-tier controllers -- run_experiment (runner.hpp:155-172) per scenario,
+    all scenarios' windows in four device calls (daysim.run_day_sweep).
+    Scenarios s = 0 .. n_scen - 1 of each rank (trace seed 1000 + global
+    index) at the SLO pair (600, 100) ms."""
+    from paper_2602_18755_b200 import daysim as Dy
+    from paper_2602_18755_b200 import pdsim as P
+    from paper_2602_18755_b200 import workloads as Wk
+
+    lad = Wk.ladder(8)
+    models = Wk.llama_models(lad)
+    cfg = P.RunnerConfig(slo=P.SLOSpec(600.0, 100.0), total_gpus=16, tp_options=[1, 2, 4, 8], ladder=lad,
+                         scheduler=P.SchedulerPolicy(max_batch_tokens=2048), rampup_s=30.0)
+    cfg.plan.policy = P.SchedulerPolicy(max_batch_tokens=2048)
+    first = rank * n_scen
+    t0 = time.perf_counter()
+    days = [Dy.gen_day(1000 + first + s) for s in range(n_scen)]
+    t_gen = time.perf_counter() - t0
+    Dy.run_day_sweep([Dy.DayTrace(days[0].requests[days[0].requests["arrival_ms"] < Dy.HOUR_MS], Dy.HOUR_MS)],
+                     300e3, cfg, models, dev)  # warm-up (one hour of one scenario)
+    _barrier(world)
+    t0 = time.perf_counter()
+    res = Dy.run_day_sweep(days, 300e3, cfg, models, dev)
+    t_run = _dist_max(time.perf_counter() - t0, world, local)
+    n_req = sum(len(d.requests) for d in days)
+    out = {"workload": f"C4 as configured on {n_scen * world} of the 1024 scenarios (declared contiguous fraction: "
+                       f"scenarios 0..{n_scen * world - 1}, trace seeds 1000+): 24 h diurnal day (24 x 1 h gamma(0.5), "
+                       "6 -> 20 rps), 288 five-minute windows each planned from the previous one (config table of "
+                       "2 phases x TP{1,2,4,8} x 8 rungs, ILP + max-throughput baseline, 16 GPUs) and replayed with the "
+                       "two-tier controllers, SLO 600/100 ms",
+           "value": n_scen * world / t_run, "unit": "scenarios/s", "seconds": t_run,
+           "windows_per_s": res.n_windows * world / t_run, "decisions_per_s_rank0": res.decisions / t_run,
+           "requests_per_scenario": n_req // max(1, n_scen), "phase_s_rank0": res.seconds,
+           "trace_synthesis_s_rank0": t_gen,
+           "timing": "end to end through daysim.run_day_sweep (host traces in, per-window plans and reports out)"}
+    if with_cpu and rank == 0:
+        import oracle
+
+        ref = oracle.load_ref()
+        keep: list = []
+        c = oracle.ref_runner_config()
+        c.slo = P.c_slo(cfg.slo)
+        c.total_gpus = cfg.total_gpus
+        tps = (C.c_int32 * 4)(*cfg.tp_options)
+        ld = (C.c_double * len(lad.freqs_mhz))(*lad.freqs_mhz)
+        keep += [tps, ld]
+        c.n_tp, c.tp_options, c.ladder, c.n_ladder = 4, tps, ld, len(lad.freqs_mhz)
+        c.scheduler = P.c_policy(cfg.scheduler)
+        c.alpha, c.peak_subwindow_s = cfg.plan.alpha, cfg.plan.peak_subwindow_s
+        c.search, c.plan_policy = P.c_search(cfg.plan.search), P.c_policy(cfg.plan.policy)
+        c.rampup_s, c.switch_latency_ms = cfg.rampup_s, cfg.switch_latency_ms
+        c.mpc_k, c.mpc_n, c.mpc_margin = cfg.mpc_horizon_k, cfg.mpc_ladder_n, cfg.mpc_margin
+        c.kv_threshold, c.decode_margin = cfg.kv_threshold, cfg.decode_margin
+        # the reference's run_experiment on scenario 0's first hour (its first 12 windows), two-tier policy
+        hour0 = P.gen_gamma_trace(Dy.diurnal_profile()[0], 0.5, Dy.HOUR_MS,
+                                  P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), 1000 * 1000)
+        o = (oracle.ref_window_run * 16)()
+        n_out, tt = C.c_int(), C.c_int32()
+        cm, ct = P.c_model_set(models, keep), P.c_trace(hour0, keep)
+        pa = (C.c_int32 * 1)(int(P.Policy.two_tier))
+        t0 = time.perf_counter()
+        rc = ref.ref_run_experiment(C.byref(cm), C.byref(ct), 300e3, pa, 1, C.byref(c), o, 16, C.byref(n_out),
+                                    C.byref(tt))
+        t_cpu = time.perf_counter() - t0
+        same = rc == 0 and n_out.value == 12 and all(
+            (o[w].gpus_used, o[w].objective_w, o[w].report.n_decisions, o[w].report.prefill_energy_j,
+             o[w].report.decode_energy_j, o[w].report.ttft_violations) ==
+            (res.plans[0][w].ilp.gpus_used, res.plans[0][w].ilp.objective_w, res.results[0][w].n_decisions,
+             res.results[0][w].report.prefill_energy_j, res.results[0][w].report.decode_energy_j,
+             res.results[0][w].report.ttft_violations) for w in range(12))
+        w_per_s = n_out.value / t_cpu
+        out["cpu_baseline"] = {"value": w_per_s / 288.0, "unit": "scenarios/s", "cores": cpu_threads(),
+                               "kind": "reference", "seconds": t_cpu, "windows_per_s": w_per_s,
+                               "sample": "scenario 0's first hour (12 of its 288 windows): pdsim::run_experiment, "
+                                         "two-tier policy (build_config_table on std::async threads); scenarios/s "
+                                         "= windows/s / 288"}
         out["identical_on_sample"] = bool(same)
     return out
 
@@ -745,7 +830,7 @@ def bench_c4_experiment(dev, with_cpu: bool) -> dict:
 
 def run_extras(args, dev, rank, world, local) -> dict:
     with_cpu = world == 1 and not args.no_cpu_baseline
-    todo = [args.only] if args.only else ["c1", "c2l", "c3", "c4", "c4x", "c5g", "c5x"]
+    todo = [args.only] if args.only else ["c1", "c2l", "c3", "c4", "c4d", "c4x", "c5g", "c5x"]
     out = {}
     for k in todo:
         if k == "c1":
@@ -759,6 +844,8 @@ def run_extras(args, dev, rank, world, local) -> dict:
                                            n_windows=args.c3_windows)
         elif k == "c4":
             out["c4_replay"] = bench_c4(dev, rank, world, local, args.c4_scenarios, with_cpu)
+        elif k == "c4d":
+            out["c4_day"] = bench_c4_day(dev, rank, world, local, args.c4_day_scenarios, with_cpu)
         elif k == "c4x":
             if world == 1:
                 out["c4_experiment"] = bench_c4_experiment(dev, with_cpu)

@@ -308,7 +308,8 @@ struct Writer {
     ++n_idl;
   }
   __device__ void decision(double t, int trigger, double f, int feasible, long long eval) {
-    if (n_dec < I->dec_cap) {
+    if (!R->dec) {  // no logs requested: decisions are only counted
+    } else if (n_dec < I->dec_cap) {
       if (leader) R->dec[I->dec0 + n_dec] = DDec{t, f, eval, trigger, feasible};
     } else {
       overflow = 1;
@@ -1866,19 +1867,24 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
         const long long B = I.list_n + tok / std::max<long long>(1, C.max_batch_tokens) + 2;
         rc = 3 * B + I.list_n + 16;
         ic = 3 * B + I.list_n + 16;
-        dc = 2 * B + I.list_n + 16;
+        dc = want_logs ? 2 * B + I.list_n + 16 : 0;
       } else {
+        // decode iterations (one batch record each, at most one idle between
+        // two): an estimate from the instance's share of the window's output
+        // tokens (routing weight) at ~8 residents per iteration; an overflow
+        // re-runs with the device's exact counts (need_*)
         const long long so = plan[I.scen].sum_out;
-        const long long est = attempt == 0 ? so / 4 + D.n + 256 : so + D.n + 256;
+        const long long est = static_cast<long long>((static_cast<double>(so) / 8.0 + static_cast<double>(D.n)) *
+                                                     std::min(1.0, std::max(0.0, I.weight))) + 256;
         rc = 2 * est + 16;
         ic = 2 * est + 16;
-        dc = 2 * est + 16;
+        dc = want_logs ? 2 * est + 16 : 0;
         I.res0 = nres;
         nres += std::min<long long>(C.max_batch_requests, std::max<long long>(D.n, 1));
       }
       if (need_rec[g] >= 0) rc = std::max(rc, need_rec[g] + 16);
       if (need_idl[g] >= 0) ic = std::max(ic, need_idl[g] + 16);
-      if (need_dec[g] >= 0) dc = std::max(dc, need_dec[g] + 16);
+      if (need_dec[g] >= 0 && want_logs) dc = std::max(dc, need_dec[g] + 16);
       I.rec0 = nrec;
       I.rec_cap = rc;
       I.idl0 = nidl;
@@ -1909,7 +1915,8 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
                  o_done = take(sizeof(DDone) * NP), o_dlist = take(8 * NR), o_djoin = take(8 * NR),
                  o_mslot = take(4 * NR), o_mr = take(8 * NR), o_rec = take(sizeof(DRec) * nrec),
                  o_recx = want_logs ? take(sizeof(DRecX) * nrec) : 0, o_idl = take(sizeof(DRec) * nidl),
-                 o_idlx = want_logs ? take(sizeof(DIdlX) * nidl) : 0, o_decr = take(sizeof(DDec) * ndec),
+                 o_idlx = want_logs ? take(sizeof(DIdlX) * nidl) : 0,
+                 o_decr = want_logs ? take(sizeof(DDec) * ndec) : 0,
                  o_res = take(sizeof(DResident) * std::max<long long>(nres, 1)),
                  o_recc = take(8 * nrec), o_idlc = take(8 * nidl);
     const size_t total = o;
@@ -1977,7 +1984,7 @@ extern "C" int bs_replay(bs_ctx_t ctx, bs_models_t sim_models, bs_models_t ctl_m
     R.recx = want_logs ? reinterpret_cast<DRecX*>(d + o_recx) : nullptr;
     R.idl = reinterpret_cast<DRec*>(d + o_idl);
     R.idlx = want_logs ? reinterpret_cast<DIdlX*>(d + o_idlx) : nullptr;
-    R.dec = reinterpret_cast<DDec*>(d + o_decr);
+    R.dec = want_logs ? reinterpret_cast<DDec*>(d + o_decr) : nullptr;
     R.res = reinterpret_cast<DResident*>(d + o_res);
     R.rec_c = reinterpret_cast<double*>(d + o_recc);
     R.idl_c = reinterpret_cast<double*>(d + o_idlc);
