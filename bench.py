@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--only", choices=["c1", "c2l", "c3", "c4", "c4d", "c4x", "c5g", "c5x"], default=None,
                     help="run one sub-benchmark alone and print its JSON object")
     ap.add_argument("--c4-scenarios", type=int, default=1024)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for --gpus > 1 (gloo: CPU tests of the rank plumbing)")
     ap.add_argument("--c4-day-scenarios", type=int, default=8, help="full-day C4 scenarios per rank")
     ap.add_argument("--c3-windows", type=int, default=24, help="1-hour windows in the C3 table stream")
     ap.add_argument("--c5x-decisions", type=int, default=4096)
@@ -870,39 +872,41 @@ def spawn_ranks(args) -> int:
     return subprocess.call(cmd)
 
 
-def main():
-    args = parse()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        return spawn_ranks(args)
-    if args.impl == "reference":
-        return run_reference(args)
+def init_dist(args, world: int, local: int) -> None:
+    """One process per GPU: NCCL over the node's GPUs (gloo only for the CPU
+    tests of the multi-rank plumbing)."""
+    if world <= 1:
+        return
+    import torch
+    import torch.distributed as dist
 
-    rank, local, world = dist_env()
-    if world != args.gpus:
-        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dist_backend == "nccl":
+        torch.cuda.set_device(local)
+    dist.init_process_group(args.dist_backend)
+
+
+def make_device(local: int):
+    from paper_2602_18755_b200 import pdsim as P
+
+    return P.Device(local)
+
+
+def measure_c2(args, dev, rank: int, world: int, local: int) -> dict:
+    """The C2 leg on this rank's GPU: its own corpus (seed 0xC2 + 1000 rank)
+    as a resident plan, `steps` timed steps (CUDA events on the library's
+    stream, L2 flushed between steps, a barrier before the timed region),
+    per-kernel times from extra untimed steps, then the same batch end to end
+    through bs_mpc_exhaustive with host buffers.  Local numbers only: the
+    ranks are combined by combine_c2."""
     import torch
 
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
     from paper_2602_18755_b200 import _abi as A
     from paper_2602_18755_b200 import pdsim as P
     from paper_2602_18755_b200 import workloads as Wk
 
-    dev = P.Device(local)
-    if args.only:
-        extra = run_extras(args, dev, rank, world, local)
-        if rank == 0:
-            print(json.dumps(extra), flush=True)
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return 0
     lib = dev._lib
     torch.cuda.set_device(local)
     stream = torch.cuda.ExternalStream(lib.bs_ctx_stream(dev.handle), device=f"cuda:{local}")
-
     D = args.decisions
     models, cfg, pol, snaps = Wk.c2_corpus(0xC2 + 1000 * rank, D, args.ttft)
     keep: list = []
@@ -910,8 +914,6 @@ def main():
     cp = (A.bs_scheduler_policy * 1)(P.c_policy(pol))
     probs = P.c_problems(snaps, None, keep)
     mh = dev.models(models)
-
-    # --- resident plan (value) -------------------------------------------------
     plan = C.c_void_p()
     dev.check(lib.bs_mpc_plan_create(dev.handle, mh, cc, cp, 1, probs, D, 0, C.byref(plan)))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")  # > 126 MB L2
@@ -931,9 +933,7 @@ def main():
         dev.check(lib.bs_mpc_plan_results(dev.handle, plan, out))
         trajectories = sum(out[i].trajectories for i in range(D))
         feasible = sum(out[i].feasible_count for i in range(D))
-
-        if world > 1:
-            torch.distributed.barrier()
+        _barrier(world)
         torch.cuda.synchronize()
         clocks = ClockSampler(local)
         clocks.start()
@@ -956,14 +956,6 @@ def main():
             phase_ms.append(list(ms))
             leaf_ms.append(ms[3])
             flush.zero_()
-        total_ms = sum(step_ms)
-        if world > 1:
-            t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            total_ms = float(t.item())
-            torch.distributed.barrier()
-    value = world * D * TRAJ_PER_DECISION * args.steps / (total_ms * 1e-3)
-
     # --- end to end through the C ABI with host buffers (e2e) ------------------
     res = (A.bs_mpc_result * D)()
     for _ in range(2):
@@ -975,32 +967,74 @@ def main():
         dev.check(lib.bs_mpc_exhaustive(dev.handle, mh, cc, cp, 1, probs, D, res))
         e2e_times.append(time.perf_counter() - t0)
         lib.bs_ctx_last_transfer(dev.handle, C.byref(h2d), C.byref(d2h))
-    e2e_s = statistics.median(e2e_times)
     clk = clocks.stop()  # sampled across the timed steps and the e2e calls (the device-timed region is ms-short)
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
     same = all(res[i].best_code == out[i].best_code and res[i].objective_w == out[i].objective_w
                for i in range(D))
     lib.bs_mpc_plan_destroy(dev.handle, plan)
-    gathered = None
-    if world > 1:  # the final gather of per-decision results over NCCL (outside the timed region)
-        import struct
+    import struct
+
+    rows = [[struct.unpack("<q", struct.pack("<d", out[i].objective_w))[0],
+             int(out[i].best_code) & 0x7FFFFFFFFFFFFFFF, int(out[i].feasible_count)] for i in range(D)]
+    peak, peak_ms = C.c_double(), C.c_double()
+    dev.check(lib.bs_fp64_peak(dev.handle, C.byref(peak), C.byref(peak_ms)))
+    return {"D": D, "total_ms": sum(step_ms), "step_ms": step_ms, "launches": launches, "leaf_ms": leaf_ms,
+            "phase_ms": phase_ms, "e2e_s": statistics.median(e2e_times), "h2d": int(h2d.value),
+            "d2h": int(d2h.value), "same": bool(same), "clocks": clk, "trajectories": trajectories,
+            "feasible": feasible, "rows": rows, "peak": peak.value, "corpus": (models, cfg, pol, snaps),
+            "out": out}
+
+
+def combine_c2(m: dict, rank: int, world: int, local: int, args) -> dict:
+    """The ranks' C2 measurements as one job: the max over ranks of the timed
+    region and of the end-to-end time (barrier-aligned starts), and the final
+    all-gather of every rank's per-decision results (the only collective of
+    the path, outside the timed region)."""
+    total_ms, e2e_s, gathered = m["total_ms"], m["e2e_s"], None
+    if world > 1:
+        import torch
 
         from paper_2602_18755_b200 import sharding as S
 
-        rows = torch.tensor([[struct.unpack("<q", struct.pack("<d", out[i].objective_w))[0],
-                              int(out[i].best_code) & 0x7FFFFFFFFFFFFFFF, int(out[i].feasible_count)]
-                             for i in range(D)], dtype=torch.int64, device=f"cuda:{local}")
-        table = S.gather_rows(rows, world * D)
+        dev_t = f"cuda:{local}" if args.dist_backend == "nccl" else "cpu"
+        total_ms = S.max_over_ranks(total_ms, device=dev_t)
+        e2e_s = S.max_over_ranks(e2e_s, device=dev_t)
+        rows = torch.tensor(m["rows"], dtype=torch.int64, device=dev_t).reshape(-1, 3)
+        table = S.gather_rows(rows, world * m["D"])
         gathered = {"rows": int(table.shape[0]), "bytes": int(table.numel() * 8),
-                    "rank0_rows_match": bool(torch.equal(table[:D], rows)) if rank == 0 else None}
+                    "rank0_rows_match": bool(torch.equal(table[: m["D"]], rows)) if rank == 0 else None,
+                    "rows_sha": __import__("hashlib").sha256(table.cpu().numpy().tobytes()).hexdigest()[:16]}
+    return {"total_ms": total_ms, "e2e_s": e2e_s, "gathered": gathered}
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    init_dist(args, world, local)
+    dev = make_device(local)
+    if args.only:
+        extra = run_extras(args, dev, rank, world, local)
+        if rank == 0:
+            print(json.dumps(extra), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return 0
+    m = measure_c2(args, dev, rank, world, local)
+    agg = combine_c2(m, rank, world, local, args)
+    D = m["D"]
+    total_ms, e2e_s = agg["total_ms"], agg["e2e_s"]
+    value = world * D * TRAJ_PER_DECISION * args.steps / (total_ms * 1e-3)
 
     # --- roofline ----------------------------------------------------------------
-    peak, peak_ms = C.c_double(), C.c_double()
-    dev.check(lib.bs_fp64_peak(dev.handle, C.byref(peak), C.byref(peak_ms)))
-    leaf_avg_ms = statistics.mean(leaf_ms)
+    leaf_avg_ms = statistics.mean(m["leaf_ms"])
     achieved = W_OPS * D * TRAJ_PER_DECISION / (leaf_avg_ms * 1e-3)
     traffic, executed, prof_src = None, None, None
     tpath = ROOT / "profiles" / "leaf_traffic.json"
@@ -1019,6 +1053,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = cpu_threads()
+            models, cfg, pol, snaps = m["corpus"]
+            out = m["out"]
             # ~7 s per C2 decision per core for the reference loop: one decision per thread
             sample = min(D, max(1, threads))
             dt, ref_out = cpu_reference_run(models, cfg, pol, snaps[:sample], threads)
@@ -1044,23 +1080,25 @@ def main():
                        "(compute-bound, lat_coef 366, TP2)", "l2": "flushed between steps (256 MB write)",
                        "parallelism": f"independent decisions sharded over {world} GPU(s)"},
             "decisions_per_s": world * D * args.steps / (total_ms * 1e-3),
-            "feasible_fraction": feasible / max(1, trajectories),
-            "phase_ms_avg": {k: statistics.mean(p[i] for p in phase_ms)
+            "feasible_fraction": m["feasible"] / max(1, m["trajectories"]),
+            "phase_ms_avg": {k: statistics.mean(p[i] for p in m["phase_ms"])
                              for i, k in enumerate(["prepare", "thresholds", "bfs", "sweep", "finalize"])},
             "e2e": {"value": world * D * TRAJ_PER_DECISION / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value),
-                    "matches_resident": bool(same)},
-            "roofline": roofline_obj(achieved, peak.value, leaf_avg_ms, traffic, executed, prof_src),
-            "gpu_launches": int(launches),
+                    "h2d_bytes_per_step": m["h2d"], "d2h_bytes_per_step": m["d2h"],
+                    "matches_resident": m["same"]},
+            "roofline": roofline_obj(achieved, m["peak"], leaf_avg_ms, traffic, executed, prof_src),
+            "gpu_launches": int(m["launches"]),
             "parity": identical,
-            "gather": gathered,
-            "clocks": clk,
+            "gather": agg["gathered"],
+            "clocks": m["clocks"],
             "cpu_baseline": cpu,
         }
         line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
-        torch.distributed.destroy_process_group()
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
     return 0
 
 
