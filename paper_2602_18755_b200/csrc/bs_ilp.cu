@@ -107,8 +107,10 @@ struct DIlpOut {
   int status;           // 0 ok, 1 infeasible, 2 leaf capacity exceeded, 3 frontier state overflow
   int gpus_used;
   double objective;
+  double cut;                   // placement: cost of a known feasible leaf (a strict bound; +inf: none)
   unsigned long long leaves;    // max-throughput: feasible leaves enumerated
   unsigned long long leaf_off;  // their offset in the leaf list
+  unsigned long long leaf_best; // the selected leaf (ordinal in the problem's list; ~0: none)
 };
 
 // Frontier node storage (per problem region of f_cap nodes; two ping-pong
@@ -127,6 +129,7 @@ __device__ __forceinline__ double pos_part(double x) { return 0.0 < x ? x : 0.0;
 struct View {
   int n, mode;
   double need;
+  double cut;  // placement: subtrees whose lower bound exceeds it hold no optimum
   const double* r;
   const double* e;
   const int* g;
@@ -143,6 +146,7 @@ __device__ __forceinline__ View view_of(const DIlpProb& P, const DIlpEntries& E,
   v.n = P.n;
   v.mode = P.mode;
   v.need = P.need;
+  v.cut = INFINITY;
   v.r = E.r + P.e_off;
   v.e = E.e + P.e_off;
   v.g = E.g + P.e_off;
@@ -172,6 +176,7 @@ __device__ __forceinline__ int node_test(const View& v, int i, const IlpSt& s, d
   if (def_p > 0.0) lb = lb + def_p * v.mep[i];
   if (def_d > 0.0) lb = lb + def_d * v.med[i];
   *lb_out = lb;
+  if (lb > v.cut) return 0;  // above a known feasible leaf's cost: no optimum below
   double gn = 0.0;
   if (def_p > 0.0) gn = gn + def_p / v.mrp[i];
   if (def_d > 0.0) gn = gn + def_d / v.mrd[i];
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(kIlpThreads) ilp_frontier_kernel(const DIlpPro
   const int p = blockIdx.x;
   const DIlpProb P = probs[p];
   DIlpOut* o = &outs[p];
-  const View v = view_of(P, E, p);
+  View v = view_of(P, E, p);
   if (threadIdx.x == 0) {  // placement.hpp:371-390 (solve_max_throughput does not use them)
     double* mep = E.min_e_p + P.e_off + p;
     double* med = E.min_e_d + P.e_off + p;
@@ -322,9 +327,47 @@ __global__ void __launch_bounds__(kIlpThreads) ilp_frontier_kernel(const DIlpPro
     o->status = 0;
     o->leaves = 0;
     o->leaf_off = 0;
+    o->cut = INFINITY;
   }
   __syncthreads();
   __threadfence_block();
+  if (P.mode == 0) {  // a feasible leaf to bound the search: one prefill and one decode entry
+    __shared__ double s_min[kIlpThreads / 32];
+    double best = INFINITY;
+    for (int e = threadIdx.x; e < P.n * P.n; e += blockDim.x) {
+      const int i = e / P.n, j = e - i * P.n;
+      if (!v.use[i] || !v.use[j] || v.ph[i] != BS_PHASE_PREFILL || v.ph[j] != BS_PHASE_DECODE) continue;
+      // the fewest instances whose goodput fold n r_c (r + 0 * ... = r) reaches need
+      auto fewest = [&](int x) {
+        double q = ceil(v.need / v.r[x]);
+        long long n = q > 4096.0 ? 4097 : static_cast<long long>(q);
+        while (n > 1 && static_cast<double>(n - 1) * v.r[x] >= v.need) --n;
+        while (n <= 4096 && static_cast<double>(n) * v.r[x] < v.need) ++n;
+        return n;
+      };
+      const long long ni = fewest(i), nj = fewest(j);
+      if (ni > 4096 || nj > 4096 || ni * v.g[i] + nj * v.g[j] > P.total_gpus) continue;
+      // the leaf's cost fold in table order (other entries add (0 e) r = 0)
+      const int a = i < j ? i : j, b = i < j ? j : i;
+      const long long na = i < j ? ni : nj, nb = i < j ? nj : ni;
+      double c = 0.0 + static_cast<double>(na) * v.e[a] * v.r[a];
+      c = c + static_cast<double>(nb) * v.e[b] * v.r[b];
+      best = c < best ? c : best;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, best, off);
+      best = y < best ? y : best;
+    }
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kIlpThreads / 32; ++w) best = s_min[w] < best ? s_min[w] : best;
+      o->cut = s_min[0] < best ? s_min[0] : best;
+    }
+    __syncthreads();
+    v.cut = o->cut;
+  }
   DFront F = front_at(front_base + P.f_off, P.f_cap);
   __shared__ int s_cnt, s_lv;
   if (threadIdx.x == 0) {  // level 0: the root, advanced to its first choice
@@ -500,7 +543,8 @@ __global__ void __launch_bounds__(kIlpSubThreads) ilp_subtree_kernel(const DIlpP
   const int nfront = o->n_front;
   if (j >= nfront || o->status) return;
   if (stage == 1 && P.mode == 0) return;
-  const View v = view_of(P, E, p);
+  View v = view_of(P, E, p);
+  if (P.mode == 0) v.cut = o->cut;
   DFront F = front_at(front_base + P.f_off, P.f_cap);
   const int cur = o->n_levels & 1;
   const IlpSt s0 = F.st[cur][j];
@@ -590,12 +634,50 @@ __global__ void ilp_finish_kernel(const DIlpProb* probs, DIlpEntries E, DIlpOut*
                                   const double* leaf_score, const int* leaf_used, unsigned long long leaf_cap,
                                   long long* counts_out) {
   const int p = blockIdx.x;
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
   const DIlpProb P = probs[p];
   DIlpOut* o = &outs[p];
   const View v = view_of(P, E, p);
   DFront F = front_at(front_base + P.f_off, P.f_cap);
   long long* counts = counts_out + P.c_off;
+  if (P.mode == 1 && o->status == 0 && o->leaf_off + o->leaves <= leaf_cap) {
+    // the reference's `better` rule in leaf order (placement.hpp:448-461),
+    // 32 leaves at a time: the first leaf of a group that is better than the
+    // current best (in order) updates it, and the scan resumes after it --
+    // the same sequence of updates as one thread walking every leaf
+    bool found = false;
+    double best_score = -1.0;
+    int best_gpus = 0;
+    unsigned long long best_k = 0;
+    const unsigned long long L = o->leaves;
+    for (unsigned long long k = 0; k < L;) {
+      const unsigned long long idx = k + static_cast<unsigned long long>(lane);
+      bool better = false;
+      double score = 0.0;
+      int used = 0;
+      if (idx < L) {
+        score = leaf_score[o->leaf_off + idx];
+        used = leaf_used[o->leaf_off + idx];
+        better = !found || score > best_score + 1e-12 || (fabs(score - best_score) <= 1e-12 && used < best_gpus);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, better);
+      if (!m) {
+        k += 32;
+        continue;
+      }
+      const int first = __ffs(m) - 1;
+      best_score = __shfl_sync(0xffffffffu, score, first);
+      best_gpus = __shfl_sync(0xffffffffu, used, first);
+      best_k = k + static_cast<unsigned long long>(first);
+      found = true;
+      k = best_k + 1;
+    }
+    if (lane == 0) {
+      o->leaf_best = found ? best_k : ~0ull;
+    }
+  }
+  __syncwarp();
+  if (threadIdx.x != 0) return;
   for (int i = 0; i < P.n; ++i) counts[i] = 0;
   if (o->status) return;
   const int cur = o->n_levels & 1;
@@ -612,23 +694,8 @@ __global__ void ilp_finish_kernel(const DIlpProb* probs, DIlpEntries E, DIlpOut*
       o->status = 2;
       return;
     }
-    // the reference's `better` rule in leaf order (placement.hpp:448-461)
-    bool found = false;
-    double best_score = -1.0;
-    int best_gpus = 0;
-    unsigned long long best_k = 0;
-    for (unsigned long long k = 0; k < o->leaves; ++k) {
-      const double score = leaf_score[o->leaf_off + k];
-      const int used = leaf_used[o->leaf_off + k];
-      const bool better = !found || score > best_score + 1e-12 || (fabs(score - best_score) <= 1e-12 && used < best_gpus);
-      if (better) {
-        found = true;
-        best_score = score;
-        best_gpus = used;
-        best_k = k;
-      }
-    }
-    if (!found) {
+    const unsigned long long best_k = o->leaf_best;  // the warp's scan above
+    if (best_k == ~0ull) {
       o->status = 1;
       return;
     }

@@ -712,6 +712,20 @@ int bs_goodput_tables(bs_ctx_t ctx, bs_models_t models, const bs_trace* bases, i
       for (long long i = 0; i < probe_total; ++i) idx[i] = i;
       std::partial_sort(idx.begin(), idx.begin() + std::min<long long>(8, probe_total), idx.end(),
                         [&](long long a, long long b) { return hp[a].ns > hp[b].ns; });
+      double ns_ph[2] = {0.0, 0.0};
+      long long n_ph[2] = {0, 0};
+      for (long long i = 0; i < probe_total; ++i) {
+        int t = 0;
+        while (t + 1 < n_tables && tabs[t + 1].probe_off <= i) ++t;
+        const long long c = (i - tabs[t].probe_off) / tabs[t].n_streams;
+        const int ph = cands[c].phase == BS_PHASE_PREFILL ? 0 : 1;
+        if (hp[i].ns > 0) {
+          ns_ph[ph] += static_cast<double>(hp[i].ns);
+          ++n_ph[ph];
+        }
+      }
+      std::fprintf(stderr, "probes run: prefill %lld (%.1f ms total), decode %lld (%.1f ms total)\n", n_ph[0],
+                   ns_ph[0] / 1e6, n_ph[1], ns_ph[1] / 1e6);
       for (long long q = 0; q < std::min<long long>(8, probe_total); ++q) {
         const long long i = idx[q];
         int t = 0;

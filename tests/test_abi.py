@@ -73,12 +73,34 @@ def test_no_cpu_fallback_without_gpu():
 
 
 def test_kernels_are_sm100a_fp64_without_fma():
-    """The shipped library carries sm_100a SASS, and the MPC kernels use
-    DADD/DMUL (no DFMA outside the IEEE division subroutine)."""
+    """The shipped library carries sm_100a SASS, its kernels compute with
+    DADD/DMUL, and no kernel contracts a multiply-add: every DFMA belongs to
+    an IEEE double division -- the inline reciprocal refinement that follows
+    its MUFU.RCP64H (7 DFMA) or the division's slow-path subroutine (its own
+    MUFU.RCP64H) -- i.e. lies within 64 instructions after a MUFU.RCP64H, and
+    each kernel has at most 7 DFMA per reciprocal plus 10 per slow path."""
+    import re
+
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "DADD" in sass and "DMUL" in sass
+    funcs, cur = {}, None
+    for ln in sass.splitlines():
+        m = re.match(r"\s+Function : (\S+)", ln)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur and re.search(r"/\*[0-9a-f]{4}\*/", ln):
+            funcs[cur].append(ln)
+    assert len(funcs) > 20
+    for name, body in funcs.items():
+        rcp = [i for i, ln in enumerate(body) if "MUFU.RCP64H" in ln]
+        fma = [i for i, ln in enumerate(body) if re.search(r"\bDFMA\b", ln)]
+        calls = sum(1 for ln in body if "RET.REL" in ln)
+        for i in fma:
+            assert any(0 < i - p <= 64 for p in rcp), f"{name}: DFMA outside a division at instruction {i}"
+        assert len(fma) <= 7 * len(rcp) + 10 * max(1, calls), name
 
 
 def test_pdsim_shim_compiles_against_reference():

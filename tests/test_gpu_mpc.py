@@ -226,7 +226,14 @@ def test_exhaustive_c2_shape_16_7M(gpu_device, ref_lib, seed):
         assert (g.feasible_count, g.best_code) == (out.feasible_count, out.best_code)
 
 
-def test_eval_codes_and_tables_match_reference(gpu_device, oracle_lib):
+def test_eval_codes_and_tables_match_reference(gpu_device, oracle_lib, ref_lib):
+    """Per-trajectory feasibility and objective vs the C restatement, and the
+    (k, f) tables bitwise vs the reference's own MpcEvaluator memo
+    (dvfs.hpp:150-160: lat = wf L, pow = P, energy = lat pow)."""
+    import ctypes as C
+
+    from helpers import Packed
+    from paper_2602_18755_b200 import _abi as A
     rng = random.Random(77)
     for m, cfg, pol, q in _instances(71, 30):
         n = len(cfg.candidates().freqs_mhz)
@@ -237,6 +244,16 @@ def test_eval_codes_and_tables_match_reference(gpu_device, oracle_lib):
         assert gf == feas and go == obj
         lat, pw, en = P.mpc_tables(q, cfg, m, pol)
         assert len(lat) == K
+        p = Packed(m, cfg, pol, q)
+        rk, rn = C.c_int32(), C.c_int32()
+        size = A.BS_MAX_K * A.BS_MAX_CAND
+        rl, rp, re_ = (C.c_double * size)(), (C.c_double * size)(), (C.c_double * size)()
+        assert ref_lib.ref_tables(C.byref(p.models), C.byref(p.cfg), C.byref(p.policy), C.byref(p.snap), C.byref(rk),
+                                  C.byref(rn), rl, rp, re_) == 0
+        assert (rk.value, rn.value) == (K, n)
+        for k in range(K):
+            for f in range(n):
+                assert (lat[k][f], pw[k][f], en[k][f]) == (rl[k * n + f], rp[k * n + f], re_[k * n + f])
 
 
 def test_decode_matches_oracle(gpu_device, oracle_lib):

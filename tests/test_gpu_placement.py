@@ -317,3 +317,21 @@ def test_empty_saturated_probe_without_idle_tp_matches_reference(gpu_device, ref
     want = _ref_table(ref_lib, m, base, P.SLOSpec(600.0, 100.0), P.SchedulerPolicy(), found, cands)
     assert [_cmp(e) for e in got] == [_cmp(e) for e in want]
     assert want[0].saturated and want[0].r_c == 0.0 and "tp 4" in want[0].error
+
+
+def test_c3_full_hour_table_matches_reference(gpu_device, ref_lib):
+    """BASELINE C3 at full size: a bursty 1-hour gamma(0.5) window at 12 rps
+    (~43k requests), 2 phases x TP {1,2,4,8} x 16 rungs = 128 candidates,
+    max_batch_tokens 2048 -- every entry equal to the reference's
+    build_config_table (placement.hpp:240-260), then the ILP for 16 GPUs."""
+    lad = W.ladder(16)
+    m = W.llama_models(lad)
+    base = P.gen_gamma_trace(12.0, 0.5, 3600e3, P.LengthDistribution(lognormal=P.Lognormal(6.2, 0.6, 5.3, 0.7)), 7)
+    cands = P.enumerate_candidates(lad, [1, 2, 4, 8])
+    pol, slo = P.SchedulerPolicy(max_batch_tokens=2048), P.SLOSpec(600.0, 100.0)
+    got = P.build_config_table(cands, base, slo, m, pol, P.GoodputSearch(), device=gpu_device)
+    want = _ref_table(ref_lib, m, base, slo, pol, P.GoodputSearch(), cands)
+    assert len(base.requests) > 40000
+    assert [_cmp(e) for e in got] == [_cmp(e) for e in want]
+    plan = P.solve_placement(P.PlacementProblem(got, 16, P.peak_rps(base, 10.0), 0.05), gpu_device)
+    assert plan.gpus_used <= 16 and sum(plan.counts) >= 2
