@@ -258,6 +258,12 @@ struct DTables {
   // leaf worse than the seed when fl(num - fl(nb_beta den)) > fl(nb_R + fl(num 2^-40)).
   double nb_beta;
   double nb_R;
+  // exact leaf-existence bounds of the two bottom levels (leaf_exists_bounds,
+  // exhaustive search): a node at depth K-2 with clock t and last digit l has
+  // a feasible leaf iff t <= rexist[l]
+  double rexist[kMaxCand];
+  int rex_ok;
+  int _pad_rex;
 };
 
 // Compact per-problem result written by the device; the host expands it

@@ -30,7 +30,8 @@ struct ExCtl {
   unsigned long long n_loose;   // decisions prepare_kernel found loose (candidates for BFS-settled final nodes)
   unsigned long long n_thr;     // decisions listed for thr_kernel (three swept levels, or loose)
 #ifdef BS_SWEEP_STATS
-  unsigned long long st_nodes, st_children, st_rows_eval, st_leaves_eval, st_div, st_thr_nodes, st_slow_nodes;
+  unsigned long long st_nodes, st_children, st_rows_eval, st_leaves_eval, st_div, st_thr_nodes, st_slow_nodes,
+      st_empty_nodes;
 #endif
 };
 
@@ -199,6 +200,39 @@ __device__ double leaf_threshold(double s1, double m1, double s2, double m2, dou
       hi = mid;
   }
   return dval(lo);
+}
+
+// rexist[l] = sup{t : a node at depth K-2 with clock t and last digit l has
+// a feasible leaf} = max(max_{g != l} rho_S[g], rho_N[l]), rho[g] the largest
+// threshold of row g -- its head, the leaf with the smallest step (taus are
+// non-increasing in the leaf step): min(B0[K-1][g], the smallest switched
+// step of another rung).  A node has a feasible leaf iff clock <= rexist[l]
+// (the supremum is attained: thresholds are doubles where both checks pass).
+// 2 nc thresholds, one per thread; the whole CTA must call it.
+__device__ __noinline__ void leaf_exists_bounds(DTables* __restrict__ T) {
+  __shared__ double s_rho[2 * kMaxCand];
+  const int K = T->K, nc = T->nc, k = K - 2, kl = K - 1;
+  const bool ok = T->sorted_ok && nc >= 1;
+  if (ok && threadIdx.x < 2 * nc) {
+    const int g = threadIdx.x % nc;
+    const bool sw = threadIdx.x < nc;
+    double s2 = T->B0[kl][g];
+    if (nc > 1) {
+      const double other = T->ord[kl][0] != g ? T->sb[kl][0] : T->sb[kl][1];
+      s2 = other < s2 ? other : s2;
+    }
+    s_rho[threadIdx.x] = leaf_threshold(sw ? T->B1[k][g] : T->B0[k][g], T->minarr[k], s2, T->minarr[kl], T->ttft);
+  }
+  __syncthreads();
+  if (threadIdx.x < nc && ok) {
+    const int l = threadIdx.x;
+    double r = s_rho[nc + l];
+    for (int g = 0; g < nc; ++g)
+      if (g != l && s_rho[g] > r) r = s_rho[g];
+    T->rexist[l] = r;
+  }
+  if (threadIdx.x == 0) T->rex_ok = ok ? 1 : 0;
+  __syncthreads();
 }
 
 // Builds H for decision T (K >= 3, sorted tables) with the whole CTA
@@ -502,6 +536,9 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
     to_final = (k + 1) == T->FD;
     if (T->sorted_ok) {
       const bool prune = to_final && k + 1 < T->K;
+      // final nodes at depth K-2 are kept only with a feasible leaf (exact:
+      // clock <= rexist[digit], leaf_exists_bounds)
+      const bool rex = prune && T->rex_ok && k + 1 == T->K - 2;
       const int c = feasible_prefix(T, k, nc, t);
       const unsigned char* __restrict__ ord = T->ord[k];
       const double* __restrict__ sb = T->sb[k];
@@ -511,7 +548,9 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
         const int f = ord[j];
         if (f == last) continue;
         bool ok = true;
-        if (prune) {
+        if (rex) {
+          ok = !(__dadd_rn(t, sb[j]) > T->rexist[f]);
+        } else if (prune) {
           const double ct = __dadd_rn(t, sb[j]);
           if (cl < 0) {
             cl = feasible_prefix(T, kl, nc, ct);
@@ -526,7 +565,9 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
       }
       if (diag_passes(T, k, t, last)) {
         bool ok = true;
-        if (prune) {
+        if (rex) {
+          ok = !(__dadd_rn(t, T->B0[k][last]) > T->rexist[last]);
+        } else if (prune) {
           const double ct = __dadd_rn(t, T->B0[k][last]);
           ok = feasible_prefix(T, kl, nc, ct) > 0 || diag_passes(T, kl, ct, last);
         }
@@ -763,9 +804,12 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
     T->nc_magic = nc > 1 ? 0xffffffffu / static_cast<unsigned>(nc) + 1u : 0u;
     T->fuse = 0;
     T->thr_ok = 0;
+    T->rex_ok = 0;
     T->nb_beta = INFINITY;
     T->nb_R = INFINITY;
   }
+  // exact leaf-existence bounds of the two bottom levels (rexist)
+  if (K >= 3) leaf_exists_bounds(T);
   // A slice whose leading digits lie below the first list this kernel
   // writes (trees of at most 3 levels, or shallow final depths): every leaf
   // of the slice evaluated here, in the sweep's op sequence.
@@ -933,7 +977,9 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       }
       if (ok && sl.digits) ok = in_slice(sl, static_cast<unsigned long long>(e), D0, nc);  // sl.digits <= D0 here
       // a final node none of whose children passes has no feasible leaf (as in bfs_node_kernel)
-      if (ok && to_final && T->sorted_ok && FD < K) ok = feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
+      if (ok && to_final && T->sorted_ok && FD < K)
+        ok = (T->rex_ok && FD == K - 2) ? !(t > T->rexist[last])
+                                         : feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
     }
     if (FD > 2) {  // one more level here: the depth-2 nodes never reach global memory (FD is uniform per CTA)
       const unsigned m3 = expand_node<false>(tables, 2, ctl, ok, d, t, num, den, last,
@@ -1374,6 +1420,7 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
         two_sorted(T, FD, nc, t, num, den, last, cb, hint, a);
       } else if (MINB == kSweepMinB3) {  // three swept levels only occur in batches launched with MINB 4
         for_feasible_children(T, FD, nc, t, num, den, last, [&](int e, double t3, double n3, double d3) {
+          if (T->rex_ok && t3 > T->rexist[e]) return;  // no feasible leaf below this child
           if (use_thr && (node_dom_seed(T, n3, d3) || node_dominated(a, n3, d3))) {
             a.count += static_cast<unsigned long long>(thr_leaf_count(H, nc, t3, e));
 #ifdef BS_SWEEP_STATS
@@ -1412,6 +1459,7 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
     atomicAdd(&wctl->st_leaves_eval, a.st_leaves);
     atomicAdd(&wctl->st_div, a.st_div);
     atomicAdd(&wctl->st_thr_nodes, a.st_thr);
+    if (a.count == 0) atomicAdd(&wctl->st_empty_nodes, 1ull);
     atomicAdd(&wctl->st_slow_nodes, a.st_slow);
 #endif
   }

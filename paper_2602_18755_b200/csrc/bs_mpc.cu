@@ -893,9 +893,10 @@ int bs_mpc_plan_results(bs_ctx_t ctx, bs_mpc_plan_t plan, bs_mpc_result* out) {
       std::fprintf(stderr, " final=%llu overflow=%llu\n", c.final_count, c.overflow);
 #ifdef BS_SWEEP_STATS
       std::fprintf(stderr, "bs_mpc sweep: nodes %llu children %llu rows evaluated %llu leaves %llu divisions %llu "
-                   "depth-(K-2) nodes counted by thresholds %llu / walked %llu\n",
+                   "depth-(K-2) nodes counted by thresholds %llu / walked %llu; final nodes without a feasible "
+                   "leaf %llu\n",
                    c.st_nodes, c.st_children, c.st_rows_eval, c.st_leaves_eval, c.st_div, c.st_thr_nodes,
-                   c.st_slow_nodes);
+                   c.st_slow_nodes, c.st_empty_nodes);
 #endif
     }
   }
