@@ -258,10 +258,10 @@ struct DTables {
   // leaf worse than the seed when fl(num - fl(nb_beta den)) > fl(nb_R + fl(num 2^-40)).
   double nb_beta;
   double nb_R;
-  // exact leaf-existence bounds of the two bottom levels (leaf_exists_bounds,
-  // exhaustive search): a node at depth K-2 with clock t and last digit l has
-  // a feasible leaf iff t <= rexist[l]
-  double rexist[kMaxCand];
+  // exact completion bounds (leaf_exists_bounds, exhaustive search): a node
+  // at depth d (1 <= d <= K-2) with clock t and last digit l has a feasible
+  // leaf iff t <= rexist[d][l]
+  double rexist[kMaxK][kMaxCand];
   int rex_ok;
   int _pad_rex;
 };

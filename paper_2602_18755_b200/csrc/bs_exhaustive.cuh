@@ -151,20 +151,17 @@ __device__ __forceinline__ double dval(unsigned long long k) {
 
 // The largest double t for which both bottom-level checks pass (-inf: none;
 // +inf: every finite t).
-__device__ double leaf_threshold(double s1, double m1, double s2, double m2, double ttft) {
-  auto ok = [&](double t) {
-    const double t2 = __dadd_rn(t, s1);
-    if (__dsub_rn(t2, m1) > ttft) return false;                 // dvfs.hpp:117 at level K-2
-    return !(__dsub_rn(__dadd_rn(t2, s2), m2) > ttft);          // and at level K-1
-  };
+// The largest double t with ok(t) for a predicate that holds on a down-set
+// of the doubles (-inf: none; +inf: every finite t): the boundary bracketed
+// by galloping from the real-arithmetic estimate x0 (within a few ulps
+// unless an operand swamps another), then bisected, on the order-preserving
+// integer image of the doubles.
+template <typename Ok>
+__device__ double sup_down_set(Ok&& ok, double x0) {
   const double big = 1.7976931348623157e308;
   if (ok(big)) return INFINITY;
   if (!ok(-big)) return -INFINITY;
-  // bracket the boundary by galloping from the real-arithmetic estimate
-  // (within a few ulps unless an operand swamps another), then bisect
   const unsigned long long kmin = dkey(-big), kmax = dkey(big);
-  const double x1 = __dsub_rn(__dadd_rn(ttft, m1), s1), x2 = __dsub_rn(__dsub_rn(__dadd_rn(ttft, m2), s1), s2);
-  double x0 = x1 < x2 ? x1 : x2;
   if (!(x0 == x0)) x0 = 0.0;
   unsigned long long k0 = dkey(x0 < -big ? -big : (x0 > big ? big : x0));
   unsigned long long lo, hi;  // ok(lo), !ok(hi)
@@ -202,34 +199,69 @@ __device__ double leaf_threshold(double s1, double m1, double s2, double m2, dou
   return dval(lo);
 }
 
-// rexist[l] = sup{t : a node at depth K-2 with clock t and last digit l has
-// a feasible leaf} = max(max_{g != l} rho_S[g], rho_N[l]), rho[g] the largest
-// threshold of row g -- its head, the leaf with the smallest step (taus are
-// non-increasing in the leaf step): min(B0[K-1][g], the smallest switched
-// step of another rung).  A node has a feasible leaf iff clock <= rexist[l]
-// (the supremum is attained: thresholds are doubles where both checks pass).
-// 2 nc thresholds, one per thread; the whole CTA must call it.
+// Both bottom checks of leaf (g, f) from a depth-(K-2) clock t: level-K-2
+// step s1 and deadline m1, leaf step s2 and deadline m2.
+__device__ double leaf_threshold(double s1, double m1, double s2, double m2, double ttft) {
+  auto ok = [&](double t) {
+    const double t2 = __dadd_rn(t, s1);
+    if (__dsub_rn(t2, m1) > ttft) return false;                 // dvfs.hpp:117 at level K-2
+    return !(__dsub_rn(__dadd_rn(t2, s2), m2) > ttft);          // and at level K-1
+  };
+  const double x1 = __dsub_rn(__dadd_rn(ttft, m1), s1), x2 = __dsub_rn(__dsub_rn(__dadd_rn(ttft, m2), s1), s2);
+  return sup_down_set(ok, x1 < x2 ? x1 : x2);
+}
+
+// Completion bounds (exhaustive search): rexist[d][l] = sup{t : a node at
+// depth d (1 <= d <= K-2) with clock t and last digit l has a feasible leaf}; a node has one
+// iff its clock <= rexist[d][l] (each supremum is attained: it is a double
+// where every check passes).  With sigma_S / sigma_N[d][g] the supremum for
+// the switched / non-switching child g,
+//   rexist[d][l] = max(max_{g != l} sigma_S[d][g], sigma_N[d][l]);
+// at d = K-2, sigma[g] is the largest threshold of row g -- its head, the leaf
+// with the smallest step (taus are non-increasing in the leaf step):
+// min(B0[K-1][g], the smallest switched step of another rung); above, the
+// child must pass level d and then reach its own bound:
+//   sigma[d][g] = sup{t : fl(fl(t + s) - m_d) <= ttft, fl(t + s) <= rexist[d+1][g]}
+// (both monotone in t).  Levels K-2 down to 1, 2N suprema per level (one per
+// thread); the whole CTA must call it.
 __device__ __noinline__ void leaf_exists_bounds(DTables* __restrict__ T) {
   __shared__ double s_rho[2 * kMaxCand];
-  const int K = T->K, nc = T->nc, k = K - 2, kl = K - 1;
+  const int K = T->K, nc = T->nc;
   const bool ok = T->sorted_ok && nc >= 1;
-  if (ok && threadIdx.x < 2 * nc) {
-    const int g = threadIdx.x % nc;
-    const bool sw = threadIdx.x < nc;
-    double s2 = T->B0[kl][g];
-    if (nc > 1) {
-      const double other = T->ord[kl][0] != g ? T->sb[kl][0] : T->sb[kl][1];
-      s2 = other < s2 ? other : s2;
+  for (int d = K - 2; d >= 1 && ok; --d) {
+    if (threadIdx.x < 2 * nc) {
+      const int g = threadIdx.x % nc;
+      const bool sw = threadIdx.x < nc;
+      const double s = sw ? T->B1[d][g] : T->B0[d][g], m = T->minarr[d], ttft = T->ttft;
+      double sig;
+      if (d == K - 2) {
+        const int kl = K - 1;
+        double s2 = T->B0[kl][g];
+        if (nc > 1) {
+          const double other = T->ord[kl][0] != g ? T->sb[kl][0] : T->sb[kl][1];
+          s2 = other < s2 ? other : s2;
+        }
+        sig = leaf_threshold(s, m, s2, T->minarr[kl], ttft);
+      } else {
+        const double rn = T->rexist[d + 1][g];
+        auto child_ok = [&](double t) {
+          const double t2 = __dadd_rn(t, s);
+          return !(__dsub_rn(t2, m) > ttft) && !(t2 > rn);
+        };
+        const double x1 = __dsub_rn(__dadd_rn(ttft, m), s), x2 = __dsub_rn(rn, s);
+        sig = sup_down_set(child_ok, x1 < x2 ? x1 : x2);
+      }
+      s_rho[threadIdx.x] = sig;
     }
-    s_rho[threadIdx.x] = leaf_threshold(sw ? T->B1[k][g] : T->B0[k][g], T->minarr[k], s2, T->minarr[kl], T->ttft);
-  }
-  __syncthreads();
-  if (threadIdx.x < nc && ok) {
-    const int l = threadIdx.x;
-    double r = s_rho[nc + l];
-    for (int g = 0; g < nc; ++g)
-      if (g != l && s_rho[g] > r) r = s_rho[g];
-    T->rexist[l] = r;
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      const int l = threadIdx.x;
+      double r = s_rho[nc + l];
+      for (int g = 0; g < nc; ++g)
+        if (g != l && s_rho[g] > r) r = s_rho[g];
+      T->rexist[d][l] = r;
+    }
+    __syncthreads();
   }
   if (threadIdx.x == 0) T->rex_ok = ok ? 1 : 0;
   __syncthreads();
@@ -536,9 +568,9 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
     to_final = (k + 1) == T->FD;
     if (T->sorted_ok) {
       const bool prune = to_final && k + 1 < T->K;
-      // final nodes at depth K-2 are kept only with a feasible leaf (exact:
-      // clock <= rexist[digit], leaf_exists_bounds)
-      const bool rex = prune && T->rex_ok && k + 1 == T->K - 2;
+      // children at depths 2..K-2 are kept only with a feasible leaf below
+      // (exact: clock <= rexist[depth][digit], leaf_exists_bounds)
+      const bool rex = T->rex_ok && k + 1 <= T->K - 2;
       const int c = feasible_prefix(T, k, nc, t);
       const unsigned char* __restrict__ ord = T->ord[k];
       const double* __restrict__ sb = T->sb[k];
@@ -549,7 +581,7 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
         if (f == last) continue;
         bool ok = true;
         if (rex) {
-          ok = !(__dadd_rn(t, sb[j]) > T->rexist[f]);
+          ok = !(__dadd_rn(t, sb[j]) > T->rexist[kl][f]);
         } else if (prune) {
           const double ct = __dadd_rn(t, sb[j]);
           if (cl < 0) {
@@ -566,7 +598,7 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
       if (diag_passes(T, k, t, last)) {
         bool ok = true;
         if (rex) {
-          ok = !(__dadd_rn(t, T->B0[k][last]) > T->rexist[last]);
+          ok = !(__dadd_rn(t, T->B0[k][last]) > T->rexist[kl][last]);
         } else if (prune) {
           const double ct = __dadd_rn(t, T->B0[k][last]);
           ok = feasible_prefix(T, kl, nc, ct) > 0 || diag_passes(T, kl, ct, last);
@@ -976,9 +1008,10 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
         last = f1;
       }
       if (ok && sl.digits) ok = in_slice(sl, static_cast<unsigned long long>(e), D0, nc);  // sl.digits <= D0 here
+      if (ok && T->rex_ok && D0 <= K - 2) ok = !(t > T->rexist[D0][last]);  // a feasible leaf below (exact)
       // a final node none of whose children passes has no feasible leaf (as in bfs_node_kernel)
       if (ok && to_final && T->sorted_ok && FD < K)
-        ok = (T->rex_ok && FD == K - 2) ? !(t > T->rexist[last])
+        ok = (T->rex_ok && FD == K - 2) ? !(t > T->rexist[FD][last])
                                          : feasible_prefix(T, FD, nc, t) > 0 || diag_passes(T, FD, t, last);
     }
     if (FD > 2) {  // one more level here: the depth-2 nodes never reach global memory (FD is uniform per CTA)
@@ -1010,21 +1043,19 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       }
     }
   }
-  // Loose trees (more than 98 % of the depth-3 prefixes feasible: every
-  // decision of the 1200 ms C2 corpus, almost none of the 600 ms one, whose
-  // decisions are 0-68 % feasible at depth 3) are candidates for the BFS to
-  // settle the final nodes the seed's node bound dominates (thr_kernel
-  // decides for the whole batch).
-  //
-  // Leaf-count thresholds of the two bottom levels (build_thresholds) for
-  // the decisions that use them:
+  // Loose trees (more than 85 % of the depth-3 prefixes with a feasible
+  // leaf: 96 % at C2 TTFT 1200 ms; the 600 ms corpus' decisions are at most
+  // 68 % feasible at depth 3) are candidates for the BFS to settle the final
+  // nodes the seed's node bound dominates (thr_kernel decides for the whole
+  // batch).  Leaf-count thresholds of the two bottom levels
+  // (build_thresholds) are listed for the decisions that use them:
   //  * three swept levels: the sweep counts a dominated child's leaves with
   //    three binary searches;
   //  * loose decisions with two swept levels: the BFS settles their dominated
   //    final nodes when at least 10 % of the batch is loose (measured at C2
   //    TTFT 1200 ms: 92 % of the final nodes; step 7.9 -> 1.9 ms).
   __syncthreads();
-  const bool loose = FD >= 4 && FD == K - 2 && 50ll * T->n_ok3 > 49ll * nc * nc * nc;
+  const bool loose = FD >= 4 && FD == K - 2 && 20ll * T->n_ok3 > 17ll * nc * nc * nc;
   if (threadIdx.x == 0 && K >= 3 && FD >= 1 && T->sorted_ok && T->filter_ok && sl.digits <= (FD < 2 ? FD : 2) &&
       (K - FD == 3 || loose)) {  // listed for thr_kernel
     if (loose) {
@@ -1420,7 +1451,7 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
         two_sorted(T, FD, nc, t, num, den, last, cb, hint, a);
       } else if (MINB == kSweepMinB3) {  // three swept levels only occur in batches launched with MINB 4
         for_feasible_children(T, FD, nc, t, num, den, last, [&](int e, double t3, double n3, double d3) {
-          if (T->rex_ok && t3 > T->rexist[e]) return;  // no feasible leaf below this child
+          if (T->rex_ok && t3 > T->rexist[K - 2][e]) return;  // no feasible leaf below this child
           if (use_thr && (node_dom_seed(T, n3, d3) || node_dominated(a, n3, d3))) {
             a.count += static_cast<unsigned long long>(thr_leaf_count(H, nc, t3, e));
 #ifdef BS_SWEEP_STATS
