@@ -207,7 +207,7 @@ struct DProblem {
 //   minarr[k]= min completing arrival (+inf if none): monotone-subtraction
 //              reduction of meets_slo's per-request test (SURVEY.md appx. 5)
 struct __align__(16) SRec {
-  double sb, E, A, B0n;
+  double sb, E, A, th0n;  // th0n: the next level's non-switching threshold of this child's rung (thn below)
 };
 
 struct DTables {
@@ -244,6 +244,13 @@ struct DTables {
   SRec srec[kMaxK][kMaxCand];
   unsigned short sinfo[kMaxK][kMaxCand];
   int sorted_ok;
+  // Per-step thresholds (levels >= 1, set by prepare_kernel): a node with
+  // clock t passes level k's check with the switched step of sorted position
+  // j iff t <= thsw[k][j] (non-increasing in j), with rung f's non-switching
+  // step iff t <= th0[k][f] -- the suprema of meets_slo's monotone test
+  // (step_thresholds), so each check is one comparison.
+  double thsw[kMaxK][kMaxCand];
+  double th0[kMaxK][kMaxCand];
   int thr_ok;  // exhaustive search: the two bottom levels' leaf-count thresholds are built (DThr, bs_exhaustive.cuh)
   int fuse;    // exhaustive search: the BFS settles dominated final nodes (thr_kernel)
   int n_ok3;   // exhaustive search: feasible depth-3 prefixes (prepare_kernel)

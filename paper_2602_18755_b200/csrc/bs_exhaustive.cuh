@@ -211,6 +211,29 @@ __device__ double leaf_threshold(double s1, double m1, double s2, double m2, dou
   return sup_down_set(ok, x1 < x2 ? x1 : x2);
 }
 
+// Per-step thresholds (DTables::thsw / th0, levels 1 .. K-1): the supremum
+// of the clocks t with !(fl(fl(t + s) - minarr[k]) > ttft) for every
+// switched step (sorted position) and non-switching step of a level, so the
+// search's checks are single comparisons; the child records' th0n field is
+// filled from them.  The whole CTA must call it (sorted tables).
+__device__ __noinline__ void step_thresholds(DTables* __restrict__ T) {
+  const int K = T->K, nc = T->nc;
+  const double ttft = T->ttft;
+  for (int e = threadIdx.x; e < (K - 1) * 2 * nc; e += blockDim.x) {
+    const int k = 1 + e / (2 * nc), r = e % (2 * nc), j = r % nc;
+    const bool sw = r < nc;
+    const double s = sw ? T->sb[k][j] : T->B0[k][j], m = T->minarr[k];
+    auto ok = [&](double t) { return !(__dsub_rn(__dadd_rn(t, s), m) > ttft); };
+    (sw ? T->thsw : T->th0)[k][j] = sup_down_set(ok, __dsub_rn(__dadd_rn(ttft, m), s));
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < (K - 1) * nc; e += blockDim.x) {
+    const int k = e / nc, r = e % nc;
+    T->srec[k][r].th0n = T->th0[k + 1][T->ord[k][r]];
+  }
+  __syncthreads();
+}
+
 // Completion bounds (exhaustive search): rexist[d][l] = sup{t : a node at
 // depth d (1 <= d <= K-2) with clock t and last digit l has a feasible leaf}; a node has one
 // iff its clock <= rexist[d][l] (each supremum is attained: it is a double
@@ -409,13 +432,23 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
 // by monotonicity of correctly rounded add/subtract in the step, the
 // passing candidates form a prefix of the sorted order ord[k].
 __device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, int k, int nc, double t) {
-  const double m = T->minarr[k], ttft = T->ttft;
-  const double* __restrict__ sb = T->sb[k];
   int lo = 0, hi = nc;  // first failing position
+  if (k == 0) {  // level 0's keys are the clocks themselves (T1)
+    const double m = T->minarr[0], ttft = T->ttft;
+    const double* __restrict__ sb = T->sb[0];
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__dsub_rn(sb[mid], m) > ttft)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    return lo;
+  }
+  const double* __restrict__ th = T->thsw[k];  // t passes position j iff t <= th[j]
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    const double tl = k == 0 ? sb[mid] : __dadd_rn(t, sb[mid]);
-    if (__dsub_rn(tl, m) > ttft)
+    if (t > th[mid])
       hi = mid;
     else
       lo = mid + 1;
@@ -425,7 +458,7 @@ __device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, in
 
 // Does the non-switching child (step B0[k][last], k >= 1) pass meets_slo's check?
 __device__ __forceinline__ bool diag_passes(const DTables* __restrict__ T, int k, double t, int last) {
-  return !(__dsub_rn(__dadd_rn(t, T->B0[k][last]), T->minarr[k]) > T->ttft);
+  return !(t > T->th0[k][last]);
 }
 
 // Number of children of (t, last) at level k that pass the check, without
@@ -587,9 +620,8 @@ __device__ __forceinline__ unsigned expand_node(const DTables* __restrict__ tabl
           if (cl < 0) {
             cl = feasible_prefix(T, kl, nc, ct);
           } else {
-            const double ml = T->minarr[kl], ttft = T->ttft;
-            const double* __restrict__ sbl = T->sb[kl];
-            while (cl > 0 && __dsub_rn(__dadd_rn(ct, sbl[cl - 1]), ml) > ttft) --cl;
+            const double* __restrict__ thl = T->thsw[kl];
+            while (cl > 0 && ct > thl[cl - 1]) --cl;
           }
           ok = cl > 0 || diag_passes(T, kl, ct, f);
         }
@@ -840,7 +872,8 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
     T->nb_beta = INFINITY;
     T->nb_R = INFINITY;
   }
-  // exact leaf-existence bounds of the two bottom levels (rexist)
+  // per-step thresholds, then the exact completion bounds (rexist)
+  if (T->sorted_ok) step_thresholds(T);
   if (K >= 3) leaf_exists_bounds(T);
   // A slice whose leading digits lie below the first list this kernel
   // writes (trees of at most 3 levels, or shallow final depths): every leaf
@@ -1220,9 +1253,9 @@ __device__ __forceinline__ int for_feasible_children(const DTables* __restrict__
 // with a feasible leaf (most rows have none: the last batch's deadline binds).
 __device__ __forceinline__ void leaves_counted(const DTables* __restrict__ T, int k, int nc, double t, double num_p,
                                                double den_p, double e_row, double a_row, int last, int rank_last,
-                                               double b0_last, int c, unsigned long long code_base, double hint,
+                                               double th0_last, int c, unsigned long long code_base, double hint,
                                                LeafAcc& a) {
-  const bool diag = !(__dsub_rn(__dadd_rn(t, b0_last), T->minarr[k]) > T->ttft);  // diag_passes
+  const bool diag = !(t > th0_last);  // diag_passes
   const int passed = c - (rank_last < c ? 1 : 0) + (diag ? 1 : 0);
   if (passed == 0) return;
   a.count += static_cast<unsigned long long>(passed);
@@ -1276,8 +1309,7 @@ __device__ __forceinline__ void two_sorted(const DTables* __restrict__ T, int k,
   const SRec* __restrict__ sr = T->srec[k];
   const unsigned short* __restrict__ si = T->sinfo[k];
   const int kl = k + 1;
-  const double ml = T->minarr[kl], ttft = T->ttft;
-  const double* __restrict__ sbl = T->sb[kl];
+  const double* __restrict__ thl = T->thsw[kl];
   int cl = -1;
   for (int j = 0; j < c; ++j) {
     const unsigned info = si[j];
@@ -1288,17 +1320,17 @@ __device__ __forceinline__ void two_sorted(const DTables* __restrict__ T, int k,
     if (cl < 0) {
       cl = feasible_prefix(T, kl, nc, t2);
     } else {
-      while (cl > 0 && __dsub_rn(__dadd_rn(t2, sbl[cl - 1]), ml) > ttft) --cl;
+      while (cl > 0 && t2 > thl[cl - 1]) --cl;
     }
 #ifdef BS_SWEEP_STATS
     a.st_children += 1;
 #endif
-    leaves_counted(T, kl, nc, t2, num, den, r.E, r.A, g, static_cast<int>(info >> 8), r.B0n, cl,
+    leaves_counted(T, kl, nc, t2, num, den, r.E, r.A, g, static_cast<int>(info >> 8), r.th0n, cl,
                    (code_base + static_cast<unsigned long long>(g)) * nc, hint, a);
   }
   if (k > 0 && diag_passes(T, k, t, last)) {
     const double t2 = __dadd_rn(t, T->B0[k][last]);
-    leaves_counted(T, kl, nc, t2, num, den, T->E[k][last], T->A[k][last], last, T->rank[kl][last], T->B0[kl][last],
+    leaves_counted(T, kl, nc, t2, num, den, T->E[k][last], T->A[k][last], last, T->rank[kl][last], T->th0[kl][last],
                    feasible_prefix(T, kl, nc, t2), (code_base + static_cast<unsigned long long>(last)) * nc, hint, a);
   }
 }

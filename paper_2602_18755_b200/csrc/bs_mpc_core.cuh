@@ -189,7 +189,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     T->sb[k][r] = v;
     T->ord[k][r] = static_cast<unsigned char>(f);
     T->rank[k][f] = static_cast<unsigned char>(r);
-    T->srec[k][r] = SRec{v, T->E[k][f], A, k + 1 < K ? T->B0[k + 1][f] : 0.0};
+    T->srec[k][r] = SRec{v, T->E[k][f], A, 0.0};  // th0n: step_thresholds
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     double amax = 0.0, pmin = INFINITY;
