@@ -705,24 +705,82 @@ __device__ inline SimOut simulate_decode(const DModels& m, const SimTrace& tr, c
 // Warp-cooperative simulate_decode_instance (simulator.hpp:441-578), no
 // controller, bit-identical to simulate_decode.
 //
-// Between two events -- the next retirement (known in advance: a resident
-// admitted at iteration i with o output tokens retires at the end of
-// iteration i + o - 1) and the next admissible arrival -- the batch size n is
-// constant and the summed context grows by n per iteration, so the features
-// of up to 32 future iterations are known before their start times are.  The
-// 32 lanes evaluate those iterations' latency and power interpolations in
-// parallel; lane 0 then runs the only truly serial part, the FP64 chain
-// t_done = t_start + 1.0 * L, and the warp locates the first iteration whose
-// end admits a waiting arrival (the window ends there), checks every token
-// gap, and accumulates the energy terms in record order.  All lanes hold the
-// same scalar state (redundant, divergence-free); the resident heap and the
-// per-window arrays live in the warp's shared memory.
+// The batch only gains members at an admission, and admissions happen only at
+// the first boundary after an arrival (or, while a request waits for KV room,
+// after a retirement).  Between two such points the composition of every
+// future iteration is known in advance: a resident admitted at iteration i
+// with o output tokens retires at the end of iteration i + o - 1, so the
+// batch size n and summed context s of iteration it0 + l follow from the
+// residents sorted by retirement (n = residents not yet retired, s = the
+// context at it0 plus every token generated since, minus the retired
+// residents' final contexts).  The 32 lanes derive those features for 32
+// consecutive iterations with warp scans, evaluate the latency and power
+// interpolations in parallel, lane 0 runs the only truly serial part (the
+// FP64 chain t_done = t_start + 1.0 * L), and the warp locates the first
+// iteration whose end reaches the next arrival (the window stops there),
+// checks every token gap and accumulates the energy terms in record order.
+// All lanes hold the same scalar state (redundant, divergence-free); the
+// residents (an array sorted by retirement) and the per-chunk arrays live in
+// the warp's shared memory.
 struct WarpScratch {
-  Resident* heap;  // heap_cap entries
+  Resident* heap;  // heap_cap entries: the residents, ascending retirement
   double* L;       // 32
   double* P;       // 32
   double* T;       // 32
 };
+
+// Insert r after every resident retiring no later (warp-cooperative).
+__device__ __forceinline__ void res_insert(Resident* a, int n, Resident r, int lane) {
+  int pos = 0;
+  for (int b = 0; b < n; b += 32) {
+    const int j = b + lane;
+    const unsigned le = __ballot_sync(0xffffffffu, j < n && !(r.retire < a[j].retire));
+    pos += __popc(le);
+    if (le != 0xffffffffu) break;
+  }
+  for (int top = n; top > pos; top -= 32) {  // shift [pos, n) up by one, highest first
+    const int j = top - 1 - lane;
+    const bool act = j >= pos;
+    Resident v;
+    if (act) v = a[j];
+    __syncwarp();
+    if (act) a[j + 1] = v;
+    __syncwarp();
+  }
+  if (lane == 0) a[pos] = r;
+  __syncwarp();
+}
+
+// Retire every resident with retire <= last_it (a prefix of the array);
+// returns how many, their summed needs in *need_sum.
+__device__ __forceinline__ int res_retire(Resident* a, int n, long long last_it, long long* need_sum, int lane) {
+  int c = 0;
+  long long s = 0;
+  for (int b = 0; b < n; b += 32) {
+    const int j = b + lane;
+    const bool r = j < n && a[j].retire <= last_it;
+    long long v = r ? a[j].need : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    s += v;
+    const unsigned m = __ballot_sync(0xffffffffu, r);
+    c += __popc(m);
+    if (m != 0xffffffffu) break;
+  }
+  if (c > 0) {
+    for (int b = 0; b < n - c; b += 32) {  // shift the survivors down, lowest first
+      const int j = b + lane;
+      const bool act = j < n - c;
+      Resident v;
+      if (act) v = a[j + c];
+      __syncwarp();
+      if (act) a[j] = v;
+      __syncwarp();
+    }
+  }
+  *need_sum = s;
+  return c;
+}
 
 __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& tr, const SimParams& p, WarpScratch ws,
                                        int heap_cap, int lane) {
@@ -744,7 +802,7 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
   int n_res = 0;
   long long sum_ctx = 0, reserved = 0, it = 0;
   double prev_end = 0.0;
-  Resident* heap = ws.heap;
+  Resident* res = ws.heap;
 
   auto record_idle = [&](double from, double to) -> bool {
     if (to <= from) return true;
@@ -757,22 +815,10 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
     return true;
   };
 
-  // the next not-yet-pulled request (index arr), cached: its arrival and KV
-  // need are read once per request instead of at every event window
-  int r_nx = -1;
+  // the next not-yet-pulled request (index arr), cached: its arrival is read
+  // once per request instead of at every event window
   double a_nx = INFINITY;
-  long long need_nx = 0;
-  auto refresh_next = [&]() {
-    if (arr < tr.n) {
-      r_nx = tr.kept[arr];
-      a_nx = tr.arrival[r_nx];
-      need_nx = tr.input[r_nx] + tr.output[r_nx];
-    } else {
-      r_nx = -1;
-      a_nx = INFINITY;
-      need_nx = 0;
-    }
-  };
+  auto refresh_next = [&]() { a_nx = arr < tr.n ? tr.arrival[tr.kept[arr]] : INFINITY; };
   refresh_next();
   int poll = 0;
   while (arr < tr.n || whead < arr || n_res > 0) {
@@ -809,9 +855,7 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
       Resident rs;
       rs.retire = it + tr.output[r] - 1;
       rs.need = need;
-      int nn = n_res;
-      if (lane == 0) heap_push(heap, nn, rs);
-      __syncwarp();
+      res_insert(res, n_res, rs, lane);
       n_res += 1;
       reserved += need;
       sum_ctx += tr.input[r];
@@ -832,41 +876,65 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
       now = t_next;
       continue;
     }
-    // ---- the event window: iterations it .. R at constant n (R = next retirement)
-    const long long R = heap[0].retire;
-    // the next arrival matters at the first boundary it has reached, unless
-    // admission stays blocked until a retirement (n and reserved are constant
-    // inside the window); a request too large for the KV cache always stops
-    // the window (admit throws, simulator.hpp:459-462)
-    bool arrival_cuts = false;
-    double t_a = INFINITY;
-    if (whead == arr && arr < tr.n) {
-      arrival_cuts =
-          need_nx > p.kv_capacity || (n_res < p.max_batch_requests && reserved + need_nx <= p.kv_capacity);
-      t_a = a_nx;
-    }
+    // ---- the event window: from iteration it to the next admission point.
+    // Every arrival stops the window at the first boundary it has reached
+    // (pulling it early changes nothing; a request too large for the KV cache
+    // must stop it, admit throws, simulator.hpp:459-462).  While a request
+    // waits for KV room the window also stops at the next retirement.
+    const bool blocked = whead < arr;
+    const double t_a = a_nx;
     bool first_chunk = true, cut = false;
     long long it0 = it;
-    // brackets of the window's constant axes (fixed ones and n_requests = n_res)
-    FastBrk bl, bp;
-    if (!lat.bad) fast_brackets_nreq(lat, n_res, bl);
-    if (!pw.bad && !share) fast_brackets_nreq(pw, n_res, bp);
     while (!cut) {
-      const long long left = R - it0 + 1;
-      const int mcount = left < 32 ? static_cast<int>(left) : 32;
-      // parallel: features and predictions of iterations it0 .. it0 + mcount - 1
-      // latency is needed for every iteration (t_done); power only for a
-      // segment of positive length (record_segment returns before
-      // exec_power when to <= from, simulator.hpp:214-215)
+      // how many iterations this chunk may cover: the batch empties after the
+      // last retirement; lanes see at most 32 retirements before their start
+      long long lim = res[n_res - 1].retire - it0 + 1;
+      if (n_res > 32) lim = min(lim, res[32].retire - it0 + 1);
+      if (blocked) lim = min(lim, res[0].retire - it0 + 1);
+      const int mcount = lim < 32 ? static_cast<int>(lim) : 32;
+      // composition of iteration it0 + lane: residents retired before it
+      const long long rl = lane < n_res ? res[lane].retire : LLONG_MAX;
+      long long ndp = lane < n_res ? res[lane].need : 0;  // -> inclusive prefix of needs
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, ndp, o2);
+        if (lane >= o2) ndp += v;
+      }
+      int cend = 0;  // residents retiring by the end of iteration it0 + lane (capped at 32)
+      {
+        const long long x = it0 + lane;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const long long v = __shfl_sync(0xffffffffu, rl, cend + step - 1);
+          if (v <= x) cend += step;
+        }
+        const long long v = __shfl_sync(0xffffffffu, rl, cend < 31 ? cend : 31);
+        if (cend == 31 && v <= x) cend = 32;
+      }
+      int cbeg = __shfl_up_sync(0xffffffffu, cend, 1);
+      if (lane == 0) cbeg = 0;
+      const int nl = n_res - cbeg;
+      const long long ndb = __shfl_sync(0xffffffffu, ndp, (cbeg - 1) & 31);
+      const long long gone = cbeg > 0 ? ndb : 0;
+      int ninc = nl;  // inclusive prefix of the batch sizes
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, ninc, o2);
+        if (lane >= o2) ninc += v;
+      }
+      // parallel: predictions of iterations it0 .. it0 + mcount - 1; latency
+      // is needed for every iteration (t_done), power only for a segment of
+      // positive length (record_segment returns before exec_power when
+      // to <= from, simulator.hpp:214-215)
       bool bad = false, pbad = false;
       if (lane < mcount) {
-        const long long s = sum_ctx + static_cast<long long>(lane) * n_res;
+        const long long s = sum_ctx + static_cast<long long>(ninc - nl) - gone;
         double Lv = 0.0, Pv = 0.0;
-        // predict_at(lat / pw, n_res, s) with the window's brackets
+        FastBrk bl;
         if (lat.bad) {
           bad = true;
         } else {
-          fast_brackets_sum(lat, s, bl);
+          fast_brackets(lat, nl, s, bl);
           Lv = fast_corners(lat, bl);
           bad = !model_value_ok(Lv);
         }
@@ -876,7 +944,8 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
           if (share) {
             Pv = fast_corners(pw, bl);
           } else {
-            fast_brackets_sum(pw, s, bp);
+            FastBrk bp;
+            fast_brackets(pw, nl, s, bp);
             Pv = fast_corners(pw, bp);
           }
           pbad = !model_value_ok(Pv);
@@ -887,7 +956,7 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
       const unsigned badm = __ballot_sync(0xffffffffu, bad);
       const unsigned pbadm = __ballot_sync(0xffffffffu, pbad);
       const int first_bad = badm ? __ffs(badm) - 1 : mcount;
-      // serial: end times of the window's iterations (simulator.hpp:362, 537)
+      // serial: end times of the chunk's iterations (simulator.hpp:362, 537)
       __syncwarp();
       if (lane == 0) {  // 1.0 * L == L exactly, so the chain is one DADD per iteration
         double t = now;
@@ -898,14 +967,15 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
         }
       }
       __syncwarp();
-      // where does the window stop?  at the first iteration whose end admits
-      // the waiting arrival, at the retirement, or at a model error
+      // where does the window stop?  at the first iteration whose end reaches
+      // the next arrival, or at a model error
       bool stop_here = false;
-      if (lane < first_bad) stop_here = arrival_cuts && ws.T[lane] >= t_a;
+      if (lane < first_bad) stop_here = ws.T[lane] >= t_a;
       const unsigned stopm = __ballot_sync(0xffffffffu, stop_here);
       int last = first_bad - 1;  // last iteration simulated in this chunk
       if (stopm) last = min(last, __ffs(stopm) - 1);
-      // token gaps (max_tbt_ms, simulator.hpp:81-89) for iterations 0..last
+      // token gaps (max_tbt_ms, simulator.hpp:81-89) for iterations 0..last;
+      // a resident of iteration l > 0 also produced a token in iteration l - 1
       bool viol = false;
       if (lane <= last) {
         const double t_start = lane == 0 ? now : ws.T[lane - 1];
@@ -922,7 +992,7 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
         o.meets_slo = 0;
         if (p.early_exit) return o;
       }
-      // energy of the segments, in record order (simulator.hpp:213-228)
+      // energy of the segments, in record order (simulator.hpp:213-228):
       // each lane forms its segment's energy term; lane 0 adds them in record
       // order (the only serial part)
       bool seg = false;
@@ -936,12 +1006,11 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
       const unsigned perrm = segm & pbadm;
       const int perr = perrm ? __ffs(perrm) - 1 : -1;
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) {  // a skipped segment's term is +0.0 and busy >= +0.0: adding it is exact
         double busy = o.busy_j;
         const int upto = perr >= 0 ? perr - 1 : last;
 #pragma unroll 8
-        for (int l = 0; l <= upto; ++l)
-          if ((segm >> l) & 1u) busy = __dadd_rn(busy, ws.L[l]);
+        for (int l = 0; l <= upto; ++l) busy = __dadd_rn(busy, ws.L[l]);
         ws.P[0] = busy;
       }
       __syncwarp();
@@ -953,12 +1022,21 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
         o.model_err = 2;
         return o;
       }
+      int retired = 0;
       if (last >= 0) {
         const double t_end = ws.T[last];
-        sum_ctx += n_res * static_cast<long long>(last + 1);
+        sum_ctx += __shfl_sync(0xffffffffu, ninc, last);
         it0 += last + 1;
         now = t_end;
         prev_end = t_end;
+        __syncwarp();
+        // retirements at the ends of the chunk's iterations (simulator.hpp:546-555)
+        long long freed = 0;
+        retired = res_retire(res, n_res, it0 - 1, &freed, lane);
+        n_res -= retired;
+        reserved -= freed;
+        sum_ctx -= freed;
+        o.completed += retired;
       }
       __syncwarp();
       if (first_bad < mcount && last == first_bad - 1 && !stopm) {
@@ -967,21 +1045,9 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
         return o;
       }
       first_chunk = false;
-      cut = stopm != 0 || it0 > R;
+      cut = stopm != 0 || n_res == 0 || (blocked && retired > 0);
     }
     it = it0;
-    // retirements at the end of iteration it - 1 (simulator.hpp:546-555)
-    while (n_res > 0 && heap[0].retire <= it - 1) {
-      const Resident r = heap[0];
-      int nn = n_res;
-      __syncwarp();
-      if (lane == 0) heap_pop(heap, nn);
-      __syncwarp();
-      n_res -= 1;
-      reserved -= r.need;
-      sum_ctx -= r.need;
-      ++o.completed;
-    }
   }
   o.horizon_ms = fmax(tr.duration_ms, now);
   record_idle(now, o.horizon_ms);
