@@ -830,6 +830,51 @@ def bench_c4_experiment(dev, with_cpu: bool) -> dict:
     return out
 
 
+EXTRA_ROOF = {"c1_demo": "c1", "c2_loose_slo": "c2l", "c3_placement": "c3", "c4_replay": "c4", "c4_day": "c4d",
+              "c4_experiment": "c4x", "c5_greedy": "c5g", "c5_exhaustive": "c5x"}
+
+
+def extra_roofline(cfg: str, fp64_peak: float | None) -> dict | None:
+    """Executed roofline of a sub-benchmark's dominant kernel: ncu's FP64-pipe
+    and issue fractions, occupancy and DRAM bytes of one launch
+    (profiles/r02_rooflines.json, tools/ncu_rooflines.sh), against the FP64
+    issue peak of this box and the measured HBM bandwidth."""
+    path = ROOT / "profiles" / "r02_rooflines.json"
+    try:
+        doc = json.loads(path.read_text())
+        r = doc["configs"][cfg]
+    except Exception:
+        return None
+    hbm = None
+    try:
+        hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs")
+    except Exception:
+        pass
+    traffic = r.get("dram_read_bytes", 0.0) + r.get("dram_write_bytes", 0.0)
+    dur = r.get("duration_us")
+    gbs = traffic / (dur * 1e-6) / 1e9 if dur else None
+    frac = r.get("fp64_pipe_active_frac")
+    return {"bound": "fp64-issue (latency: dependent FP64 chains)", "kernel": r.get("kernel"), "unit": "TFLOP/s",
+            "peak": fp64_peak / 1e12 if fp64_peak else None, "frac": frac,
+            "achieved": frac * fp64_peak / 1e12 if (frac is not None and fp64_peak) else None,
+            "issue_slots_busy_frac": r.get("issue_slots_busy_frac"),
+            "achieved_occupancy": r.get("achieved_occupancy"),
+            "avg_active_threads_per_warp": r.get("avg_active_threads_per_warp"),
+            "traffic": traffic, "hbm_gbs": gbs, "hbm_frac": gbs / hbm if (gbs is not None and hbm) else None,
+            "duration_us_ncu": dur, "launch": {k: r.get(k) for k in ("grid", "block", "registers")},
+            "source": f"profiles/r02_rooflines.json ({doc.get('source', '')})"}
+
+
+def fp64_peak_of(dev) -> float | None:
+    try:
+        lib = dev._lib
+        peak, peak_ms = C.c_double(), C.c_double()
+        dev.check(lib.bs_fp64_peak(dev.handle, C.byref(peak), C.byref(peak_ms)))
+        return peak.value
+    except Exception:
+        return None
+
+
 def run_extras(args, dev, rank, world, local) -> dict:
     with_cpu = world == 1 and not args.no_cpu_baseline
     todo = [args.only] if args.only else ["c1", "c2l", "c3", "c4", "c4d", "c4x", "c5g", "c5x"]
@@ -855,6 +900,13 @@ def run_extras(args, dev, rank, world, local) -> dict:
             out["c5_greedy"] = bench_c5(dev, "greedy", rank, world, local, 4096, with_cpu)
         else:
             out["c5_exhaustive"] = bench_c5(dev, "exhaustive", rank, world, local, args.c5x_decisions, with_cpu)
+    if rank == 0:
+        peak = fp64_peak_of(dev)
+        for key, obj in out.items():
+            if isinstance(obj, dict) and key in EXTRA_ROOF:
+                roof = extra_roofline(EXTRA_ROOF[key], peak)
+                if roof is not None:
+                    obj["roofline"] = roof
     return out
 
 

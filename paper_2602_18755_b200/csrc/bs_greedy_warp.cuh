@@ -107,10 +107,44 @@ __device__ __forceinline__ bool wstep(const WTables& T, const DProblem& pr, cons
 // All mutations of one level with a common prefix (digits 0..J-1 fixed =
 // `prefix`, digit i <-> position pos[i]); folds feasible ones into
 // (bo, bc, feas).  digit -> candidate: 0 target, 1 r1, 2 r2.
+// Division-free leaf filter (exactness argument 5; the level's
+// tables must have every A >= 0 and finite and E finite): a mutation whose
+// objective provably exceeds min(incumbent, this thread's best) is only
+// counted.  One above the incumbent can never be accepted (dvfs.hpp:242-249)
+// and one above the thread's best never wins its reduction; ties are never
+// skipped, so the lexicographic rule holds.
+constexpr double kGFilterScale = 1.0 + 0x1p-50;
+constexpr double kGFilterMinBest = 0x1p-100;
+constexpr double kGFilterMinDen = 0x1p-900;
+
+__device__ __forceinline__ double gfilter_scaled(double thr) {
+  return thr >= kGFilterMinBest ? __dmul_rn(thr, kGFilterScale) : (thr == 0.0 ? 0.0 : INFINITY);
+}
+
+struct GLeafAcc {
+  unsigned long long bo, bc, feas;
+  double thr_s;  // scaled filter threshold (INFINITY: no filter)
+  double incumbent;
+  bool filt;
+};
+
+__device__ __forceinline__ void gleaf(GLeafAcc& g, double n, double d, unsigned long long code,
+                                      unsigned long long lex) {
+  if (code == 0) return;  // the unmutated assignment is not a mutation
+  ++g.feas;
+  if (g.filt && d >= kGFilterMinDen && n > __dmul_rn(g.thr_s, d)) return;  // objective > threshold
+  const double obj = d > 0.0 ? __ddiv_rn(n, d) : 0.0;
+  const unsigned long long ob = static_cast<unsigned long long>(__double_as_longlong(obj));
+  if (key_less(ob, lex, g.bo, g.bc)) {
+    g.bo = ob;
+    g.bc = lex;
+    g.thr_s = gfilter_scaled(obj < g.incumbent ? obj : g.incumbent);
+  }
+}
+
 __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* cur,
                            const int* pos, int np, int base, int target, int r1, int r2, int J,
-                           unsigned long long prefix, unsigned long long& bo, unsigned long long& bc,
-                           unsigned long long& feas) {
+                           unsigned long long prefix, GLeafAcc& g) {
   const int K = T.K;
   auto cand_of = [&](int d) { return d == 0 ? target : (d == 1 ? r1 : r2); };
   // prefix digits (least significant = earliest position)
@@ -138,16 +172,7 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
   }
   unsigned long long lexp = 0;  // lex key of the prefix digits
   for (int i = 0; i < J; ++i) lexp = lexp * base + static_cast<unsigned long long>(base - 1 - dig[i]);
-  auto leaf = [&](double n, double d, unsigned long long code, unsigned long long lex) {
-    if (code == 0) return;  // the unmutated assignment is not a mutation
-    ++feas;
-    const double obj = d > 0.0 ? __ddiv_rn(n, d) : 0.0;
-    const unsigned long long ob = static_cast<unsigned long long>(__double_as_longlong(obj));
-    if (key_less(ob, lex, bo, bc)) {
-      bo = ob;
-      bc = lex;
-    }
-  };
+  auto leaf = [&](double n, double d, unsigned long long code, unsigned long long lex) { gleaf(g, n, d, code, lex); };
   if (J == np) {
     leaf(num, den, prefix, lexp);
     return;
@@ -198,6 +223,62 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
   }
 }
 
+// The same mutations as wlevel_dfs for R = np - J <= 2 remaining digits, by
+// nested loops in registers (no per-depth stack): the latency mode of a
+// decision spread over a whole CTA, where every thread owns few prefixes.
+// pwJ = base^J.
+__device__ void wlevel_tail(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* cur,
+                            const int* pos, int np, int base, int target, int r1, int r2, int J,
+                            unsigned long long pwJ, unsigned prefix, GLeafAcc& g) {
+  const int K = T.K;
+  auto cand_of = [&](int d) { return d == 0 ? target : (d == 1 ? r1 : r2); };
+  double t = pr.now, num = 0.0, den = 0.0;
+  int last = -1;
+  unsigned rem = prefix;
+  unsigned long long lexp = 0;
+  int pi = 0;
+  const int stop0 = J < np ? pos[J] : K;
+  for (int k = 0; k < stop0; ++k) {
+    int f = cur[k];
+    if (pi < J && pos[pi] == k) {
+      const unsigned q = base == 3 ? rem / 3u : rem >> 1;
+      const int d = static_cast<int>(rem - q * static_cast<unsigned>(base));
+      rem = q;
+      f = cand_of(d);
+      lexp = lexp * base + static_cast<unsigned long long>(base - 1 - d);
+      ++pi;
+    }
+    if (!wstep(T, pr, c, k, f, t, num, den, last)) return;
+  }
+  if (J == np) {
+    gleaf(g, num, den, prefix, lexp);
+    return;
+  }
+  const int e0 = J + 1 < np ? pos[J + 1] : K;
+  for (int d0 = 0; d0 < base; ++d0) {
+    double t1 = t, n1 = num, dn1 = den;
+    int l1 = last;
+    bool ok = wstep(T, pr, c, pos[J], cand_of(d0), t1, n1, dn1, l1);
+    for (int k = pos[J] + 1; ok && k < e0; ++k) ok = wstep(T, pr, c, k, cur[k], t1, n1, dn1, l1);
+    if (!ok) continue;
+    const unsigned long long code1 = prefix + static_cast<unsigned long long>(d0) * pwJ;
+    const unsigned long long lex1 = lexp * base + static_cast<unsigned long long>(base - 1 - d0);
+    if (J + 1 == np) {
+      gleaf(g, n1, dn1, code1, lex1);
+      continue;
+    }
+    for (int d1 = 0; d1 < base; ++d1) {  // digit J + 1, the last (R == 2)
+      double t2 = t1, n2 = n1, dn2 = dn1;
+      int l2 = l1;
+      bool ok2 = wstep(T, pr, c, pos[J + 1], cand_of(d1), t2, n2, dn2, l2);
+      for (int k = pos[J + 1] + 1; ok2 && k < K; ++k) ok2 = wstep(T, pr, c, k, cur[k], t2, n2, dn2, l2);
+      if (!ok2) continue;
+      gleaf(g, n2, dn2, code1 + static_cast<unsigned long long>(d1) * pwJ * base,
+            lex1 * base + static_cast<unsigned long long>(base - 1 - d1));
+    }
+  }
+}
+
 // greedy_freq_select for one decision by NW cooperating warps: the calling
 // warp (NW == 1: any warp of a CTA running several decisions) or the whole
 // CTA (NW > 1, blockDim.x == 32 NW: one decision per CTA, for batches too
@@ -210,6 +291,17 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
 // stats.  Results in *o (thread 0 writes; the group is synchronised on return).
 //   share: every fl[f] (and every fp[f]) has the brackets of fl[0] (fp[0])
 //   (fast_same_brackets), so each batch is bracketed once for all candidates.
+#ifdef BS_GREEDY_PHASES  // diagnostics build: globaltimer at phase ends, printed by thread 0
+#define BS_GPH(i)                                                 \
+  if (tid == 0) {                                                 \
+    unsigned long long t_;                                        \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+    gph[i] = t_;                                                  \
+  }
+#else
+#define BS_GPH(i)
+#endif
+
 template <int NW>
 __device__ __forceinline__ void greedy_sync() {
   if (NW == 1)
@@ -226,6 +318,11 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
   const int lane = threadIdx.x & 31;
   const int tid = NW == 1 ? lane : static_cast<int>(threadIdx.x);
   WTables& T = S.T;
+#ifdef BS_GREEDY_PHASES
+  unsigned long long gph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int gph_levels = 0;
+#endif
+  BS_GPH(0);
   if (tid == 0) {
     T.nc = c.nc;
     T.ttft = c.ttft;
@@ -238,6 +335,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
     o->K = T.K;
   }
   greedy_sync<NW>();
+  BS_GPH(1);
   if (T.status != BS_OK) return;
   const int K = T.K, nc = c.nc;
   if (K == 0) {  // dvfs.hpp:194-197
@@ -245,7 +343,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
     greedy_sync<NW>();
     return;
   }
-  unsigned anybad = 0;
+  unsigned anybad = 0, nofilt = 0;
   const bool shared_brk = fl && share;
   if (shared_brk) {
     if (tid < K) {
@@ -280,17 +378,21 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
     T.A[e] = A;
     T.P[e] = P;
     T.E[e] = __dmul_rn(A, P);                                               // dvfs.hpp:167
+    if (!(A >= 0.0) || !isfinite(A) || !isfinite(T.E[e])) nofilt = 1;
     T.B0[e] = __dmul_rn(A, c.one_plus_margin);                              // dvfs.hpp:115
     T.B1[e] = __dmul_rn(__dadd_rn(A, c.switch_ms), c.one_plus_margin);      // dvfs.hpp:114-115
     if (k == 0) T.T1[f] = __dadd_rn(pr.now, c.cand[f] != pr.cur_freq ? T.B1[e] : T.B0[e]);
   }
-  bool bad;
+  bool bad, filt;
   if (NW == 1) {
     bad = __any_sync(0xffffffffu, anybad);
+    filt = !__any_sync(0xffffffffu, nofilt);
     __syncwarp();
   } else {
     bad = __syncthreads_or(anybad) != 0;
+    filt = __syncthreads_or(nofilt) == 0;
   }
+  BS_GPH(2);
   // all-max initialization (dvfs.hpp:201-205)
   if (tid == 0) {
     for (int k = 0; k < K; ++k) S.cur[k] = static_cast<unsigned char>(nc - 1);
@@ -317,6 +419,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
     o->objective = obj;
   }
   greedy_sync<NW>();
+  BS_GPH(3);
   if (o->status != BS_OK) return;
   if (S.accepted && nc > 1) {
     const int last_level = nc >= 3 ? nc - 2 : 1;
@@ -342,15 +445,45 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
       const unsigned long long combos = ipow(static_cast<unsigned long long>(base), np);
       unsigned long long bo = ~0ull, bc = ~0ull, feas = 0, errkey = ~0ull;
       if (!bad) {
-        // prefixes of the first J digits spread over lanes
-        int J = 0;
-        unsigned long long tasks = 1;
-        while (J < np && tasks < 2ull * NT) {
-          tasks *= base;
-          ++J;
+        GLeafAcc g;
+        g.bo = ~0ull;
+        g.bc = ~0ull;
+        g.feas = 0;
+        g.filt = filt;
+        g.incumbent = S.obj;
+        g.thr_s = gfilter_scaled(S.obj);
+        if (NW > 1 && combos <= (1ull << 31)) {
+          // latency mode: prefixes of all but the last R <= 2 digits, R
+          // chosen for the shortest per-thread path (rounds x steps)
+          int J = np;
+          unsigned long long best_cost = ~0ull;
+          for (int R = 0; R <= 2 && R <= np; ++R) {
+            const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), np - R);
+            const unsigned long long rounds = (tasks + NT - 1) / NT;
+            const unsigned long long steps = K + (R >= 1 ? base : 0) + (R == 2 ? base * base : 0);
+            if (rounds * steps < best_cost) {
+              best_cost = rounds * steps;
+              J = np - R;
+            }
+          }
+          const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), J);
+          const unsigned long long pwJ = tasks;
+          for (unsigned long long p = tid; p < tasks; p += NT)
+            wlevel_tail(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, pwJ, static_cast<unsigned>(p), g);
+        } else {
+          // prefixes of the first J digits spread over lanes
+          int J = 0;
+          unsigned long long tasks = 1;
+          while (J < np && tasks < 2ull * NT) {
+            tasks *= base;
+            ++J;
+          }
+          for (unsigned long long p = tid; p < tasks; p += NT)
+            wlevel_dfs(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, p, g);
         }
-        for (unsigned long long p = tid; p < tasks; p += NT)
-          wlevel_dfs(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, p, bo, bc, feas);
+        bo = g.bo;
+        bc = g.bc;
+        feas = g.feas;
       } else {
         unsigned char mut[kMaxK];
         for (int k = 0; k < K; ++k) mut[k] = S.cur[k];
@@ -445,12 +578,21 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
         S.accepted = Lv.accepted;
       }
       greedy_sync<NW>();
+#ifdef BS_GREEDY_PHASES
+      ++gph_levels;
+#endif
       if (o->status != BS_OK || S.accepted == 0) break;
     }
   }
+  BS_GPH(4);
   if (tid == 0 && o->status == BS_OK)
     for (int k = 0; k < K; ++k) o->idx[k] = S.cur[k];
   greedy_sync<NW>();
+#ifdef BS_GREEDY_PHASES
+  if (tid == 0 && NW > 1)
+    printf("greedy phases ns: project %llu tables %llu init %llu levels %llu (%d levels, K %d nc %d)\n",
+           gph[1] - gph[0], gph[2] - gph[1], gph[3] - gph[2], gph[4] - gph[3], gph_levels, K, nc);
+#endif
 }
 
 // One decision per warp (the batch kernels and the cluster replay).

@@ -245,14 +245,19 @@ __host__ __device__ inline FastGrid fast_grid2(const DGrid& rd, const DGrid& st_
 
 __device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double freq) { return fast_grid2(g, g, tp, freq); }
 
-// bracket() without a dependent load chain: std::upper_bound's index in a
-// sorted knot vector is the number of knots k with !(x < k); the loads are
-// independent and the count is branch-free.
+// bracket() as a branch-free search: std::upper_bound's index in a sorted
+// knot vector (the number of knots k with !(x < k)) by halving steps whose
+// count depends on n only, so the lanes of a warp never diverge.
 __device__ __forceinline__ void bracket_count(const double* __restrict__ k, int n, double x, int* lo, double* frac) {
   const double k0 = __ldg(k), kn = __ldg(k + n - 1);
   if (x < k0 || x > kn) x = x < k0 ? k0 : (kn < x ? kn : x);
-  int cnt = 0;
-  for (int i = 0; i < n; ++i) cnt += !(x < __ldg(k + i)) ? 1 : 0;
+  int base = 0;
+  for (int len = n; len > 1;) {
+    const int half = len >> 1;
+    base = !(x < __ldg(k + base + half)) ? base + half : base;
+    len -= half;
+  }
+  const int cnt = base + (!(x < __ldg(k + base)) ? 1 : 0);
   const int hi = cnt < 1 ? 1 : (cnt > n - 1 ? n - 1 : cnt);
   *lo = hi - 1;
   const double klo = __ldg(k + hi - 1), khi = __ldg(k + hi);
