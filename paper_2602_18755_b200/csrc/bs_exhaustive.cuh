@@ -109,22 +109,42 @@ struct DThr {
   double rn[kMaxCand * kMaxCand];  // row g: tau_N[g][*] (g the node's last digit), descending
 };
 
-// Number of leading entries >= t of a descending array.
+// Number of leading entries >= t of a descending array, by branch-free
+// halving: the step count depends on n only, and a step's load does not wait
+// on a branch.
 __device__ __forceinline__ int count_ge(const double* __restrict__ a, int n, double t) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] >= t)
-      lo = mid + 1;
-    else
-      hi = mid;
+  if (n <= 0) return 0;
+  int base = 0;
+  for (int len = n; len > 1;) {
+    const int half = len >> 1;
+    base = a[base + half] >= t ? base + half : base;
+    len -= half;
   }
-  return lo;
+  return base + (a[base] >= t ? 1 : 0);
 }
 
-// Feasible leaves below a node at depth K-2 (clock t, last digit l).
+// Feasible leaves below a node at depth K-2 (clock t, last digit l).  The
+// three searches run in lockstep (the two row searches finish within the
+// table-wide one), so their loads are in flight together.
 __device__ __forceinline__ int thr_leaf_count(const DThr* __restrict__ H, int nc, double t, int l) {
-  return count_ge(H->cs, nc * nc, t) - count_ge(H->rs + l * nc, nc, t) + count_ge(H->rn + l * nc, nc, t);
+  const double* __restrict__ cs = H->cs;
+  const double* __restrict__ rs = H->rs + l * nc;
+  const double* __restrict__ rn = H->rn + l * nc;
+  int b0 = 0, b1 = 0, b2 = 0, l1 = nc;
+  for (int l0 = nc * nc; l0 > 1;) {
+    const int h0 = l0 >> 1;
+    const double v0 = cs[b0 + h0];
+    if (l1 > 1) {
+      const int h1 = l1 >> 1;
+      const double v1 = rs[b1 + h1], v2 = rn[b2 + h1];
+      b1 = v1 >= t ? b1 + h1 : b1;
+      b2 = v2 >= t ? b2 + h1 : b2;
+      l1 -= h1;
+    }
+    b0 = v0 >= t ? b0 + h0 : b0;
+    l0 -= h0;
+  }
+  return (b0 + (cs[b0] >= t ? 1 : 0)) - (b1 + (rs[b1] >= t ? 1 : 0)) + (b2 + (rn[b2] >= t ? 1 : 0));
 }
 
 // The seed's node bound ("seed node bound"): every leaf below a
@@ -432,28 +452,26 @@ __device__ __forceinline__ unsigned long long warp_append(unsigned long long* co
 // by monotonicity of correctly rounded add/subtract in the step, the
 // passing candidates form a prefix of the sorted order ord[k].
 __device__ __forceinline__ int feasible_prefix(const DTables* __restrict__ T, int k, int nc, double t) {
-  int lo = 0, hi = nc;  // first failing position
+  // the passing positions are a prefix: branch-free halving for its length
+  if (nc <= 0) return 0;
+  int base = 0;
   if (k == 0) {  // level 0's keys are the clocks themselves (T1)
     const double m = T->minarr[0], ttft = T->ttft;
     const double* __restrict__ sb = T->sb[0];
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (__dsub_rn(sb[mid], m) > ttft)
-        hi = mid;
-      else
-        lo = mid + 1;
+    for (int len = nc; len > 1;) {
+      const int half = len >> 1;
+      base = !(__dsub_rn(sb[base + half], m) > ttft) ? base + half : base;
+      len -= half;
     }
-    return lo;
+    return base + (!(__dsub_rn(sb[base], m) > ttft) ? 1 : 0);
   }
   const double* __restrict__ th = T->thsw[k];  // t passes position j iff t <= th[j]
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (t > th[mid])
-      hi = mid;
-    else
-      lo = mid + 1;
+  for (int len = nc; len > 1;) {
+    const int half = len >> 1;
+    base = !(t > th[base + half]) ? base + half : base;
+    len -= half;
   }
-  return lo;
+  return base + (!(t > th[base]) ? 1 : 0);
 }
 
 // Does the non-switching child (step B0[k][last], k >= 1) pass meets_slo's check?
@@ -1127,7 +1145,12 @@ __global__ void __launch_bounds__(kPrepThreads) thr_kernel(DTables* tables, DThr
 // for two swept levels, 4 (64) for three, where more warps hide the longer
 // per-thread walks (measured: C2 0.42 vs 0.45 ms; C5 3,838 vs 4,298
 // decisions/s).
-constexpr int kSweepMinB2 = 3, kSweepMinB3 = 4;
+#ifndef BS_SWEEP2_MINB
+#define BS_SWEEP2_MINB 4  // 64 registers (spills to L1) and 4 CTAs/SM: C2 sweep 0.152 -> 0.140 ms, loose 0.61 -> 0.55 ms
+#endif
+// resident CTAs per SM of the two-level (kSweep2) and three-level (kSweep3) sweep instances
+constexpr int kSweepMinB2 = BS_SWEEP2_MINB, kSweepMinB3 = 4;
+constexpr int kSweep2 = 2, kSweep3 = 3;
 
 // Per-thread accumulator of the sweep.
 struct LeafAcc {
@@ -1428,7 +1451,7 @@ __device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsig
 }
 
 // One thread per final node: the I bottom levels of its subtree.
-template <int MINB>
+template <int MINB, int LEVELS>
 __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restrict__ tables,
                                                           const DThr* __restrict__ thr, const ExCtl* ctl,
                                                           FinalList fin, Key128* best, unsigned long long* feas,
@@ -1481,7 +1504,7 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
         a.st_slow += 1;
 #endif
         two_sorted(T, FD, nc, t, num, den, last, cb, hint, a);
-      } else if (MINB == kSweepMinB3) {  // three swept levels only occur in batches launched with MINB 4
+      } else if (LEVELS == kSweep3) {  // three swept levels only occur in batches launched with this instance
         for_feasible_children(T, FD, nc, t, num, den, last, [&](int e, double t3, double n3, double d3) {
           if (T->rex_ok && t3 > T->rexist[K - 2][e]) return;  // no feasible leaf below this child
           if (use_thr && (node_dom_seed(T, n3, d3) || node_dominated(a, n3, d3))) {

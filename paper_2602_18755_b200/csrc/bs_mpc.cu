@@ -523,8 +523,8 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   if (!run->bfs_grid) {  // occupancy queries once per context
     if (!ctx->grid_cache[0]) {
       ctx->grid_cache[0] = grid_for(ctx, reinterpret_cast<const void*>(bfs_node_kernel), 256);
-      ctx->grid_cache[1] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2>), 256);
-      ctx->grid_cache[2] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3>), 256);
+      ctx->grid_cache[1] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2, kSweep2>), 256);
+      ctx->grid_cache[2] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3, kSweep3>), 256);
     }
     run->bfs_grid = ctx->grid_cache[0];
     run->sweep_grid2 = ctx->grid_cache[1];
@@ -557,11 +557,11 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   }
   BS_REC(3);
   if (run->sweep3)
-    BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB3>, dim3(run->sweep_grid3), dim3(256), ctx->stream,
+    BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB3, kSweep3>, dim3(run->sweep_grid3), dim3(256), ctx->stream,
                                 static_cast<const DTables*>(run->dT), static_cast<const DThr*>(run->dThr),
                                 static_cast<const ExCtl*>(run->dCtl), fin, run->dBest, run->dFeas, run->cap_final));
   else
-    BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB2>, dim3(run->sweep_grid2), dim3(256), ctx->stream,
+    BS_CUDA_TRY(ctx, launch_pdl(sweep_kernel<kSweepMinB2, kSweep2>, dim3(run->sweep_grid2), dim3(256), ctx->stream,
                                 static_cast<const DTables*>(run->dT), static_cast<const DThr*>(run->dThr),
                                 static_cast<const ExCtl*>(run->dCtl), fin, run->dBest, run->dFeas, run->cap_final));
   BS_LAUNCH_CHECK(ctx);
