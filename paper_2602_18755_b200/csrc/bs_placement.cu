@@ -173,18 +173,29 @@ __device__ __forceinline__ SimParams make_params(const DCand& c, const PolicyDev
 }
 
 // Per-warp shared scratch of the warp-cooperative decode simulator: the
-// resident heap (when it fits) and the 3 x 32-entry window arrays.
+// resident array and the batch-size bracket table (when they fit) and the
+// 3 x 32-entry window arrays.
+__host__ __device__ inline size_t ntab_bytes(int heap_cap) {
+  return (static_cast<size_t>(heap_cap) + 1) * sizeof(double) + ((static_cast<size_t>(heap_cap) + 1 + 15) / 16) * 16;
+}
+
 __host__ __device__ inline size_t warp_scratch_bytes(int heap_cap, bool heap_in_smem) {
-  return (heap_in_smem ? static_cast<size_t>(heap_cap) * sizeof(Resident) : 0) + 3 * 32 * sizeof(double);
+  return (heap_in_smem ? static_cast<size_t>(heap_cap) * sizeof(Resident) + ntab_bytes(heap_cap) : 0) +
+         3 * 32 * sizeof(double);
 }
 
 __device__ __forceinline__ WarpScratch carve_scratch(unsigned char* smem, int warp, int heap_cap, bool heap_in_smem,
                                                     Resident* gheap) {
   unsigned char* p = smem + static_cast<size_t>(warp) * warp_scratch_bytes(heap_cap, heap_in_smem);
   WarpScratch ws;
+  ws.nfrac = nullptr;
+  ws.nlo = nullptr;
   if (heap_in_smem) {
     ws.heap = reinterpret_cast<Resident*>(p);
     p += static_cast<size_t>(heap_cap) * sizeof(Resident);
+    ws.nfrac = reinterpret_cast<double*>(p);
+    ws.nlo = p + (static_cast<size_t>(heap_cap) + 1) * sizeof(double);
+    p += ntab_bytes(heap_cap);
   } else {
     ws.heap = gheap;
   }

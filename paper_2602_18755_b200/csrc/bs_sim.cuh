@@ -250,6 +250,14 @@ __device__ __forceinline__ FastGrid fast_grid(const DGrid& g, int tp, double fre
 // count depends on n only, so the lanes of a warp never diverge.
 __device__ __forceinline__ void bracket_count(const double* __restrict__ k, int n, double x, int* lo, double* frac) {
   const double k0 = __ldg(k), kn = __ldg(k + n - 1);
+  if (!(x < kn)) {  // at or beyond the last knot: the last interval, (kn - kp) / (kn - kp) == 1 exactly
+    const double d = __dsub_rn(kn, __ldg(k + n - 2));
+    if (d > 0.0 && d < INFINITY) {
+      *lo = n - 2;
+      *frac = 1.0;
+      return;
+    }
+  }
   if (x < k0 || x > kn) x = x < k0 ? k0 : (kn < x ? kn : x);
   int base = 0;
   for (int len = n; len > 1;) {
@@ -732,7 +740,29 @@ struct WarpScratch {
   double* L;       // 32
   double* P;       // 32
   double* T;       // 32
+  double* nfrac;   // heap_cap + 1 entries (or null): the n_requests axis bracket of every batch size
+  unsigned char* nlo;
 };
+
+// fast_brackets with the n_requests axis (active axis `na`) read from the
+// per-simulation table (the same bracket_count results, computed once).
+__device__ __forceinline__ void fast_brackets_ntab(const FastGrid& g, long long n_req, long long sum_len, FastBrk& b,
+                                                   int na, const unsigned char* nlo, const double* nfrac) {
+#pragma unroll
+  for (int a = 0; a < kMaxRank; ++a) {
+    if (a >= g.na) break;
+    if (g.fixed[a]) {
+      b.lo[a] = g.lo[a];
+      b.frac[a] = g.frac[a];
+    } else if (a == na) {
+      b.lo[a] = nlo[n_req];
+      b.frac[a] = nfrac[n_req];
+    } else {
+      bracket_count(g.knots[a], g.n[a], static_cast<double>(g.role[a] == BS_AXIS_SUM_LEN ? sum_len : n_req),
+                    &b.lo[a], &b.frac[a]);
+    }
+  }
+}
 
 // Insert r after every resident retiring no later (warp-cooperative).
 __device__ __forceinline__ void res_insert(Resident* a, int n, Resident r, int lane) {
@@ -808,6 +838,22 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
   long long sum_ctx = 0, reserved = 0, it = 0;
   double prev_end = 0.0;
   Resident* res = ws.heap;
+  // the n_requests axis's bracket for every batch size 1..heap_cap, once per
+  // simulation (the latency grid's; the power grid shares it when share)
+  int na = -1;
+  if (ws.nfrac && share && !lat.bad)
+    for (int a = 0; a < lat.na; ++a)
+      if (!lat.fixed[a] && lat.role[a] == BS_AXIS_N_REQUESTS && lat.n[a] <= 255) na = a;
+  if (na >= 0) {
+    for (int v = 1 + lane; v <= heap_cap; v += 32) {
+      int lo;
+      double fr;
+      bracket_count(lat.knots[na], lat.n[na], static_cast<double>(v), &lo, &fr);
+      ws.nlo[v] = static_cast<unsigned char>(lo);
+      ws.nfrac[v] = fr;
+    }
+    __syncwarp();
+  }
 
   auto record_idle = [&](double from, double to) -> bool {
     if (to <= from) return true;
@@ -939,7 +985,10 @@ __device__ inline SimOut simulate_decode_warp(const DModels& m, const SimTrace& 
         if (lat.bad) {
           bad = true;
         } else {
-          fast_brackets(lat, nl, s, bl);
+          if (na >= 0)
+            fast_brackets_ntab(lat, nl, s, bl, na, ws.nlo, ws.nfrac);
+          else
+            fast_brackets(lat, nl, s, bl);
           Lv = fast_corners(lat, bl);
           bad = !model_value_ok(Lv);
         }
