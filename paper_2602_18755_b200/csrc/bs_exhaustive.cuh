@@ -1451,7 +1451,13 @@ __device__ __forceinline__ void flush_acc(int d, LeafAcc& a, Key128* best, unsig
   }
 }
 
-constexpr unsigned long long kSweepClaim = 128;  // final-list entries per warp claim (three-level sweep)
+#ifndef BS_SWEEP2_CLAIM
+#define BS_SWEEP2_CLAIM 0  // 1: the two-level sweep claims runs too (A/B experiments)
+#endif
+#ifndef BS_SWEEP_CLAIM_N
+#define BS_SWEEP_CLAIM_N 128
+#endif
+constexpr unsigned long long kSweepClaim = BS_SWEEP_CLAIM_N;  // final-list entries per warp claim (three-level sweep)
 
 // One thread per final node: the I bottom levels of its subtree.  Two swept
 // levels: grid stride (a block's 8 warps take 256 consecutive entries, one
@@ -1469,7 +1475,7 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the BFS lists (programmatic dependent launch)
   if (ctl->overflow) return;  // the run is repeated with larger lists (one_shot): skip the sweep
   const unsigned long long n_fin = ctl->final_count < cap_final ? ctl->final_count : cap_final;
-  constexpr bool kClaim = LEVELS == kSweep3;
+  constexpr bool kClaim = LEVELS == kSweep3 || BS_SWEEP2_CLAIM;
   const int lane = threadIdx.x & 31;
   unsigned long long* next = &const_cast<ExCtl*>(ctl)->sweep_next;
   unsigned long long claim = 0;  // three levels: the warp's current run
