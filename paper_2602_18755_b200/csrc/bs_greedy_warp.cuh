@@ -310,13 +310,23 @@ __device__ __forceinline__ void greedy_sync() {
     __syncthreads();
 }
 
-template <int NW>
+// CL > 1: the CTA is one of a thread-block cluster of CL CTAs (one per SM)
+// deciding together: each CTA builds the same tables, a level's mutations
+// are spread over all CL x NT threads, and the CTAs' partial (objective,
+// lexicographic) minima, feasible counts and first errors are combined
+// through distributed shared memory after one cluster barrier per level, so
+// every CTA takes the same accept step.  Only rank 0 writes level records.
+template <int NW, int CL = 1>
 __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
                             const DRunning* R, WGreedyShared& S, DMpcOut* o, DLevel* lv, const FastGrid* fl,
                             const FastGrid* fp, bool share = false) {
   constexpr int NT = 32 * NW;
+  constexpr int GNT = NT * CL;  // threads deciding together
   const int lane = threadIdx.x & 31;
   const int tid = NW == 1 ? lane : static_cast<int>(threadIdx.x);
+  int crank = 0;
+  if constexpr (CL > 1) crank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  const int gtid = crank * NT + tid;
   WTables& T = S.T;
 #ifdef BS_GREEDY_PHASES
   unsigned long long gph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -459,7 +469,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
           unsigned long long best_cost = ~0ull;
           for (int R = 0; R <= 2 && R <= np; ++R) {
             const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), np - R);
-            const unsigned long long rounds = (tasks + NT - 1) / NT;
+            const unsigned long long rounds = (tasks + GNT - 1) / GNT;
             const unsigned long long steps = K + (R >= 1 ? base : 0) + (R == 2 ? base * base : 0);
             if (rounds * steps < best_cost) {
               best_cost = rounds * steps;
@@ -468,17 +478,17 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
           }
           const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), J);
           const unsigned long long pwJ = tasks;
-          for (unsigned long long p = tid; p < tasks; p += NT)
+          for (unsigned long long p = gtid; p < tasks; p += GNT)
             wlevel_tail(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, pwJ, static_cast<unsigned>(p), g);
         } else {
           // prefixes of the first J digits spread over lanes
           int J = 0;
           unsigned long long tasks = 1;
-          while (J < np && tasks < 2ull * NT) {
+          while (J < np && tasks < 2ull * GNT) {
             tasks *= base;
             ++J;
           }
-          for (unsigned long long p = tid; p < tasks; p += NT)
+          for (unsigned long long p = gtid; p < tasks; p += GNT)
             wlevel_dfs(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, p, g);
         }
         bo = g.bo;
@@ -487,7 +497,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
       } else {
         unsigned char mut[kMaxK];
         for (int k = 0; k < K; ++k) mut[k] = S.cur[k];
-        for (unsigned long long code = 1 + tid; code < combos; code += NT) {
+        for (unsigned long long code = 1 + gtid; code < combos; code += GNT) {
           unsigned long long cc = code, lex = 0;
           for (int i = 0; i < np; ++i) {  // digit i -> pos[i], least significant first (dvfs.hpp:233-237)
             const unsigned long long digit = cc % base;
@@ -548,6 +558,32 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
             errkey = r_err[v] < errkey ? r_err[v] : errkey;
           }
       }
+      if constexpr (CL > 1) {  // across the cluster's CTAs (distributed shared memory)
+        __shared__ unsigned long long c_part[2][4];  // by level parity: one barrier per level
+        const int par = l & 1;
+        if (tid == 0) {
+          c_part[par][0] = bo;
+          c_part[par][1] = bc;
+          c_part[par][2] = feas;
+          c_part[par][3] = errkey;
+        }
+        cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        cl.sync();
+        if (tid == 0) {
+          bo = bc = errkey = ~0ull;
+          feas = 0;
+          for (int r = 0; r < CL; ++r) {
+            const unsigned long long* q = cl.map_shared_rank(&c_part[par][0], r);
+            const unsigned long long qo = q[0], qc = q[1], qf = q[2], qe = q[3];
+            if (key_less(qo, qc, bo, bc)) {
+              bo = qo;
+              bc = qc;
+            }
+            feas += qf;
+            errkey = qe < errkey ? qe : errkey;
+          }
+        }
+      }
       if (tid == 0) {
         o->eval_count += static_cast<long long>(combos - 1);  // every mutation counts (dvfs.hpp:238)
         DLevel Lv;
@@ -572,7 +608,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
             o->objective = bp;
             Lv.accepted = 1;
           }
-          if (lv) lv[o->n_levels] = Lv;
+          if (lv && crank == 0) lv[o->n_levels] = Lv;
           o->n_levels += 1;
         }
         S.accepted = Lv.accepted;

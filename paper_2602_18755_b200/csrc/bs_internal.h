@@ -48,7 +48,8 @@ struct bs_ctx_s {
   unsigned long long ex_final_cap = 2000000000ull;
   std::unique_ptr<bs::HostPool> host_pool;  // started on first use (parallel_chunks)
   cudaEvent_t slice_ev[4] = {};  // per-slice D2H events of the MPC result copy (created once, bs_mpc.cu)
-  size_t greedy_smem[5] = {};     // dynamic shared memory the greedy kernels were opened to (bs_mpc.cu)
+  size_t greedy_smem[6] = {};     // dynamic shared memory the greedy kernels were opened to (bs_mpc.cu)
+  int greedy_no_cluster = -1;     // BS_GREEDY_NO_CLUSTER set: no cluster launch for single decisions (A/B)
   std::string fg_key;             // (models, pairs) of the reduced grids in the one-shot slot (bs_mpc.cu)
   bs::HostPool& pool();
 

@@ -30,6 +30,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "bs_internal.h"
 #include "bs_sim.cuh"
 
@@ -154,6 +156,37 @@ __global__ void __launch_bounds__(32 * NW) greedy_coop_kernel(DModels m, const D
   greedy_coop<NW>(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o, levels + static_cast<size_t>(d) * lv_stride,
                   fp ? fp->lat : nullptr, fp ? fp->pw : nullptr, fp && fp->share);
   if (threadIdx.x == 0) out[d] = *o;
+}
+
+// One decision per thread-block cluster of CL CTAs of NW warps (one CTA per
+// SM): the latency of a single controller call, a level's mutations spread
+// over CL SMs (greedy_coop<NW, CL>).
+constexpr int kGreedyCluster = 8;
+
+template <int NW, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(32 * NW)
+    greedy_cluster_kernel(DModels m, const DMpcCfg* cfgs, const DProblem* probs, const DWaiting* W,
+                          const DRunning* R, DMpcOut* out, DLevel* levels, int n, int max_h, int max_nc,
+                          const DFastPair* fg, int lv_stride) {
+  extern __shared__ __align__(16) unsigned char gdsm[];
+  const int d = blockIdx.x / CL;  // uniform over the cluster (the grid is n x CL)
+  const int rank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  auto a16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  WGreedyShared& S = *reinterpret_cast<WGreedyShared*>(gdsm);
+  DMpcOut* o = reinterpret_cast<DMpcOut*>(gdsm + a16(sizeof(WGreedyShared)));
+  double* tab = reinterpret_cast<double*>(gdsm + a16(sizeof(WGreedyShared)) + a16(sizeof(DMpcOut)));
+  if (d < n) {
+    const DProblem pr = probs[d];
+    const DMpcCfg& c = cfgs[pr.cfg];
+    if (threadIdx.x == 0) wtables_bind(S.T, tab, c.horizon, c.nc);
+    __syncthreads();
+    const DFastPair* fp = fg ? fg + pr.fgi : nullptr;
+    greedy_coop<NW, CL>(m, pr, c, W + pr.wait_off, R + pr.run_off, S, o,
+                        levels + static_cast<size_t>(d) * lv_stride, fp ? fp->lat : nullptr, fp ? fp->pw : nullptr,
+                        fp && fp->share);
+    if (threadIdx.x == 0 && rank == 0) out[d] = *o;
+  }
+  cooperative_groups::this_cluster().sync();  // no CTA leaves while another may read its shared memory
 }
 
 // ---------------------------------------------------------------------------
@@ -508,11 +541,25 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
         return BS_OK;
       };
       int rc = BS_OK;
-      switch (nw) {
-        case 2: rc = go(greedy_coop_kernel<2>, 1); break;
-        case 4: rc = go(greedy_coop_kernel<4>, 2); break;
-        case 8: rc = go(greedy_coop_kernel<8>, 3); break;
-        default: rc = go(greedy_coop_kernel<16>, 4); break;
+      if (ctx->greedy_no_cluster < 0) ctx->greedy_no_cluster = std::getenv("BS_GREEDY_NO_CLUSTER") ? 1 : 0;
+      if (nw == 16 && static_cast<long long>(n) * kGreedyCluster <= ctx->sm_count && !ctx->greedy_no_cluster) {
+        // a handful of decisions: one cluster of kGreedyCluster SMs each
+        auto kern = greedy_cluster_kernel<16, kGreedyCluster>;
+        if (one > ctx->greedy_smem[5]) {
+          BS_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(one)));
+          ctx->greedy_smem[5] = one;
+        }
+        kern<<<n * kGreedyCluster, 32 * 16, one, ctx->stream>>>(models->dm, pk.cfgs, pk.problems, pk.waiting,
+                                                                pk.running, run->dOut, run->dLv, n, pk.max_horizon,
+                                                                pk.max_nc, run->dFG, run->lv_stride);
+      } else {
+        switch (nw) {
+          case 2: rc = go(greedy_coop_kernel<2>, 1); break;
+          case 4: rc = go(greedy_coop_kernel<4>, 2); break;
+          case 8: rc = go(greedy_coop_kernel<8>, 3); break;
+          default: rc = go(greedy_coop_kernel<16>, 4); break;
+        }
       }
       if (rc) return rc;
     }

@@ -36,6 +36,8 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "bs_internal.h"
 #include "bs_sim.cuh"
 
