@@ -333,10 +333,33 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
   int gph_levels = 0;
 #endif
   BS_GPH(0);
+  // latency mode: the waiting rows the projection scans are copied to shared
+  // memory by every thread at once (one round trip instead of one per
+  // request), and the reduced grids the tables read are prefetched into L1
+  // while thread 0 projects
+  constexpr int kStageW = NW > 1 ? 256 : 1;
+  __shared__ long long s_wrem[kStageW];
+  __shared__ double s_warr[kStageW];
+  const bool staged_w = NW > 1 && pr.n_wait <= kStageW;
+  if constexpr (NW > 1) {
+    if (staged_w)
+      for (int i = tid; i < pr.n_wait; i += NT) {
+        s_wrem[i] = W[i].remaining;
+        s_warr[i] = W[i].arrival;
+      }
+    if (fl) {
+      const char* g0 = reinterpret_cast<const char*>(fl);
+      const char* g1 = reinterpret_cast<const char*>(fp);
+      const int lines = static_cast<int>((sizeof(FastGrid) * c.nc + 127) / 128);
+      for (int i = tid; i < 2 * lines; i += NT)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"((i < lines ? g0 : g1) + 128ll * (i < lines ? i : i - lines)));
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     T.nc = c.nc;
     T.ttft = c.ttft;
-    int st = project_dev(pr, c, W, R, &T);
+    int st = staged_w ? project_wa(pr, c, WaitStaged{s_wrem, s_warr}, R, &T) : project_dev(pr, c, W, R, &T);
     if (st == BS_OK && (m.grid[0].bad_axis || m.grid[2].bad_axis) && T.K > 0) st = BS_MODEL_ERROR;
     T.status = st;
     for (int k = 0; k < kMaxK; ++k) T.bad_lat[k] = T.bad_pow[k] = 0u;

@@ -16,8 +16,30 @@ __host__ __device__ inline unsigned long long ipow(unsigned long long b, int e) 
 // (scheduler.hpp:40-66).  Only the queue head can be partially consumed (a
 // partial chunk ends a batch), so the state is (head, head_remaining).
 // ---------------------------------------------------------------------------
+// The waiting queue's (remaining, arrival) as the projection reads them: from
+// the problem's global rows, or from a shared-memory copy.
+struct WaitRows {
+  const DWaiting* W;
+  __device__ __forceinline__ long long rem(int i) const { return W[i].remaining; }
+  __device__ __forceinline__ double arr(int i) const { return W[i].arrival; }
+};
+struct WaitStaged {
+  const long long* r;
+  const double* a;
+  __device__ __forceinline__ long long rem(int i) const { return r[i]; }
+  __device__ __forceinline__ double arr(int i) const { return a[i]; }
+};
+
+template <class Tab, class WA>
+__device__ int project_wa(const DProblem& pr, const DMpcCfg& c, WA W, const DRunning* R, Tab* T);
+
 template <class Tab>
 __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting* W, const DRunning* R, Tab* T) {
+  return project_wa(pr, c, WaitRows{W}, R, T);
+}
+
+template <class Tab, class WA>
+__device__ int project_wa(const DProblem& pr, const DMpcCfg& c, WA W, const DRunning* R, Tab* T) {
   int K = 0;
   if (pr.run_active) {
     T->n_req[0] = pr.run_n;
@@ -41,7 +63,7 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
     K = 1;
   }
   int head = 0;
-  long long head_rem = pr.n_wait > 0 ? W[0].remaining : 0;
+  long long head_rem = pr.n_wait > 0 ? W.rem(0) : 0;
   while (head < pr.n_wait && K < c.horizon) {
     long long tokens = 0, npick = 0, sum = 0;
     int consumed = 0, ncomp = 0;
@@ -49,7 +71,7 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
     long long partial_rem = -1;
     for (int i = head; i < pr.n_wait; ++i) {
       if (npick >= c.max_batch_requests) break;
-      const long long rem = i == head ? head_rem : W[i].remaining;
+      const long long rem = i == head ? head_rem : W.rem(i);
       if (rem <= 0) {
         T->K = K;
         return BS_SIMULATION_ERROR;  // scheduler.hpp:47
@@ -66,7 +88,7 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
             ++npick;
             sum += rem;
             ++ncomp;
-            const double a = W[i].arrival;
+            const double a = W.arr(i);
             mn = a < mn ? a : mn;
             ++consumed;
           }
@@ -80,7 +102,7 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
       sum += take;
       if (take == rem) {
         ++ncomp;
-        const double a = W[i].arrival;
+        const double a = W.arr(i);
         mn = a < mn ? a : mn;
         ++consumed;
       } else {
@@ -98,7 +120,7 @@ __device__ int project_dev(const DProblem& pr, const DMpcCfg& c, const DWaiting*
     if (partial_rem >= 0) {
       head_rem = partial_rem;
     } else if (head < pr.n_wait) {
-      head_rem = W[head].remaining;
+      head_rem = W.rem(head);
     }
   }
   T->K = K;
