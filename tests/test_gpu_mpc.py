@@ -164,6 +164,27 @@ def test_greedy_batch_c1_shape(gpu_device, oracle_lib):
         assert gpu_result_tuple(g, ref.K) == result_tuple(ref)
 
 
+def test_greedy_single_calls_c1_shape(gpu_device, oracle_lib):
+    """One decision per call takes the latency path (a cluster of 8 CTAs, a
+    level's 3^8 - 1 mutations over 4096 threads, minima combined through
+    distributed shared memory): same results as the batch kernels and the
+    C restatement, level records included."""
+    rng = random.Random(11)
+    ladder = h100_ladder(8)
+    m = llama_models(ladder)
+    cfg = P.MpcConfig(horizon_K=8, ladder_N=7, ladder=ladder)
+    pol = P.SchedulerPolicy(max_batch_tokens=512)
+    snaps = [random_snapshot(rng, n_lo=4, n_hi=30, ladder=ladder, running_prob=0.5,
+                             arrival_window=rng.choice([50.0, 200.0, 800.0])) for _ in range(24)]
+    batch = P.greedy_freq_select_batch(snaps, cfg, m, pol)
+    for q, b in zip(snaps, batch):
+        g = P.greedy_freq_select(q, cfg, m, pol)
+        rc, ref = cpu_mpc(oracle_lib, "greedy", m, cfg, pol, q)
+        assert rc == 0
+        assert gpu_result_tuple(g, ref.K) == result_tuple(ref)
+        assert gpu_result_tuple(g, ref.K) == gpu_result_tuple(b, ref.K)
+
+
 def test_exhaustive_matches_oracle_bitwise(gpu_device, oracle_lib):
     insts = _instances(51, 40, levels=8, ladder_n=5, horizon=4)
     for m, cfg, pol, q in insts:
