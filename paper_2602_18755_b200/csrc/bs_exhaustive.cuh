@@ -148,6 +148,22 @@ __device__ __forceinline__ int thr_leaf_count(const DThr* __restrict__ H, int nc
   return (b0 + (cs[b0] >= t ? 1 : 0)) - (b1 + (rs[b1] >= t ? 1 : 0)) + (b2 + (rn[b2] >= t ? 1 : 0));
 }
 
+// thr_leaf_count for siblings visited in increasing clock order (the sorted
+// switched order): the table-wide count is non-increasing in t, so the
+// previous sibling's count bounds it and a short walk down usually finds it
+// (a bounded walk, then a binary search below it).  *hint: the previous
+// count (nc * nc before the first sibling), updated.
+__device__ __forceinline__ int thr_leaf_count_walk(const DThr* __restrict__ H, int nc, double t, int l, int* hint) {
+  const double* __restrict__ cs = H->cs;
+  int c = *hint;
+  const int r1 = count_ge(H->rs + l * nc, nc, t), r2 = count_ge(H->rn + l * nc, nc, t);
+#pragma unroll 1
+  for (int s = 0; s < 4 && c > 0 && !(cs[c - 1] >= t); ++s) --c;
+  if (c > 0 && !(cs[c - 1] >= t)) c = count_ge(cs, c, t);
+  *hint = c;
+  return c - r1 + r2;
+}
+
 // The seed's node bound ("seed node bound"): every leaf below a
 // node at depth K-2 with (num, den) has a rounded objective above the seed's
 // (a genuine feasible key, so none of them is the argmin).  With beta =
@@ -1540,10 +1556,12 @@ __global__ void __launch_bounds__(256, MINB) sweep_kernel(const DTables* __restr
 #endif
           two_sorted(T, FD, nc, t, num, den, last, cb, hint, a);
         } else if (LEVELS == kSweep3) {  // three swept levels only occur in batches launched with this instance
+          int cs_hint = nc * nc;  // switched children come in clock order (the diag child last)
           for_feasible_children(T, FD, nc, t, num, den, last, [&](int e, double t3, double n3, double d3) {
             if (T->rex_ok && t3 > T->rexist[K - 2][e]) return;  // no feasible leaf below this child
             if (use_thr && (node_dom_seed(T, n3, d3) || node_dominated(a, n3, d3))) {
-              a.count += static_cast<unsigned long long>(thr_leaf_count(H, nc, t3, e));
+              a.count += static_cast<unsigned long long>(
+                  e == last ? thr_leaf_count(H, nc, t3, e) : thr_leaf_count_walk(H, nc, t3, e, &cs_hint));
 #ifdef BS_SWEEP_STATS
               a.st_thr += 1;
 #endif
