@@ -156,7 +156,18 @@ __device__ __forceinline__ int thr_leaf_count(const DThr* __restrict__ H, int nc
 __device__ __forceinline__ int thr_leaf_count_walk(const DThr* __restrict__ H, int nc, double t, int l, int* hint) {
   const double* __restrict__ cs = H->cs;
   int c = *hint;
-  const int r1 = count_ge(H->rs + l * nc, nc, t), r2 = count_ge(H->rn + l * nc, nc, t);
+  // the node's two rows (same length) searched in lockstep: their loads in flight together
+  const double* __restrict__ rs = H->rs + l * nc;
+  const double* __restrict__ rn = H->rn + l * nc;
+  int b1 = 0, b2 = 0;
+  for (int len = nc; len > 1;) {
+    const int half = len >> 1;
+    const double v1 = rs[b1 + half], v2 = rn[b2 + half];
+    b1 = v1 >= t ? b1 + half : b1;
+    b2 = v2 >= t ? b2 + half : b2;
+    len -= half;
+  }
+  const int r1 = b1 + (rs[b1] >= t ? 1 : 0), r2 = b2 + (rn[b2] >= t ? 1 : 0);
 #pragma unroll 1
   for (int s = 0; s < 4 && c > 0 && !(cs[c - 1] >= t); ++s) --c;
   if (c > 0 && !(cs[c - 1] >= t)) c = count_ge(cs, c, t);
