@@ -223,9 +223,8 @@ __device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& 
   }
 }
 
-// The same mutations as wlevel_dfs for R = np - J <= 2 remaining digits, by
-// nested loops in registers (no per-depth stack): the latency mode of a
-// decision spread over a whole CTA, where every thread owns few prefixes.
+// The same mutations as wlevel_dfs for R = np - J <= 3 remaining digits, by
+// nested loops in registers (no per-depth stack in local memory).
 // pwJ = base^J.
 __device__ void wlevel_tail(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* cur,
                             const int* pos, int np, int base, int target, int r1, int r2, int J,
@@ -267,14 +266,28 @@ __device__ void wlevel_tail(const WTables& T, const DProblem& pr, const DMpcCfg&
       gleaf(g, n1, dn1, code1, lex1);
       continue;
     }
-    for (int d1 = 0; d1 < base; ++d1) {  // digit J + 1, the last (R == 2)
+    const int e1 = J + 2 < np ? pos[J + 2] : K;
+    for (int d1 = 0; d1 < base; ++d1) {  // digit J + 1
       double t2 = t1, n2 = n1, dn2 = dn1;
       int l2 = l1;
       bool ok2 = wstep(T, pr, c, pos[J + 1], cand_of(d1), t2, n2, dn2, l2);
-      for (int k = pos[J + 1] + 1; ok2 && k < K; ++k) ok2 = wstep(T, pr, c, k, cur[k], t2, n2, dn2, l2);
+      for (int k = pos[J + 1] + 1; ok2 && k < e1; ++k) ok2 = wstep(T, pr, c, k, cur[k], t2, n2, dn2, l2);
       if (!ok2) continue;
-      gleaf(g, n2, dn2, code1 + static_cast<unsigned long long>(d1) * pwJ * base,
-            lex1 * base + static_cast<unsigned long long>(base - 1 - d1));
+      const unsigned long long code2 = code1 + static_cast<unsigned long long>(d1) * pwJ * base;
+      const unsigned long long lex2 = lex1 * base + static_cast<unsigned long long>(base - 1 - d1);
+      if (J + 2 == np) {
+        gleaf(g, n2, dn2, code2, lex2);
+        continue;
+      }
+      for (int d2 = 0; d2 < base; ++d2) {  // digit J + 2, the last (R == 3)
+        double t3 = t2, n3 = n2, dn3 = dn2;
+        int l3 = l2;
+        bool ok3 = wstep(T, pr, c, pos[J + 2], cand_of(d2), t3, n3, dn3, l3);
+        for (int k = pos[J + 2] + 1; ok3 && k < K; ++k) ok3 = wstep(T, pr, c, k, cur[k], t3, n3, dn3, l3);
+        if (!ok3) continue;
+        gleaf(g, n3, dn3, code2 + static_cast<unsigned long long>(d2) * pwJ * base * base,
+              lex2 * base + static_cast<unsigned long long>(base - 1 - d2));
+      }
     }
   }
 }
@@ -485,15 +498,16 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
         g.filt = filt;
         g.incumbent = S.obj;
         g.thr_s = gfilter_scaled(S.obj);
-        if (NW > 1 && combos <= (1ull << 31)) {
-          // latency mode: prefixes of all but the last R <= 2 digits, R
-          // chosen for the shortest per-thread path (rounds x steps)
+        if (combos <= (1ull << 31)) {
+          // prefixes of all but the last R <= 3 digits, R chosen for the
+          // shortest per-thread path (rounds x steps)
           int J = np;
           unsigned long long best_cost = ~0ull;
-          for (int R = 0; R <= 2 && R <= np; ++R) {
+          for (int R = 0; R <= 3 && R <= np; ++R) {
             const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), np - R);
             const unsigned long long rounds = (tasks + GNT - 1) / GNT;
-            const unsigned long long steps = K + (R >= 1 ? base : 0) + (R == 2 ? base * base : 0);
+            const unsigned long long steps =
+                K + (R >= 1 ? base : 0) + (R >= 2 ? base * base : 0) + (R == 3 ? base * base * base : 0);
             if (rounds * steps < best_cost) {
               best_cost = rounds * steps;
               J = np - R;
