@@ -8,17 +8,20 @@
 // warp):
 //   * compact per-warp tables in shared memory, row stride = |cand|;
 //   * positions of a level by a ballot over batches;
-//   * a level's mutations by an exact prefix-sharing depth-first walk:
-//     lanes own prefixes of the first J mutated positions (digit 0 = the
-//     earliest position, as in the reference's code), and walk the rest in
-//     batch order keeping (t, num, den) per depth.  A step that violates
-//     meets_slo ends every mutation below it (meets_slo returns false at the
-//     first violation, dvfs.hpp:117), so the subtree is skipped.  Each
-//     surviving mutation's clock and sums are built by the same additions in
-//     the same k order as eval_assignment, so objectives are bit-identical.
-//     Used only when no (k, f) prediction of the decision is bad; otherwise
-//     every mutation is evaluated in full (exact ModelError order).
+//   * a level's mutations by exact prefix-sharing walks: threads own
+//     prefixes of all but the last R <= 3 mutated positions (digit 0 = the
+//     earliest position, as in the reference's code) and extend them by
+//     nested loops in registers, keeping (t, num, den) per depth.  A step
+//     that violates meets_slo ends every mutation below it (meets_slo returns
+//     false at the first violation, dvfs.hpp:117), so the subtree is skipped.
+//     Each surviving mutation's clock and sums are built by the same
+//     additions in the same k order as eval_assignment, so objectives are
+//     bit-identical.  Used only when no (k, f) prediction of the decision is
+//     bad; otherwise every mutation is evaluated in full (exact ModelError
+//     order).
 #pragma once
+
+static_assert(kMaxK <= 19, "a level's 3^K' mutations must index in 32 bits");
 
 struct WTables {
   int K, nc, status, anybad;
@@ -104,9 +107,7 @@ __device__ __forceinline__ bool wstep(const WTables& T, const DProblem& pr, cons
   return true;
 }
 
-// All mutations of one level with a common prefix (digits 0..J-1 fixed =
-// `prefix`, digit i <-> position pos[i]); folds feasible ones into
-// (bo, bc, feas).  digit -> candidate: 0 target, 1 r1, 2 r2.
+
 // Division-free leaf filter (exactness argument 5; the level's
 // tables must have every A >= 0 and finite and E finite): a mutation whose
 // objective provably exceeds min(incumbent, this thread's best) is only
@@ -142,89 +143,14 @@ __device__ __forceinline__ void gleaf(GLeafAcc& g, double n, double d, unsigned 
   }
 }
 
-__device__ void wlevel_dfs(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* cur,
-                           const int* pos, int np, int base, int target, int r1, int r2, int J,
-                           unsigned long long prefix, GLeafAcc& g) {
-  const int K = T.K;
-  auto cand_of = [&](int d) { return d == 0 ? target : (d == 1 ? r1 : r2); };
-  // prefix digits (least significant = earliest position)
-  int dig[kMaxK];
-  unsigned long long pw[kMaxK + 1];
-  pw[0] = 1;
-  for (int i = 0; i < np; ++i) pw[i + 1] = pw[i] * static_cast<unsigned long long>(base);
-  // prefix < base^J <= 3^16 < 2^32: 32-bit digit extraction, division by the
-  // constant 3 (a multiply-high) or a shift
-  unsigned rem = static_cast<unsigned>(prefix);
-  for (int i = 0; i < J; ++i) {
-    const unsigned q = base == 3 ? rem / 3u : rem >> 1;
-    dig[i] = static_cast<int>(rem - q * static_cast<unsigned>(base));
-    rem = q;
-  }
-  // walk k = 0 .. (J < np ? pos[J] - 1 : K - 1) with the prefix applied
-  double t = pr.now, num = 0.0, den = 0.0;
-  int last = -1;
-  const int stop0 = J < np ? pos[J] : K;
-  int pi = 0;
-  for (int k = 0; k < stop0; ++k) {
-    int f = cur[k];
-    if (pi < J && pos[pi] == k) f = cand_of(dig[pi++]);
-    if (!wstep(T, pr, c, k, f, t, num, den, last)) return;
-  }
-  unsigned long long lexp = 0;  // lex key of the prefix digits
-  for (int i = 0; i < J; ++i) lexp = lexp * base + static_cast<unsigned long long>(base - 1 - dig[i]);
-  auto leaf = [&](double n, double d, unsigned long long code, unsigned long long lex) { gleaf(g, n, d, code, lex); };
-  if (J == np) {
-    leaf(num, den, prefix, lexp);
-    return;
-  }
-  // iterative DFS over digits J..np-1
-  double st_t[kMaxK + 1], st_n[kMaxK + 1], st_d[kMaxK + 1];
-  int st_l[kMaxK + 1];
-  unsigned long long st_code[kMaxK + 1], st_lex[kMaxK + 1];
-  st_t[J] = t;
-  st_n[J] = num;
-  st_d[J] = den;
-  st_l[J] = last;
-  st_code[J] = prefix;
-  st_lex[J] = lexp;
-  int i = J;
-  dig[J] = 0;
-  for (;;) {
-    if (dig[i] == base) {
-      if (i == J) break;
-      --i;
-      ++dig[i];
-      continue;
-    }
-    double tt = st_t[i], nn = st_n[i], dd = st_d[i];
-    int ll = st_l[i];
-    const int end = i + 1 < np ? pos[i + 1] : K;
-    bool ok = wstep(T, pr, c, pos[i], cand_of(dig[i]), tt, nn, dd, ll);
-    for (int k = pos[i] + 1; ok && k < end; ++k) ok = wstep(T, pr, c, k, cur[k], tt, nn, dd, ll);
-    if (!ok) {  // meets_slo fails below this digit: no feasible mutation in the subtree
-      ++dig[i];
-      continue;
-    }
-    const unsigned long long code = st_code[i] + static_cast<unsigned long long>(dig[i]) * pw[i];
-    const unsigned long long lex = st_lex[i] * base + static_cast<unsigned long long>(base - 1 - dig[i]);
-    if (i + 1 == np) {
-      leaf(nn, dd, code, lex);
-      ++dig[i];
-      continue;
-    }
-    st_t[i + 1] = tt;
-    st_n[i + 1] = nn;
-    st_d[i + 1] = dd;
-    st_l[i + 1] = ll;
-    st_code[i + 1] = code;
-    st_lex[i + 1] = lex;
-    ++i;
-    dig[i] = 0;
-  }
-}
-
-// The same mutations as wlevel_dfs for R = np - J <= 3 remaining digits, by
-// nested loops in registers (no per-depth stack in local memory).
+// All mutations of one level whose first J digits are `prefix` (digit i <->
+// position pos[i]; digit -> candidate: 0 target, 1 r1, 2 r2), the remaining
+// R = np - J <= 3 digits by nested loops in registers (no per-depth stack in
+// local memory): the prefix is walked once, each nested digit extends its
+// parent's (t, num, den), and a step that violates meets_slo ends every
+// mutation below it (meets_slo returns false at the first violation,
+// dvfs.hpp:117).  Each surviving mutation's clock and sums are built by the
+// same additions in the same k order as eval_assignment.  pwJ = base^J.
 // pwJ = base^J.
 __device__ void wlevel_tail(const WTables& T, const DProblem& pr, const DMpcCfg& c, const unsigned char* cur,
                             const int* pos, int np, int base, int target, int r1, int r2, int J,
@@ -498,36 +424,24 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
         g.filt = filt;
         g.incumbent = S.obj;
         g.thr_s = gfilter_scaled(S.obj);
-        if (combos <= (1ull << 31)) {
-          // prefixes of all but the last R <= 3 digits, R chosen for the
-          // shortest per-thread path (rounds x steps)
-          int J = np;
-          unsigned long long best_cost = ~0ull;
-          for (int R = 0; R <= 3 && R <= np; ++R) {
-            const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), np - R);
-            const unsigned long long rounds = (tasks + GNT - 1) / GNT;
-            const unsigned long long steps =
-                K + (R >= 1 ? base : 0) + (R >= 2 ? base * base : 0) + (R == 3 ? base * base * base : 0);
-            if (rounds * steps < best_cost) {
-              best_cost = rounds * steps;
-              J = np - R;
-            }
+        // prefixes of all but the last R <= 3 digits (base^np <= 3^kMaxK < 2^31
+        // tasks), R chosen for the shortest per-thread path (rounds x steps)
+        int J = np;
+        unsigned long long best_cost = ~0ull;
+        for (int R = 0; R <= 3 && R <= np; ++R) {
+          const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), np - R);
+          const unsigned long long rounds = (tasks + GNT - 1) / GNT;
+          const unsigned long long steps =
+              K + (R >= 1 ? base : 0) + (R >= 2 ? base * base : 0) + (R == 3 ? base * base * base : 0);
+          if (rounds * steps < best_cost) {
+            best_cost = rounds * steps;
+            J = np - R;
           }
-          const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), J);
-          const unsigned long long pwJ = tasks;
-          for (unsigned long long p = gtid; p < tasks; p += GNT)
-            wlevel_tail(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, pwJ, static_cast<unsigned>(p), g);
-        } else {
-          // prefixes of the first J digits spread over lanes
-          int J = 0;
-          unsigned long long tasks = 1;
-          while (J < np && tasks < 2ull * GNT) {
-            tasks *= base;
-            ++J;
-          }
-          for (unsigned long long p = gtid; p < tasks; p += GNT)
-            wlevel_dfs(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, p, g);
         }
+        const unsigned long long tasks = ipow(static_cast<unsigned long long>(base), J);
+        const unsigned long long pwJ = tasks;
+        for (unsigned long long p = gtid; p < tasks; p += GNT)
+          wlevel_tail(T, pr, c, S.cur, S.pos, np, base, target, r1, r2, J, pwJ, static_cast<unsigned>(p), g);
         bo = g.bo;
         bc = g.bc;
         feas = g.feas;
