@@ -201,8 +201,18 @@ enum ErrKind : int {
   kErrCtl = 16,
 };
 
-__device__ __forceinline__ bool predict(const DGrid& g, long long n, long long sum, int tp, double f, double* out,
-                                        int* err, int kind) {
+// The replay kernels are large (tens of thousands of instructions) and their
+// warps sit at different points of the event loop, so instruction-cache
+// misses dominate their stalls: the predictors, called from many sites, are
+// kept as single out-of-line copies (BS_REPLAY_INLINE=1 inlines them).
+#ifndef BS_REPLAY_INLINE
+#define BS_RP_FN __noinline__
+#else
+#define BS_RP_FN __forceinline__
+#endif
+
+__device__ BS_RP_FN bool predict(const DGrid& g, long long n, long long sum, int tp, double f, double* out,
+                                 int* err, int kind) {
   if (g.bad_axis) {
     *err = kErrAxis;
     return false;
@@ -216,8 +226,8 @@ __device__ __forceinline__ bool predict(const DGrid& g, long long n, long long s
   return true;
 }
 
-__device__ __forceinline__ bool predict_fast(const FastGrid& g, long long n, long long sum, double* out, int* err,
-                                             int kind) {
+__device__ BS_RP_FN bool predict_fast(const FastGrid& g, long long n, long long sum, double* out, int* err,
+                                      int kind) {
   if (g.bad) {
     *err = kErrAxis;
     return false;
@@ -233,8 +243,8 @@ __device__ __forceinline__ bool predict_fast(const FastGrid& g, long long n, lon
 
 // predict_fast with the iteration's cached brackets when the slot's grid
 // shares them (`shared`), else its own.
-__device__ __forceinline__ bool predict_slot(const FastGrid& g, int shared, const FastBrk& b, long long n, long long sum,
-                                             double* out, int* err, int kind) {
+__device__ BS_RP_FN bool predict_slot(const FastGrid& g, int shared, const FastBrk& b, long long n, long long sum,
+                                      double* out, int* err, int kind) {
   if (g.bad) {
     *err = kErrAxis;
     return false;
