@@ -325,12 +325,27 @@ __device__ __noinline__ void leaf_exists_bounds(DTables* __restrict__ T) {
       s_rho[threadIdx.x] = sig;
     }
     __syncthreads();
-    if (threadIdx.x < nc) {
+    if (threadIdx.x < 32) {  // max over g != l of s_rho[g] from the top two (max is exact in any order)
       const int l = threadIdx.x;
-      double r = s_rho[nc + l];
-      for (int g = 0; g < nc; ++g)
-        if (g != l && s_rho[g] > r) r = s_rho[g];
-      T->rexist[d][l] = r;
+      const double v = l < nc ? s_rho[l] : -INFINITY;
+      double m1 = v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, m1, o);
+        m1 = w > m1 ? w : m1;
+      }
+      const int i1 = __ffs(__ballot_sync(0xffffffffu, l < nc && v == m1)) - 1;
+      double m2 = l == i1 ? -INFINITY : v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, m2, o);
+        m2 = w > m2 ? w : m2;
+      }
+      if (l < nc) {
+        const double other = l == i1 ? m2 : m1;
+        const double own = s_rho[nc + l];
+        T->rexist[d][l] = other > own ? other : own;
+      }
     }
     __syncthreads();
   }
@@ -886,6 +901,19 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   __shared__ int s_status;
   const int d = blockIdx.x;
   if (d >= n) return;
+#ifdef BS_PREP_PHASES  // diagnostics build: globaltimer at phase ends, printed by thread 0 of every 64th CTA
+  unsigned long long pph[10] = {0};
+  int pphn = 0;
+#define BS_PPH()                                                            \
+  if (threadIdx.x == 0) {                                                   \
+    unsigned long long t_;                                                  \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+    pph[pphn++] = t_;                                                       \
+  }
+#else
+#define BS_PPH()
+#endif
+  BS_PPH();
   const DProblem pr = probs[d];
   const DMpcCfg& c = cfgs[pr.cfg];
   DTables* T = &tables[d];
@@ -906,6 +934,7 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
     feas[d] = 0ull;
   }
   __syncthreads();
+  BS_PPH();
   const int K = T->K, nc = T->nc;
   if (s_status != BS_OK || K == 0) return;
   const int FD = K - sweep_levels(K, nc, sweep3_min);
@@ -920,7 +949,9 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   }
   // per-step thresholds, then the exact completion bounds (rexist)
   if (T->sorted_ok) step_thresholds(T);
+  BS_PPH();
   if (K >= 3) leaf_exists_bounds(T);
+  BS_PPH();
   // A slice whose leading digits lie below the first list this kernel
   // writes (trees of at most 3 levels, or shallow final depths): every leaf
   // of the slice evaluated here, in the sweep's op sequence.
@@ -1019,6 +1050,7 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
       best[d].obj = ko;
       best[d].code = kc;
     }
+    BS_PPH();
     // the seed's node bound over the two bottom levels (node_dom_seed), one
     // warp: lane x takes candidate x of each level
     const double thr_s = __longlong_as_double(static_cast<long long>(ko));
@@ -1066,6 +1098,7 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   }
   const int D0 = FD < 2 ? FD : 2;
   const int width = D0 == 1 ? nc : nc * nc;
+  BS_PPH();
   if (threadIdx.x == 0) T->n_ok3 = 0;
   __syncthreads();
   const bool to_final = D0 == FD;
@@ -1133,6 +1166,7 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
   //  * loose decisions with two swept levels: the BFS settles their dominated
   //    final nodes when at least 10 % of the batch is loose (measured at C2
   //    TTFT 1200 ms: 92 % of the final nodes; step 7.9 -> 1.9 ms).
+  BS_PPH();
   __syncthreads();
   const bool loose = FD >= 4 && FD == K - 2 && 20ll * T->n_ok3 > 17ll * nc * nc * nc;
   if (threadIdx.x == 0 && K >= 3 && FD >= 1 && T->sorted_ok && T->filter_ok && sl.digits <= (FD < 2 ? FD : 2) &&
@@ -1143,6 +1177,14 @@ __global__ void __launch_bounds__(kPrepThreads, BS_PREP_MINB) prepare_kernel(DMo
     }
     thr_list[atomicAdd(&ctl->n_thr, 1ull)] = d;
   }
+#ifdef BS_PREP_PHASES
+  BS_PPH();
+  if (threadIdx.x == 0 && (d & 63) == 0) {
+    printf("prep phases ns:");
+    for (int i = 1; i < pphn; ++i) printf(" %llu", pph[i] - pph[i - 1]);
+    printf("\n");
+  }
+#endif
 }
 
 // The thresholds of the listed decisions (prepare_kernel), a few CTAs per SM

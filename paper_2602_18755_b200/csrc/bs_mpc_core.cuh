@@ -145,26 +145,63 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
                              const DRunning* R, DTables* T, int* s_status, const FastGrid* fl = nullptr,
                              const FastGrid* fp = nullptr, bool share = false) {
   __shared__ FastBrk s_bl[kMaxK], s_bp[kMaxK];
+  // The projection is one thread's serial scan of the waiting queue: its rows
+  // are first copied to shared memory by the whole block (one round trip),
+  // the reduced grids prefetched into L1 meanwhile, and the projected
+  // batches kept in shared memory for the table loop (then copied to T).
+  constexpr int kStageW = 256;
+  __shared__ long long s_wrem[kStageW];
+  __shared__ double s_warr[kStageW];
+  __shared__ struct {
+    long long n_req[kMaxK], sum_len[kMaxK];
+    double wf[kMaxK], minarr[kMaxK];
+    int ncomp[kMaxK];
+    int K;
+  } s_pj;
+  const bool staged = pr.n_wait <= kStageW;
+  if (staged)
+    for (int i = threadIdx.x; i < pr.n_wait; i += blockDim.x) {
+      s_wrem[i] = W[i].remaining;
+      s_warr[i] = W[i].arrival;
+    }
+  if (fl) {
+    const int lines = static_cast<int>((sizeof(FastGrid) * c.nc + 127) / 128);
+    for (int i = threadIdx.x; i < 2 * lines; i += blockDim.x)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(i < lines ? fl : fp) +
+                                                  128ll * (i < lines ? i : i - lines)));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int st = staged ? project_wa(pr, c, WaitStaged{s_wrem, s_warr}, R, &s_pj) : project_dev(pr, c, W, R, &s_pj);
+    if (st == BS_OK && (m.grid[0].bad_axis || m.grid[2].bad_axis) && s_pj.K > 0) st = BS_MODEL_ERROR;
+    *s_status = st;
+  }
+  __syncthreads();
+  const int K = s_pj.K;
+  const int nc = c.nc;
   if (threadIdx.x == 0) {
     T->nc = c.nc;
     T->ttft = c.ttft;
-    int st = project_dev(pr, c, W, R, T);
-    if (st == BS_OK && (m.grid[0].bad_axis || m.grid[2].bad_axis) && T->K > 0) st = BS_MODEL_ERROR;
-    *s_status = st;
-    for (int k = 0; k < kMaxK; ++k) {
-      T->bad_lat[k] = 0u;
-      T->bad_pow[k] = 0u;
+    T->K = K;
+  }
+  for (int k = threadIdx.x; k < kMaxK; k += blockDim.x) {
+    T->bad_lat[k] = 0u;
+    T->bad_pow[k] = 0u;
+    if (k < K) {
+      T->n_req[k] = s_pj.n_req[k];
+      T->sum_len[k] = s_pj.sum_len[k];
+      T->wf[k] = s_pj.wf[k];
+      T->minarr[k] = s_pj.minarr[k];
+      T->ncomp[k] = s_pj.ncomp[k];
     }
   }
   __syncthreads();
-  const int K = T->K;
-  const int nc = c.nc;
   if (*s_status != BS_OK) return;
   const bool shared_brk = fl && share;
   if (shared_brk) {
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
-      fast_brackets(fl[0], T->n_req[k], T->sum_len[k], s_bl[k]);
-      fast_brackets(fp[0], T->n_req[k], T->sum_len[k], s_bp[k]);
+      fast_brackets(fl[0], s_pj.n_req[k], s_pj.sum_len[k], s_bl[k]);
+      fast_brackets(fp[0], s_pj.n_req[k], s_pj.sum_len[k], s_bp[k]);
     }
     __syncthreads();
   }
@@ -175,16 +212,16 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
       L = fast_corners(fl[f], s_bl[k]);
       P = fast_corners(fp[f], s_bp[k]);
     } else if (fl) {
-      L = fast_interp(fl[f], T->n_req[k], T->sum_len[k]);
-      P = fast_interp(fp[f], T->n_req[k], T->sum_len[k]);
+      L = fast_interp(fl[f], s_pj.n_req[k], s_pj.sum_len[k]);
+      P = fast_interp(fp[f], s_pj.n_req[k], s_pj.sum_len[k]);
     } else {
-      const Query q = make_query(T->n_req[k], T->sum_len[k], pr.tp, c.cand[f]);
+      const Query q = make_query(s_pj.n_req[k], s_pj.sum_len[k], pr.tp, c.cand[f]);
       L = interp(m.grid[0], q, nullptr);
       P = interp(m.grid[2], q, nullptr);
     }
     if (!model_value_ok(L)) atomicOr(&T->bad_lat[k], 1u << f);
     if (!model_value_ok(P)) atomicOr(&T->bad_pow[k], 1u << f);
-    const double A = __dmul_rn(T->wf[k], L);                               // dvfs.hpp:112-113, 154-155
+    const double A = __dmul_rn(s_pj.wf[k], L);                               // dvfs.hpp:112-113, 154-155
     T->A[k][f] = A;
     T->P[k][f] = P;
     T->E[k][f] = __dmul_rn(A, P);                                          // dvfs.hpp:167
