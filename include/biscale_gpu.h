@@ -378,7 +378,10 @@ int bs_project_batches(bs_ctx_t ctx, const bs_mpc_config* cfgs, const bs_schedul
                        int n_cfgs, const bs_mpc_problem* problems, int n, bs_projected_batch* out,
                        int32_t* out_K, int32_t* out_status);
 
-/* greedy_freq_select for n independent decisions (one CTA per decision). */
+/* greedy_freq_select for n independent decisions: one warp per decision for
+ * batches that fill the GPU, a CTA of 2-16 warps per decision for smaller
+ * ones, and a thread-block cluster of 8 CTAs per decision when n x 8 <= SMs
+ * (a single controller call).  Results are identical in every mode. */
 int bs_mpc_greedy(bs_ctx_t ctx, bs_models_t models, const bs_mpc_config* cfgs,
                   const bs_scheduler_policy* policies, int n_cfgs, const bs_mpc_problem* problems, int n,
                   bs_mpc_result* out);
