@@ -569,6 +569,15 @@ int run_enqueue(bs_ctx_t ctx, bs_models_t models, MpcRun* run, bool timing) {
   }
   if (!run->bfs_grid) {  // occupancy queries once per context
     if (!ctx->grid_cache[0]) {
+#ifdef BS_SWEEP_CARVEOUT
+      // A/B: the L1 / shared-memory split of the list kernels (percent shared)
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2, kSweep2>),
+                           cudaFuncAttributePreferredSharedMemoryCarveout, BS_SWEEP_CARVEOUT);
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3, kSweep3>),
+                           cudaFuncAttributePreferredSharedMemoryCarveout, BS_SWEEP_CARVEOUT);
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(bfs_node_kernel),
+                           cudaFuncAttributePreferredSharedMemoryCarveout, BS_SWEEP_CARVEOUT);
+#endif
       ctx->grid_cache[0] = grid_for(ctx, reinterpret_cast<const void*>(bfs_node_kernel), 256);
       ctx->grid_cache[1] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB2, kSweep2>), 256);
       ctx->grid_cache[2] = grid_for(ctx, reinterpret_cast<const void*>(sweep_kernel<kSweepMinB3, kSweep3>), 256);
