@@ -141,9 +141,24 @@ struct DFastPair {
 // fl / fp (optional): the latency / power grids reduced to (pr.tp, cand[f])
 // for every candidate f -- bit-identical values with 2^(active axes) corners
 // instead of 2^rank; share: each batch is bracketed once for all candidates.
+#ifdef BS_PREP_PHASES
+#define BS_BT_MARK(i)                                                              \
+  if (threadIdx.x == 0 && (blockIdx.x & 63) == 0) {                                 \
+    unsigned long long t_;                                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+    bt_t[i] = t_;                                                                   \
+  }
+#else
+#define BS_BT_MARK(i)
+#endif
+
 __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg& c, const DWaiting* W,
                              const DRunning* R, DTables* T, int* s_status, const FastGrid* fl = nullptr,
                              const FastGrid* fp = nullptr, bool share = false) {
+#ifdef BS_PREP_PHASES
+  unsigned long long bt_t[8] = {0};
+#endif
+  BS_BT_MARK(0);
   __shared__ FastBrk s_bl[kMaxK], s_bp[kMaxK];
   // The projection is one thread's serial scan of the waiting queue: its rows
   // are first copied to shared memory by the whole block (one round trip),
@@ -171,12 +186,14 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
                                                   128ll * (i < lines ? i : i - lines)));
   }
   __syncthreads();
+  BS_BT_MARK(1);
   if (threadIdx.x == 0) {
     int st = staged ? project_wa(pr, c, WaitStaged{s_wrem, s_warr}, R, &s_pj) : project_dev(pr, c, W, R, &s_pj);
     if (st == BS_OK && (m.grid[0].bad_axis || m.grid[2].bad_axis) && s_pj.K > 0) st = BS_MODEL_ERROR;
     *s_status = st;
   }
   __syncthreads();
+  BS_BT_MARK(2);
   const int K = s_pj.K;
   const int nc = c.nc;
   if (threadIdx.x == 0) {
@@ -196,6 +213,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     }
   }
   __syncthreads();
+  BS_BT_MARK(3);
   if (*s_status != BS_OK) return;
   const bool shared_brk = fl && share;
   if (shared_brk) {
@@ -204,6 +222,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
       fast_brackets(fp[0], s_pj.n_req[k], s_pj.sum_len[k], s_bp[k]);
     }
     __syncthreads();
+  BS_BT_MARK(4);
   }
   for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {
     const int k = e / nc, f = e - k * nc;
@@ -230,6 +249,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     if (k == 0) T->T1[f] = __dadd_rn(pr.now, c.cand[f] != pr.cur_freq ? T->B1[0][f] : T->B0[0][f]);
   }
   __syncthreads();
+  BS_BT_MARK(5);
   // per-level sorted order of the switched steps: one thread per (k, f)
   // computes its rank (ties by index), then scatters
   int finite = 1, filt = 1;
@@ -261,6 +281,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
   }
   const int all_finite = __syncthreads_and(finite);
   const int all_filt = __syncthreads_and(filt);
+  BS_BT_MARK(6);
   for (int e = threadIdx.x; e < K * nc; e += blockDim.x) {  // ranks of every level are in place
     const int k = e / nc, f = e - k * nc;
     T->sinfo[k][T->rank[k][f]] =
@@ -271,6 +292,11 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     T->sorted_ok = all_finite && isfinite(T->ttft);
   }
   __syncthreads();
+#ifdef BS_PREP_PHASES
+  if (threadIdx.x == 0 && (blockIdx.x & 63) == 0)
+    printf("tables ns: stage %llu project %llu copy %llu brackets %llu corners %llu ranks %llu\n", bt_t[1] - bt_t[0],
+           bt_t[2] - bt_t[1], bt_t[3] - bt_t[2], bt_t[4] - bt_t[3], bt_t[5] - bt_t[4], bt_t[6] - bt_t[5]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
