@@ -292,6 +292,7 @@ __device__ void greedy_coop(const DModels& m, const DProblem& pr, const DMpcCfg&
       const int lines = static_cast<int>((sizeof(FastGrid) * c.nc + 127) / 128);
       for (int i = tid; i < 2 * lines; i += NT)
         asm volatile("prefetch.global.L1 [%0];" ::"l"((i < lines ? g0 : g1) + 128ll * (i < lines ? i : i - lines)));
+      prefetch_knots(fl, fp, tid - (NT - 2 * kMaxRank));
     }
     __syncthreads();
   }

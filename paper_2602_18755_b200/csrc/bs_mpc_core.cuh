@@ -138,6 +138,18 @@ struct DFastPair {
   int _pad;
 };
 
+// The knot vectors of candidate 0's reduced grids (the brackets' binary
+// searches read them next) prefetched into L1 by thread `t` in
+// [0, 2 kMaxRank): grid t / kMaxRank, axis t % kMaxRank.
+__device__ __forceinline__ void prefetch_knots(const FastGrid* fl, const FastGrid* fp, int t) {
+  if (t < 0 || t >= 2 * kMaxRank) return;
+  const FastGrid* g = t < kMaxRank ? fl : fp;
+  const int a = t % kMaxRank;
+  if (a >= g->na || g->fixed[a]) return;
+  const double* k = g->knots[a];
+  for (int i = 0; i < g->n[a]; i += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(k + i));
+}
+
 // fl / fp (optional): the latency / power grids reduced to (pr.tp, cand[f])
 // for every candidate f -- bit-identical values with 2^(active axes) corners
 // instead of 2^rank; share: each batch is bracketed once for all candidates.
@@ -184,6 +196,7 @@ __device__ void build_tables(const DModels& m, const DProblem& pr, const DMpcCfg
     for (int i = threadIdx.x; i < 2 * lines; i += blockDim.x)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(i < lines ? fl : fp) +
                                                   128ll * (i < lines ? i : i - lines)));
+    prefetch_knots(fl, fp, static_cast<int>(threadIdx.x) - (blockDim.x - 2 * kMaxRank));
   }
   __syncthreads();
   BS_BT_MARK(1);
